@@ -1,0 +1,114 @@
+"""Pins for the oracle's counter-based Gaussian generator.
+
+Pinned against: Random123 known-answer vectors (tests/golden/philox_kat.json), libm log/cos
+(a library routine the self-written polynomials must reproduce), distributional tests
+(moments, Kolmogorov-Smirnov against the exact N(0,1) CDF) and the (row, col) indexing
+contract that makes S_{d=b} the leading rows of S_{d>b}.
+"""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+from scipy import stats
+
+import oracle
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def test_philox_known_answers():
+    vecs = json.load(open(os.path.join(GOLD, "philox_kat.json")))["vectors"]
+    for v in vecs:
+        out = oracle.philox4x32_10([int(x, 16) for x in v["ctr"]], [int(x, 16) for x in v["key"]])
+        assert ["%08x" % x for x in out] == v["out"]
+
+
+def test_log_matches_libm():
+    rng = np.random.default_rng(1)
+    xs = np.concatenate([
+        rng.random(20000),
+        1.0 - rng.random(2000) * 1e-6,  # near 1: log -> 0, relative accuracy matters
+        np.ldexp(rng.random(2000) + 0.5, -rng.integers(1, 60, 2000)),
+        [2.0 ** -53, 0.5 * 2.0 ** -52, 0.5, 1.0, math.sqrt(0.5), 0.7071067811865476],
+    ])
+    xs = xs[(xs > 0) & (xs <= 1)]
+    for x in xs:
+        ref = math.log(x)
+        got = oracle.log(x)
+        assert abs(got - ref) <= 4 * np.spacing(abs(ref)) + 1e-300, (x, got, ref)
+
+
+def test_cos2pi_matches_libm():
+    rng = np.random.default_rng(2)
+    us = np.concatenate([rng.random(20000), np.arange(0, 1, 1 / 64), [0.125, 0.375, 0.999999999]])
+    for u in us:
+        ref = math.cos(2 * math.pi * u)
+        got = oracle.cos2pi(u)
+        # libm's own argument 2*pi*u carries ~2e-16 absolute error
+        assert abs(got - ref) <= 1e-15, (u, got, ref)
+    # exact quadrant points
+    assert oracle.cos2pi(0.0) == 1.0
+    assert oracle.cos2pi(0.5) == -1.0
+    assert abs(oracle.cos2pi(0.25)) < 1e-16 and abs(oracle.cos2pi(0.75)) < 1e-16
+
+
+def test_gauss_is_pure_function_of_counter():
+    a = [oracle.gauss(7, 0, i, j) for i in range(3) for j in range(5)]
+    b = [oracle.gauss(7, 0, i, j) for i in range(3) for j in range(5)]
+    assert a == b
+    assert oracle.gauss(7, 0, 1, 2) != oracle.gauss(7, 1, 1, 2)  # streams differ
+    assert oracle.gauss(7, 0, 1, 2) != oracle.gauss(8, 0, 1, 2)  # seeds differ
+    assert oracle.gauss(7, 0, 1, 2) != oracle.gauss(7, 0, 2, 1)  # (i,j) not symmetric
+    # 64-bit column index reaches the hi word of the counter
+    assert oracle.gauss(7, 0, 0, 1) != oracle.gauss(7, 0, 0, 1 + (1 << 32))
+
+
+def test_gauss_distribution():
+    S = oracle.sketch_operator(64, 4096, seed=123)
+    z = S.ravel()
+    assert abs(z.mean()) < 0.02
+    assert 0.97 < z.var() < 1.03
+    assert stats.kstest(z, "norm").pvalue > 1e-3
+    # 4th moment of N(0,1) is 3
+    assert 2.85 < np.mean(z ** 4) < 3.15
+
+
+def test_sketch_rows_are_prefix_stable():
+    """S(i,j) depends on (i,j) only, so S_{d=b} = S_{d>b}(:b, :) (needed for the P:603 pin)."""
+    S1 = oracle.sketch_operator(8, 50, seed=5)
+    S2 = oracle.sketch_operator(10, 50, seed=5)
+    assert np.array_equal(S1, S2[:8])
+
+
+def test_sketch_of_identity_is_operator():
+    """S . I = S exactly: one nonzero product per sum."""
+    S = oracle.sketch_operator(6, 9, seed=11)
+    MskT = oracle.sketch(np.eye(9), 6, seed=11)
+    assert np.array_equal(MskT.T, S)
+
+
+def test_sketch_matches_library_matmul():
+    import inputs
+
+    A = inputs.gaussian(300, 70, seed=3)
+    d = 24
+    S = oracle.sketch_operator(d, 300, seed=9)
+    MskT = oracle.sketch(A, d, seed=9)
+    ref = (S @ A).T
+    assert np.linalg.norm(MskT - ref) / np.linalg.norm(ref) < 1e-14
+
+
+def test_sketch_integer_inputs_exact():
+    import inputs
+
+    A = inputs.integer_valued(40, 12, seed=4)
+    MskT = oracle.sketch(A, 5, seed=2)
+    S = oracle.sketch_operator(5, 40, seed=2)
+    # S entries are not integers, but each product a*S with |a| <= 4 integer is exact only
+    # up to rounding of the sum; compare with exact rational accumulation via math.fsum
+    for j in range(12):
+        for i in range(5):
+            exact = math.fsum(A[l, j] * S[i, l] for l in range(40))
+            assert abs(MskT[j, i] - exact) <= 40 * np.spacing(max(abs(exact), 1.0))
