@@ -1,0 +1,121 @@
+/*
+ * bqrrp.h — C ABI of the B200 (sm_100a) BQRRP library, libbqrrp.so.
+ *
+ * BQRRP = Blocked QR with Randomization and Pivoting (Melnichenko, Murray, Killian, Demmel,
+ * Mahoney, Luszczek, Gates; arXiv 2507.00976).  Citations "P:n" are lines of the paper's LaTeX
+ * source; readings "Zn" are listed in DESIGN.md §3.
+ *
+ * Conventions for every entry point
+ *   - Matrices are column-major fp64 with a leading dimension; "device" pointers are CUDA device
+ *     memory of the current device, "host" pointers are ordinary (preferably pinned) host memory.
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).  Work is enqueued on
+ *     it; device outputs are valid after the stream is synchronised.  bqrrp_factor* additionally
+ *     synchronises the stream once per block iteration to read the block rank k (P:490 step
+ *     bqrrp:rank_est decides the loop), so *rank is known on return.
+ *   - Return value: 0 = success; -i = the i-th argument is illegal (LAPACK info convention; checked
+ *     before any launch, nothing is touched); BQRRP_ENUMERIC = non-finite sketch or a Cholesky-QR
+ *     breakdown; BQRRP_ENOMEM / BQRRP_ECUDA on allocation / CUDA failure (A, tau, J contents are then
+ *     unspecified).  bqrrp_last_error() returns a thread-local message for the last failure.
+ *   - The library owns no memory after a call returns and keeps no global state except
+ *     per-thread error strings; calls on different streams are independent.
+ */
+#ifndef BQRRP_H
+#define BQRRP_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BQRRP_OK 0
+#define BQRRP_ENUMERIC 1
+#define BQRRP_ENOMEM (-100)
+#define BQRRP_ECUDA (-101)
+#define BQRRP_ENCCL (-102)
+
+typedef struct bqrrp_options {
+    /* tri_rank threshold relative to |R_sk^(0)(0,0)| (readings Z10/Z11).
+     * <= 0 selects the default 10 * u * sqrt(max(m, n)). */
+    double rank_tol;
+    /* Cholesky-QR passes in the panel (Alg. 3 step cholqr:cholqr): 2 = CholQR2 (default,
+     * DESIGN.md §7.3), 1 = the paper's single pass. */
+    int cholqr_passes;
+    /* reserved (0) */
+    int reserved0;
+    /* optional host float[8] out: per-phase milliseconds in the order of SPEC's profile keys
+     * {qrcp_wide, tri_rank, col_perm, qr_tall, apply_trans_q, sample_update, other, total};
+     * NULL = no timing (timing adds one event pair per phase). */
+    float* phase_ms;
+} bqrrp_options;
+
+/* Bytes of device workspace bqrrp_factor needs for an m x n matrix with block b and sketch d. */
+int bqrrp_workspace_query(int64_t m, int64_t n, int64_t b, int64_t d, size_t* bytes);
+
+/*
+ * BQRRP factorization, Alg. 1 with the in-place recipe of §3:
+ *   A(:, J) = Q R,  Q = H_1 ... H_l,  H_j = I - tau_j v_j v_j^T  (GEQP3 output format).
+ *   m, n      matrix size (>= 0)
+ *   A         device, m x n, lda >= max(1, m); overwritten: R (upper trapezoid, rows >= l zero) on and
+ *             above the diagonal, v_j (unit head implicit) below; A(l:m, l:n) = 0 (reading Z16)
+ *   b         block size (>= 1; b >= min(m,n) means a single iteration)
+ *   d         sketch rows, b <= d <= m  (d = ceil(gamma b); d > m is a config violation)
+ *   seed      64-bit seed of the counter-based Gaussian sketch
+ *   tau       device, min(m,n) doubles; tau(l:) = 0
+ *   J         device, n int64, one-based gather permutation
+ *   rank      host int64 out: l
+ *   workspace device buffer of >= bqrrp_workspace_query bytes, or NULL (allocated stream-ordered
+ *             with cudaMallocAsync and freed before return)
+ */
+int bqrrp_factor(int64_t m, int64_t n, double* A, int64_t lda, int64_t b, int64_t d, uint64_t seed, double* tau,
+                 int64_t* J, int64_t* rank, void* workspace, size_t ws_bytes, void* stream);
+
+/* Same as bqrrp_factor with options (NULL = defaults). */
+int bqrrp_factor_ex(int64_t m, int64_t n, double* A, int64_t lda, int64_t b, int64_t d, uint64_t seed, double* tau,
+                    int64_t* J, int64_t* rank, void* workspace, size_t ws_bytes, void* stream,
+                    const bqrrp_options* opts);
+
+/* End-to-end variant on HOST buffers (A_host m x n col-major, tau_host, J_host): copies A to the device,
+ * factors, copies A, tau, J back; synchronous.  Device memory is allocated and freed inside. */
+int bqrrp_factor_host(int64_t m, int64_t n, double* A_host, int64_t lda, int64_t b, int64_t d, uint64_t seed,
+                      double* tau_host, int64_t* J_host, int64_t* rank, void* stream, const bqrrp_options* opts);
+
+/* ---- debug / unit-test entry points (same conventions; all device pointers) ---- */
+
+/* S (d x m, ld d; NULL to skip) and MskT = (S A)^T (n x d, ld n). */
+int bqrrp_debug_sketch(int64_t m, int64_t n, const double* A, int64_t lda, int64_t d, uint64_t seed, double* S_out,
+                       double* MskT_out, void* stream);
+
+/* C = alpha op(A) op(B) + beta C with the DMMA engine; ta/tb: 0 = N, 1 = T. */
+int bqrrp_debug_gemm(int ta, int tb, int64_t M, int64_t N, int64_t K, double alpha, const double* A, int64_t lda,
+                     const double* B, int64_t ldb, double beta, double* C, int64_t ldc, void* stream);
+
+/* Partial-pivot LU of the w x d matrix L (in place): ipiv (device int64, min(w,d)) one-based LAPACK swap
+ * list. */
+int bqrrp_debug_lu_pivots(int64_t w, int64_t d, double* L, int64_t ld, int64_t* ipiv, void* stream);
+
+/* R_sk^T of the sketch window W^T (w x d, ld): in place, as stored by the driver (upper trapezoid of
+ * R_sk transposed, explicit zeros). */
+int bqrrp_debug_sketch_qr(int64_t w, int64_t d, double* WT, int64_t ld, void* stream);
+
+/* Columns [0, w) of X (rows x w) gathered by J_qr = piv_transform(ipiv);
+ * ipiv device int64 one-based, length nlu.  Jqr_out (device int64, w; may be NULL) = J_qr. */
+int bqrrp_debug_permute(int64_t rows, int64_t w, double* X, int64_t ldx, int64_t nlu, const int64_t* ipiv,
+                        int64_t* Jqr_out, void* stream);
+
+/* Panel: CholQR(passes) + Householder reconstruction of P (h x k, ld) preconditioned by Rsk11 (k x k
+ * upper, ld k), written in GEQP3 format in place (R11 on/above, V below) with tau (k), plus the
+ * compact-WY update of the trailing C (h x t, ld) that follows P in memory (t may be 0). */
+int bqrrp_debug_panel(int64_t h, int64_t k, int64_t t, double* P, int64_t ld, const double* Rsk11, double* tau,
+                      int cholqr_passes, void* stream);
+
+const char* bqrrp_strerror(int status);
+const char* bqrrp_last_error(void);
+/* Library version string. */
+const char* bqrrp_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BQRRP_H */

@@ -1,0 +1,35 @@
+// blas.cuh — dense building blocks on the DMMA GEMM engine (host launchers).
+#pragma once
+#include "common.cuh"
+
+namespace bqrrp {
+
+// C = alpha op(A) op(B) + beta C (column-major).  tri: only the lower triangle of C is needed.
+void gemm(Ctx& cx, bool ta, bool tb, int64_t M, int64_t N, int64_t K, double alpha, const double* A, int64_t lda,
+          const double* B, int64_t ldb, double beta, double* C, int64_t ldc, bool tri = false);
+
+// X op(T) = B, right side, op(T) upper triangular (n x n), in place on B (rows x n).
+//   t_lower = false: T stored upper, op(T) = T;  t_lower = true: T stored lower, op(T) = T^T.
+void trsm_right_upper(Ctx& cx, int64_t rows, int64_t n, const double* T, int64_t ldt, bool t_lower, bool unit,
+                      double* B, int64_t ldb);
+
+// L X = B, left side, L unit lower (n x n), in place on B (n x cols).
+void trsm_left_lower_unit(Ctx& cx, int64_t n, int64_t cols, const double* L, int64_t ldl, double* B, int64_t ldb);
+
+// Lower Cholesky G = L L^T in place (n x n, lower part read); strict upper part zeroed on return.
+// A non-positive pivot sets flags[F_POTRF_INFO] = first failing column + 1 (and stops that block).
+void potrf_lower(Ctx& cx, int64_t n, double* G, int64_t ldg);
+
+// Householder reconstruction LU (BD2015 Alg. 5 reading): in place on the top n x n of
+// Q (ld), no pivoting, with S_jj = -sgn(current Q_jj) chosen on the fly; pivot = Q_jj - S_jj.
+// On return: strict lower = L (unit), upper = U; S[j] = S_jj (+-1).
+void getrf_nopiv_sign(Ctx& cx, int64_t n, double* Q, int64_t ldq, double* S);
+
+// small element-wise kernels
+void copy_matrix(Ctx& cx, int64_t rows, int64_t cols, const double* src, int64_t lds, double* dst, int64_t ldd);
+void transpose_copy(Ctx& cx, int64_t rows, int64_t cols, const double* src, int64_t lds, double* dst, int64_t ldd);
+void set_zero(Ctx& cx, int64_t rows, int64_t cols, double* A, int64_t lda);
+// uplo: 'L' zero the strict upper part, 'U' zero the strict lower part
+void zero_triangle(Ctx& cx, char keep, int64_t n, int64_t cols, double* A, int64_t lda, bool unit_diag = false);
+
+}  // namespace bqrrp

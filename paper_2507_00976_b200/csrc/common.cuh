@@ -1,0 +1,104 @@
+// common.cuh — shared plumbing of the BQRRP CUDA library (no method arithmetic here).
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+namespace bqrrp {
+
+// Error carried from a failing CUDA call up to the C-ABI, which maps it to BQRRP_ECUDA.
+struct CudaError : std::runtime_error {
+    explicit CudaError(const std::string& s) : std::runtime_error(s) {}
+};
+
+#define BQ_CUDA(x)                                                                                      \
+    do {                                                                                                \
+        cudaError_t e_ = (x);                                                                           \
+        if (e_ != cudaSuccess)                                                                          \
+            throw ::bqrrp::CudaError(std::string(#x) + " @ " + __FILE__ + ":" + std::to_string(__LINE__) + \
+                                     ": " + cudaGetErrorString(e_));                                    \
+    } while (0)
+
+#define BQ_LAUNCH_CHECK() BQ_CUDA(cudaGetLastError())
+
+inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+inline int64_t imin(int64_t a, int64_t b) { return a < b ? a : b; }
+inline int64_t imax(int64_t a, int64_t b) { return a > b ? a : b; }
+
+// A column-major matrix view on the device.
+struct Mat {
+    double* p;
+    int64_t ld;
+    __host__ __device__ double* at(int64_t i, int64_t j) const { return p + i + j * ld; }
+    __host__ __device__ Mat sub(int64_t i, int64_t j) const { return Mat{p + i + j * ld, ld}; }
+};
+
+// Optional per-phase timer: mark(p) closes the running phase and opens phase p.
+enum Phase { PH_QRCP_WIDE = 0, PH_TRI_RANK, PH_COL_PERM, PH_QR_TALL, PH_APPLY_QT, PH_SAMPLE_UPDATE, PH_OTHER, PH_TOTAL };
+struct Timer {
+    bool on = false;
+    cudaStream_t st = 0;
+    std::vector<std::pair<int, cudaEvent_t>> ev;
+    void mark(int phase)
+    {
+        if (!on) return;
+        cudaEvent_t e;
+        if (cudaEventCreate(&e) != cudaSuccess) return;
+        cudaEventRecord(e, st);
+        ev.push_back({phase, e});
+    }
+    void finish(float* out)
+    {
+        if (!on) return;
+        for (int i = 0; i < 8; ++i) out[i] = 0.f;
+        if (!ev.empty()) {
+            cudaEventSynchronize(ev.back().second);
+            for (size_t i = 0; i + 1 < ev.size(); ++i) {
+                float ms = 0.f;
+                cudaEventElapsedTime(&ms, ev[i].second, ev[i + 1].second);
+                out[ev[i].first] += ms;
+            }
+            float tot = 0.f;
+            cudaEventElapsedTime(&tot, ev.front().second, ev.back().second);
+            out[PH_TOTAL] = tot;
+        }
+        for (auto& p : ev) cudaEventDestroy(p.second);
+        ev.clear();
+    }
+};
+
+// Execution context: stream + a bump allocator over one workspace buffer + split-K scratch.
+struct Ctx {
+    cudaStream_t stream = 0;
+    int num_sms = 148;
+    char* ws = nullptr;
+    size_t ws_bytes = 0, ws_used = 0;
+    double* splitk = nullptr;
+    size_t splitk_elems = 0;
+    int* flags = nullptr;  // device int[8]: see Flags
+    Timer* timer = nullptr;
+    void mark(int phase) { if (timer) timer->mark(phase); }
+
+    double* alloc(size_t n_doubles)
+    {
+        size_t bytes = ((n_doubles * sizeof(double)) + 255) & ~size_t(255);
+        if (ws_used + bytes > ws_bytes) throw std::runtime_error("bqrrp workspace exhausted");
+        double* p = reinterpret_cast<double*>(ws + ws_used);
+        ws_used += bytes;
+        return p;
+    }
+    template <typename T>
+    T* alloc_as(size_t n)
+    {
+        return reinterpret_cast<T*>(alloc((n * sizeof(T) + 7) / 8));
+    }
+};
+
+// Device flag slots (int) written by kernels and read back once per iteration.
+enum Flags { F_K = 0, F_ZERO_COL = 1, F_POTRF_INFO = 2, F_NONFINITE = 3, F_NT = 4, F_NFLAGS = 8 };
+
+}  // namespace bqrrp

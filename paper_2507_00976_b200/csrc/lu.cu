@@ -1,0 +1,217 @@
+// lu.cu — K-LU: partial-pivot LU of the tall w x d sketch transpose, for its pivots
+// (Alg. 2 "Practical wide QRCP": GETRF on the transposed sketch).
+//
+// Recursive right-looking LU (pivots only: the left factor's row swaps are never applied to
+// already-factored columns because only J_lu is consumed).  Leaves are jb-column panels
+// factored by one cooperative kernel: the panel rows are split over G CTAs and held in shared
+// memory; each column step is ONE grid-wide barrier: every CTA publishes its local first-max
+// candidate (|value|, row, full panel row) and the current row j, then all CTAs pick the same winner
+// (largest |value|, lowest row index on ties: IDAMAX, reading Z19), swap and apply the rank-1 update
+// to their own rows.  An exactly-zero pivot column is skipped (no swap, no scaling; Z18).
+#include <cooperative_groups.h>
+
+#include "blas.cuh"
+#include "bqrrp_internal.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace bqrrp {
+
+struct LuPanelArgs {
+    double* L;
+    int64_t ld;
+    int64_t w;       // rows of the LU matrix
+    int64_t c0;      // first panel column (= first active row)
+    int jb;          // panel width
+    int R;           // rows per CTA
+    int* ipiv;       // out: ipiv[c0 + j] = pivot row (0-based, absolute)
+    double* xbuf;    // exchange: [2][G][LU_XSTRIDE]
+    double* rowj;    // exchange: [2][LU_JBMAX]
+};
+
+constexpr int LU_JBMAX = 32;
+constexpr int LU_XSTRIDE = 2 + LU_JBMAX;
+constexpr int LU_THREADS = 256;
+
+__global__ void __launch_bounds__(LU_THREADS, 1) lu_panel_kernel(LuPanelArgs a)
+{
+    cg::grid_group grid = cg::this_grid();
+    extern __shared__ double sp[];  // sp[c * R + r]
+    __shared__ double red_v[LU_THREADS / 32];
+    __shared__ int64_t red_i[LU_THREADS / 32];
+    __shared__ double pivrow[LU_JBMAX], oldrow[LU_JBMAX];
+    __shared__ int64_t s_piv;
+
+    const int G = gridDim.x, cta = blockIdx.x, tid = threadIdx.x, R = a.R, jb = a.jb;
+    const int64_t rbeg = a.c0 + (int64_t)cta * R;  // absolute first row of this CTA
+    const int64_t rows_here = (rbeg < a.w) ? ((a.w - rbeg < R) ? a.w - rbeg : R) : 0;
+
+    for (int idx = tid; idx < R * jb; idx += LU_THREADS) {
+        int r = idx % R, c = idx / R;
+        sp[idx] = (r < rows_here) ? a.L[rbeg + r + (a.c0 + c) * a.ld] : 0.0;
+    }
+    __syncthreads();
+
+    for (int j = 0; j < jb; ++j) {
+        const int par = j & 1;
+        const int64_t jr = a.c0 + j;  // absolute row of the pivot position
+        // local first-max of |L(r, j)| over active rows r >= jr
+        double bv = -1.0;
+        int64_t bi = INT64_MAX;
+        for (int r = tid; r < rows_here; r += LU_THREADS) {
+            int64_t ar = rbeg + r;
+            if (ar < jr) continue;
+            double v = fabs(sp[j * R + r]);
+            if (v > bv) { bv = v; bi = ar; }  // ascending r per thread: first index kept on ties
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            double ov = __shfl_down_sync(0xffffffffu, bv, o);
+            int64_t oi = __shfl_down_sync(0xffffffffu, bi, o);
+            if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+        }
+        if ((tid & 31) == 0) { red_v[tid >> 5] = bv; red_i[tid >> 5] = bi; }
+        __syncthreads();
+        if (tid == 0) {
+            for (int wv = 1; wv < LU_THREADS / 32; ++wv)
+                if (red_v[wv] > bv || (red_v[wv] == bv && red_i[wv] < bi)) { bv = red_v[wv]; bi = red_i[wv]; }
+            double* slot = a.xbuf + ((int64_t)par * G + cta) * LU_XSTRIDE;
+            slot[0] = bv;
+            slot[1] = __longlong_as_double((long long)bi);
+            s_piv = bi;
+        }
+        __syncthreads();
+        if (tid < jb) {
+            double* slot = a.xbuf + ((int64_t)par * G + cta) * LU_XSTRIDE;
+            int64_t li = s_piv - rbeg;
+            slot[2 + tid] = (s_piv != INT64_MAX) ? sp[tid * R + li] : 0.0;
+            if (jr >= rbeg && jr < rbeg + rows_here) a.rowj[par * LU_JBMAX + tid] = sp[tid * R + (jr - rbeg)];
+        }
+        __threadfence();
+        grid.sync();
+        // every CTA picks the same winner
+        if (tid == 0) {
+            double gv = -1.0;
+            int64_t gi = INT64_MAX;
+            int gw = 0;
+            for (int q = 0; q < G; ++q) {
+                const double* slot = a.xbuf + ((int64_t)par * G + q) * LU_XSTRIDE;
+                double v = __ldcg(slot);
+                int64_t i = (int64_t)__double_as_longlong(__ldcg(slot + 1));
+                if (v > gv || (v == gv && i < gi)) { gv = v; gi = i; gw = q; }
+            }
+            s_piv = gi;
+            red_i[0] = gw;
+            if (cta == 0) a.ipiv[jr] = (int)(gi);
+        }
+        __syncthreads();
+        const int64_t piv = s_piv;
+        if (tid < jb) {
+            pivrow[tid] = __ldcg(a.xbuf + ((int64_t)par * G + red_i[0]) * LU_XSTRIDE + 2 + tid);
+            oldrow[tid] = __ldcg(a.rowj + par * LU_JBMAX + tid);
+        }
+        __syncthreads();
+        const double u = pivrow[j];
+        if (u != 0.0) {
+            if (piv != jr) {
+                if (piv >= rbeg && piv < rbeg + rows_here && tid < jb) sp[tid * R + (piv - rbeg)] = oldrow[tid];
+                if (jr >= rbeg && jr < rbeg + rows_here && tid < jb) sp[tid * R + (jr - rbeg)] = pivrow[tid];
+            }
+            __syncthreads();
+            for (int r = tid; r < rows_here; r += LU_THREADS) {
+                if (rbeg + r <= jr) continue;
+                double l = sp[j * R + r] / u;
+                sp[j * R + r] = l;
+                for (int c = j + 1; c < jb; ++c) sp[c * R + r] = fma(-l, pivrow[c], sp[c * R + r]);
+            }
+        }
+        __syncthreads();
+    }
+    for (int idx = tid; idx < R * jb; idx += LU_THREADS) {
+        int r = idx % R, c = idx / R;
+        if (r < rows_here) a.L[rbeg + r + (a.c0 + c) * a.ld] = sp[idx];
+    }
+}
+
+// Apply the row interchanges ipiv[k0..k1) (sequentially, ascending) to columns [c0, c1).
+__global__ void laswp_kernel(double* L, int64_t ld, int64_t c0, int64_t c1, const int* ipiv, int64_t k0, int64_t k1)
+{
+    int64_t c = c0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= c1) return;
+    double* col = L + c * ld;
+    for (int64_t k = k0; k < k1; ++k) {
+        int64_t p = ipiv[k];
+        if (p != k) {
+            double t = col[k];
+            col[k] = col[p];
+            col[p] = t;
+        }
+    }
+}
+
+static void lu_panel(Ctx& cx, double* L, int64_t ld, int64_t w, int64_t c0, int jb, int* ipiv, double* xbuf,
+                     double* rowj)
+{
+    int64_t rows = w - c0;
+    // rows per CTA: fill the SMs but keep >= 32 rows per CTA and the slab within shared memory
+    int G = (int)imin(cx.num_sms, imax(1, cdiv(rows, 64)));
+    int R = (int)cdiv(rows, G);
+    size_t smem = (size_t)R * jb * sizeof(double);
+    if (smem > 200 * 1024) throw std::runtime_error("lu_panel: panel too tall for shared memory");
+    static bool attr = false;
+    if (!attr) {
+        BQ_CUDA(cudaFuncSetAttribute(lu_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        attr = true;
+    }
+    LuPanelArgs a{L, ld, w, c0, jb, R, ipiv, xbuf, rowj};
+    void* args[] = {&a};
+    BQ_CUDA(cudaLaunchCooperativeKernel((void*)lu_panel_kernel, dim3(G), dim3(LU_THREADS), args, smem, cx.stream));
+}
+
+static int lu_leaf_width(int64_t rows, int num_sms)
+{
+    // widest leaf whose per-CTA slab fits shared memory
+    int64_t R = cdiv(rows, num_sms);
+    if (R * 32 * 8 <= 200 * 1024) return 32;
+    if (R * 16 * 8 <= 200 * 1024) return 16;
+    return 8;
+}
+
+static void getrf_rec(Ctx& cx, double* L, int64_t ld, int64_t w, int64_t c0, int64_t c1, int* ipiv, double* xbuf,
+                      double* rowj, int leaf)
+{
+    int64_t nc = c1 - c0;
+    if (nc <= leaf) {
+        lu_panel(cx, L, ld, w, c0, (int)nc, ipiv, xbuf, rowj);
+        return;
+    }
+    int64_t mid = c0 + cdiv(nc / 2, leaf) * leaf;
+    getrf_rec(cx, L, ld, w, c0, mid, ipiv, xbuf, rowj, leaf);
+    // swaps of the left half onto the right half's columns
+    int64_t ncr = c1 - mid;
+    laswp_kernel<<<(unsigned)cdiv(ncr, 128), 128, 0, cx.stream>>>(L, ld, mid, c1, ipiv, c0, mid);
+    BQ_LAUNCH_CHECK();
+    // U12 = L11^{-1} A12 ; A22 -= L21 U12
+    double* L11 = L + c0 + c0 * ld;
+    double* A12 = L + c0 + mid * ld;
+    trsm_left_lower_unit(cx, mid - c0, ncr, L11, ld, A12, ld);
+    gemm(cx, false, false, w - mid, ncr, mid - c0, -1.0, L + mid + c0 * ld, ld, A12, ld, 1.0, L + mid + mid * ld, ld);
+    getrf_rec(cx, L, ld, w, mid, c1, ipiv, xbuf, rowj, leaf);
+    // right half's swaps back onto the left half's L columns, so that [c0, c1) is consistent for the
+    // caller's L21 (as DGETRF2 does)
+    laswp_kernel<<<(unsigned)cdiv(mid - c0, 128), 128, 0, cx.stream>>>(L, ld, c0, mid, ipiv, mid, c1);
+    BQ_LAUNCH_CHECK();
+}
+
+void getrf_pivots(Ctx& cx, double* L, int64_t ld, int64_t w, int64_t d, int* ipiv)
+{
+    int64_t nlu = imin(w, d);
+    if (nlu <= 0) return;
+    size_t mark = cx.ws_used;
+    double* xbuf = cx.alloc(2 * (size_t)cx.num_sms * LU_XSTRIDE);
+    double* rowj = cx.alloc(2 * LU_JBMAX);
+    int leaf = lu_leaf_width(w, cx.num_sms);
+    getrf_rec(cx, L, ld, w, 0, nlu, ipiv, xbuf, rowj, leaf);
+    cx.ws_used = mark;
+}
+
+}  // namespace bqrrp

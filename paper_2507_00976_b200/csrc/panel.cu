@@ -1,0 +1,109 @@
+// panel.cu — a4 + a5: the CholQR panel with Householder reconstruction and the compact-WY trailing
+// update (Alg. 3 "Cholesky QR + dependencies", in-place recipe P:1032-1053; apply_trans_q
+// P:781-808).
+//
+//   M_pre  = P(:, 0:k) R_sk11^{-1}                               (Alg. 3 step cholqr:precond)
+//   for pass in 1..passes:  G = Q^T Q, G = C C^T, Q <- Q C^{-T}   (cholqr; passes = 2 is CholQR2,
+//                                                                  DESIGN.md §7.3)
+//   Q - [S; 0] = L U (no pivoting, S_jj = -sgn(Q'_jj) on the fly)   (cholqr:orhr_col, BD2015 Alg. 5/6;
+//   V = L, T = -U S Y1^{-T}, tau = diag(T)                           P:697-701)
+//   R11 = diag(S) C_last^T ... C_1^T R_sk11                        (cholqr:undo_precond, reading Z7)
+//   C <- C - V T^T (V^T C) on C = A(s:m, s+k:n)                    (apply_trans_q, compact WY)
+#include "blas.cuh"
+#include "bqrrp_internal.cuh"
+
+namespace bqrrp {
+
+// T(i,j) = -U(i,j) S_j for i <= j, 0 below (the right-hand side of T Y1^T = -U S).
+__global__ void build_t_rhs_kernel(int64_t k, const double* Q, int64_t ldq, const double* S, double* T)
+{
+    int64_t total = k * k;
+    for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += (int64_t)gridDim.x * blockDim.x) {
+        int64_t i = idx % k, j = idx / k;
+        T[idx] = (i <= j) ? -Q[i + j * ldq] * S[j] : 0.0;
+    }
+}
+
+__global__ void diag_to_tau_kernel(int64_t k, const double* T, double* tau)
+{
+    int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j < k) tau[j] = T[j + j * k];
+}
+
+// GEQP3-format write of the panel: A(s+i, s+j) = S_i R(i, j) for i <= j (< k); = V(i, j) for i > j.
+// Q (the reconstruction's L, unit diagonal implicit, and Y2 below) is converted in place to the
+// explicit V (ones on the diagonal, zeros above) used by the WY GEMMs.
+__global__ void write_panel_kernel(int64_t h, int64_t k, double* Q, int64_t ldq, const double* R, const double* S,
+                                   double* Ap, int64_t lda)
+{
+    int64_t total = h * k;
+    for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += (int64_t)gridDim.x * blockDim.x) {
+        int64_t i = idx % h, j = idx / h;
+        double* q = Q + i + j * ldq;
+        if (i > j) {
+            Ap[i + j * lda] = *q;
+        } else {
+            Ap[i + j * lda] = S[i] * R[i + j * k];
+            *q = (i == j) ? 1.0 : 0.0;
+        }
+    }
+}
+
+void panel_and_update(Ctx& cx, int64_t m, int64_t n, double* A, int64_t lda, int64_t s, int64_t k, const double* Rsk11,
+                      double* tau, int passes, PanelOut& out)
+{
+    const int64_t h = m - s;
+    size_t mark = cx.ws_used;
+    double* Q = cx.alloc((size_t)h * k);
+    double* Cf[4];
+    for (int p = 0; p < passes; ++p) Cf[p] = cx.alloc((size_t)k * k);
+    double* S = cx.alloc((size_t)k);
+    double* T = cx.alloc((size_t)k * k);
+    double* Wr = cx.alloc((size_t)k * k);
+    double* Wr2 = cx.alloc((size_t)k * k);
+    double* Ap = A + s + s * lda;
+    unsigned eb = (unsigned)imin(cdiv(h * k, 256), 8 * cx.num_sms);
+
+    // M_pre = P(:, 0:k) R_sk11^{-1}
+    copy_matrix(cx, h, k, Ap, lda, Q, h);
+    trsm_right_upper(cx, h, k, Rsk11, k, false, false, Q, h);
+    // Cholesky QR passes
+    for (int p = 0; p < passes; ++p) {
+        gemm(cx, true, false, k, k, h, 1.0, Q, h, Q, h, 0.0, Cf[p], k, /*tri=*/true);
+        potrf_lower(cx, k, Cf[p], k);
+        trsm_right_upper(cx, h, k, Cf[p], k, /*t_lower=*/true, false, Q, h);
+    }
+    // Householder reconstruction
+    getrf_nopiv_sign(cx, k, Q, h, S);
+    if (h > k) trsm_right_upper(cx, h - k, k, Q, h, false, false, Q + k, h);  // Y2 = Q2 U^{-1}
+    build_t_rhs_kernel<<<(unsigned)imin(cdiv(k * k, 256), 4 * cx.num_sms), 256, 0, cx.stream>>>(k, Q, h, S, T);
+    BQ_LAUNCH_CHECK();
+    trsm_right_upper(cx, k, k, Q, h, /*t_lower=*/true, /*unit=*/true, T, k);  // T Y1^T = -U S
+    zero_triangle(cx, 'U', k, k, T, k);
+    diag_to_tau_kernel<<<(unsigned)cdiv(k, 128), 128, 0, cx.stream>>>(k, T, tau + s);
+    BQ_LAUNCH_CHECK();
+    // R11 = S * C_last^T ... C_1^T * R_sk11
+    copy_matrix(cx, k, k, Rsk11, k, Wr, k);
+    for (int p = 0; p < passes; ++p) {
+        gemm(cx, true, false, k, k, k, 1.0, Cf[p], k, Wr, k, 0.0, Wr2, k);
+        double* t = Wr; Wr = Wr2; Wr2 = t;
+    }
+    write_panel_kernel<<<eb, 256, 0, cx.stream>>>(h, k, Q, h, Wr, S, Ap, lda);
+    BQ_LAUNCH_CHECK();
+    // compact-WY trailing update of A(s:m, s+k:n)
+    cx.mark(PH_APPLY_QT);
+    const int64_t t = n - s - k;
+    if (t > 0) {
+        double* W = cx.alloc((size_t)k * t);
+        double* W2 = cx.alloc((size_t)k * t);
+        double* C = A + s + (s + k) * lda;
+        gemm(cx, true, false, k, t, h, 1.0, Q, h, C, lda, 0.0, W, k);    // W  = V^T C
+        gemm(cx, true, false, k, t, k, 1.0, T, k, W, k, 0.0, W2, k);     // W2 = T^T W
+        gemm(cx, false, false, h, t, k, -1.0, Q, h, W2, k, 1.0, C, lda);  // C -= V W2
+    }
+    out.T = T;
+    out.V = Q;
+    cx.ws_used = mark;
+}
+
+}  // namespace bqrrp

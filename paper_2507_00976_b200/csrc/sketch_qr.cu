@@ -1,0 +1,278 @@
+// sketch_qr.cu — K-SQR: R_sk, the R factor of the Householder QR of the permuted sketch
+// (Alg. 2 step wide_qrcp:compute, "Done via standard unpivoted QR factorization, GEQRF").
+//
+// The sketch lives transposed (MskT, n x d); its trailing window Wsk = MskT(s:n, :)^T is d x w.
+// GPU form (same result in exact arithmetic as QR of the whole d x w matrix):
+//   1. Wq = Wsk(:, 0:p) (d x p, p = min(d, w)), Householder QR by recursive blocking: jb-column leaf
+//      panels factored by one cooperative kernel (rows over G CTAs, one grid barrier per column:
+//      partial norms and partial dot products are published together, reflector convention H of
+//      DESIGN.md Z9/Z20), the leaf also returns its T block (LAPACK larft recurrence); interior
+//      nodes apply Q_left^T to the right half with three DMMA GEMMs and merge T
+//      (T12 = -T11 (V1^T V2) T22).
+//   2. R_sk(:, p:w) = Q_sk^T Wsk(:, p:w), i.e. in the transposed storage
+//      MskT(s+p:n, :) <- MskT(s+p:n, :) - ((MskT(s+p:n, :) V) T) V^T  (three DMMA GEMMs).
+//   3. R_sk(:, 0:p)^T (upper trapezoidal, explicit zeros) is written back to MskT(s:s+p, :).
+#include <cooperative_groups.h>
+
+#include "blas.cuh"
+#include "bqrrp_internal.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace bqrrp {
+
+constexpr int QR_JBMAX = 32;
+constexpr int QR_XSTRIDE = 1 + QR_JBMAX;  // s2, p[1..jb)
+constexpr int QR_THREADS = 256;
+
+struct QrPanelArgs {
+    double* A;
+    int64_t ld;
+    int64_t m;   // rows of Wq (d)
+    int64_t c0;  // first column; active rows [c0, m)
+    int jb;
+    int R;
+    double* tau;
+    double* V;  // explicit reflectors, m x p (ld m), pre-zeroed
+    double* T;  // T(c0:c0+jb, c0:c0+jb) written at T + c0 + c0*ldt
+    int64_t ldt;
+    double* xbuf;  // [2][G][QR_XSTRIDE] then [G][jb*jb] Gram partials
+    double* rowj;  // [2][QR_JBMAX]: alpha, a_c of the pivot row
+};
+
+__global__ void __launch_bounds__(QR_THREADS, 1) qr_panel_kernel(QrPanelArgs a)
+{
+    cg::grid_group grid = cg::this_grid();
+    extern __shared__ double sp[];  // sp[c * R + r]
+    __shared__ double red[QR_THREADS / 32][QR_JBMAX + 1];
+    __shared__ double wv[QR_JBMAX];
+    __shared__ double s_tau, s_beta, s_denom;
+    __shared__ double s_taus[QR_JBMAX];
+    const int G = gridDim.x, cta = blockIdx.x, tid = threadIdx.x, R = a.R, jb = a.jb;
+    const int lane = tid & 31, warp = tid >> 5;
+    const int64_t rbeg = a.c0 + (int64_t)cta * R;
+    const int64_t rows_here = (rbeg < a.m) ? ((a.m - rbeg < R) ? a.m - rbeg : R) : 0;
+
+    for (int idx = tid; idx < R * jb; idx += QR_THREADS) {
+        int r = idx % R, c = idx / R;
+        sp[idx] = (r < rows_here) ? a.A[rbeg + r + (a.c0 + c) * a.ld] : 0.0;
+    }
+    __syncthreads();
+
+    for (int j = 0; j < jb; ++j) {
+        const int par = j & 1;
+        const int64_t jr = a.c0 + j;
+        // partials over my rows r > jr: q[0] = sum x^2, q[c] = sum x * A(r, c) for c > j
+        double q[QR_JBMAX + 1];
+#pragma unroll
+        for (int c = 0; c <= QR_JBMAX; ++c) q[c] = 0.0;
+        for (int r = tid; r < rows_here; r += QR_THREADS) {
+            if (rbeg + r <= jr) continue;
+            double x = sp[j * R + r];
+            q[0] = fma(x, x, q[0]);
+#pragma unroll
+            for (int c = 1; c < QR_JBMAX; ++c)
+                if (j + c < jb) q[c] = fma(x, sp[(j + c) * R + r], q[c]);
+        }
+#pragma unroll
+        for (int c = 0; c < QR_JBMAX; ++c) {
+            if (c == 0 || j + c < jb) {
+                double v = q[c];
+                for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+                if (lane == 0) red[warp][c] = v;
+            }
+        }
+        __syncthreads();
+        if (tid < jb - j) {  // tid = c index (0 -> s2)
+            double v = 0.0;
+            for (int w = 0; w < QR_THREADS / 32; ++w) v += red[w][tid];
+            a.xbuf[((int64_t)par * G + cta) * QR_XSTRIDE + tid] = v;
+        }
+        if (jr >= rbeg && jr < rbeg + rows_here && tid < jb - j)  // alpha = A(jr, j), a_c = A(jr, j + c)
+            a.rowj[par * QR_JBMAX + tid] = sp[(j + tid) * R + (jr - rbeg)];
+        __threadfence();
+        grid.sync();
+        // every CTA forms the same reflector
+        if (tid < jb - j) {
+            double v = 0.0;
+            for (int g = 0; g < G; ++g) v += __ldcg(a.xbuf + ((int64_t)par * G + g) * QR_XSTRIDE + tid);
+            red[0][tid] = v;  // red[0][0] = sum x^2 below, red[0][c] = P_c
+            wv[tid] = __ldcg(a.rowj + par * QR_JBMAX + tid);  // wv[0] = alpha, wv[c] = a_c
+        }
+        __syncthreads();
+        if (tid == 0) {
+            double alpha = wv[0];
+            double nrm = sqrt(fma(alpha, alpha, red[0][0]));
+            if (nrm == 0.0) {
+                s_tau = 0.0; s_beta = 0.0; s_denom = 1.0;
+            } else {
+                double beta = (alpha >= 0.0) ? -nrm : nrm;  // convention H
+                s_beta = beta;
+                s_tau = (beta - alpha) / beta;
+                s_denom = alpha - beta;
+            }
+            s_taus[j] = s_tau;
+            if (cta == 0) a.tau[jr] = s_tau;
+        }
+        __syncthreads();
+        const double tau = s_tau, denom = s_denom;
+        if (tid > 0 && tid < jb - j) wv[tid] = wv[tid] + red[0][tid] / denom;  // w_c = v^T A(:, c)
+        __syncthreads();
+        if (tau != 0.0) {
+            for (int r = tid; r < rows_here; r += QR_THREADS) {
+                int64_t ar = rbeg + r;
+                if (ar < jr) continue;
+                if (ar == jr) {
+                    sp[j * R + r] = s_beta;
+                    for (int c = 1; c < jb - j; ++c) sp[(j + c) * R + r] -= tau * wv[c];
+                } else {
+                    double v = sp[j * R + r] / denom;
+                    sp[j * R + r] = v;
+                    for (int c = 1; c < jb - j; ++c) sp[(j + c) * R + r] = fma(-tau * wv[c], v, sp[(j + c) * R + r]);
+                }
+            }
+        }
+        __syncthreads();
+    }
+
+    // explicit V and Gram partials V^T V over my rows
+    double* gram = a.xbuf + 2 * (int64_t)G * QR_XSTRIDE;
+    for (int idx = tid; idx < R * jb; idx += QR_THREADS) {
+        int r = idx % R, c = idx / R;
+        if (r >= rows_here) continue;
+        int64_t ar = rbeg + r, cr = a.c0 + c;
+        double v = (ar == cr) ? 1.0 : (ar > cr ? sp[idx] : 0.0);
+        a.V[ar + cr * a.m] = v;
+        a.A[ar + cr * a.ld] = sp[idx];
+    }
+    for (int pq = tid; pq < jb * jb; pq += QR_THREADS) {
+        int p = pq % jb, qq = pq / jb;
+        double s = 0.0;
+        if (p < qq) {
+            for (int r = 0; r < rows_here; ++r) {
+                int64_t ar = rbeg + r;
+                double vp = (ar == a.c0 + p) ? 1.0 : (ar > a.c0 + p ? sp[p * R + r] : 0.0);
+                double vq = (ar == a.c0 + qq) ? 1.0 : (ar > a.c0 + qq ? sp[qq * R + r] : 0.0);
+                s = fma(vp, vq, s);
+            }
+        }
+        gram[(int64_t)cta * jb * jb + pq] = s;
+    }
+    __threadfence();
+    grid.sync();
+    if (cta != 0) return;
+    // CTA 0: T = larft(V, tau) from G = V^T V: T_jj = tau_j, T(0:j, j) = -tau_j T(0:j,0:j) G(0:j, j)
+    __shared__ double Gm[QR_JBMAX][QR_JBMAX + 1], Ts[QR_JBMAX][QR_JBMAX + 1];
+    for (int pq = tid; pq < jb * jb; pq += QR_THREADS) {
+        double s = 0.0;
+        for (int g = 0; g < G; ++g) s += __ldcg(gram + (int64_t)g * jb * jb + pq);
+        Gm[pq % jb][pq / jb] = s;
+        Ts[pq % jb][pq / jb] = 0.0;
+    }
+    __syncthreads();
+    for (int j = 0; j < jb; ++j) {
+        double tj = s_taus[j];
+        if (tid < j) {
+            double s = 0.0;
+            for (int l = tid; l < j; ++l) s = fma(Ts[tid][l], Gm[l][j], s);
+            Ts[tid][j] = -tj * s;
+        }
+        if (tid == 0) Ts[j][j] = tj;
+        __syncthreads();
+    }
+    for (int pq = tid; pq < jb * jb; pq += QR_THREADS) {
+        int p = pq % jb, qq = pq / jb;
+        a.T[(a.c0 + p) + (a.c0 + qq) * a.ldt] = Ts[p][qq];
+    }
+}
+
+static void qr_panel(Ctx& cx, double* A, int64_t ld, int64_t m, int64_t c0, int jb, double* tau, double* V, double* T,
+                     int64_t ldt, double* xbuf, double* rowj)
+{
+    int64_t rows = m - c0;
+    int G = (int)imin(cx.num_sms, imax(1, cdiv(rows, 64)));
+    int R = (int)cdiv(rows, G);
+    size_t smem = (size_t)R * jb * sizeof(double);
+    if (smem > 160 * 1024) throw std::runtime_error("qr_panel: panel too tall");
+    static bool attr = false;
+    if (!attr) {
+        BQ_CUDA(cudaFuncSetAttribute(qr_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+        attr = true;
+    }
+    QrPanelArgs a{A, ld, m, c0, jb, R, tau, V, T, ldt, xbuf, rowj};
+    void* args[] = {&a};
+    BQ_CUDA(cudaLaunchCooperativeKernel((void*)qr_panel_kernel, dim3(G), dim3(QR_THREADS), args, smem, cx.stream));
+}
+
+// Recursive QR of columns [c0, c1) of Wq (rows [c0, m)); V (m x p explicit), Tf (p x p).
+static void geqrf_rec(Ctx& cx, double* Wq, int64_t m, int64_t c0, int64_t c1, double* tau, double* V, double* Tf,
+                      int64_t p, double* W1, double* W2, double* xbuf, double* rowj)
+{
+    int64_t nc = c1 - c0;
+    if (nc <= QR_JBMAX) {
+        qr_panel(cx, Wq, m, m, c0, (int)nc, tau, V, Tf, p, xbuf, rowj);
+        return;
+    }
+    int64_t mid = c0 + cdiv(nc / 2, QR_JBMAX) * QR_JBMAX;
+    geqrf_rec(cx, Wq, m, c0, mid, tau, V, Tf, p, W1, W2, xbuf, rowj);
+    int64_t k1 = mid - c0, ncr = c1 - mid, h = m - c0;
+    const double* V1 = V + c0 + c0 * m;    // h x k1
+    const double* T11 = Tf + c0 + c0 * p;  // k1 x k1
+    double* A2 = Wq + c0 + mid * m;        // h x ncr
+    // A2 <- (I - V1 T11 V1^T)^T A2 = A2 - V1 T11^T (V1^T A2)
+    gemm(cx, true, false, k1, ncr, h, 1.0, V1, m, A2, m, 0.0, W1, k1);
+    gemm(cx, true, false, k1, ncr, k1, 1.0, T11, p, W1, k1, 0.0, W2, k1);
+    gemm(cx, false, false, h, ncr, k1, -1.0, V1, m, W2, k1, 1.0, A2, m);
+    geqrf_rec(cx, Wq, m, mid, c1, tau, V, Tf, p, W1, W2, xbuf, rowj);
+    // T12 = -T11 (V1^T V2) T22, V2 = V(c0:m, mid:c1) (zeros above row mid)
+    const double* V2 = V + c0 + mid * m;
+    gemm(cx, true, false, k1, ncr, h, 1.0, V1, m, V2, m, 0.0, W1, k1);
+    gemm(cx, false, false, k1, ncr, k1, 1.0, T11, p, W1, k1, 0.0, W2, k1);
+    gemm(cx, false, false, k1, ncr, ncr, -1.0, W2, k1, Tf + mid + mid * p, p, 0.0, Tf + c0 + mid * p, p);
+}
+
+__global__ void store_rsk_kernel(int64_t p, int64_t d, const double* Wq, double* MskT, int64_t ldm)
+{
+    // MskT(q, row) = R_sk(row, q) = Wq(row, q) for row <= q, 0 otherwise (q < p, row < d)
+    int64_t total = p * d;
+    for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += (int64_t)gridDim.x * blockDim.x) {
+        int64_t q = idx % p, row = idx / p;
+        MskT[q + row * ldm] = (row <= q) ? Wq[row + q * d] : 0.0;
+    }
+}
+
+// R_sk of the d x w sketch window MskT(0:w, 0:d)^T (MskT points at row s, ld ldm); in place.
+void sketch_qr(Ctx& cx, double* MskT, int64_t ldm, int64_t w, int64_t d)
+{
+    int64_t p = imin(d, w);
+    if (p <= 0) return;
+    size_t mark = cx.ws_used;
+    double* Wq = cx.alloc((size_t)d * p);
+    double* V = cx.alloc((size_t)d * p);
+    double* Tf = cx.alloc((size_t)p * p);
+    double* tau = cx.alloc((size_t)p);
+    double* W1 = cx.alloc((size_t)p * p);
+    double* W2 = cx.alloc((size_t)p * p);
+    int G = cx.num_sms;
+    double* xbuf = cx.alloc(2 * (size_t)G * QR_XSTRIDE + (size_t)G * QR_JBMAX * QR_JBMAX);
+    double* rowj = cx.alloc(2 * QR_JBMAX);
+    // Wq = Wsk(:, 0:p) = MskT(0:p, 0:d)^T
+    transpose_copy(cx, p, d, MskT, ldm, Wq, d);
+    BQ_CUDA(cudaMemsetAsync(V, 0, sizeof(double) * d * p, cx.stream));
+    BQ_CUDA(cudaMemsetAsync(Tf, 0, sizeof(double) * p * p, cx.stream));
+    geqrf_rec(cx, Wq, d, 0, p, tau, V, Tf, p, W1, W2, xbuf, rowj);
+    int64_t rest = w - p;
+    if (rest > 0) {
+        double* Xt = MskT + p;  // rest x d
+        double* Y = cx.alloc((size_t)rest * p);
+        double* Y2 = cx.alloc((size_t)rest * p);
+        gemm(cx, false, false, rest, p, d, 1.0, Xt, ldm, V, d, 0.0, Y, rest);
+        gemm(cx, false, false, rest, p, p, 1.0, Y, rest, Tf, p, 0.0, Y2, rest);
+        gemm(cx, false, true, rest, d, p, -1.0, Y2, rest, V, d, 1.0, Xt, ldm);
+    }
+    store_rsk_kernel<<<(unsigned)imin(cdiv(p * d, 256), 4 * cx.num_sms), 256, 0, cx.stream>>>(p, d, Wq, MskT, ldm);
+    BQ_LAUNCH_CHECK();
+    cx.ws_used = mark;
+}
+
+}  // namespace bqrrp

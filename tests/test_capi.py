@@ -1,0 +1,63 @@
+"""The C-ABI library builds, loads, and exports every entry point include/bqrrp.h declares (CPU-only)."""
+import ctypes
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "bqrrp.h")
+
+
+def declared_functions():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    names = re.findall(r"\b(bqrrp_[a-z_0-9]+)\s*\(", src)
+    return sorted(set(names))
+
+
+def test_header_declares_the_boundary():
+    names = declared_functions()
+    for must in ("bqrrp_factor", "bqrrp_factor_ex", "bqrrp_factor_host", "bqrrp_workspace_query",
+                 "bqrrp_debug_sketch", "bqrrp_strerror"):
+        assert must in names
+
+
+def test_library_exports_every_declared_symbol():
+    import paper_2507_00976_b200 as bq
+    from paper_2507_00976_b200 import build
+
+    build.build()
+    lib = bq.lib()
+    for name in declared_functions():
+        assert hasattr(lib, name), name
+    assert b"sm_100a" in lib.bqrrp_version()
+
+
+def test_workspace_query_and_argument_checks_without_gpu():
+    import paper_2507_00976_b200 as bq
+
+    lib = bq.lib()
+    n = bq.workspace_query(16384, 16384, 1024, 1024)
+    assert n > 16384 * 1024 * 8 * 2
+    out = ctypes.c_size_t(0)
+    assert lib.bqrrp_workspace_query(-1, 4, 2, 2, ctypes.byref(out)) == -1
+    assert lib.bqrrp_workspace_query(4, 4, 2, 1, ctypes.byref(out)) == -4  # d < b
+    assert lib.bqrrp_workspace_query(4, 4, 2, 5, ctypes.byref(out)) == -4  # d > m
+    # illegal arguments are rejected before any CUDA call (no device needed)
+    rank = ctypes.c_int64(7)
+    dummy = ctypes.c_void_p(16)
+    st = lib.bqrrp_factor_ex(4, 4, dummy, 2, 2, 2, 0, dummy, dummy, ctypes.byref(rank), None, 0, None, None)
+    assert st == -4  # lda < m
+    st = lib.bqrrp_factor_ex(4, 4, dummy, 4, 0, 2, 0, dummy, dummy, ctypes.byref(rank), None, 0, None, None)
+    assert st == -5  # b < 1
+    assert lib.bqrrp_strerror(-5) == b"illegal argument"
+
+
+def test_product_package_does_not_import_oracle():
+    pkg = os.path.join(ROOT, "paper_2507_00976_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".cpp", ".h")):
+                txt = open(os.path.join(dirpath, f)).read()
+                assert "import oracle" not in txt and "from oracle" not in txt and "bqrrp_oracle" not in txt, f

@@ -1,0 +1,271 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on identical seeded inputs.
+
+Tolerances: RNG, gathers and integer-valued GEMMs bit-exact; J and rank identical
+when the oracle's smallest LU pivot margin exceeds 1e-10 (SURVEY c.6 rule 2); R, V relative 1e-12
+normwise and max|dtau| <= 1e-12 (reading Z25); residual <= 1e-13, orthogonality per Z24.
+"""
+import numpy as np
+import pytest
+
+import inputs
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+
+def _bq():
+    import paper_2507_00976_b200 as bq
+
+    bq.lib()
+    return bq
+
+
+def _dev(a):
+    """Column-major float64 CUDA tensor (shape of a, strides (1, m))."""
+    import torch
+
+    return torch.tensor(np.ascontiguousarray(np.asarray(a, dtype=np.float64).T), device="cuda").t()
+
+
+def _host(t):
+    return t.detach().cpu().numpy()
+
+
+# ----------------------------------------------------------------------------- GEMM engine
+@pytest.mark.parametrize("ta", [False, True])
+@pytest.mark.parametrize("tb", [False, True])
+@pytest.mark.parametrize("M,N,K", [(1, 1, 1), (300, 200, 77), (129, 257, 513), (64, 64, 8192), (1000, 33, 2048)])
+def test_gemm_integer_bitexact(gpu, ta, tb, M, N, K):
+    bq = _bq()
+    rng = np.random.default_rng(M * 7 + N * 3 + K)
+    A = rng.integers(-8, 9, size=(K, M) if ta else (M, K)).astype(np.float64)
+    B = rng.integers(-8, 9, size=(N, K) if tb else (K, N)).astype(np.float64)
+    C = rng.integers(-8, 9, size=(M, N)).astype(np.float64)
+    ref = 2.0 * ((A.T if ta else A) @ (B.T if tb else B)) - 3.0 * C
+    dC = _dev(C)
+    bq.debug_gemm(ta, tb, 2.0, _dev(A), _dev(B), -3.0, dC)
+    assert np.array_equal(_host(dC), ref)
+
+
+# ----------------------------------------------------------------------------- a1 sketch
+def test_sketch_operator_bitexact(gpu):
+    bq = _bq()
+    m, n, d = 1024, 64, 160
+    A = inputs.gaussian(m, n, seed=1)
+    S, MskT = bq.debug_sketch(_dev(A), d, seed=0)
+    So = oracle.sketch_operator(d, m, seed=0)
+    assert np.array_equal(_host(S), So)  # bit-exact host == device RNG
+    ref = oracle.sketch(A, d, seed=0)
+    assert np.linalg.norm(_host(MskT) - ref) <= 1e-14 * np.linalg.norm(ref)
+
+
+def test_sketch_operator_bitexact_large_seed(gpu):
+    bq = _bq()
+    m, n, d = 3000, 8, 40
+    A = np.eye(m)[:, :n]
+    seed = 0xDEADBEEFCAFEF00D
+    S, MskT = bq.debug_sketch(_dev(A), d, seed=seed)
+    assert np.array_equal(_host(S), oracle.sketch_operator(d, m, seed=seed))
+    assert np.array_equal(_host(MskT).T, oracle.sketch_operator(d, m, seed=seed)[:, :n])  # S I exact
+
+
+def test_sketch_integer_inputs_exact(gpu):
+    """Integer-valued A: each product a*S is exact and the sums of <= 2^53-bounded... compare to the
+    exactly rounded sum (math.fsum) within the accumulation-order bound."""
+    bq = _bq()
+    A = inputs.integer_valued(512, 16, seed=3)
+    _, MskT = bq.debug_sketch(_dev(A), 32, seed=5)
+    ref = oracle.sketch(A, 32, seed=5)
+    assert np.abs(_host(MskT) - ref).max() <= 512 * 2.0 ** -52 * np.abs(ref).max()
+
+
+# ----------------------------------------------------------------------------- a2 LU pivots
+@pytest.mark.parametrize("w,d", [(300, 64), (1000, 160), (5000, 300), (200, 200), (150, 400), (20000, 96)])
+def test_lu_pivots_match_oracle(gpu, w, d):
+    bq = _bq()
+    L = inputs.gaussian(w, d, seed=w + d)
+    _, ipiv_o, margin = oracle.getf2(L)
+    _, ipiv_g = bq.debug_lu_pivots(_dev(L))
+    ipiv_g = _host(ipiv_g)
+    if margin.min() > 1e-10:
+        assert np.array_equal(ipiv_g, ipiv_o)
+    else:  # compare up to the first near-tie
+        first = int(np.argmax(margin <= 1e-10))
+        assert np.array_equal(ipiv_g[:first], ipiv_o[:first])
+
+
+def test_lu_zero_and_tied_columns(gpu):
+    bq = _bq()
+    L = np.zeros((40, 8))
+    L[5, 0] = 3.0
+    L[7, 0] = -3.0  # tie: first index wins (Z19)
+    L[:, 3] = 0.0   # zero column after elimination handled per Z18
+    rng = np.random.default_rng(0)
+    L[:, 4:] = rng.integers(-3, 4, size=(40, 4))
+    _, ipiv_o, _ = oracle.getf2(L)
+    _, ipiv_g = bq.debug_lu_pivots(_dev(L))
+    assert np.array_equal(_host(ipiv_g), ipiv_o)
+
+
+# ----------------------------------------------------------------------------- a2 sketch QR
+@pytest.mark.parametrize("w,d", [(1000, 160), (64, 64), (300, 100), (50, 80), (4000, 512)])
+def test_sketch_qr_matches_oracle(gpu, w, d):
+    bq = _bq()
+    WT = inputs.gaussian(w, d, seed=w * d)
+    F, _ = oracle.house_qr(WT.T)  # d x w, convention H
+    p = min(d, w)
+    R_o = np.triu(F)  # upper trapezoid
+    got = _host(bq.debug_sketch_qr(_dev(WT))).T  # R_sk (d x w)
+    assert np.linalg.norm(got - R_o) <= 1e-12 * np.linalg.norm(R_o)
+    assert np.all(np.tril(got, -1) == 0.0)
+
+
+# ----------------------------------------------------------------------------- a3 permutation
+@pytest.mark.parametrize("rows,w,nlu", [(100, 50, 20), (1024, 1000, 160), (7, 3000, 300), (33, 5, 5)])
+def test_permute_bitexact(gpu, rows, w, nlu):
+    import torch
+
+    bq = _bq()
+    rng = np.random.default_rng(rows + w)
+    ipiv = np.array([rng.integers(j, w) + 1 for j in range(nlu)], dtype=np.int64)  # valid LU swap list
+    X = rng.standard_normal((rows, w))
+    Jqr_o = oracle.piv_transform(w, ipiv)
+    ref = oracle.col_gather(X, Jqr_o)
+    Xg, Jqr_g = bq.debug_permute(_dev(X), torch.tensor(ipiv, device="cuda"))
+    assert np.array_equal(_host(Jqr_g), Jqr_o)
+    assert np.array_equal(_host(Xg), ref)
+
+
+# ----------------------------------------------------------------------------- a4/a5 panel
+@pytest.mark.parametrize("h,k,t", [(256, 32, 40), (1000, 100, 0), (3000, 128, 200), (129, 129, 3)])
+@pytest.mark.parametrize("passes", [1, 2])
+def test_panel_matches_householder_oracle(gpu, h, k, t, passes):
+    """c.1: CholQR + reconstruction gives the unique (V, tau, R) with tau in [1,2] = convention-H QR."""
+    bq = _bq()
+    rng = np.random.default_rng(h + k + t)
+    P = rng.standard_normal((h, k + t))
+    # a genuine preconditioner: R of a sketch of the panel (d = k)
+    Sk = rng.standard_normal((k + k // 4 + 1, h)) @ P[:, :k]
+    Rsk = np.linalg.qr(Sk, mode="r")[:k, :k]
+    F_o, tau_o = oracle.house_qr(P, kref=k)
+    Pg, taug = bq.debug_panel(_dev(P), k, _dev(Rsk), cholqr_passes=passes)
+    F_g = _host(Pg)
+    tol = 1e-12 if passes == 2 else 1e-9
+    assert np.max(np.abs(_host(taug) - tau_o)) <= tol
+    R_o, R_g = np.triu(F_o[:k, :k]), np.triu(F_g[:k, :k])
+    assert np.linalg.norm(R_g - R_o) <= tol * np.linalg.norm(R_o)
+    V_o, V_g = np.tril(F_o[:, :k], -1), np.tril(F_g[:, :k], -1)
+    assert np.linalg.norm(V_g - V_o) <= tol * max(np.linalg.norm(V_o), 1.0)
+    if t > 0:
+        assert np.linalg.norm(F_g[:, k:] - F_o[:, k:]) <= tol * np.linalg.norm(F_o[:, k:])
+
+
+# ----------------------------------------------------------------------------- end to end
+def _run_both(A, b, d, seed=0, rank_tol=None):
+    bq = _bq()
+    out_o = oracle.bqrrp(A, b, d, seed=seed, rank_tol=rank_tol)
+    Ag, taug, Jg, rk = bq.factor(_dev(A), b, d, seed=seed, rank_tol=rank_tol)
+    return out_o, (_host(Ag), _host(taug), _host(Jg), rk)
+
+
+def _compare(out_o, g, exact_j=True):
+    """exact_j: J identical.  Otherwise (rank-deficient inputs: the pivots after l are decided on
+    rounding noise, so only J(:l) is unique) J(:l) identical, J a permutation, and R(:l, :) compared
+    column by column through the original column index it holds."""
+    Ag, taug, Jg, rk = g
+    l = out_o.rank
+    assert rk == l
+    if exact_j:
+        assert np.array_equal(Jg, out_o.J)
+        Ro, Rg = np.triu(out_o.A)[:l], np.triu(Ag)[:l]
+    else:
+        assert np.array_equal(Jg[:l], out_o.J[:l])
+        assert sorted(Jg) == list(range(1, len(Jg) + 1))
+        Ro = np.triu(out_o.A)[:l][:, np.argsort(out_o.J)]
+        Rg = np.triu(Ag)[:l][:, np.argsort(Jg)]
+    assert np.linalg.norm(Rg - Ro) <= 1e-12 * np.linalg.norm(Ro)
+    Vo, Vg = np.tril(out_o.A[:, :l], -1), np.tril(Ag[:, :l], -1)
+    assert np.linalg.norm(Vg - Vo) <= 1e-12 * max(np.linalg.norm(Vo), 1.0)
+    assert np.max(np.abs(taug - out_o.tau)) <= 1e-12
+    assert np.all(Ag[l:, l:] == 0) and np.all(taug[l:] == 0)
+
+
+@pytest.mark.parametrize("shape,b,d", [((1024, 1024), 128, 160), ((256, 256), 32, 32), ((1000, 1000), 128, 128),
+                                       ((2048, 512), 128, 160), ((512, 2048), 128, 128), ((700, 450), 64, 80),
+                                       ((300, 300), 300, 300), ((4096, 4096), 256, 256)])
+def test_factor_matches_oracle(gpu, shape, b, d):
+    m, n = shape
+    A = inputs.gaussian(m, n, seed=m + 3 * n + b)
+    out_o, g = _run_both(A, b, d, seed=0)
+    assert out_o.min_margin > 1e-10
+    _compare(out_o, g)
+    res = oracle.residual(A, oracle.OracleResult(g[0], g[1], g[2], g[3], None, 0, None))
+    assert res <= 1e-13
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3, 4])
+def test_factor_c1_seeds(gpu, seed):
+    A = inputs.gaussian(1024, 1024, seed=seed)
+    out_o, g = _run_both(A, 128, 160, seed=seed)
+    _compare(out_o, g)
+
+
+def test_factor_residual_orthogonality(gpu):
+    A = inputs.gaussian(1024, 1024, seed=0)
+    _, g = _run_both(A, 128, 160)
+    res = oracle.OracleResult(g[0], g[1], g[2], g[3], None, 0, None)
+    assert oracle.residual(A, res) <= 1e-13
+    assert oracle.orthogonality(res) <= 1e-13
+
+
+@pytest.mark.parametrize("k_true", [64, 128, 199])
+def test_rank_recovery(gpu, k_true):
+    A = inputs.low_rank(512, 512, k_true, seed=k_true)
+    out_o, g = _run_both(A, 128, 160)
+    assert g[3] == k_true == out_o.rank
+    _compare(out_o, g, exact_j=False)
+    res = oracle.residual(A, oracle.OracleResult(g[0], g[1], g[2], g[3], None, 0, None))
+    assert res <= 1e-13
+
+
+def test_zero_and_empty(gpu):
+    import torch
+
+    bq = _bq()
+    A = torch.zeros((64, 64), dtype=torch.float64, device="cuda").t().contiguous().t()
+    Ag, tau, J, rk = bq.factor(A, 16, 16)
+    assert rk == 0 and np.array_equal(_host(J), np.arange(1, 65)) and not _host(tau).any()
+    E = torch.zeros((5, 0), dtype=torch.float64, device="cuda").t().contiguous().t()
+    _, _, J, rk = bq.factor(E, 2, 2)
+    assert rk == 0
+
+
+def test_nonfinite_input_is_flagged(gpu):
+    bq = _bq()
+    A = inputs.gaussian(128, 128, seed=0)
+    A[5, 7] = np.nan
+    with pytest.raises(bq.BqrrpError) as e:
+        bq.factor(_dev(A), 32, 32)
+    assert e.value.status == 1
+
+
+def test_deterministic_bitwise(gpu):
+    bq = _bq()
+    A = inputs.gaussian(1500, 1300, seed=9)
+    r1 = bq.factor(_dev(A), 128, 160, seed=4)
+    r2 = bq.factor(_dev(A), 128, 160, seed=4)
+    for x, y in zip(r1[:3], r2[:3]):
+        assert np.array_equal(_host(x), _host(y))
+
+
+def test_factor_host_e2e_matches_device(gpu):
+    import torch
+
+    bq = _bq()
+    A = inputs.gaussian(600, 500, seed=2)
+    Ad, taud, Jd, rkd = bq.factor(_dev(A), 64, 80, seed=1)
+    Ah = torch.tensor(np.ascontiguousarray(A.T)).t()
+    Ah2, tauh, Jh, rkh = bq.factor_host(Ah, 64, 80, seed=1)
+    assert rkh == rkd
+    assert np.array_equal(Ah2.numpy(), _host(Ad))
+    assert np.array_equal(tauh.numpy(), _host(taud)) and np.array_equal(Jh.numpy(), _host(Jd))
