@@ -1,0 +1,320 @@
+#!/usr/bin/env python
+"""bench.py — effective FP64 TFLOP/s of BQRRP (GEQRF flop count 2mn^2 - 2n^3/3) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl ours|reference]
+
+One step = one full BQRRP factorization (all hot-path rows a1-a7: sketch, LU/QR pivot selection,
+touched-set permutation, CholQR2 panel + reconstruction, WY trailing update, sketch update) of the
+config's synthetic matrix, inputs resident in HBM.  A is restored from a pristine device copy before
+every step OUTSIDE the timed events (the factorization is in place); each step is timed with CUDA events
+on the library's stream; the K step times are summed.  Inputs (2.1 GB at C2) are larger than L2.
+
+N > 1 (torchrun): each rank factors its own independent matrix (replicas, "scaling": "weak"); the
+distributed block-column factorization is the NEXT row of SURVEY §8(e).  value = total flops of all
+ranks / max-over-ranks time.
+
+--impl reference: the reference arm of this tier is the plain CPU oracle (oracle/), timed on the host
+cores, each step a bounded sample of the workload (rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "fp64 BQRRP effective TFLOP/s (GEQRF flops) at 1/2/4/8 B200, % FP64 TC peak"
+
+# BASELINE.json configs; the bench line is C2 (configs[1]) by default.
+CONFIGS = {
+    "C1": dict(m=1024, n=1024, b=128, d=160, desc="1024x1024 fp64 Gaussian, b=128, d=1.25b=160, seed 0"),
+    "C2": dict(m=16384, n=16384, b=1024, d=1024, desc="16384x16384 fp64 Gaussian, b=1024, d=b, seed 0"),
+    "C3": dict(m=65536, n=65536, b=2048, d=2048, desc="65536x65536 fp64 Gaussian, b=2048, d=b, seed 0"),
+    "C4": dict(m=262144, n=8192, b=512, d=512, desc="262144x8192 tall fp64 Gaussian, b=512, d=b, seed 0"),
+}
+# CPU-oracle sample per config (a bounded piece of the same workload: same generator, same b and d)
+ORACLE_SAMPLE = {"C1": (1024, 1024), "C2": (4096, 4096), "C3": (4096, 4096), "C4": (16384, 1024)}
+
+PEAKS_FILE = os.path.join(ROOT, "profiles", "fp64_peak_r01.json")
+NCU_SUMMARY = os.path.join(ROOT, "profiles", "ncu_summary_r01.json")
+
+
+def canonical_flops(m: int, n: int) -> float:
+    """BASELINE.json's GEQRF count 2 m n^2 - 2 n^3 / 3 (m >= n; mirrored for wide)."""
+    if m < n:
+        m, n = n, m
+    return 2.0 * m * n * n - 2.0 * n ** 3 / 3.0
+
+
+def trailing_update_flops(m: int, n: int, b: int) -> float:
+    """Algorithmic flops of the a5 compact-WY update over a full-rank run: per iteration
+    GEMM1 2hkt + TRMM-as-GEMM 2k^2 t + GEMM2 2hkt (h = m-s, k = b, t = n-s-k)."""
+    tot = 0.0
+    s = 0
+    mn = min(m, n)
+    while s < mn:
+        k = min(b, mn - s)
+        h, t = m - s, n - s - k
+        if t > 0:
+            tot += 4.0 * h * k * t + 2.0 * k * k * t
+        s += b
+    return tot
+
+
+def peak_fp64() -> tuple[float, str]:
+    try:
+        d = json.load(open(PEAKS_FILE))
+        return float(d["dmma_tflops"]), "measured DMMA.8x8x4 issue rate, profiles/fp64_peak_r01.json"
+    except Exception:
+        return 37.2, "spec 148 SM x 128 flop/clk x 1.965 GHz (no measurement file)"
+
+
+# ------------------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region (B200_PROFILING.md clocks line)."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+               0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index),
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.out = ""
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        for line in (self.out or "").splitlines():
+            p = [x.strip() for x in line.split(",")]
+            if len(p) < 3:
+                continue
+            try:
+                sm.append(float(p[0]))
+                mx = max(mx, float(p[1]))
+                bits = int(p[2], 16)
+            except ValueError:
+                continue
+            for bit, name in self.REASONS.items():
+                if bits & bit and name != "gpu_idle":
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------------------------- oracle timing
+def oracle_sample(cfg_name: str, seed: int = 0):
+    """Time the CPU oracle as it stands on a bounded sample of the workload; returns (TFLOP/s, seconds, desc)."""
+    import inputs
+    import oracle
+
+    cfg = CONFIGS[cfg_name]
+    sm, sn = ORACLE_SAMPLE[cfg_name]
+    b, d = min(cfg["b"], sm, sn), min(cfg["d"], sm)
+    A = inputs.gaussian(sm, sn, seed=seed)
+    t0 = time.perf_counter()
+    out = oracle.bqrrp(A, b, d, seed=seed)
+    dt = time.perf_counter() - t0
+    desc = (f"oracle_bqrrp (plain C, OpenMP over independent columns) on a {sm}x{sn} Gaussian sample "
+            f"of the {cfg_name} workload (same generator, b={b}, d={d}); rank {out.rank}; "
+            f"canonical GEQRF flops / wall time")
+    return canonical_flops(sm, sn) / dt / 1e12, dt, desc
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    cores = os.cpu_count()
+    times = []
+    desc = ""
+    for it in range(args.warmup + args.steps):
+        v, dt, desc = oracle_sample(args.config)
+        if it >= args.warmup:
+            times.append((v, dt))
+    tot_t = sum(t for _, t in times)
+    sm, sn = ORACLE_SAMPLE[args.config]
+    value = canonical_flops(sm, sn) * len(times) / tot_t / 1e12
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / max(len(times), 1),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": args.config + " " + CONFIGS[args.config]["desc"], "sample": f"{sm}x{sn}"},
+        "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": cores, "kind": "oracle", "sample": desc},
+        "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+# ------------------------------------------------------------------------------------- our arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C2", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+
+    import inputs
+    import paper_2507_00976_b200 as bq
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream()
+
+    cfg = CONFIGS[args.config]
+    m, n, b, d = cfg["m"], cfg["n"], cfg["b"], cfg["d"]
+    A0 = inputs.gaussian_cuda(m, n, seed=args.seed + rank, device=dev)  # column-major view
+    A = torch.empty_like(A0.t()).t()
+    ws = torch.empty(bq.workspace_query(m, n, b, d), dtype=torch.uint8, device=dev)
+    tau = torch.empty(min(m, n), dtype=torch.float64, device=dev)
+    J = torch.empty(n, dtype=torch.int64, device=dev)
+
+    def step(phase=False):
+        return bq.factor(A, b, d, seed=args.seed, workspace=ws, tau=tau, J=J, phase_times=phase)
+
+    for _ in range(args.warmup):
+        A.copy_(A0)
+        step()
+    torch.cuda.synchronize()
+
+    # ---- timed region: K steps, per-step CUDA events (restore outside the events)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    phases_acc = {}
+    launches0 = bq.launch_count()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            A.copy_(A0)
+            ev[i][0].record(stream)
+            out = step(phase=True)
+            ev[i][1].record(stream)
+            for k_, v_ in out[4].items():
+                phases_acc[k_] = phases_acc.get(k_, 0.0) + v_
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches = bq.launch_count() - launches0
+    ranks_found = out[3]
+    t_ms = sum(s.elapsed_time(e) for s, e in ev)
+    t_max = torch.tensor([t_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
+    t_ms = float(t_max.item())
+    flops_step = canonical_flops(m, n)
+    value = flops_step * args.steps * world / (t_ms * 1e-3) / 1e12
+    peak, peak_src = peak_fp64()
+
+    # ---- roofline of the dominant kernel: the a5 trailing-update DMMA GEMMs (phase apply_trans_q)
+    tr_flops = trailing_update_flops(m, n, b)
+    apply_ms = phases_acc.get("apply_trans_q", 0.0) / args.steps
+    achieved = tr_flops / (apply_ms * 1e-3) / 1e12 if apply_ms > 0 else None
+    traffic = None
+    try:
+        traffic = json.load(open(NCU_SUMMARY)).get("dgemm_trailing_dram_bytes_per_launch")
+    except Exception:
+        pass
+    roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                "kernel": "a5 compact-WY trailing update (dgemm_kernel: W=V^T C, W=T^T W, C-=V W) per factorization",
+                "algorithmic_flops_per_step": tr_flops, "kernel_ms_per_step": apply_ms,
+                "peak_source": peak_src, "share_of_step": apply_ms / (t_ms / args.steps)}
+
+    # ---- end to end through the C ABI with host buffers (H2D + factor + D2H inside the timed region)
+    e2e = None
+    if not args.no_e2e:
+        A_host0 = torch.empty((n, m), dtype=torch.float64).pin_memory()
+        A_host0.copy_(A0.t())
+        A_host0 = A_host0.t()  # m x n column-major (pinned)
+        A_host = torch.empty((n, m), dtype=torch.float64).pin_memory().t()
+        tau_h = torch.empty(min(m, n), dtype=torch.float64).pin_memory()
+        J_h = torch.empty(n, dtype=torch.int64).pin_memory()
+        ks = max(1, min(args.steps, 3))
+        tot = 0.0
+        for i in range(ks + 1):
+            A_host.copy_(A_host0)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            bq.factor_host(A_host, b, d, seed=args.seed, tau_host=tau_h, J_host=J_h)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            if i > 0:
+                tot += e0.elapsed_time(e1)
+        te = torch.tensor([tot / ks], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": flops_step * world / (float(te.item()) * 1e-3) / 1e12, "unit": "TFLOP/s",
+               "h2d_bytes_per_step": m * n * 8, "d2h_bytes_per_step": m * n * 8 + min(m, n) * 8 + n * 8,
+               "ms_per_step": float(te.item()), "api": "bqrrp_factor_host (pinned host buffers)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, dt, desc = oracle_sample(args.config)
+        cpu = {"value": v, "unit": "TFLOP/s", "cores": os.cpu_count(), "kind": "oracle", "sample": desc,
+               "seconds": dt}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{args.config} {cfg['desc']}", "m": m, "n": n, "b": b, "d": d,
+                       "parallelism": "replicas" if world > 1 else "single",
+                       "l2": "inputs larger than L2 (A = %.2f GB)" % (m * n * 8 / 1e9),
+                       "timing": "per-step CUDA events around bqrrp_factor; A restored from a pristine copy outside the events",
+                       "rank_found": ranks_found},
+            "pct_fp64_peak": 100.0 * (value / world) / peak,
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "clocks": clk.summary(), "phase_ms_per_step": {k_: v_ / args.steps for k_, v_ in phases_acc.items()},
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -110,6 +110,9 @@ int bqrrp_debug_permute(int64_t rows, int64_t w, double* X, int64_t ldx, int64_t
 int bqrrp_debug_panel(int64_t h, int64_t k, int64_t t, double* P, int64_t ld, const double* Rsk11, double* tau,
                       int cholqr_passes, void* stream);
 
+/* Number of CUDA kernels this library has launched in the calling process (all threads). */
+unsigned long long bqrrp_launch_count(void);
+
 const char* bqrrp_strerror(int status);
 const char* bqrrp_last_error(void);
 /* Library version string. */

@@ -315,6 +315,7 @@ void oracle_house_qr(int64_t p, int64_t q, double *M, int64_t ld, int64_t kref, 
 {
     for (int64_t j = 0; j < kref; ++j) {
         tau[j] = oracle_house_vec(p - j, M + IDX(j, j, ld));
+#pragma omp parallel for schedule(static) if ((p - j) * (kref - j) > 65536)
         for (int64_t c = j + 1; c < kref; ++c) apply_reflector(p - j, M + IDX(j, j, ld), tau[j], M + IDX(j, c, ld));
     }
 #pragma omp parallel for schedule(dynamic, 4)

@@ -57,8 +57,14 @@ def lib() -> ctypes.CDLL:
         L.bqrrp_strerror.argtypes = [i32]
         L.bqrrp_last_error.restype = ctypes.c_char_p
         L.bqrrp_version.restype = ctypes.c_char_p
+        L.bqrrp_launch_count.restype = ctypes.c_ulonglong
         _lib = L
     return _lib
+
+
+def launch_count() -> int:
+    """Kernels launched by libbqrrp.so in this process so far."""
+    return int(lib().bqrrp_launch_count())
 
 
 def default_rank_tol(m: int, n: int) -> float:

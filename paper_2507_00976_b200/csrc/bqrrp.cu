@@ -22,6 +22,7 @@
 namespace bqrrp {
 
 static thread_local std::string g_last_error;
+unsigned long long g_launches = 0;
 
 // ----------------------------------------------------------------------------------- small kernels
 __global__ void init_j_kernel(int64_t n, int64_t* J)
@@ -446,7 +447,10 @@ int bqrrp_debug_lu_pivots(int64_t w, int64_t d, double* L, int64_t ld, int64_t* 
         int* ip = cx.alloc_as<int>((size_t)imax(1, d));
         getrf_pivots(cx, L, ld, w, d, ip);
         int64_t nlu = imin(w, d);
-        if (nlu > 0) ipiv_to_i64_kernel<<<(unsigned)cdiv(nlu, 128), 128, 0, cx.stream>>>(nlu, ip, ipiv);
+        if (nlu > 0) {
+            ipiv_to_i64_kernel<<<(unsigned)cdiv(nlu, 128), 128, 0, cx.stream>>>(nlu, ip, ipiv);
+            BQ_LAUNCH_CHECK();
+        }
         cudaFreeAsync(ws, cx.stream);
         BQ_CUDA(cudaStreamSynchronize(cx.stream));
         return 0;
@@ -504,13 +508,18 @@ int bqrrp_debug_permute(int64_t rows, int64_t w, double* X, int64_t ldx, int64_t
         T.nt = cx.alloc_as<int>(2);
         int* ip = cx.alloc_as<int>((size_t)imax(1, nlu));
         double* scr = cx.alloc((size_t)2 * imax(1, nlu) * imax(1, rows));
-        if (nlu > 0) ipiv_to_int_kernel<<<(unsigned)cdiv(nlu, 128), 128, 0, cx.stream>>>(nlu, ipiv, ip);
+        if (nlu > 0) {
+            ipiv_to_int_kernel<<<(unsigned)cdiv(nlu, 128), 128, 0, cx.stream>>>(nlu, ipiv, ip);
+            BQ_LAUNCH_CHECK();
+        }
         touched_set(cx, nlu, ip, T);
         permute_columns(cx, rows, X, ldx, T, scr);
         if (Jqr_out && w > 0) {
             jqr_from_touched_kernel<<<(unsigned)imin(cdiv(w, 256), 1024), 256, 0, cx.stream>>>(w, T.tq, T.tsrc, T.nt,
                                                                                                Jqr_out);
+            BQ_LAUNCH_CHECK();
             jqr_apply_touched_kernel<<<16, 256, 0, cx.stream>>>(T.tq, T.tsrc, T.nt, Jqr_out);
+            BQ_LAUNCH_CHECK();
         }
         cudaFreeAsync(ws, cx.stream);
         BQ_CUDA(cudaStreamSynchronize(cx.stream));
@@ -557,6 +566,8 @@ const char* bqrrp_strerror(int status)
 }
 
 const char* bqrrp_last_error(void) { return g_last_error.c_str(); }
+
+unsigned long long bqrrp_launch_count(void) { return g_launches; }
 
 const char* bqrrp_version(void) { return "bqrrp-b200 0.1 (sm_100a, DMMA f64)"; }
 

@@ -23,7 +23,14 @@ struct CudaError : std::runtime_error {
                                      ": " + cudaGetErrorString(e_));                                    \
     } while (0)
 
-#define BQ_LAUNCH_CHECK() BQ_CUDA(cudaGetLastError())
+// Every kernel launch of the library is followed by BQ_LAUNCH_CHECK (or counted explicitly for
+// cooperative launches): g_launches is the count bqrrp_launch_count() reports.
+extern unsigned long long g_launches;
+#define BQ_LAUNCH_CHECK()                \
+    do {                                 \
+        ++::bqrrp::g_launches;           \
+        BQ_CUDA(cudaGetLastError());     \
+    } while (0)
 
 inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 inline int64_t imin(int64_t a, int64_t b) { return a < b ? a : b; }

@@ -165,6 +165,7 @@ static void lu_panel(Ctx& cx, double* L, int64_t ld, int64_t w, int64_t c0, int 
     LuPanelArgs a{L, ld, w, c0, jb, R, ipiv, xbuf, rowj};
     void* args[] = {&a};
     BQ_CUDA(cudaLaunchCooperativeKernel((void*)lu_panel_kernel, dim3(G), dim3(LU_THREADS), args, smem, cx.stream));
+    ++g_launches;
 }
 
 static int lu_leaf_width(int64_t rows, int num_sms)

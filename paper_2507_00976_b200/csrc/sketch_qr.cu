@@ -202,6 +202,7 @@ static void qr_panel(Ctx& cx, double* A, int64_t ld, int64_t m, int64_t c0, int 
     QrPanelArgs a{A, ld, m, c0, jb, R, tau, V, T, ldt, xbuf, rowj};
     void* args[] = {&a};
     BQ_CUDA(cudaLaunchCooperativeKernel((void*)qr_panel_kernel, dim3(G), dim3(QR_THREADS), args, smem, cx.stream));
+    ++g_launches;
 }
 
 // Recursive QR of columns [c0, c1) of Wq (rows [c0, m)); V (m x p explicit), Tf (p x p).
