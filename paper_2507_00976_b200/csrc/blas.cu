@@ -56,33 +56,110 @@ void gemm(Ctx& cx, bool ta, bool tb, int64_t M, int64_t N, int64_t K, double alp
 // ------------------------------------------------------------------------------------------- TRSM
 constexpr int TRSM_NB = 64;
 
-// Right side: one thread per row r solves x op(T) = b (left-looking, ascending l).
-__global__ void __launch_bounds__(128) trsm_ru_base(int64_t rows, int n, const double* __restrict__ T, int64_t ldt,
-                                                     int t_lower, int unit, double* __restrict__ B, int64_t ldb)
+// Base triangular solve on a 64-wide triangular dimension, tiled over the independent dimension.
+// Element (t, r) of the right-hand side (t: triangular index, r: independent index) lives at
+// B[t * st + r * sr].  coef(l, t) (l < t) is the coupling of unknown l into equation t and diag(t) the
+// pivot:  x_t = (b_t - sum_{l<t} coef(l, t) x_l) / diag(t).
+//   right side, X op(T) = B:  st = ldb, sr = 1,   coef(l, t) = op(T)(l, t), diag = op(T)(t, t)
+//   left side,  L X = B:      st = 1,   sr = ldb, coef(l, t) = L(t, l),     diag = 1 (unit)
+// A CTA owns 64 independent indices; thread (r = tid % 64, g = tid / 64) keeps x_t for t = g mod 4
+// in registers; the solved x_t is broadcast through shared memory (one barrier per t).
+constexpr int TB_R = 64, TB_G = 4, TB_THREADS = TB_R * TB_G;
+
+__global__ void __launch_bounds__(TB_THREADS) trsm_base_kernel(int n, int64_t nr, const double* __restrict__ T,
+                                                                int64_t ldt, int mode, int unit, double* __restrict__ B,
+                                                                int64_t st, int64_t sr)
 {
-    __shared__ double U[TRSM_NB][TRSM_NB + 1];  // U[l][j] = op(T)(l, j)
-    for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) {
-        int l = idx % n, j = idx / n;
-        U[l][j] = (l <= j) ? (t_lower ? T[j + (int64_t)l * ldt] : T[l + (int64_t)j * ldt]) : 0.0;
+    // mode 0: right, T stored upper (op(T) = T); mode 1: right, T stored lower (op(T) = T^T);
+    // mode 2: left, T stored lower (unit)
+    extern __shared__ double dsm[];
+    double(*C)[TRSM_NB + 1] = reinterpret_cast<double(*)[TRSM_NB + 1]>(dsm);                        // C[l][t]
+    double(*Bs)[TB_R + 1] = reinterpret_cast<double(*)[TB_R + 1]>(dsm + TRSM_NB * (TRSM_NB + 1));  // Bs[t][r]
+    double(*xs)[TB_R] = reinterpret_cast<double(*)[TB_R]>(dsm + TRSM_NB * (TRSM_NB + 1) + TRSM_NB * (TB_R + 1));
+    const int tid = threadIdx.x;
+    for (int idx = tid; idx < n * n; idx += TB_THREADS) {
+        int l = idx % n, t = idx / n;
+        double v = 0.0;
+        if (l <= t) {
+            if (mode == 0) v = T[l + (int64_t)t * ldt];
+            else if (mode == 1) v = T[t + (int64_t)l * ldt];
+            else v = (l < t) ? T[t + (int64_t)l * ldt] : 1.0;
+        }
+        C[l][t] = v;
+    }
+    const int64_t r0 = (int64_t)blockIdx.x * TB_R;
+    const int nloc = (int)((nr - r0 < TB_R) ? nr - r0 : TB_R);
+    // coalesced load of the n x 64 tile along whichever axis is contiguous
+    if (sr == 1) {
+        for (int idx = tid; idx < n * TB_R; idx += TB_THREADS) {
+            int r = idx % TB_R, t = idx / TB_R;
+            Bs[t][r] = (r < nloc) ? B[t * st + (r0 + r)] : 0.0;
+        }
+    } else {
+        for (int idx = tid; idx < n * TB_R; idx += TB_THREADS) {
+            int t = idx % n, r = idx / n;
+            Bs[t][r] = (r < nloc) ? B[t + (r0 + r) * sr] : 0.0;
+        }
     }
     __syncthreads();
-    int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= rows) return;
-    double x[TRSM_NB];
+    const int r = tid % TB_R, g = tid / TB_R;
+    constexpr int PER = TRSM_NB / TB_G;
+    double x[PER];
 #pragma unroll
-    for (int j = 0; j < TRSM_NB; ++j) x[j] = (j < n) ? B[r + (int64_t)j * ldb] : 0.0;
+    for (int q = 0; q < PER; ++q) {
+        int t = g + q * TB_G;
+        x[q] = (t < n) ? Bs[t][r] : 0.0;
+    }
 #pragma unroll
-    for (int j = 0; j < TRSM_NB; ++j) {
-        if (j < n) {
-            double v = x[j];
+    for (int t = 0; t < TRSM_NB; ++t) {
+        if (t < n) {
+            const int q = t / TB_G;
+            if (g == t % TB_G) {
+                double v = x[q];
+                if (!unit) v = v / C[t][t];
+                x[q] = v;
+                xs[t & 1][r] = v;
+            }
+            __syncthreads();
+            const double xt = xs[t & 1][r];
 #pragma unroll
-            for (int l = 0; l < j; ++l) v = fma(-x[l], U[l][j], v);
-            x[j] = unit ? v : v / U[j][j];
+            for (int qq = q; qq < PER; ++qq) {
+                int tt = g + qq * TB_G;
+                if (tt > t && tt < n) x[qq] = fma(-xt, C[t][tt], x[qq]);
+            }
         }
     }
 #pragma unroll
-    for (int j = 0; j < TRSM_NB; ++j)
-        if (j < n) B[r + (int64_t)j * ldb] = x[j];
+    for (int q = 0; q < PER; ++q) {
+        int t = g + q * TB_G;
+        if (t < n) Bs[t][r] = x[q];
+    }
+    __syncthreads();
+    if (sr == 1) {
+        for (int idx = tid; idx < n * TB_R; idx += TB_THREADS) {
+            int rr = idx % TB_R, t = idx / TB_R;
+            if (rr < nloc) B[t * st + (r0 + rr)] = Bs[t][rr];
+        }
+    } else {
+        for (int idx = tid; idx < n * TB_R; idx += TB_THREADS) {
+            int t = idx % n, rr = idx / n;
+            if (rr < nloc) B[t + (r0 + rr) * sr] = Bs[t][rr];
+        }
+    }
+}
+
+constexpr size_t TB_SMEM = sizeof(double) * (TRSM_NB * (TRSM_NB + 1) + TRSM_NB * (TB_R + 1) + 2 * TB_R);
+
+static void trsm_base(Ctx& cx, int n, int64_t nr, const double* T, int64_t ldt, int mode, int unit, double* B,
+                      int64_t st, int64_t sr)
+{
+    static bool attr = false;
+    if (!attr) {
+        BQ_CUDA(cudaFuncSetAttribute(trsm_base_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TB_SMEM));
+        attr = true;
+    }
+    trsm_base_kernel<<<(unsigned)cdiv(nr, TB_R), TB_THREADS, TB_SMEM, cx.stream>>>(n, nr, T, ldt, mode, unit, B, st, sr);
+    BQ_LAUNCH_CHECK();
 }
 
 void trsm_right_upper(Ctx& cx, int64_t rows, int64_t n, const double* T, int64_t ldt, bool t_lower, bool unit,
@@ -90,8 +167,7 @@ void trsm_right_upper(Ctx& cx, int64_t rows, int64_t n, const double* T, int64_t
 {
     if (rows <= 0 || n <= 0) return;
     if (n <= TRSM_NB) {
-        trsm_ru_base<<<(unsigned)cdiv(rows, 128), 128, 0, cx.stream>>>(rows, (int)n, T, ldt, t_lower, unit, B, ldb);
-        BQ_LAUNCH_CHECK();
+        trsm_base(cx, (int)n, rows, T, ldt, t_lower ? 1 : 0, unit ? 1 : 0, B, ldb, 1);
         return;
     }
     int64_t n1 = cdiv(n / 2, TRSM_NB) * TRSM_NB;
@@ -104,41 +180,11 @@ void trsm_right_upper(Ctx& cx, int64_t rows, int64_t n, const double* T, int64_t
     trsm_right_upper(cx, rows, n2, T + n1 + n1 * ldt, ldt, t_lower, unit, B + n1 * ldb, ldb);
 }
 
-// Left side, unit lower: one thread per column c solves L x = b.
-__global__ void __launch_bounds__(128) trsm_llu_base(int n, int64_t cols, const double* __restrict__ L, int64_t ldl,
-                                                      double* __restrict__ B, int64_t ldb)
-{
-    __shared__ double Ls[TRSM_NB][TRSM_NB + 1];
-    for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) {
-        int i = idx % n, l = idx / n;
-        Ls[i][l] = (l < i) ? L[i + (int64_t)l * ldl] : 0.0;
-    }
-    __syncthreads();
-    int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= cols) return;
-    double x[TRSM_NB];
-#pragma unroll
-    for (int i = 0; i < TRSM_NB; ++i) x[i] = (i < n) ? B[i + c * ldb] : 0.0;
-#pragma unroll
-    for (int i = 0; i < TRSM_NB; ++i) {
-        if (i < n) {
-            double v = x[i];
-#pragma unroll
-            for (int l = 0; l < i; ++l) v = fma(-Ls[i][l], x[l], v);
-            x[i] = v;
-        }
-    }
-#pragma unroll
-    for (int i = 0; i < TRSM_NB; ++i)
-        if (i < n) B[i + c * ldb] = x[i];
-}
-
 void trsm_left_lower_unit(Ctx& cx, int64_t n, int64_t cols, const double* L, int64_t ldl, double* B, int64_t ldb)
 {
     if (n <= 0 || cols <= 0) return;
     if (n <= TRSM_NB) {
-        trsm_llu_base<<<(unsigned)cdiv(cols, 128), 128, 0, cx.stream>>>((int)n, cols, L, ldl, B, ldb);
-        BQ_LAUNCH_CHECK();
+        trsm_base(cx, (int)n, cols, L, ldl, 2, 1, B, 1, ldb);
         return;
     }
     int64_t n1 = cdiv(n / 2, TRSM_NB) * TRSM_NB;

@@ -47,16 +47,23 @@ __global__ void nonfinite_kernel(int64_t rows, int64_t cols, const double* X, in
 __global__ void tri_rank_kernel(const double* MskT_s, int64_t ldm, int64_t kmax, int first, double rank_tol, double* ref,
                                 int* flags)
 {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    if (first) *ref = fabs(MskT_s[0]);
-    double r = *ref;
-    int64_t k = 0;
+    __shared__ int first_fail;
+    if (threadIdx.x == 0) first_fail = (int)kmax;
+    __syncthreads();
+    const double r = first ? fabs(MskT_s[0]) : *ref;
     if (r > 0.0) {
-        double tol = rank_tol * r;
-        while (k < kmax && fabs(MskT_s[k + k * ldm]) > tol) ++k;
+        const double tol = rank_tol * r;
+        for (int64_t j = threadIdx.x; j < kmax; j += blockDim.x)
+            if (!(fabs(MskT_s[j + j * ldm]) > tol)) atomicMin(&first_fail, (int)j);
+    } else if (threadIdx.x == 0) {
+        first_fail = 0;
     }
-    flags[F_K] = (int)k;
-    flags[F_ZERO_COL] = 1;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        if (first) *ref = r;
+        flags[F_K] = first_fail;  // largest prefix with |R_sk(j,j)| > tol
+        flags[F_ZERO_COL] = 1;
+    }
 }
 
 __global__ void zero_col_kernel(int64_t h, const double* col, int* flags)
@@ -103,7 +110,7 @@ static Layout layout(int64_t m, int64_t n, int64_t b, int64_t d)
     P += r((size_t)2 * d * m > (size_t)m * d ? (size_t)2 * d * m : (size_t)m * d);  // column scratch / S^T
     P += r((size_t)2 * d * d);             // row scratch
     P += r((size_t)2 * d) * 3;             // vec tmp (int64), tq, tsrc
-    P += r((size_t)d) + r(8);              // ipiv, nt
+    P += r((size_t)d) + r(8) + r((size_t)n);  // ipiv, nt, perm
     P += r(bb * bb) * 2;                   // Rsk11, X
     P += r(8) * 2;                         // ref, flags
     // temporaries: sketch QR vs panel (never live together)
@@ -130,7 +137,6 @@ static int validate(int64_t m, int64_t n, const void* A, int64_t lda, int64_t b,
     if (!tau && m > 0 && n > 0) return -8;
     if (!J && n > 0) return -9;
     if (!rank) return -10;
-    if (d > 4096) return -6;  // touched-set table bound (perm.cu)
     return 0;
 }
 
@@ -149,6 +155,7 @@ static int64_t factor_impl(Ctx& cx, int64_t m, int64_t n, double* A, int64_t lda
     T.tsrc = cx.alloc_as<int>((size_t)2 * d);
     T.nt = cx.alloc_as<int>(2);
     int* ipiv = cx.alloc_as<int>((size_t)d);
+    int* perm = cx.alloc_as<int>((size_t)n);
     int64_t bb = imin(b, mn);
     double* Rsk11 = cx.alloc((size_t)bb * bb);
     double* X = cx.alloc((size_t)bb * bb);
@@ -173,13 +180,13 @@ static int64_t factor_impl(Ctx& cx, int64_t m, int64_t n, double* A, int64_t lda
         // ---- a2: pivots from LU of the sketch transpose, then R_sk
         cx.mark(PH_QRCP_WIDE);
         copy_matrix(cx, w, d, MskT + s, n, Lb, n);
-        getrf_pivots(cx, Lb, n, w, d, ipiv);
+        getrf_pivots(cx, Lb, n, w, d, ipiv, perm);
         const int64_t nlu = imin(w, d);
-        touched_set(cx, nlu, ipiv, T);
+        touched_from_perm(cx, w, nlu, perm, T);
         permute_rows(cx, d, MskT + s, n, T, rowscr);
         sketch_qr(cx, MskT + s, n, w, d);
         cx.mark(PH_TRI_RANK);
-        tri_rank_kernel<<<1, 32, 0, cx.stream>>>(MskT + s, n, kmax, i == 0, rank_tol, ref, cx.flags);
+        tri_rank_kernel<<<1, 1024, 0, cx.stream>>>(MskT + s, n, kmax, i == 0, rank_tol, ref, cx.flags);
         BQ_LAUNCH_CHECK();
         // ---- a3: column permutation of A (all m rows) and J
         cx.mark(PH_COL_PERM);
@@ -445,7 +452,8 @@ int bqrrp_debug_lu_pivots(int64_t w, int64_t d, double* L, int64_t ld, int64_t* 
         Layout Ly{0, 0, (size_t)16 * imax(1, d * d) * 8 + (4u << 20), 0};
         carve(cx, ws, wsb, Ly);
         int* ip = cx.alloc_as<int>((size_t)imax(1, d));
-        getrf_pivots(cx, L, ld, w, d, ip);
+        int* pm = cx.alloc_as<int>((size_t)imax(1, w));
+        getrf_pivots(cx, L, ld, w, d, ip, pm);
         int64_t nlu = imin(w, d);
         if (nlu > 0) {
             ipiv_to_i64_kernel<<<(unsigned)cdiv(nlu, 128), 128, 0, cx.stream>>>(nlu, ip, ipiv);
@@ -493,11 +501,11 @@ int bqrrp_debug_permute(int64_t rows, int64_t w, double* X, int64_t ldx, int64_t
 {
     if (rows < 0) return -1;
     if (w < 0) return -2;
-    if (nlu < 0 || nlu > w || nlu > 4096) return -5;
+    if (nlu < 0 || nlu > w) return -5;
     return guarded([&]() -> int {
         Ctx cx;
         setup_ctx(cx, stream);
-        size_t wsb = (size_t)(8u << 20) + (size_t)2 * imax(1, nlu) * imax(1, rows) * 8;
+        size_t wsb = (size_t)(8u << 20) + (size_t)2 * imax(1, nlu) * imax(1, rows) * 8 + (size_t)w * 4;
         void* ws = nullptr;
         BQ_CUDA(cudaMallocAsync(&ws, wsb, cx.stream));
         Layout Ly{0, 0, 4096, 0};
@@ -506,13 +514,10 @@ int bqrrp_debug_permute(int64_t rows, int64_t w, double* X, int64_t ldx, int64_t
         T.tq = cx.alloc_as<int>((size_t)2 * imax(1, nlu));
         T.tsrc = cx.alloc_as<int>((size_t)2 * imax(1, nlu));
         T.nt = cx.alloc_as<int>(2);
-        int* ip = cx.alloc_as<int>((size_t)imax(1, nlu));
+        int* pm = cx.alloc_as<int>((size_t)imax(1, w));
         double* scr = cx.alloc((size_t)2 * imax(1, nlu) * imax(1, rows));
-        if (nlu > 0) {
-            ipiv_to_int_kernel<<<(unsigned)cdiv(nlu, 128), 128, 0, cx.stream>>>(nlu, ipiv, ip);
-            BQ_LAUNCH_CHECK();
-        }
-        touched_set(cx, nlu, ip, T);
+        perm_from_ipiv(cx, w, nlu, ipiv, pm);
+        touched_from_perm(cx, w, nlu, pm, T);
         permute_columns(cx, rows, X, ldx, T, scr);
         if (Jqr_out && w > 0) {
             jqr_from_touched_kernel<<<(unsigned)imin(cdiv(w, 256), 1024), 256, 0, cx.stream>>>(w, T.tq, T.tsrc, T.nt,

@@ -18,13 +18,15 @@ void sketch_operator_T(Ctx& cx, int64_t m, int64_t d, uint64_t seed, double* St,
 void sketch_apply(Ctx& cx, int64_t m, int64_t n, const double* A, int64_t lda, int64_t d, uint64_t seed, double* MskT,
                   int64_t ldm, double* St /* m x d scratch */);
 
-// a2: partial-pivot LU of the w x d matrix L (in place), ipiv[j] = 0-based pivot row, j < min(w,d).
-void getrf_pivots(Ctx& cx, double* L, int64_t ld, int64_t w, int64_t d, int* ipiv);
+// a2: partial-pivot LU of the w x d matrix L (in place), ipiv[j] = 0-based pivot row, j < min(w,d);
+// perm (w) = the row permutation of piv_transform (J_qr - 1).
+void getrf_pivots(Ctx& cx, double* L, int64_t ld, int64_t w, int64_t d, int* ipiv, int* perm);
 // a2: R_sk of the sketch window (transposed storage), in place.
 void sketch_qr(Ctx& cx, double* MskT, int64_t ldm, int64_t w, int64_t d);
 
 // a3: touched set and gathers
-void touched_set(Ctx& cx, int64_t nlu, const int* ipiv, Touched& T);
+void touched_from_perm(Ctx& cx, int64_t w, int64_t nlu, const int* perm, Touched& T);
+void perm_from_ipiv(Ctx& cx, int64_t w, int64_t nlu, const int64_t* ipiv1, int* perm);
 void permute_columns(Ctx& cx, int64_t rows, double* X, int64_t ldx, const Touched& T, double* scratch);
 void permute_rows(Ctx& cx, int64_t cols, double* X, int64_t ldx, const Touched& T, double* scratch);
 void permute_vector(Ctx& cx, int64_t* J, const Touched& T, int64_t* tmp);

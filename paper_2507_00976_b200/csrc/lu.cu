@@ -1,13 +1,15 @@
 // lu.cu — K-LU: partial-pivot LU of the tall w x d sketch transpose, for its pivots
 // (Alg. 2 "Practical wide QRCP": GETRF on the transposed sketch).
 //
-// Recursive right-looking LU (pivots only: the left factor's row swaps are never applied to
-// already-factored columns because only J_lu is consumed).  Leaves are jb-column panels
-// factored by one cooperative kernel: the panel rows are split over G CTAs and held in shared
-// memory; each column step is ONE grid-wide barrier: every CTA publishes its local first-max
-// candidate (|value|, row, full panel row) and the current row j, then all CTAs pick the same winner
-// (largest |value|, lowest row index on ties: IDAMAX, reading Z19), swap and apply the rank-1 update
-// to their own rows.  An exactly-zero pivot column is skipped (no swap, no scaling; Z18).
+// Recursive right-looking LU.  Leaves are jb-column panels factored by one cooperative kernel: the
+// panel rows are split over G CTAs and held in shared memory; each column step is ONE grid-wide
+// barrier: every CTA publishes its local first-max candidate (|value|, row, full panel row) and the
+// current row j, then all CTAs pick the same winner (largest |value|, lowest row index on ties:
+// IDAMAX, reading Z19), swap and apply the rank-1 update to their own rows.  An exactly-zero pivot
+// column is skipped (no swap, no scaling; Z18).  Each interchange is applied at once to the whole row
+// of the LU matrix (all d columns, as LAPACK's laswp on both sides would) and to the permutation
+// vector perm (perm = J_qr - 1 of piv_transform), so no separate laswp pass exists and the
+// touched set of the permutation is read straight off perm.
 #include <cooperative_groups.h>
 
 #include "blas.cuh"
@@ -20,18 +22,25 @@ namespace bqrrp {
 struct LuPanelArgs {
     double* L;
     int64_t ld;
-    int64_t w;       // rows of the LU matrix
-    int64_t c0;      // first panel column (= first active row)
-    int jb;          // panel width
-    int R;           // rows per CTA
-    int* ipiv;       // out: ipiv[c0 + j] = pivot row (0-based, absolute)
-    double* xbuf;    // exchange: [2][G][LU_XSTRIDE]
-    double* rowj;    // exchange: [2][LU_JBMAX]
+    int64_t w;   // rows of the LU matrix
+    int64_t d;   // columns of the LU matrix
+    int64_t c0;  // first panel column (= first active row)
+    int jb;      // panel width
+    int R;       // rows per CTA
+    int* ipiv;   // out: ipiv[c0 + j] = pivot row (0-based, absolute)
+    int* perm;   // running row permutation (w)
+    double* xbuf;  // exchange: [2][G][LU_XSTRIDE]
+    double* rowj;  // exchange: [2][LU_JBMAX]
 };
 
 constexpr int LU_JBMAX = 32;
 constexpr int LU_XSTRIDE = 2 + LU_JBMAX;
 constexpr int LU_THREADS = 256;
+
+__device__ __forceinline__ bool better(double v, int64_t i, double bv, int64_t bi)
+{
+    return v > bv || (v == bv && i < bi);
+}
 
 __global__ void __launch_bounds__(LU_THREADS, 1) lu_panel_kernel(LuPanelArgs a)
 {
@@ -39,12 +48,17 @@ __global__ void __launch_bounds__(LU_THREADS, 1) lu_panel_kernel(LuPanelArgs a)
     extern __shared__ double sp[];  // sp[c * R + r]
     __shared__ double red_v[LU_THREADS / 32];
     __shared__ int64_t red_i[LU_THREADS / 32];
+    __shared__ int red_w[LU_THREADS / 32];
     __shared__ double pivrow[LU_JBMAX], oldrow[LU_JBMAX];
     __shared__ int64_t s_piv;
+    __shared__ int s_win;
 
     const int G = gridDim.x, cta = blockIdx.x, tid = threadIdx.x, R = a.R, jb = a.jb;
+    const int lane = tid & 31, warp = tid >> 5;
     const int64_t rbeg = a.c0 + (int64_t)cta * R;  // absolute first row of this CTA
     const int64_t rows_here = (rbeg < a.w) ? ((a.w - rbeg < R) ? a.w - rbeg : R) : 0;
+    const int64_t n_out = a.d - jb;  // columns outside the panel
+    const int64_t gtid = (int64_t)cta * LU_THREADS + tid, gstride = (int64_t)G * LU_THREADS;
 
     for (int idx = tid; idx < R * jb; idx += LU_THREADS) {
         int r = idx % R, c = idx / R;
@@ -62,18 +76,18 @@ __global__ void __launch_bounds__(LU_THREADS, 1) lu_panel_kernel(LuPanelArgs a)
             int64_t ar = rbeg + r;
             if (ar < jr) continue;
             double v = fabs(sp[j * R + r]);
-            if (v > bv) { bv = v; bi = ar; }  // ascending r per thread: first index kept on ties
+            if (v > bv) { bv = v; bi = ar; }  // ascending rows per thread: first index kept on ties
         }
         for (int o = 16; o > 0; o >>= 1) {
             double ov = __shfl_down_sync(0xffffffffu, bv, o);
             int64_t oi = __shfl_down_sync(0xffffffffu, bi, o);
-            if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+            if (better(ov, oi, bv, bi)) { bv = ov; bi = oi; }
         }
-        if ((tid & 31) == 0) { red_v[tid >> 5] = bv; red_i[tid >> 5] = bi; }
+        if (lane == 0) { red_v[warp] = bv; red_i[warp] = bi; }
         __syncthreads();
         if (tid == 0) {
             for (int wv = 1; wv < LU_THREADS / 32; ++wv)
-                if (red_v[wv] > bv || (red_v[wv] == bv && red_i[wv] < bi)) { bv = red_v[wv]; bi = red_i[wv]; }
+                if (better(red_v[wv], red_i[wv], bv, bi)) { bv = red_v[wv]; bi = red_i[wv]; }
             double* slot = a.xbuf + ((int64_t)par * G + cta) * LU_XSTRIDE;
             slot[0] = bv;
             slot[1] = __longlong_as_double((long long)bi);
@@ -82,31 +96,41 @@ __global__ void __launch_bounds__(LU_THREADS, 1) lu_panel_kernel(LuPanelArgs a)
         __syncthreads();
         if (tid < jb) {
             double* slot = a.xbuf + ((int64_t)par * G + cta) * LU_XSTRIDE;
-            int64_t li = s_piv - rbeg;
-            slot[2 + tid] = (s_piv != INT64_MAX) ? sp[tid * R + li] : 0.0;
+            slot[2 + tid] = (s_piv != INT64_MAX) ? sp[tid * R + (s_piv - rbeg)] : 0.0;
             if (jr >= rbeg && jr < rbeg + rows_here) a.rowj[par * LU_JBMAX + tid] = sp[tid * R + (jr - rbeg)];
         }
-        __threadfence();
         grid.sync();
-        // every CTA picks the same winner
-        if (tid == 0) {
-            double gv = -1.0;
-            int64_t gi = INT64_MAX;
-            int gw = 0;
-            for (int q = 0; q < G; ++q) {
+        // every CTA picks the same winner: parallel first-max over the G candidates
+        {
+            double v = -1.0;
+            int64_t i = INT64_MAX;
+            int wq = 0;
+            for (int q = tid; q < G; q += LU_THREADS) {
                 const double* slot = a.xbuf + ((int64_t)par * G + q) * LU_XSTRIDE;
-                double v = __ldcg(slot);
-                int64_t i = (int64_t)__double_as_longlong(__ldcg(slot + 1));
-                if (v > gv || (v == gv && i < gi)) { gv = v; gi = i; gw = q; }
+                double cv = __ldcg(slot);
+                int64_t ci = (int64_t)__double_as_longlong(__ldcg(slot + 1));
+                if (better(cv, ci, v, i)) { v = cv; i = ci; wq = q; }
             }
-            s_piv = gi;
-            red_i[0] = gw;
-            if (cta == 0) a.ipiv[jr] = (int)(gi);
+            for (int o = 16; o > 0; o >>= 1) {
+                double ov = __shfl_down_sync(0xffffffffu, v, o);
+                int64_t oi = __shfl_down_sync(0xffffffffu, i, o);
+                int ow = __shfl_down_sync(0xffffffffu, wq, o);
+                if (better(ov, oi, v, i)) { v = ov; i = oi; wq = ow; }
+            }
+            if (lane == 0) { red_v[warp] = v; red_i[warp] = i; red_w[warp] = wq; }
+            __syncthreads();
+            if (tid == 0) {
+                for (int wv = 1; wv < LU_THREADS / 32; ++wv)
+                    if (better(red_v[wv], red_i[wv], v, i)) { v = red_v[wv]; i = red_i[wv]; wq = red_w[wv]; }
+                s_piv = i;
+                s_win = wq;
+                if (cta == 0) a.ipiv[jr] = (int)i;
+            }
+            __syncthreads();
         }
-        __syncthreads();
         const int64_t piv = s_piv;
         if (tid < jb) {
-            pivrow[tid] = __ldcg(a.xbuf + ((int64_t)par * G + red_i[0]) * LU_XSTRIDE + 2 + tid);
+            pivrow[tid] = __ldcg(a.xbuf + ((int64_t)par * G + s_win) * LU_XSTRIDE + 2 + tid);
             oldrow[tid] = __ldcg(a.rowj + par * LU_JBMAX + tid);
         }
         __syncthreads();
@@ -115,6 +139,19 @@ __global__ void __launch_bounds__(LU_THREADS, 1) lu_panel_kernel(LuPanelArgs a)
             if (piv != jr) {
                 if (piv >= rbeg && piv < rbeg + rows_here && tid < jb) sp[tid * R + (piv - rbeg)] = oldrow[tid];
                 if (jr >= rbeg && jr < rbeg + rows_here && tid < jb) sp[tid * R + (jr - rbeg)] = pivrow[tid];
+                // the same interchange on the rest of the row (columns outside the panel) and on perm
+                for (int64_t e = gtid; e < n_out; e += gstride) {
+                    int64_t c = (e < a.c0) ? e : e + jb;
+                    double* pc = a.L + c * a.ld;
+                    double t = pc[jr];
+                    pc[jr] = pc[piv];
+                    pc[piv] = t;
+                }
+                if (gtid == 0) {
+                    int t = a.perm[jr];
+                    a.perm[jr] = a.perm[piv];
+                    a.perm[piv] = t;
+                }
             }
             __syncthreads();
             for (int r = tid; r < rows_here; r += LU_THREADS) {
@@ -132,29 +169,17 @@ __global__ void __launch_bounds__(LU_THREADS, 1) lu_panel_kernel(LuPanelArgs a)
     }
 }
 
-// Apply the row interchanges ipiv[k0..k1) (sequentially, ascending) to columns [c0, c1).
-__global__ void laswp_kernel(double* L, int64_t ld, int64_t c0, int64_t c1, const int* ipiv, int64_t k0, int64_t k1)
-{
-    int64_t c = c0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= c1) return;
-    double* col = L + c * ld;
-    for (int64_t k = k0; k < k1; ++k) {
-        int64_t p = ipiv[k];
-        if (p != k) {
-            double t = col[k];
-            col[k] = col[p];
-            col[p] = t;
-        }
-    }
-}
-
-static void lu_panel(Ctx& cx, double* L, int64_t ld, int64_t w, int64_t c0, int jb, int* ipiv, double* xbuf,
-                     double* rowj)
+static void lu_panel(Ctx& cx, double* L, int64_t ld, int64_t w, int64_t d, int64_t c0, int jb, int* ipiv, int* perm,
+                     double* xbuf, double* rowj)
 {
     int64_t rows = w - c0;
-    // rows per CTA: fill the SMs but keep >= 32 rows per CTA and the slab within shared memory
-    int G = (int)imin(cx.num_sms, imax(1, cdiv(rows, 64)));
+    // few enough CTAs that the barrier stays cheap, enough that the slab fits shared memory
+    int G = (int)imin(cx.num_sms, imax(1, cdiv(rows, 256)));
     int R = (int)cdiv(rows, G);
+    if ((size_t)R * jb * sizeof(double) > 200 * 1024) {
+        G = (int)imin(cx.num_sms, cdiv(rows * jb * (int64_t)sizeof(double), 200 * 1024));
+        R = (int)cdiv(rows, G);
+    }
     size_t smem = (size_t)R * jb * sizeof(double);
     if (smem > 200 * 1024) throw std::runtime_error("lu_panel: panel too tall for shared memory");
     static bool attr = false;
@@ -162,7 +187,7 @@ static void lu_panel(Ctx& cx, double* L, int64_t ld, int64_t w, int64_t c0, int 
         BQ_CUDA(cudaFuncSetAttribute(lu_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         attr = true;
     }
-    LuPanelArgs a{L, ld, w, c0, jb, R, ipiv, xbuf, rowj};
+    LuPanelArgs a{L, ld, w, d, c0, jb, R, ipiv, perm, xbuf, rowj};
     void* args[] = {&a};
     BQ_CUDA(cudaLaunchCooperativeKernel((void*)lu_panel_kernel, dim3(G), dim3(LU_THREADS), args, smem, cx.stream));
     ++g_launches;
@@ -177,41 +202,43 @@ static int lu_leaf_width(int64_t rows, int num_sms)
     return 8;
 }
 
-static void getrf_rec(Ctx& cx, double* L, int64_t ld, int64_t w, int64_t c0, int64_t c1, int* ipiv, double* xbuf,
-                      double* rowj, int leaf)
+static void getrf_rec(Ctx& cx, double* L, int64_t ld, int64_t w, int64_t d, int64_t c0, int64_t c1, int* ipiv,
+                      int* perm, double* xbuf, double* rowj, int leaf)
 {
     int64_t nc = c1 - c0;
     if (nc <= leaf) {
-        lu_panel(cx, L, ld, w, c0, (int)nc, ipiv, xbuf, rowj);
+        lu_panel(cx, L, ld, w, d, c0, (int)nc, ipiv, perm, xbuf, rowj);
         return;
     }
     int64_t mid = c0 + cdiv(nc / 2, leaf) * leaf;
-    getrf_rec(cx, L, ld, w, c0, mid, ipiv, xbuf, rowj, leaf);
-    // swaps of the left half onto the right half's columns
-    int64_t ncr = c1 - mid;
-    laswp_kernel<<<(unsigned)cdiv(ncr, 128), 128, 0, cx.stream>>>(L, ld, mid, c1, ipiv, c0, mid);
-    BQ_LAUNCH_CHECK();
+    getrf_rec(cx, L, ld, w, d, c0, mid, ipiv, perm, xbuf, rowj, leaf);
+    // (the left half's interchanges were applied to whole rows inside its panels)
     // U12 = L11^{-1} A12 ; A22 -= L21 U12
+    int64_t ncr = c1 - mid;
     double* L11 = L + c0 + c0 * ld;
     double* A12 = L + c0 + mid * ld;
     trsm_left_lower_unit(cx, mid - c0, ncr, L11, ld, A12, ld);
     gemm(cx, false, false, w - mid, ncr, mid - c0, -1.0, L + mid + c0 * ld, ld, A12, ld, 1.0, L + mid + mid * ld, ld);
-    getrf_rec(cx, L, ld, w, mid, c1, ipiv, xbuf, rowj, leaf);
-    // right half's swaps back onto the left half's L columns, so that [c0, c1) is consistent for the
-    // caller's L21 (as DGETRF2 does)
-    laswp_kernel<<<(unsigned)cdiv(mid - c0, 128), 128, 0, cx.stream>>>(L, ld, c0, mid, ipiv, mid, c1);
-    BQ_LAUNCH_CHECK();
+    getrf_rec(cx, L, ld, w, d, mid, c1, ipiv, perm, xbuf, rowj, leaf);
 }
 
-void getrf_pivots(Ctx& cx, double* L, int64_t ld, int64_t w, int64_t d, int* ipiv)
+__global__ void iota_kernel(int64_t n, int* p)
+{
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        p[i] = (int)i;
+}
+
+void getrf_pivots(Ctx& cx, double* L, int64_t ld, int64_t w, int64_t d, int* ipiv, int* perm)
 {
     int64_t nlu = imin(w, d);
+    iota_kernel<<<(unsigned)imin(cdiv(w, 256), 1024), 256, 0, cx.stream>>>(w, perm);
+    BQ_LAUNCH_CHECK();
     if (nlu <= 0) return;
     size_t mark = cx.ws_used;
     double* xbuf = cx.alloc(2 * (size_t)cx.num_sms * LU_XSTRIDE);
     double* rowj = cx.alloc(2 * LU_JBMAX);
     int leaf = lu_leaf_width(w, cx.num_sms);
-    getrf_rec(cx, L, ld, w, 0, nlu, ipiv, xbuf, rowj, leaf);
+    getrf_rec(cx, L, ld, w, nlu, 0, nlu, ipiv, perm, xbuf, rowj, leaf);
     cx.ws_used = mark;
 }
 

@@ -1,9 +1,9 @@
 // perm.cu — K-PERM: pivot-format conversion and the touched-set column permutation.
 //
 // piv_transform ("Permutation formats"): J_qr = (1..w); for j < len(J_lu):
-// swap(J_qr(j), J_qr(J_lu(j) - 1)).  J_qr is a product of at most nlu = min(w, d) transpositions,
-// so it moves at most 2*nlu positions: T = {0..nlu-1} U {ipiv(j)}.  The kernels here compute the
-// touched set (tq[t] = position, tsrc[t] = J_qr(tq[t]) - 1) and apply the gather semantics of
+// swap(J_qr(j), J_qr(J_lu(j) - 1)).  K-LU maintains perm = J_qr - 1 as it pivots.  J_qr is a product
+// of at most nlu = min(w, d) transpositions, so it moves at most 2*nlu positions.  The kernels here
+// read the touched set (tq[t] = position, tsrc[t] = J_qr(tq[t]) - 1) off perm and apply the gather semantics of
 // col_perm (Alg. 5): new(:, q) = old(:, J_qr(q) - 1), moving only T, to the
 // columns of A (all m rows, steps bqrrp:permute_r + permute_m merged), to the rows of
 // the transposed sketch (Alg. 2 step wide_qrcp:permute) and to J (step bqrrp:update_j).
@@ -12,56 +12,31 @@
 
 namespace bqrrp {
 
-constexpr int PT_HASH = 8192;  // open-addressing table for positions >= nlu (<= nlu <= 4096 entries)
-
-// One CTA.  ipiv: 0-based absolute rows (length nlu).  Output: tq, tsrc (length nt <= 2 nlu), nt.
-__global__ void piv_to_touched_kernel(int nlu, const int* __restrict__ ipiv, int* tq, int* tsrc, int* nt_out)
+// Touched set straight off the permutation vector: positions q with perm[q] != q (at most 2 nlu of
+// them).  Emission order is arbitrary (atomic counter); the gather/scatter result does not depend on it.
+__global__ void touched_from_perm_kernel(int64_t w, const int* __restrict__ perm, int* tq, int* tsrc, int* nt)
 {
-    extern __shared__ int sh[];
-    int* direct = sh;               // direct[q] = current source of position q < nlu
-    int* hkey = sh + nlu;           // hash: position (>= nlu) or -1
-    int* hval = hkey + PT_HASH;     // its current source
-    int* hord = hval + PT_HASH;     // insertion order of hash slots
-    __shared__ int nins, cnt;
-    for (int i = threadIdx.x; i < nlu; i += blockDim.x) direct[i] = i;
-    for (int i = threadIdx.x; i < PT_HASH; i += blockDim.x) hkey[i] = -1;
-    if (threadIdx.x == 0) { nins = 0; cnt = 0; }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        for (int j = 0; j < nlu; ++j) {
-            int p = ipiv[j];
-            if (p == j) continue;
-            int vj = direct[j];
-            if (p < nlu) {
-                direct[j] = direct[p];
-                direct[p] = vj;
-            } else {
-                unsigned h = ((unsigned)p * 2654435761u) & (PT_HASH - 1);
-                while (hkey[h] != -1 && hkey[h] != p) h = (h + 1) & (PT_HASH - 1);
-                if (hkey[h] == -1) { hkey[h] = p; hval[h] = p; hord[nins++] = (int)h; }
-                direct[j] = hval[h];
-                hval[h] = vj;
-            }
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < w; q += (int64_t)gridDim.x * blockDim.x) {
+        int p = perm[q];
+        if (p != (int)q) {
+            int t = atomicAdd(nt, 1);
+            tq[t] = (int)q;
+            tsrc[t] = p;
         }
     }
-    __syncthreads();
-    // emit moved positions (identity entries dropped)
-    for (int q = threadIdx.x; q < nlu; q += blockDim.x)
-        if (direct[q] != q) {
-            int t = atomicAdd(&cnt, 1);
-            tq[t] = q;
-            tsrc[t] = direct[q];
-        }
-    for (int e = threadIdx.x; e < nins; e += blockDim.x) {
-        int h = hord[e];
-        if (hval[h] != hkey[h]) {
-            int t = atomicAdd(&cnt, 1);
-            tq[t] = hkey[h];
-            tsrc[t] = hval[h];
-        }
+}
+
+// Sequential piv_transform of a one-based swap list into perm (debug entry only).
+__global__ void perm_from_ipiv_kernel(int64_t w, int64_t nlu, const int64_t* __restrict__ ipiv1, int* perm)
+{
+    if (blockIdx.x != 0 || threadIdx.x != 0) return;
+    for (int64_t q = 0; q < w; ++q) perm[q] = (int)q;
+    for (int64_t j = 0; j < nlu; ++j) {
+        int64_t p = ipiv1[j] - 1;
+        int t = perm[j];
+        perm[j] = perm[p];
+        perm[p] = t;
     }
-    __syncthreads();
-    if (threadIdx.x == 0) *nt_out = cnt;
 }
 
 // scratch(:, t) = X(:, src[t]) for all `rows` rows; column-contiguous copies, 2-D grid (t, row chunk).
@@ -120,21 +95,19 @@ __global__ void permute_vec_kernel(int64_t* J, const int* __restrict__ tq, const
     for (int t = threadIdx.x; t < n; t += blockDim.x) J[tq[t]] = tmp[t];
 }
 
-void touched_set(Ctx& cx, int64_t nlu, const int* ipiv, Touched& T)
+void touched_from_perm(Ctx& cx, int64_t w, int64_t nlu, const int* perm, Touched& T)
 {
     T.maxnt = 2 * nlu;
-    if (nlu <= 0) {
-        BQ_CUDA(cudaMemsetAsync(T.nt, 0, sizeof(int), cx.stream));
-        return;
-    }
-    if (nlu > PT_HASH / 2) throw std::runtime_error("piv_to_touched: sketch size above 4096");
-    size_t smem = sizeof(int) * ((size_t)nlu + 3 * PT_HASH);
-    static bool attr = false;
-    if (!attr) {
-        BQ_CUDA(cudaFuncSetAttribute(piv_to_touched_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
-        attr = true;
-    }
-    piv_to_touched_kernel<<<1, 256, smem, cx.stream>>>((int)nlu, ipiv, T.tq, T.tsrc, T.nt);
+    BQ_CUDA(cudaMemsetAsync(T.nt, 0, sizeof(int), cx.stream));
+    if (nlu <= 0 || w <= 0) return;
+    touched_from_perm_kernel<<<(unsigned)imin(cdiv(w, 256), 4 * cx.num_sms), 256, 0, cx.stream>>>(w, perm, T.tq,
+                                                                                                   T.tsrc, T.nt);
+    BQ_LAUNCH_CHECK();
+}
+
+void perm_from_ipiv(Ctx& cx, int64_t w, int64_t nlu, const int64_t* ipiv1, int* perm)
+{
+    perm_from_ipiv_kernel<<<1, 32, 0, cx.stream>>>(w, nlu, ipiv1, perm);
     BQ_LAUNCH_CHECK();
 }
 
