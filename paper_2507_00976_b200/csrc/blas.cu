@@ -1,10 +1,44 @@
 // blas.cu — GEMM launcher (split-K heuristic), recursive TRSM, blocked POTRF and the
 // sign-choosing no-pivot LU of the Householder reconstruction.  Every O(n^3) piece is cast onto the
 // DMMA GEMM engine (dgemm.cuh); the diagonal blocks (<= 64) are factored by one CTA in shared memory.
+#include <cstdlib>
+#include <mutex>
+
 #include "blas.cuh"
 #include "dgemm.cuh"
 
 namespace bqrrp {
+
+// Optional GEMM trace (profiling aid): BQRRP_GEMM_TRACE=<file> records every engine call with its shape
+// and CUDA-event duration; written at process exit as CSV.
+namespace {
+struct GemmTraceRec {
+    int64_t M, N, K;
+    int ta, tb, tri, nsplit;
+    cudaEvent_t e0, e1;
+};
+struct GemmTrace {
+    const char* path = std::getenv("BQRRP_GEMM_TRACE");
+    std::vector<GemmTraceRec> recs;
+    std::mutex mu;
+    ~GemmTrace()
+    {
+        if (!path || recs.empty()) return;
+        FILE* f = std::fopen(path, "w");
+        if (!f) return;
+        std::fprintf(f, "M,N,K,ta,tb,tri,nsplit,ms\n");
+        for (auto& r : recs) {
+            float ms = 0.f;
+            cudaEventSynchronize(r.e1);
+            cudaEventElapsedTime(&ms, r.e0, r.e1);
+            std::fprintf(f, "%lld,%lld,%lld,%d,%d,%d,%d,%.6f\n", (long long)r.M, (long long)r.N, (long long)r.K, r.ta, r.tb,
+                         r.tri, r.nsplit, ms);
+        }
+        std::fclose(f);
+    }
+};
+GemmTrace g_trace;
+}  // namespace
 
 // ------------------------------------------------------------------------------------------- GEMM
 template <bool TA, bool TB>
@@ -41,6 +75,13 @@ void gemm(Ctx& cx, bool ta, bool tb, int64_t M, int64_t N, int64_t K, double alp
     }
     GemmArgs g{M, N, K, alpha, beta, A, lda, B, ldb, C, ldc, nsplit > 1 ? cx.splitk : nullptr, kchunk, tri ? 1 : 0};
     dim3 grid((unsigned)tm, (unsigned)tn, (unsigned)nsplit);
+    GemmTraceRec rec{};
+    if (g_trace.path) {
+        rec = GemmTraceRec{M, N, K, ta, tb, tri, nsplit, nullptr, nullptr};
+        cudaEventCreate(&rec.e0);
+        cudaEventCreate(&rec.e1);
+        cudaEventRecord(rec.e0, cx.stream);
+    }
     if (!ta && !tb) launch_gemm<false, false>(cx, g, grid);
     else if (ta && !tb) launch_gemm<true, false>(cx, g, grid);
     else if (!ta && tb) launch_gemm<false, true>(cx, g, grid);
@@ -50,6 +91,11 @@ void gemm(Ctx& cx, bool ta, bool tb, int64_t M, int64_t N, int64_t K, double alp
         int blocks = (int)imin(cdiv(total, 256), 4 * cx.num_sms);
         dgemm_splitk_reduce<<<blocks, 256, 0, cx.stream>>>(M, N, nsplit, cx.splitk, alpha, beta, C, ldc, tri ? 1 : 0);
         BQ_LAUNCH_CHECK();
+    }
+    if (g_trace.path) {
+        cudaEventRecord(rec.e1, cx.stream);
+        std::lock_guard<std::mutex> lk(g_trace.mu);
+        g_trace.recs.push_back(rec);
     }
 }
 

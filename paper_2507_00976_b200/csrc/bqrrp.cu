@@ -115,7 +115,7 @@ static Layout layout(int64_t m, int64_t n, int64_t b, int64_t d)
     P += r(8) * 2;                         // ref, flags
     // temporaries: sketch QR vs panel (never live together)
     size_t p = (size_t)d;
-    size_t sq = r(p * p) * 5 + r(p) + r(2 * 160 * 33 + 160 * 32 * 32) + r(64) + r((size_t)n * p) * 2;
+    size_t sq = r(p * p) * 7 + r(p) + r(2 * 160 * 33 + 160 * 32 * 32) + r(64) + r((size_t)n * p);
     size_t lu = r(2 * 160 * 34) + r(64);
     size_t pn = r((size_t)m * bb) + r(bb * bb) * 8 + r(bb) + r(bb * (size_t)n) * 2;
     size_t T = sq > pn ? sq : pn;

@@ -186,9 +186,217 @@ __global__ void __launch_bounds__(QR_THREADS, 1) qr_panel_kernel(QrPanelArgs a)
     }
 }
 
+// ---------------------------------------------------------------------------------------------
+// Cluster variant (the common case, d <= ~3000): the panel rows are split over the CTAs of ONE thread-
+// block cluster (<= 8 CTAs) and each column step exchanges only through distributed shared memory with
+// one cluster barrier: every CTA reduces its partials (sum x^2 and x^T A(:, c) for the 31 columns to the
+// right) with a 31-shuffle butterfly transpose-reduction, publishes them in its own shared memory, and
+// after barrier.cluster every CTA sums the CL partial vectors (fixed order) through DSMEM.
+constexpr int QC_THREADS = 256;
+constexpr int QC_CLMAX = 8;
+
+struct QrClusterArgs {
+    double* A;
+    int64_t ld;
+    int64_t m;
+    int64_t c0;
+    int jb;
+    int R;
+    double* tau;
+    double* V;
+    double* T;
+    int64_t ldt;
+};
+
+// q[l] summed over the warp ends in lane l (indices 0..31): 16+8+4+2+1 shuffles.
+__device__ __forceinline__ double warp_transpose_reduce32(double (&q)[32], int lane)
+{
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) {
+        const bool up = (lane & off) != 0;
+#pragma unroll
+        for (int i = 0; i < off; ++i) {
+            double send = up ? q[i] : q[i + off];
+            double recv = __shfl_xor_sync(0xffffffffu, send, off);
+            q[i] = (up ? q[i + off] : q[i]) + recv;
+        }
+    }
+    return q[0];
+}
+
+__global__ void __launch_bounds__(QC_THREADS, 1) qr_panel_cluster_kernel(QrClusterArgs a)
+{
+    cg::cluster_group cluster = cg::this_cluster();
+    const int CL = (int)cluster.num_blocks(), me = (int)cluster.block_rank();
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, R = a.R, jb = a.jb;
+    extern __shared__ double dyn[];
+    double* sp = dyn;                  // sp[c * R + r]
+    double* part = dyn + R * jb;       // [2][32] this CTA's partials
+    double* rowjs = part + 64;         // [2][32] alpha, a_c (owner CTA of row jr)
+    double* gram = rowjs + 64;         // [32 * 32] Gram partial
+    __shared__ double red[QC_THREADS / 32][33];
+    __shared__ double wv[32], tot[32], s_taus[32];
+    __shared__ double s_tau, s_beta, s_denom;
+    const int64_t rbeg = a.c0 + (int64_t)me * R;
+    const int64_t rows_here = (rbeg < a.m) ? ((a.m - rbeg < R) ? a.m - rbeg : R) : 0;
+
+    for (int idx = tid; idx < R * jb; idx += QC_THREADS) {
+        int r = idx % R, c = idx / R;
+        sp[idx] = (r < rows_here) ? a.A[rbeg + r + (a.c0 + c) * a.ld] : 0.0;
+    }
+    __syncthreads();
+
+    for (int j = 0; j < jb; ++j) {
+        const int par = j & 1;
+        const int64_t jr = a.c0 + j;
+        const int owner = (int)((jr - a.c0) / R);
+        double q[32];
+#pragma unroll
+        for (int c = 0; c < 32; ++c) q[c] = 0.0;
+        for (int r = tid; r < rows_here; r += QC_THREADS) {
+            if (rbeg + r <= jr) continue;
+            double x = sp[j * R + r];
+            q[0] = fma(x, x, q[0]);
+#pragma unroll
+            for (int c = 1; c < 32; ++c)
+                if (j + c < jb) q[c] = fma(x, sp[(j + c) * R + r], q[c]);
+        }
+        red[warp][lane] = warp_transpose_reduce32(q, lane);
+        if (me == owner && tid < jb - j) rowjs[par * 32 + tid] = sp[(j + tid) * R + (jr - rbeg)];
+        __syncthreads();
+        if (tid < 32) {
+            double v = 0.0;
+#pragma unroll
+            for (int w = 0; w < QC_THREADS / 32; ++w) v += red[w][tid];
+            part[par * 32 + tid] = v;
+        }
+        cluster.sync();
+        if (tid < 32) {
+            double v = 0.0;
+            for (int rk = 0; rk < CL; ++rk) v += *cluster.map_shared_rank(part + par * 32 + tid, rk);
+            tot[tid] = v;
+            wv[tid] = (tid < jb - j) ? *cluster.map_shared_rank(rowjs + par * 32 + tid, owner) : 0.0;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            double alpha = wv[0];
+            double nrm = sqrt(fma(alpha, alpha, tot[0]));
+            if (nrm == 0.0) {
+                s_tau = 0.0; s_beta = 0.0; s_denom = 1.0;
+            } else {
+                double beta = (alpha >= 0.0) ? -nrm : nrm;  // convention H
+                s_beta = beta;
+                s_tau = (beta - alpha) / beta;
+                s_denom = alpha - beta;
+            }
+            s_taus[j] = s_tau;
+            if (me == 0) a.tau[jr] = s_tau;
+        }
+        __syncthreads();
+        const double tau = s_tau, denom = s_denom;
+        if (tid > 0 && tid < jb - j) wv[tid] = wv[tid] + tot[tid] / denom;  // w_c = v^T A(:, c)
+        __syncthreads();
+        if (tau != 0.0) {
+            for (int r = tid; r < rows_here; r += QC_THREADS) {
+                int64_t ar = rbeg + r;
+                if (ar < jr) continue;
+                if (ar == jr) {
+                    sp[j * R + r] = s_beta;
+                    for (int c = 1; c < jb - j; ++c) sp[(j + c) * R + r] -= tau * wv[c];
+                } else {
+                    double v = sp[j * R + r] / denom;
+                    sp[j * R + r] = v;
+                    for (int c = 1; c < jb - j; ++c) sp[(j + c) * R + r] = fma(-tau * wv[c], v, sp[(j + c) * R + r]);
+                }
+            }
+        }
+        __syncthreads();
+    }
+    // explicit V, write-back, Gram partial of V^T V over my rows
+    for (int idx = tid; idx < R * jb; idx += QC_THREADS) {
+        int r = idx % R, c = idx / R;
+        if (r >= rows_here) continue;
+        int64_t ar = rbeg + r, cr = a.c0 + c;
+        a.V[ar + cr * a.m] = (ar == cr) ? 1.0 : (ar > cr ? sp[idx] : 0.0);
+        a.A[ar + cr * a.ld] = sp[idx];
+    }
+    for (int pq = tid; pq < jb * jb; pq += QC_THREADS) {
+        int p = pq % jb, qq = pq / jb;
+        double s = 0.0;
+        if (p < qq) {
+            for (int r = 0; r < rows_here; ++r) {
+                int64_t ar = rbeg + r;
+                double vp = (ar == a.c0 + p) ? 1.0 : (ar > a.c0 + p ? sp[p * R + r] : 0.0);
+                double vq = (ar == a.c0 + qq) ? 1.0 : (ar > a.c0 + qq ? sp[qq * R + r] : 0.0);
+                s = fma(vp, vq, s);
+            }
+        }
+        gram[pq] = s;
+    }
+    cluster.sync();
+    if (me == 0) {
+        // T = larft(V, tau): T_jj = tau_j, T(0:j, j) = -tau_j T(0:j, 0:j) G(0:j, j)
+        __shared__ double Gm[32][33], Ts[32][33];
+        for (int pq = tid; pq < jb * jb; pq += QC_THREADS) {
+            double sum = 0.0;
+            for (int rk = 0; rk < CL; ++rk) sum += *cluster.map_shared_rank(gram + pq, rk);
+            Gm[pq % jb][pq / jb] = sum;
+            Ts[pq % jb][pq / jb] = 0.0;
+        }
+        __syncthreads();
+        for (int j = 0; j < jb; ++j) {
+            double tj = s_taus[j];
+            if (tid < j) {
+                double sum = 0.0;
+                for (int l = tid; l < j; ++l) sum = fma(Ts[tid][l], Gm[l][j], sum);
+                Ts[tid][j] = -tj * sum;
+            }
+            if (tid == 0) Ts[j][j] = tj;
+            __syncthreads();
+        }
+        for (int pq = tid; pq < jb * jb; pq += QC_THREADS) {
+            int p = pq % jb, qq = pq / jb;
+            a.T[(a.c0 + p) + (a.c0 + qq) * a.ldt] = Ts[p][qq];
+        }
+    }
+    cluster.sync();  // keep every CTA's shared memory alive until CTA 0 has read it
+}
+
+static bool qr_panel_cluster(Ctx& cx, double* A, int64_t ld, int64_t m, int64_t c0, int jb, double* tau, double* V,
+                             double* T, int64_t ldt)
+{
+    int64_t rows = m - c0;
+    int CL = (int)imin(QC_CLMAX, imax(1, cdiv(rows, 256)));
+    int R = (int)cdiv(rows, CL);
+    size_t smem = ((size_t)R * jb + 64 + 64 + 32 * 32) * sizeof(double);
+    if (smem > 200 * 1024) return false;
+    static bool attr = false;
+    if (!attr) {
+        BQ_CUDA(cudaFuncSetAttribute(qr_panel_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        attr = true;
+    }
+    QrClusterArgs args{A, ld, m, c0, jb, R, tau, V, T, ldt};
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(CL);
+    cfg.blockDim = dim3(QC_THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = cx.stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = CL;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    BQ_CUDA(cudaLaunchKernelEx(&cfg, qr_panel_cluster_kernel, args));
+    ++g_launches;
+    return true;
+}
+
 static void qr_panel(Ctx& cx, double* A, int64_t ld, int64_t m, int64_t c0, int jb, double* tau, double* V, double* T,
                      int64_t ldt, double* xbuf, double* rowj)
 {
+    if (qr_panel_cluster(cx, A, ld, m, c0, jb, tau, V, T, ldt)) return;
     int64_t rows = m - c0;
     int G = (int)imin(cx.num_sms, imax(1, cdiv(rows, 64)));
     int R = (int)cdiv(rows, G);
@@ -264,12 +472,18 @@ void sketch_qr(Ctx& cx, double* MskT, int64_t ldm, int64_t w, int64_t d)
     geqrf_rec(cx, Wq, d, 0, p, tau, V, Tf, p, W1, W2, xbuf, rowj);
     int64_t rest = w - p;
     if (rest > 0) {
+        // p == d here.  Q_sk = H_1...H_p = I - V T V^T formed explicitly (d x d), then
+        // R_sk(:, p:w)^T = Wsk(:, p:w)^T Q_sk in one GEMM (2 rest d^2 flops instead of 6 rest d p).
         double* Xt = MskT + p;  // rest x d
-        double* Y = cx.alloc((size_t)rest * p);
-        double* Y2 = cx.alloc((size_t)rest * p);
-        gemm(cx, false, false, rest, p, d, 1.0, Xt, ldm, V, d, 0.0, Y, rest);
-        gemm(cx, false, false, rest, p, p, 1.0, Y, rest, Tf, p, 0.0, Y2, rest);
-        gemm(cx, false, true, rest, d, p, -1.0, Y2, rest, V, d, 1.0, Xt, ldm);
+        double* Q = cx.alloc((size_t)d * d);
+        double* Wt = cx.alloc((size_t)p * d);
+        double* Y = cx.alloc((size_t)rest * d);
+        gemm(cx, false, true, p, d, p, 1.0, Tf, p, V, d, 0.0, Wt, p);  // Wt = T V^T
+        BQ_CUDA(cudaMemsetAsync(Q, 0, sizeof(double) * d * d, cx.stream));
+        zero_triangle(cx, 'L', d, d, Q, d, /*unit_diag=*/true);
+        gemm(cx, false, false, d, d, p, -1.0, V, d, Wt, p, 1.0, Q, d);  // Q = I - V Wt
+        gemm(cx, false, false, rest, d, d, 1.0, Xt, ldm, Q, d, 0.0, Y, rest);
+        copy_matrix(cx, rest, d, Y, rest, Xt, ldm);
     }
     store_rsk_kernel<<<(unsigned)imin(cdiv(p * d, 256), 4 * cx.num_sms), 256, 0, cx.stream>>>(p, d, Wq, MskT, ldm);
     BQ_LAUNCH_CHECK();
