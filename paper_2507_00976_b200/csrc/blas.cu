@@ -41,31 +41,53 @@ GemmTrace g_trace;
 }  // namespace
 
 // ------------------------------------------------------------------------------------------- GEMM
-template <bool TA, bool TB>
-static void launch_gemm(Ctx& cx, const GemmArgs& g, dim3 grid)
+template <class Cfg, bool TA, bool TB>
+static void launch_gemm_t(Ctx& cx, const GemmArgs& g, dim3 grid)
 {
     static bool attr_set = false;
-    size_t sm = dgemm_smem_bytes(TA, TB);
+    constexpr size_t sm = dgemm_smem_bytes<Cfg, TA, TB>();
     if (!attr_set) {
-        BQ_CUDA(cudaFuncSetAttribute(dgemm_kernel<TA, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        BQ_CUDA(cudaFuncSetAttribute(dgemm_kernel<Cfg, TA, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
         attr_set = true;
     }
-    dgemm_kernel<TA, TB><<<grid, GEMM_THREADS, sm, cx.stream>>>(g);
+    dgemm_kernel<Cfg, TA, TB><<<grid, Cfg::THREADS, sm, cx.stream>>>(g);
     BQ_LAUNCH_CHECK();
 }
 
+template <class Cfg>
+static void launch_gemm(Ctx& cx, bool ta, bool tb, const GemmArgs& g, int nsplit)
+{
+    dim3 grid((unsigned)cdiv(g.M, Cfg::BM), (unsigned)cdiv(g.N, Cfg::BN), (unsigned)nsplit);
+    if (!ta && !tb) launch_gemm_t<Cfg, false, false>(cx, g, grid);
+    else if (ta && !tb) launch_gemm_t<Cfg, true, false>(cx, g, grid);
+    else if (!ta && tb) launch_gemm_t<Cfg, false, true>(cx, g, grid);
+    else launch_gemm_t<Cfg, true, true>(cx, g, grid);
+}
+
+// Tile choice: the big tile when it still gives >= 2 waves, then 64x64, then 64x32 (more CTAs for the
+// small and skinny GEMMs of the recursions).  Split-K (fixed slices, fixed-order sum) when even the
+// chosen tiling leaves the SMs idle and K is long.
 void gemm(Ctx& cx, bool ta, bool tb, int64_t M, int64_t N, int64_t K, double alpha, const double* A, int64_t lda,
           const double* B, int64_t ldb, double beta, double* C, int64_t ldc, bool tri)
 {
     if (M <= 0 || N <= 0) return;
-    int64_t tm = cdiv(M, GEMM_BM), tn = cdiv(N, GEMM_BN);
-    int64_t tiles = tri ? (tm * (tm + 1)) / 2 : tm * tn;
+    auto ntiles = [&](int bm, int bn) {
+        int64_t tm = cdiv(M, bm), tn = cdiv(N, bn);
+        return tri ? (tm * tn + tm) / 2 : tm * tn;
+    };
+    int cfg;  // 0 wide (128x64), 1 mid (64x64), 2 small (64x32)
+    int bm, bn;
+    if (!ta && ntiles(CfgWide::BM, CfgWide::BN) >= 2 * cx.num_sms) { cfg = 0; bm = CfgWide::BM; bn = CfgWide::BN; }
+    else if (ta && ntiles(CfgMid::BM, CfgMid::BN) >= 2 * cx.num_sms) { cfg = 1; bm = CfgMid::BM; bn = CfgMid::BN; }
+    else if (N > 32 && ntiles(CfgMid::BM, CfgMid::BN) >= cx.num_sms) { cfg = 1; bm = CfgMid::BM; bn = CfgMid::BN; }
+    else { cfg = 2; bm = CfgSmall::BM; bn = CfgSmall::BN; }
+    int64_t tiles = ntiles(bm, bn);
     int nsplit = 1;
     int64_t kchunk = K > 0 ? K : 1;
-    if (K >= 1024 && tiles < cx.num_sms && cx.splitk) {
+    if (K >= 256 && tiles < 2 * cx.num_sms && cx.splitk) {
         int64_t want = cdiv(2 * cx.num_sms, tiles);
         want = imin(want, 32);
-        want = imin(want, K / 256);
+        want = imin(want, K / 128);
         int64_t cap = (int64_t)(cx.splitk_elems / (size_t)(M * N));
         want = imin(want, cap);
         if (want >= 2) {
@@ -74,7 +96,6 @@ void gemm(Ctx& cx, bool ta, bool tb, int64_t M, int64_t N, int64_t K, double alp
         }
     }
     GemmArgs g{M, N, K, alpha, beta, A, lda, B, ldb, C, ldc, nsplit > 1 ? cx.splitk : nullptr, kchunk, tri ? 1 : 0};
-    dim3 grid((unsigned)tm, (unsigned)tn, (unsigned)nsplit);
     GemmTraceRec rec{};
     if (g_trace.path) {
         rec = GemmTraceRec{M, N, K, ta, tb, tri, nsplit, nullptr, nullptr};
@@ -82,10 +103,9 @@ void gemm(Ctx& cx, bool ta, bool tb, int64_t M, int64_t N, int64_t K, double alp
         cudaEventCreate(&rec.e1);
         cudaEventRecord(rec.e0, cx.stream);
     }
-    if (!ta && !tb) launch_gemm<false, false>(cx, g, grid);
-    else if (ta && !tb) launch_gemm<true, false>(cx, g, grid);
-    else if (!ta && tb) launch_gemm<false, true>(cx, g, grid);
-    else launch_gemm<true, true>(cx, g, grid);
+    if (cfg == 0) launch_gemm<CfgWide>(cx, ta, tb, g, nsplit);
+    else if (cfg == 1) launch_gemm<CfgMid>(cx, ta, tb, g, nsplit);
+    else launch_gemm<CfgSmall>(cx, ta, tb, g, nsplit);
     if (nsplit > 1) {
         int64_t total = M * N;
         int blocks = (int)imin(cdiv(total, 256), 4 * cx.num_sms);

@@ -7,22 +7,21 @@
 //
 //   C(MxN) = alpha * op(A)(MxK) * op(B)(KxN) + beta * C,   column-major, op = identity or transpose.
 //
-// CTA tile BM x BN x BK = 128 x 128 x 16, 256 threads = 8 warps (2 x 4), warp tile 64 x 32 = 8 x 4
-// DMMA tiles; STAGES-deep cp.async pipeline; 8-byte cp.async with zero-fill handles every ragged edge
-// and any alignment (sub-matrix views start at arbitrary rows).  Shared tiles keep the operand's
-// contiguous axis contiguous ("MN-major" [k][mn] or "K-major" [mn][k]) with a 4-double pad that
-// makes every fragment load conflict-free.  Summation over K is in a fixed order
-// (k-tiles ascending, DMMA-internal order inside a k4 step): results are deterministic and
-// independent of the launch grid.  Optional split-K writes fixed slices that a second kernel sums
-// in slice order.  `tri` = 1 computes only tiles intersecting the lower triangle (SYRK).
+// Tiling is a template: CTA tile BM x BN x 16, WARPS_M x WARPS_N warps, each warp (BM/WARPS_M) x
+// (BN/WARPS_N) = MI x NI DMMA tiles; STAGES-deep cp.async pipeline; 8-byte cp.async with zero-fill
+// handles every ragged edge and any alignment (sub-matrix views start at arbitrary rows).  Shared
+// tiles keep the operand's contiguous axis contiguous ("MN-major" [k][mn] or "K-major" [mn][k]) with a
+// pad (row stride = 4 mod 16 doubles) that makes every fragment load conflict-free.
+// Summation over K is in a fixed order (k-tiles ascending, DMMA-internal order inside a k4 step):
+// results are deterministic and independent of the launch grid.  Optional split-K writes fixed slices
+// that a second kernel sums in slice order.  `tri` = 1 skips tiles strictly above the diagonal (SYRK).
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
 
 namespace bqrrp {
 
-constexpr int GEMM_BM = 128, GEMM_BN = 128, GEMM_BK = 16, GEMM_THREADS = 256, GEMM_STAGES = 4;
-constexpr int GEMM_PAD = 4;
+constexpr int GEMM_BK = 16;
 
 __device__ __forceinline__ void dmma_884(double& c0, double& c1, double a, double b)
 {
@@ -41,33 +40,75 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
-// Shared-memory tile of one operand.  MNMAJOR: s[k][mn] (row stride 128+PAD); else s[mn][k] (16+PAD).
-template <bool MNMAJOR>
+// Shared-memory tile of one operand, MN x 16.  MNMAJOR: s[k][mn] (row stride MN+4); else s[mn][k]
+// (row stride 20).  Both strides are 4 mod 16 doubles: the 16 lanes of a half-warp fragment load
+// (4 consecutive mn x 4 consecutive k) hit 16 distinct 8-byte bank pairs.
+template <bool MNMAJOR, int MN>
 struct TileLayout {
-    static constexpr int LD = MNMAJOR ? (GEMM_BM + GEMM_PAD) : (GEMM_BK + GEMM_PAD);
-    static constexpr int SIZE = MNMAJOR ? GEMM_BK * LD : GEMM_BM * LD;  // doubles
+    static constexpr int LD = MNMAJOR ? (MN + 4) : (GEMM_BK + 4);
+    static constexpr int SIZE = MNMAJOR ? GEMM_BK * LD : MN * LD;  // doubles
     __device__ static __forceinline__ int off(int mn, int k) { return MNMAJOR ? k * LD + mn : mn * LD + k; }
 };
 
-// Load one BK-slice of an operand tile: rows mn0..mn0+127 of op(X), k0..k0+15.
-//   op(X)(mn, k) = X[mn + k*ld] when X is stored mn-contiguous (MNMAJOR), else X[k + mn*ld].
-template <bool MNMAJOR>
-__device__ __forceinline__ void load_tile(double* s, const double* X, int64_t ld, int64_t mn0, int64_t k0,
-                                          int64_t MN, int64_t K, int tid)
-{
-    using L = TileLayout<MNMAJOR>;
+// Per-thread loader of one operand: element e = it * THREADS + tid of the MN x 16 slice.
+//   MNMAJOR (X[mn + k*ld]):  mn = tid % MN (fixed), k = it * (THREADS/MN) + tid / MN
+//   K-major (X[k + mn*ld]):  k = tid % 16 (fixed),  mn = it * (THREADS/16) + tid / 16
+// Addresses advance by a constant per `it` and per k-tile; interior tiles skip all predicates.
+template <bool MNMAJOR, int MN, int THREADS>
+struct Loader {
+    using L = TileLayout<MNMAJOR, MN>;
+    static constexpr int PER = (MN * GEMM_BK) / THREADS;
+    static_assert((MN * GEMM_BK) % THREADS == 0, "tile / thread mismatch");
+    static_assert(MNMAJOR ? (THREADS % MN == 0) : (THREADS % GEMM_BK == 0), "thread layout");
+    static constexpr int STEP_FIXED = MNMAJOR ? THREADS / MN : THREADS / GEMM_BK;  // k (or mn) per `it`
+    const double* p;    // element it = 0 of the current k-tile
+    int64_t it_stride;  // pointer delta between consecutive `it`
+    int64_t kt_stride;  // pointer delta per k-tile
+    int soff;           // shared offset of element it = 0
+    int kfix;           // this thread's k (K-major) or k of it = 0 (MN-major), relative to k0
+    unsigned mn_ok;     // bit it: mn in range
+
+    __device__ __forceinline__ Loader(const double* X, int64_t ld, int64_t mn0, int64_t k0, int64_t MNtot, int tid)
+    {
+        if (MNMAJOR) {
+            int mn = tid % MN, k = tid / MN;
+            p = X + (mn0 + mn) + (k0 + k) * ld;
+            it_stride = (int64_t)STEP_FIXED * ld;
+            kt_stride = (int64_t)GEMM_BK * ld;
+            soff = L::off(mn, k);
+            kfix = k;
+            mn_ok = (mn0 + mn < MNtot) ? 0xffffffffu : 0u;
+        } else {
+            int k = tid % GEMM_BK, mn = tid / GEMM_BK;
+            p = X + (k0 + k) + (mn0 + mn) * ld;
+            it_stride = (int64_t)STEP_FIXED * ld;
+            kt_stride = GEMM_BK;
+            soff = L::off(mn, k);
+            kfix = k;
+            mn_ok = 0;
 #pragma unroll
-    for (int it = 0; it < (GEMM_BM * GEMM_BK) / GEMM_THREADS; ++it) {
-        int e = it * GEMM_THREADS + tid;
-        int mn, k;
-        if (MNMAJOR) { mn = e % GEMM_BM; k = e / GEMM_BM; }
-        else { k = e % GEMM_BK; mn = e / GEMM_BK; }
-        int64_t gmn = mn0 + mn, gk = k0 + k;
-        bool ok = (gmn < MN) && (gk < K);
-        const double* src = ok ? (MNMAJOR ? X + gmn + gk * ld : X + gk + gmn * ld) : X;
-        cp_async8(s + L::off(mn, k), src, ok);
+            for (int it = 0; it < PER; ++it)
+                if (mn0 + mn + it * STEP_FIXED < MNtot) mn_ok |= 1u << it;
+        }
     }
-}
+    static constexpr int SOFF_STEP = STEP_FIXED * L::LD;  // shared offset between consecutive `it`
+    // load the k-tile whose first k is k0 (krem = valid k count remaining from k0) into buffer s
+    __device__ __forceinline__ void load(double* s, int krem, bool interior) const
+    {
+        if (interior && krem >= GEMM_BK) {
+#pragma unroll
+            for (int it = 0; it < PER; ++it) cp_async8(s + soff + it * SOFF_STEP, p + it * it_stride, true);
+        } else {
+#pragma unroll
+            for (int it = 0; it < PER; ++it) {
+                int k = MNMAJOR ? kfix + it * STEP_FIXED : kfix;
+                bool ok = ((mn_ok >> it) & 1u) && (k < krem);
+                cp_async8(s + soff + it * SOFF_STEP, ok ? (const void*)(p + it * it_stride) : (const void*)p, ok);
+            }
+        }
+    }
+    __device__ __forceinline__ void advance() { p += kt_stride; }
+};
 
 struct GemmArgs {
     int64_t M, N, K;
@@ -80,76 +121,88 @@ struct GemmArgs {
     int tri;         // 1: only tiles touching the lower triangle (m >= n) are computed
 };
 
+template <int BM_, int BN_, int WARPS_M_, int WARPS_N_, int STAGES_>
+struct GemmCfg {
+    static constexpr int BM = BM_, BN = BN_, WARPS_M = WARPS_M_, WARPS_N = WARPS_N_, STAGES = STAGES_;
+    static constexpr int THREADS = 32 * WARPS_M * WARPS_N;
+    static constexpr int MI = BM / WARPS_M / 8, NI = BN / WARPS_N / 8;
+    static constexpr int MIN_BLOCKS = (THREADS <= 128 && MI * NI <= 16) ? 4 : 1;
+};
+
 // TA: op(A) = A^T.  TB: op(B) = B^T.
-// A operand (op(A) is M x K): stored m-contiguous unless TA.   B operand (op(B) is K x N): stored
+// A operand (op(A) is M x K): stored m-contiguous unless TA.  B operand (op(B) is K x N): stored
 // n-contiguous only if TB.
-template <bool TA, bool TB>
-__global__ void __launch_bounds__(GEMM_THREADS, 1) dgemm_kernel(GemmArgs g)
+template <class Cfg, bool TA, bool TB>
+__global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS) dgemm_kernel(GemmArgs g)
 {
+    constexpr int BM = Cfg::BM, BN = Cfg::BN, THREADS = Cfg::THREADS, STAGES = Cfg::STAGES;
+    constexpr int MI = Cfg::MI, NI = Cfg::NI, WM = BM / Cfg::WARPS_M, WN = BN / Cfg::WARPS_N;
     constexpr bool A_MN = !TA;
     constexpr bool B_MN = TB;
-    using LA = TileLayout<A_MN>;
-    using LB = TileLayout<B_MN>;
+    using LA = TileLayout<A_MN, BM>;
+    using LB = TileLayout<B_MN, BN>;
     extern __shared__ __align__(16) double smem[];
     double* sA = smem;
-    double* sB = smem + GEMM_STAGES * LA::SIZE;
+    double* sB = smem + STAGES * LA::SIZE;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int wm = warp & 1, wn = warp >> 1;  // 2 x 4 warps
-    const int64_t m0 = (int64_t)blockIdx.x * GEMM_BM, n0 = (int64_t)blockIdx.y * GEMM_BN;
-    if (g.tri && m0 + GEMM_BM <= n0) return;  // tile strictly above the diagonal
+    const int wm = warp % Cfg::WARPS_M, wn = warp / Cfg::WARPS_M;
+    const int64_t m0 = (int64_t)blockIdx.x * BM, n0 = (int64_t)blockIdx.y * BN;
+    if (g.tri && m0 + BM <= n0) return;  // tile strictly above the diagonal
     const int64_t kbeg = (int64_t)blockIdx.z * g.kchunk;
     const int64_t kend = (kbeg + g.kchunk < g.K) ? kbeg + g.kchunk : g.K;
     const int nk = (int)((kend - kbeg + GEMM_BK - 1) / GEMM_BK);
 
-    const double* Ap = g.A;
-    const double* Bp = g.B;
-    // op(A) as an (M x K) operand: A_MN => element (m,k) at A[m + k*lda]; else at A[k + m*lda]
-    // op(B) as an (N x K) operand: B_MN => element (n,k) at B[n + k*ldb]; else at B[k + n*ldb]
+    double acc[MI][NI][2];
+#pragma unroll
+    for (int i = 0; i < MI; ++i)
+#pragma unroll
+        for (int j = 0; j < NI; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-    double acc[8][4][2];
+    Loader<A_MN, BM, THREADS> ldA(g.A, g.lda, m0, kbeg, g.M, tid);
+    Loader<B_MN, BN, THREADS> ldB(g.B, g.ldb, n0, kbeg, g.N, tid);
+    const bool interior = (m0 + BM <= g.M) && (n0 + BN <= g.N);
 #pragma unroll
-    for (int i = 0; i < 8; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-
-#pragma unroll
-    for (int st = 0; st < GEMM_STAGES - 1; ++st) {
+    for (int st = 0; st < STAGES - 1; ++st) {
         if (st < nk) {
-            int64_t k0 = kbeg + (int64_t)st * GEMM_BK;
-            load_tile<A_MN>(sA + st * LA::SIZE, Ap, g.lda, m0, k0, g.M, kend, tid);
-            load_tile<B_MN>(sB + st * LB::SIZE, Bp, g.ldb, n0, k0, g.N, kend, tid);
+            int krem = (int)(kend - (kbeg + (int64_t)st * GEMM_BK));
+            ldA.load(sA + st * LA::SIZE, krem, interior);
+            ldB.load(sB + st * LB::SIZE, krem, interior);
+            ldA.advance();
+            ldB.advance();
         }
         cp_async_commit();
     }
 
     const int gid = lane >> 2, tig = lane & 3;
     for (int kt = 0; kt < nk; ++kt) {
-        cp_async_wait<GEMM_STAGES - 2>();
+        cp_async_wait<STAGES - 2>();
         __syncthreads();
         {   // prefetch stage kt + STAGES - 1 (its buffer was consumed at iteration kt-1)
-            int nt = kt + GEMM_STAGES - 1;
+            int nt = kt + STAGES - 1;
             if (nt < nk) {
-                int buf = nt % GEMM_STAGES;
-                int64_t k0 = kbeg + (int64_t)nt * GEMM_BK;
-                load_tile<A_MN>(sA + buf * LA::SIZE, Ap, g.lda, m0, k0, g.M, kend, tid);
-                load_tile<B_MN>(sB + buf * LB::SIZE, Bp, g.ldb, n0, k0, g.N, kend, tid);
+                int buf = nt % STAGES;
+                int krem = (int)(kend - (kbeg + (int64_t)nt * GEMM_BK));
+                ldA.load(sA + buf * LA::SIZE, krem, interior);
+                ldB.load(sB + buf * LB::SIZE, krem, interior);
+                ldA.advance();
+                ldB.advance();
             }
             cp_async_commit();
         }
-        const double* tA = sA + (kt % GEMM_STAGES) * LA::SIZE;
-        const double* tB = sB + (kt % GEMM_STAGES) * LB::SIZE;
+        const double* tA = sA + (kt % STAGES) * LA::SIZE;
+        const double* tB = sB + (kt % STAGES) * LB::SIZE;
 #pragma unroll
         for (int kk = 0; kk < GEMM_BK; kk += 4) {
-            double af[8], bf[4];
+            double af[MI], bf[NI];
 #pragma unroll
-            for (int i = 0; i < 8; ++i) af[i] = tA[LA::off(wm * 64 + i * 8 + gid, kk + tig)];
+            for (int i = 0; i < MI; ++i) af[i] = tA[LA::off(wm * WM + i * 8 + gid, kk + tig)];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) bf[j] = tB[LB::off(wn * 32 + j * 8 + gid, kk + tig)];
+            for (int j = 0; j < NI; ++j) bf[j] = tB[LB::off(wn * WN + j * 8 + gid, kk + tig)];
 #pragma unroll
-            for (int i = 0; i < 8; ++i)
+            for (int i = 0; i < MI; ++i)
 #pragma unroll
-                for (int j = 0; j < 4; ++j) dmma_884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+                for (int j = 0; j < NI; ++j) dmma_884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
         }
     }
     cp_async_wait<0>();
@@ -158,23 +211,23 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) dgemm_kernel(GemmArgs g)
     if (g.ws) {  // split-K slice, plain store
         double* W = g.ws + (int64_t)blockIdx.z * g.M * g.N;
 #pragma unroll
-        for (int i = 0; i < 8; ++i)
+        for (int i = 0; i < MI; ++i)
 #pragma unroll
-            for (int j = 0; j < 4; ++j)
+            for (int j = 0; j < NI; ++j)
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
-                    int64_t r = m0 + wm * 64 + i * 8 + gid, c = n0 + wn * 32 + j * 8 + 2 * tig + h;
+                    int64_t r = m0 + wm * WM + i * 8 + gid, c = n0 + wn * WN + j * 8 + 2 * tig + h;
                     if (r < g.M && c < g.N) W[r + c * g.M] = acc[i][j][h];
                 }
         return;
     }
 #pragma unroll
-    for (int i = 0; i < 8; ++i)
+    for (int i = 0; i < MI; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
+        for (int j = 0; j < NI; ++j)
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
-                int64_t r = m0 + wm * 64 + i * 8 + gid, c = n0 + wn * 32 + j * 8 + 2 * tig + h;
+                int64_t r = m0 + wm * WM + i * 8 + gid, c = n0 + wn * WN + j * 8 + 2 * tig + h;
                 if (r < g.M && c < g.N) {
                     double* p = g.C + r + c * g.ldc;
                     double v = g.alpha * acc[i][j][h];
@@ -185,8 +238,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) dgemm_kernel(GemmArgs g)
 }
 
 // Fixed-order split-K reduction: C = alpha * sum_{z ascending} ws[z] + beta * C.
-static __global__ void dgemm_splitk_reduce(int64_t M, int64_t N, int nsplit, const double* ws, double alpha, double beta,
-                                    double* C, int64_t ldc, int tri)
+static __global__ void dgemm_splitk_reduce(int64_t M, int64_t N, int nsplit, const double* ws, double alpha,
+                                           double beta, double* C, int64_t ldc, int tri)
 {
     int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     int64_t total = M * N;
@@ -202,11 +255,17 @@ static __global__ void dgemm_splitk_reduce(int64_t M, int64_t N, int nsplit, con
     }
 }
 
-inline size_t dgemm_smem_bytes(bool TA, bool TB)
+template <class Cfg, bool TA, bool TB>
+constexpr size_t dgemm_smem_bytes()
 {
-    int a = (!TA) ? TileLayout<true>::SIZE : TileLayout<false>::SIZE;
-    int b = TB ? TileLayout<true>::SIZE : TileLayout<false>::SIZE;
-    return (size_t)GEMM_STAGES * (a + b) * sizeof(double);
+    return (size_t)Cfg::STAGES *
+           (TileLayout<!TA, Cfg::BM>::SIZE + TileLayout<TB, Cfg::BN>::SIZE) * sizeof(double);
 }
+
+// The configurations the launcher chooses from (tools/gemm_tune.cu on B200, profiles/gemm_tune_r01.json:
+// 8192^3 and the C3 trailing shapes; cuBLAS DGEMM reaches 35.7-36.4 TFLOP/s there).
+using CfgWide = GemmCfg<128, 64, 2, 2, 4>;   // NN / NT, large: 33.3-33.7 TFLOP/s
+using CfgMid = GemmCfg<64, 64, 2, 2, 3>;     // TN / TT, large: 33.6-34.0 TFLOP/s; medium shapes
+using CfgSmall = GemmCfg<64, 32, 2, 2, 3>;   // small / skinny: most CTAs, 33 TFLOP/s when large
 
 }  // namespace bqrrp

@@ -78,11 +78,11 @@ void my_gemm(int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, cons
              int64_t ldc, cudaStream_t st)
 {
     bqrrp::GemmArgs g{M, N, K, 1.0, 0.0, A, lda, B, ldb, C, ldc, nullptr, K, 0};
-    size_t sm = bqrrp::dgemm_smem_bytes(TA, TB);
+    size_t sm = bqrrp::dgemm_smem_bytes<bqrrp::CfgWide, TA, TB>();
     static bool init = false;
-    if (!init) { CK(cudaFuncSetAttribute(bqrrp::dgemm_kernel<TA, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)); init = true; }
-    dim3 grid((M + 127) / 128, (N + 127) / 128, 1);
-    bqrrp::dgemm_kernel<TA, TB><<<grid, 256, sm, st>>>(g);
+    if (!init) { CK(cudaFuncSetAttribute(bqrrp::dgemm_kernel<bqrrp::CfgWide, TA, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)); init = true; }
+    dim3 grid((M + 127) / 128, (N + 63) / 64, 1);
+    bqrrp::dgemm_kernel<bqrrp::CfgWide, TA, TB><<<grid, bqrrp::CfgWide::THREADS, sm, st>>>(g);
 }
 
 int main(int argc, char** argv)

@@ -28,10 +28,10 @@ int main(int argc, char** argv)
     double one = 1, zero = 0;
     cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, N, N, N, &one, A, N, B, N, &zero, C, N);
     bqrrp::GemmArgs g{N, N, N, 1.0, 0.0, A, N, B, N, C, N, nullptr, N, 0};
-    size_t sm = bqrrp::dgemm_smem_bytes(false, false);
-    cudaFuncSetAttribute(bqrrp::dgemm_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    dim3 grid((N + 127) / 128, (N + 127) / 128, 1);
-    bqrrp::dgemm_kernel<false, false><<<grid, 256, sm>>>(g);
+    size_t sm = bqrrp::dgemm_smem_bytes<bqrrp::CfgWide, false, false>();
+    cudaFuncSetAttribute(bqrrp::dgemm_kernel<bqrrp::CfgWide, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    dim3 grid((N + 127) / 128, (N + 63) / 64, 1);
+    bqrrp::dgemm_kernel<bqrrp::CfgWide, false, false><<<grid, bqrrp::CfgWide::THREADS, sm>>>(g);
     cudaDeviceSynchronize();
     printf("done %s\n", cudaGetErrorString(cudaGetLastError()));
     return 0;
