@@ -9,7 +9,8 @@
  *   - Matrices are column-major fp64 with a leading dimension; "device" pointers are CUDA device
  *     memory of the current device, "host" pointers are ordinary (preferably pinned) host memory.
  *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).  Work is enqueued on
- *     it; device outputs are valid after the stream is synchronised.  bqrrp_factor* additionally
+ *     it (bqrrp_factor* fans out internally to a high-priority critical stream and a low-priority bulk
+ *     stream, both joined back to `stream`); device outputs are valid after the stream is synchronised.  bqrrp_factor* additionally
  *     synchronises the stream once per block iteration to read the block rank k (P:490 step
  *     bqrrp:rank_est decides the loop), so *rank is known on return.
  *   - Return value: 0 = success; -i = the i-th argument is illegal (LAPACK info convention; checked
@@ -44,8 +45,10 @@ typedef struct bqrrp_options {
     int cholqr_passes;
     /* reserved (0) */
     int reserved0;
-    /* optional host float[8] out: per-phase milliseconds in the order of SPEC's profile keys
-     * {qrcp_wide, tri_rank, col_perm, qr_tall, apply_trans_q, sample_update, other, total};
+    /* optional host float[9] out: per-phase milliseconds in the order of SPEC's profile keys
+     * {qrcp_wide, tri_rank, col_perm, qr_tall, apply_trans_q, sample_update, other, total} (a sequential
+     * partition of the critical stream's timeline) followed by apply_trans_q_bulk, the duration of the
+     * bulk trailing-update GEMM that runs concurrently on the low-priority stream;
      * NULL = no timing (timing adds one event pair per phase). */
     float* phase_ms;
 } bqrrp_options;

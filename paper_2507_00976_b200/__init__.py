@@ -17,7 +17,8 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(_HERE, "libbqrrp.so")
 _lib = None
 
-PHASES = ("qrcp_wide", "tri_rank", "col_perm", "qr_tall", "apply_trans_q", "sample_update", "other", "total")
+PHASES = ("qrcp_wide", "tri_rank", "col_perm", "qr_tall", "apply_trans_q", "sample_update", "other", "total",
+          "apply_trans_q_bulk")
 
 
 class BqrrpError(RuntimeError):
@@ -130,7 +131,7 @@ def factor(A, b: int, d: int | None = None, seed: int = 0, rank_tol: float | Non
     if workspace is not None:
         ws_ptr, ws_bytes = ctypes.c_void_p(workspace.data_ptr()), workspace.numel() * workspace.element_size()
     rank = ctypes.c_int64(0)
-    phases = (ctypes.c_float * 8)() if phase_times else None
+    phases = (ctypes.c_float * len(PHASES))() if phase_times else None
     opts = _options(rank_tol, cholqr_passes, phases)
     st = lib().bqrrp_factor_ex(m, n, ctypes.c_void_p(A.data_ptr()), lda, b, d, seed, ctypes.c_void_p(tau.data_ptr()),
                                ctypes.c_void_p(J.data_ptr()), ctypes.byref(rank), ws_ptr, ws_bytes,

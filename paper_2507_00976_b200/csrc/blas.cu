@@ -77,7 +77,9 @@ void gemm(Ctx& cx, bool ta, bool tb, int64_t M, int64_t N, int64_t K, double alp
     };
     int cfg;  // 0 wide (128x64), 1 mid (64x64), 2 small (64x32)
     int bm, bn;
-    if (!ta && ntiles(CfgWide::BM, CfgWide::BN) >= 2 * cx.num_sms) { cfg = 0; bm = CfgWide::BM; bn = CfgWide::BN; }
+    // (the 128x64 tile loses its edge when C must be read: beta != 0 -> 64x32, profiles/gemm_tune_r01b.json)
+    if (!ta && beta == 0.0 && ntiles(CfgWide::BM, CfgWide::BN) >= 2 * cx.num_sms) { cfg = 0; bm = CfgWide::BM; bn = CfgWide::BN; }
+    else if (!ta && beta != 0.0 && ntiles(CfgSmall::BM, CfgSmall::BN) >= 2 * cx.num_sms) { cfg = 2; bm = CfgSmall::BM; bn = CfgSmall::BN; }
     else if (ta && ntiles(CfgMid::BM, CfgMid::BN) >= 2 * cx.num_sms) { cfg = 1; bm = CfgMid::BM; bn = CfgMid::BN; }
     else if (N > 32 && ntiles(CfgMid::BM, CfgMid::BN) >= cx.num_sms) { cfg = 1; bm = CfgMid::BM; bn = CfgMid::BN; }
     else { cfg = 2; bm = CfgSmall::BM; bn = CfgSmall::BN; }

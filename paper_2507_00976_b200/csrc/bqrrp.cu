@@ -111,13 +111,14 @@ static Layout layout(int64_t m, int64_t n, int64_t b, int64_t d)
     P += r((size_t)2 * d * d);             // row scratch
     P += r((size_t)2 * d) * 3;             // vec tmp (int64), tq, tsrc
     P += r((size_t)d) + r(8) + r((size_t)n);  // ipiv, nt, perm
-    P += r(bb * bb) * 2;                   // Rsk11, X
+    P += r(bb * bb) * 3;                   // Rsk11, X, T
+    P += r((size_t)m * bb) + r(bb * (size_t)n) * 2;  // V, W, W2
     P += r(8) * 2;                         // ref, flags
     // temporaries: sketch QR vs panel (never live together)
     size_t p = (size_t)d;
     size_t sq = r(p * p) * 7 + r(p) + r(2 * 160 * 33 + 160 * 32 * 32) + r(64) + r((size_t)n * p);
     size_t lu = r(2 * 160 * 34) + r(64);
-    size_t pn = r((size_t)m * bb) + r(bb * bb) * 8 + r(bb) + r(bb * (size_t)n) * 2;
+    size_t pn = r(bb * bb) * 8 + r(bb);
     size_t T = sq > pn ? sq : pn;
     T = T > lu ? T : lu;
     size_t sk = r((size_t)16 * (p > bb ? p * p : bb * bb) + (size_t)4 * 1024 * 1024);
@@ -141,8 +142,9 @@ static int validate(int64_t m, int64_t n, const void* A, int64_t lda, int64_t b,
 }
 
 // ----------------------------------------------------------------------------------- the driver
-static int64_t factor_impl(Ctx& cx, int64_t m, int64_t n, double* A, int64_t lda, int64_t b, int64_t d, uint64_t seed,
-                           double* tau, int64_t* J, double rank_tol, int passes, int* host_flags)
+static int64_t factor_impl(Ctx& cx, Ctx* cxb, cudaEvent_t ev_top, cudaEvent_t ev_bulk, int64_t m, int64_t n, double* A,
+                           int64_t lda, int64_t b, int64_t d, uint64_t seed, double* tau, int64_t* J, double rank_tol,
+                           int passes, int* host_flags)
 {
     const int64_t mn = imin(m, n);
     double* MskT = cx.alloc((size_t)n * d);
@@ -160,6 +162,12 @@ static int64_t factor_impl(Ctx& cx, int64_t m, int64_t n, double* A, int64_t lda
     double* Rsk11 = cx.alloc((size_t)bb * bb);
     double* X = cx.alloc((size_t)bb * bb);
     double* ref = cx.alloc(1);
+    // panel outputs and WY scratch stay alive across the overlap of the bulk GEMM with the next a2
+    double* Vp = cx.alloc((size_t)m * bb);
+    double* Tp = cx.alloc((size_t)bb * bb);
+    double* W = cx.alloc((size_t)bb * n);
+    double* W2 = cx.alloc((size_t)bb * n);
+    bool bulk_pending = false;
 
     cx.mark(PH_OTHER);
     init_j_kernel<<<(unsigned)imin(cdiv(n, 256), 1024), 256, 0, cx.stream>>>(n, J);
@@ -188,8 +196,12 @@ static int64_t factor_impl(Ctx& cx, int64_t m, int64_t n, double* A, int64_t lda
         cx.mark(PH_TRI_RANK);
         tri_rank_kernel<<<1, 1024, 0, cx.stream>>>(MskT + s, n, kmax, i == 0, rank_tol, ref, cx.flags);
         BQ_LAUNCH_CHECK();
-        // ---- a3: column permutation of A (all m rows) and J
+        // ---- a3: column permutation of A (all m rows) and J (after the previous bulk update landed)
         cx.mark(PH_COL_PERM);
+        if (bulk_pending) {
+            BQ_CUDA(cudaStreamWaitEvent(cx.stream, ev_bulk, 0));
+            bulk_pending = false;
+        }
         permute_columns(cx, m, A + s * lda, lda, T, colscr);
         permute_vector(cx, J + s, T, vtmp);
         zero_col_kernel<<<(unsigned)imin(cdiv(h, 256), 64), 256, 0, cx.stream>>>(h, A + s + s * lda, cx.flags);
@@ -204,10 +216,13 @@ static int64_t factor_impl(Ctx& cx, int64_t m, int64_t n, double* A, int64_t lda
         extract_rsk11_kernel<<<(unsigned)imin(cdiv(k * k, 256), 4 * cx.num_sms), 256, 0, cx.stream>>>(k, MskT + s, n,
                                                                                                         Rsk11);
         BQ_LAUNCH_CHECK();
-        PanelOut po;
-        panel_and_update(cx, m, n, A, lda, s, k, Rsk11, tau, passes, po);
-        // ---- a7: termination
-        if (k < kmax || c == n || r == m) { ell = s + k; break; }
+        panel_factor(cx, m, A, lda, s, k, Rsk11, tau, passes, Vp, Tp);
+        // ---- a5 (the bulk rows overlap the sketch update and the next a2) and a7
+        cx.mark(PH_APPLY_QT);
+        const bool terminal = (k < kmax || c == n || r == m);
+        wy_update(cx, terminal ? nullptr : cxb, m, n, A, lda, s, k, Vp, Tp, W, W2, ev_top, ev_bulk);
+        if (!terminal && cxb && h > k && n - s - k > 0) bulk_pending = true;
+        if (terminal) { ell = s + k; break; }
         // ---- a6: sketch update (k == b here)
         cx.mark(PH_SAMPLE_UPDATE);
         copy_matrix(cx, b, b, Rsk11, k, X, b);
@@ -217,6 +232,7 @@ static int64_t factor_impl(Ctx& cx, int64_t m, int64_t n, double* A, int64_t lda
     }
     // O4: tau(ell:) = 0, A(ell:m, ell:n) = 0 (reading Z16)
     cx.mark(PH_OTHER);
+    if (bulk_pending) BQ_CUDA(cudaStreamWaitEvent(cx.stream, ev_bulk, 0));
     if (ell < mn) BQ_CUDA(cudaMemsetAsync(tau + ell, 0, sizeof(double) * (mn - ell), cx.stream));
     set_zero(cx, m - ell, n - ell, A + ell + ell * lda, lda);
     cx.mark(PH_OTHER);
@@ -316,22 +332,59 @@ int bqrrp_factor_ex(int64_t m, int64_t n, double* A, int64_t lda, int64_t b, int
             return -11;
         }
         carve(cx, ws, ws_bytes, L);
+        // critical chain on a high-priority stream, the bulk trailing GEMM on a low-priority one;
+        // both joined to the caller's stream at entry and exit
+        int prio_lo = 0, prio_hi = 0;
+        BQ_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+        cudaStream_t user = cx.stream, s_hi = nullptr, s_lo = nullptr;
+        cudaEvent_t ev_in = nullptr, ev_top = nullptr, ev_bulk = nullptr, ev_hi_done = nullptr;
+        BQ_CUDA(cudaStreamCreateWithPriority(&s_hi, cudaStreamNonBlocking, prio_hi));
+        BQ_CUDA(cudaStreamCreateWithPriority(&s_lo, cudaStreamNonBlocking, prio_lo));
+        BQ_CUDA(cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming));
+        BQ_CUDA(cudaEventCreateWithFlags(&ev_top, cudaEventDisableTiming));
+        BQ_CUDA(cudaEventCreateWithFlags(&ev_bulk, cudaEventDisableTiming));
+        BQ_CUDA(cudaEventCreateWithFlags(&ev_hi_done, cudaEventDisableTiming));
+        BQ_CUDA(cudaEventRecord(ev_in, user));
+        BQ_CUDA(cudaStreamWaitEvent(s_hi, ev_in, 0));
+        BQ_CUDA(cudaStreamWaitEvent(s_lo, ev_in, 0));
+        cx.stream = s_hi;
+        Ctx cxb = cx;
+        cxb.stream = s_lo;
+        cxb.splitk = nullptr;  // the split-K scratch belongs to the critical stream
+        cxb.splitk_elems = 0;
         Timer tm;
         if (opts && opts->phase_ms) {
             tm.on = true;
-            tm.st = cx.stream;
+            tm.st = s_hi;
             cx.timer = &tm;
+            cxb.timer = &tm;
         }
         int64_t ell = -1;
         int status = 0;
+        auto cleanup = [&]() {
+            cudaEventRecord(ev_hi_done, s_hi);
+            cudaStreamWaitEvent(user, ev_hi_done, 0);
+            cudaEventRecord(ev_bulk, s_lo);
+            cudaStreamWaitEvent(user, ev_bulk, 0);
+            cudaStreamDestroy(s_hi);
+            cudaStreamDestroy(s_lo);
+            cudaEventDestroy(ev_in);
+            cudaEventDestroy(ev_top);
+            cudaEventDestroy(ev_bulk);
+            cudaEventDestroy(ev_hi_done);
+            cx.stream = user;
+        };
         try {
-            ell = factor_impl(cx, m, n, A, lda, b, d, seed, tau, J, rank_tol, passes, pinned_flags());
+            ell = factor_impl(cx, &cxb, ev_top, ev_bulk, m, n, A, lda, b, d, seed, tau, J, rank_tol, passes,
+                              pinned_flags());
         } catch (...) {
-            if (own) cudaFreeAsync(ws, cx.stream);
+            cleanup();
+            if (own) cudaFreeAsync(ws, user);
             throw;
         }
+        cleanup();
         if (opts && opts->phase_ms) tm.finish(opts->phase_ms);
-        if (own) BQ_CUDA(cudaFreeAsync(ws, cx.stream));
+        if (own) BQ_CUDA(cudaFreeAsync(ws, user));
         if (ell < 0) {
             g_last_error = "non-finite sketch or Cholesky-QR breakdown";
             status = BQRRP_ENUMERIC;
@@ -548,8 +601,12 @@ int bqrrp_debug_panel(int64_t h, int64_t k, int64_t t, double* P, int64_t ld, co
         Layout Ly{0, 0, (size_t)16 * k * k * 8 + (4u << 20), 0};
         carve(cx, ws, wsb, Ly);
         BQ_CUDA(cudaMemsetAsync(cx.flags, 0, sizeof(int) * F_NFLAGS, cx.stream));
-        PanelOut po;
-        panel_and_update(cx, h, k + t, P, ld, 0, k, Rsk11, tau, cholqr_passes, po);
+        double* V = cx.alloc((size_t)h * k);
+        double* Tb = cx.alloc((size_t)k * k);
+        double* W = cx.alloc((size_t)k * (t + 1));
+        double* W2 = cx.alloc((size_t)k * (t + 1));
+        panel_factor(cx, h, P, ld, 0, k, Rsk11, tau, cholqr_passes, V, Tb);
+        wy_update(cx, nullptr, h, k + t, P, ld, 0, k, V, Tb, W, W2, nullptr, nullptr);
         int* hf = pinned_flags();
         BQ_CUDA(cudaMemcpyAsync(hf, cx.flags, sizeof(int) * F_NFLAGS, cudaMemcpyDeviceToHost, cx.stream));
         cudaFreeAsync(ws, cx.stream);

@@ -31,14 +31,14 @@ void permute_columns(Ctx& cx, int64_t rows, double* X, int64_t ldx, const Touche
 void permute_rows(Ctx& cx, int64_t cols, double* X, int64_t ldx, const Touched& T, double* scratch);
 void permute_vector(Ctx& cx, int64_t* J, const Touched& T, int64_t* tmp);
 
-// a4 + a5: preconditioned CholQR2 + Householder reconstruction of the panel A(s:m, s:s+k), the
-// compact-WY update of A(s:m, s+k:n) and the in-place GEQP3-format write of V, R11, tau.
-// Rsk11: k x k upper (ld k).  Returns nothing; failures are flagged in cx.flags.
-struct PanelOut {
-    double* T;   // k x k (ld k) compact-WY T (upper)
-    double* V;   // h x k explicit reflectors (ld h)
-};
-void panel_and_update(Ctx& cx, int64_t m, int64_t n, double* A, int64_t lda, int64_t s, int64_t k, const double* Rsk11,
-                      double* tau, int cholqr_passes, PanelOut& out);
+// a4: preconditioned CholQR(passes) + Householder reconstruction of the panel A(s:m, s:s+k) written in
+// GEQP3 format in place (R11 on/above, V below, tau(s:s+k)); V (h x k, ld h, explicit: unit diagonal,
+// zeros above) and the compact-WY T (k x k, ld k) are returned in caller-owned buffers.
+void panel_factor(Ctx& cx, int64_t m, double* A, int64_t lda, int64_t s, int64_t k, const double* Rsk11, double* tau,
+                  int passes, double* V, double* T);
+// a5: C = A(s:m, s+k:n) <- C - V T^T (V^T C).  With cx_bulk, rows k:h of the last GEMM run on
+// cx_bulk->stream after ev_top (recorded on cx.stream), and ev_bulk marks their completion.
+void wy_update(Ctx& cx, Ctx* cx_bulk, int64_t m, int64_t n, double* A, int64_t lda, int64_t s, int64_t k,
+               const double* V, const double* T, double* W, double* W2, cudaEvent_t ev_top, cudaEvent_t ev_bulk);
 
 }  // namespace bqrrp

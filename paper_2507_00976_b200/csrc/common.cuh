@@ -45,11 +45,31 @@ struct Mat {
 };
 
 // Optional per-phase timer: mark(p) closes the running phase and opens phase p.
-enum Phase { PH_QRCP_WIDE = 0, PH_TRI_RANK, PH_COL_PERM, PH_QR_TALL, PH_APPLY_QT, PH_SAMPLE_UPDATE, PH_OTHER, PH_TOTAL };
+enum Phase {
+    PH_QRCP_WIDE = 0, PH_TRI_RANK, PH_COL_PERM, PH_QR_TALL, PH_APPLY_QT, PH_SAMPLE_UPDATE, PH_OTHER, PH_TOTAL,
+    PH_APPLY_QT_BULK,  // the overlapped bulk GEMM of a5 (its own stream), not part of the sequential sum
+    PH_COUNT
+};
 struct Timer {
     bool on = false;
     cudaStream_t st = 0;
     std::vector<std::pair<int, cudaEvent_t>> ev;
+    struct Interval { int phase; cudaEvent_t a, b; };
+    std::vector<Interval> iv;
+    void begin_interval(cudaStream_t s, int phase)
+    {
+        if (!on) return;
+        Interval x{phase, nullptr, nullptr};
+        cudaEventCreate(&x.a);
+        cudaEventCreate(&x.b);
+        cudaEventRecord(x.a, s);
+        iv.push_back(x);
+    }
+    void end_interval(cudaStream_t s)
+    {
+        if (!on || iv.empty()) return;
+        cudaEventRecord(iv.back().b, s);
+    }
     void mark(int phase)
     {
         if (!on) return;
@@ -61,7 +81,7 @@ struct Timer {
     void finish(float* out)
     {
         if (!on) return;
-        for (int i = 0; i < 8; ++i) out[i] = 0.f;
+        for (int i = 0; i < PH_COUNT; ++i) out[i] = 0.f;
         if (!ev.empty()) {
             cudaEventSynchronize(ev.back().second);
             for (size_t i = 0; i + 1 < ev.size(); ++i) {
@@ -73,6 +93,15 @@ struct Timer {
             cudaEventElapsedTime(&tot, ev.front().second, ev.back().second);
             out[PH_TOTAL] = tot;
         }
+        for (auto& x : iv) {
+            float ms = 0.f;
+            cudaEventSynchronize(x.b);
+            cudaEventElapsedTime(&ms, x.a, x.b);
+            out[x.phase] += ms;
+            cudaEventDestroy(x.a);
+            cudaEventDestroy(x.b);
+        }
+        iv.clear();
         for (auto& p : ev) cudaEventDestroy(p.second);
         ev.clear();
     }

@@ -49,16 +49,15 @@ __global__ void write_panel_kernel(int64_t h, int64_t k, double* Q, int64_t ldq,
     }
 }
 
-void panel_and_update(Ctx& cx, int64_t m, int64_t n, double* A, int64_t lda, int64_t s, int64_t k, const double* Rsk11,
-                      double* tau, int passes, PanelOut& out)
+void panel_factor(Ctx& cx, int64_t m, double* A, int64_t lda, int64_t s, int64_t k, const double* Rsk11, double* tau,
+                  int passes, double* V, double* T)
 {
     const int64_t h = m - s;
     size_t mark = cx.ws_used;
-    double* Q = cx.alloc((size_t)h * k);
+    double* Q = V;  // h x k (ld h): M_pre -> Q_chol -> reconstruction L -> explicit V
     double* Cf[4];
     for (int p = 0; p < passes; ++p) Cf[p] = cx.alloc((size_t)k * k);
     double* S = cx.alloc((size_t)k);
-    double* T = cx.alloc((size_t)k * k);
     double* Wr = cx.alloc((size_t)k * k);
     double* Wr2 = cx.alloc((size_t)k * k);
     double* Ap = A + s + s * lda;
@@ -90,20 +89,30 @@ void panel_and_update(Ctx& cx, int64_t m, int64_t n, double* A, int64_t lda, int
     }
     write_panel_kernel<<<eb, 256, 0, cx.stream>>>(h, k, Q, h, Wr, S, Ap, lda);
     BQ_LAUNCH_CHECK();
-    // compact-WY trailing update of A(s:m, s+k:n)
-    cx.mark(PH_APPLY_QT);
-    const int64_t t = n - s - k;
-    if (t > 0) {
-        double* W = cx.alloc((size_t)k * t);
-        double* W2 = cx.alloc((size_t)k * t);
-        double* C = A + s + (s + k) * lda;
-        gemm(cx, true, false, k, t, h, 1.0, Q, h, C, lda, 0.0, W, k);    // W  = V^T C
-        gemm(cx, true, false, k, t, k, 1.0, T, k, W, k, 0.0, W2, k);     // W2 = T^T W
-        gemm(cx, false, false, h, t, k, -1.0, Q, h, W2, k, 1.0, C, lda);  // C -= V W2
-    }
-    out.T = T;
-    out.V = Q;
     cx.ws_used = mark;
+}
+
+void wy_update(Ctx& cx, Ctx* cx_bulk, int64_t m, int64_t n, double* A, int64_t lda, int64_t s, int64_t k,
+               const double* V, const double* T, double* W, double* W2, cudaEvent_t ev_top, cudaEvent_t ev_bulk)
+{
+    const int64_t h = m - s, t = n - s - k;
+    if (t <= 0) return;
+    double* C = A + s + (s + k) * lda;
+    gemm(cx, true, false, k, t, h, 1.0, V, h, C, lda, 0.0, W, k);   // W  = V^T C
+    gemm(cx, true, false, k, t, k, 1.0, T, k, W, k, 0.0, W2, k);    // W2 = T^T W
+    if (!cx_bulk || h <= k) {
+        gemm(cx, false, false, h, t, k, -1.0, V, h, W2, k, 1.0, C, lda);  // C -= V W2
+        return;
+    }
+    // rows 0:k (R12, needed next by the sketch update) on the critical stream; rows k:h (the bulk,
+    // needed only by the next column permutation) on the bulk stream
+    gemm(cx, false, false, k, t, k, -1.0, V, h, W2, k, 1.0, C, lda);
+    BQ_CUDA(cudaEventRecord(ev_top, cx.stream));
+    BQ_CUDA(cudaStreamWaitEvent(cx_bulk->stream, ev_top, 0));
+    if (cx_bulk->timer) cx_bulk->timer->begin_interval(cx_bulk->stream, PH_APPLY_QT_BULK);
+    gemm(*cx_bulk, false, false, h - k, t, k, -1.0, V + k, h, W2, k, 1.0, C + k, lda);
+    if (cx_bulk->timer) cx_bulk->timer->end_interval(cx_bulk->stream);
+    BQ_CUDA(cudaEventRecord(ev_bulk, cx_bulk->stream));
 }
 
 }  // namespace bqrrp

@@ -35,9 +35,9 @@ __global__ void maxdiff(const double* a, const double* b, size_t n, double* out)
 
 template <class Cfg, bool TA, bool TB>
 float run(int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, const double* B, int64_t ldb, double* C,
-          int reps)
+          int reps, double alpha = 1.0, double beta = 0.0)
 {
-    GemmArgs g{M, N, K, 1.0, 0.0, A, lda, B, ldb, C, M, nullptr, K, 0};
+    GemmArgs g{M, N, K, alpha, beta, A, lda, B, ldb, C, M, nullptr, K, 0};
     size_t sm = dgemm_smem_bytes<Cfg, TA, TB>();
     cudaFuncSetAttribute(dgemm_kernel<Cfg, TA, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     dim3 grid((M + Cfg::BM - 1) / Cfg::BM, (N + Cfg::BN - 1) / Cfg::BN, 1);
@@ -59,11 +59,13 @@ float run(int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, const d
 
 int main()
 {
-    struct Shape { int64_t M, N, K; bool ta, tb; const char* name; };
+    struct Shape { int64_t M, N, K; bool ta, tb; const char* name; double alpha = 1.0, beta = 0.0; };
     std::vector<Shape> shapes = {
         {8192, 8192, 8192, false, false, "sq8192_NN"},
         {16384, 16384, 2048, false, false, "trail_GEMM2_NN_K2048"},
         {16384, 15360, 1024, false, false, "c2_GEMM2_NN_K1024"},
+        {16384, 15360, 1024, false, false, "c2_GEMM2_NN_K1024_beta1", -1.0, 1.0},
+        {65536, 4096, 2048, false, false, "c3_GEMM2_slab_beta1", -1.0, 1.0},
         {2048, 16384, 16384, true, false, "trail_GEMM1_TN"},
         {8192, 8192, 8192, true, false, "sq8192_TN"},
         {8192, 8192, 8192, false, true, "sq8192_NT"},
@@ -83,7 +85,7 @@ int main()
     printf("{\n");
     for (auto& s : shapes) {
         int64_t lda = s.ta ? s.K : s.M, ldb = s.tb ? s.N : s.K;
-        double one = 1, zero = 0;
+        double one = s.alpha, zero = s.beta;
         cublasOperation_t oa = s.ta ? CUBLAS_OP_T : CUBLAS_OP_N, ob = s.tb ? CUBLAS_OP_T : CUBLAS_OP_N;
         cublasDgemm(h, oa, ob, s.M, s.N, s.K, &one, A, lda, B, ldb, &zero, Cr, s.M);
         cudaEvent_t e0, e1;
@@ -106,9 +108,10 @@ int main()
             printf(", \"%s\": %.2f, \"%s_err\": %.1e", nm, fl / (ms * 1e-3) / 1e12, nm, e);
         };
 #define RUNV(CFG, NM)                                                                                       \
-    if (!s.ta && !s.tb) report(NM, run<CFG, false, false>(s.M, s.N, s.K, A, lda, B, ldb, C, 5));            \
-    else if (s.ta && !s.tb) report(NM, run<CFG, true, false>(s.M, s.N, s.K, A, lda, B, ldb, C, 5));         \
-    else report(NM, run<CFG, false, true>(s.M, s.N, s.K, A, lda, B, ldb, C, 5));
+    cudaMemset(C, 0, (size_t)s.M * s.N * 8);                                                                        \
+    if (!s.ta && !s.tb) report(NM, run<CFG, false, false>(s.M, s.N, s.K, A, lda, B, ldb, C, 5, s.alpha, s.beta)); \
+    else if (s.ta && !s.tb) report(NM, run<CFG, true, false>(s.M, s.N, s.K, A, lda, B, ldb, C, 5, s.alpha, s.beta)); \
+    else report(NM, run<CFG, false, true>(s.M, s.N, s.K, A, lda, B, ldb, C, 5, s.alpha, s.beta));
         RUNV(CfgWide, "wide128x64");
         RUNV(CfgMid, "mid64x64");
         RUNV(CfgSmall, "small64x32");
