@@ -57,7 +57,7 @@ static void launch_gemm_t(Ctx& cx, const GemmArgs& g, dim3 grid)
 template <class Cfg>
 static void launch_gemm(Ctx& cx, bool ta, bool tb, const GemmArgs& g, int nsplit)
 {
-    dim3 grid((unsigned)cdiv(g.M, Cfg::BM), (unsigned)cdiv(g.N, Cfg::BN), (unsigned)nsplit);
+    dim3 grid((unsigned)(cdiv(g.M, Cfg::BM) * cdiv(g.N, Cfg::BN)), 1, (unsigned)nsplit);
     if (!ta && !tb) launch_gemm_t<Cfg, false, false>(cx, g, grid);
     else if (ta && !tb) launch_gemm_t<Cfg, true, false>(cx, g, grid);
     else if (!ta && tb) launch_gemm_t<Cfg, false, true>(cx, g, grid);
@@ -75,13 +75,11 @@ void gemm(Ctx& cx, bool ta, bool tb, int64_t M, int64_t N, int64_t K, double alp
         int64_t tm = cdiv(M, bm), tn = cdiv(N, bn);
         return tri ? (tm * tn + tm) / 2 : tm * tn;
     };
-    int cfg;  // 0 wide (128x64), 1 mid (64x64), 2 small (64x32)
+    // 64x64 / 3 stages / grouped rasterisation is the best tile on every large shape and operand order
+    // (33.3-34.3 TFLOP/s, profiles/gemm_tune_r01c_raster.json); 64x32 gives more CTAs to small GEMMs.
+    int cfg;  // 1 mid (64x64), 2 small (64x32)
     int bm, bn;
-    // (the 128x64 tile loses its edge when C must be read: beta != 0 -> 64x32, profiles/gemm_tune_r01b.json)
-    if (!ta && beta == 0.0 && ntiles(CfgWide::BM, CfgWide::BN) >= 2 * cx.num_sms) { cfg = 0; bm = CfgWide::BM; bn = CfgWide::BN; }
-    else if (!ta && beta != 0.0 && ntiles(CfgSmall::BM, CfgSmall::BN) >= 2 * cx.num_sms) { cfg = 2; bm = CfgSmall::BM; bn = CfgSmall::BN; }
-    else if (ta && ntiles(CfgMid::BM, CfgMid::BN) >= 2 * cx.num_sms) { cfg = 1; bm = CfgMid::BM; bn = CfgMid::BN; }
-    else if (N > 32 && ntiles(CfgMid::BM, CfgMid::BN) >= cx.num_sms) { cfg = 1; bm = CfgMid::BM; bn = CfgMid::BN; }
+    if (N > 32 && ntiles(CfgMid::BM, CfgMid::BN) >= cx.num_sms) { cfg = 1; bm = CfgMid::BM; bn = CfgMid::BN; }
     else { cfg = 2; bm = CfgSmall::BM; bn = CfgSmall::BN; }
     int64_t tiles = ntiles(bm, bn);
     int nsplit = 1;
@@ -105,8 +103,7 @@ void gemm(Ctx& cx, bool ta, bool tb, int64_t M, int64_t N, int64_t K, double alp
         cudaEventCreate(&rec.e1);
         cudaEventRecord(rec.e0, cx.stream);
     }
-    if (cfg == 0) launch_gemm<CfgWide>(cx, ta, tb, g, nsplit);
-    else if (cfg == 1) launch_gemm<CfgMid>(cx, ta, tb, g, nsplit);
+    if (cfg == 1) launch_gemm<CfgMid>(cx, ta, tb, g, nsplit);
     else launch_gemm<CfgSmall>(cx, ta, tb, g, nsplit);
     if (nsplit > 1) {
         int64_t total = M * N;

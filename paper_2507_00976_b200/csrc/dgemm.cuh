@@ -22,6 +22,7 @@
 namespace bqrrp {
 
 constexpr int GEMM_BK = 16;
+constexpr int GROUP_M = 8;  // tile-rows per rasterisation group
 
 __device__ __forceinline__ void dmma_884(double& c0, double& c1, double a, double b)
 {
@@ -147,7 +148,18 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS) dgemm_kernel(Ge
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int wm = warp % Cfg::WARPS_M, wn = warp / Cfg::WARPS_M;
-    const int64_t m0 = (int64_t)blockIdx.x * BM, n0 = (int64_t)blockIdx.y * BN;
+    // grouped rasterisation of the 1-D tile index (GROUP_M tile-rows per group) for L2 reuse of the
+    // operand tiles among the CTAs resident at the same time
+    int64_t tile_m, tile_n;
+    {
+        const int64_t tiles_m = (g.M + BM - 1) / BM, tiles_n = (g.N + BN - 1) / BN;
+        const int64_t pid = blockIdx.x, in_group = (int64_t)GROUP_M * tiles_n;
+        const int64_t first_m = (pid / in_group) * GROUP_M;
+        const int64_t gsize = (tiles_m - first_m < GROUP_M) ? tiles_m - first_m : GROUP_M;
+        tile_m = first_m + (pid % in_group) % gsize;
+        tile_n = (pid % in_group) / gsize;
+    }
+    const int64_t m0 = tile_m * BM, n0 = tile_n * BN;
     if (g.tri && m0 + BM <= n0) return;  // tile strictly above the diagonal
     const int64_t kbeg = (int64_t)blockIdx.z * g.kchunk;
     const int64_t kend = (kbeg + g.kchunk < g.K) ? kbeg + g.kchunk : g.K;

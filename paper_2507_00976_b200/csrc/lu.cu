@@ -169,9 +169,184 @@ __global__ void __launch_bounds__(LU_THREADS, 1) lu_panel_kernel(LuPanelArgs a)
     }
 }
 
+// ---------------------------------------------------------------------------------------------
+// Cluster variant (panels that fit the shared memory of one <= 16-CTA cluster): the same algorithm with
+// the exchange in distributed shared memory and one barrier.cluster per column instead of a grid
+// barrier through L2.  Records are double-buffered by column parity (see the QR panel for the argument).
+constexpr int LUC_CLMAX = 16;
+constexpr int LUC_REC = 2 + 2 * LU_JBMAX;  // val, idx, candidate row, current row j (owner only)
+
+__global__ void __launch_bounds__(LU_THREADS, 1) lu_panel_cluster_kernel(LuPanelArgs a)
+{
+    cg::cluster_group cluster = cg::this_cluster();
+    const int CL = (int)cluster.num_blocks(), me = (int)cluster.block_rank();
+    extern __shared__ double dyn[];
+    const int R = a.R, jb = a.jb, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    double* sp = dyn;                       // sp[c * R + r]
+    double* rec = dyn + (size_t)R * jb;     // [2][LUC_REC]
+    __shared__ double red_v[LU_THREADS / 32];
+    __shared__ int64_t red_i[LU_THREADS / 32];
+    __shared__ double pivrow[LU_JBMAX], oldrow[LU_JBMAX];
+    __shared__ int64_t s_piv;
+    __shared__ int s_win;
+    const int64_t rbeg = a.c0 + (int64_t)me * R;
+    const int64_t rows_here = (rbeg < a.w) ? ((a.w - rbeg < R) ? a.w - rbeg : R) : 0;
+    const int64_t n_out = a.d - jb;
+    const int64_t gtid = (int64_t)me * LU_THREADS + tid, gstride = (int64_t)CL * LU_THREADS;
+
+    for (int idx = tid; idx < R * jb; idx += LU_THREADS) {
+        int r = idx % R, c = idx / R;
+        sp[idx] = (r < rows_here) ? a.L[rbeg + r + (a.c0 + c) * a.ld] : 0.0;
+    }
+    __syncthreads();
+
+    for (int j = 0; j < jb; ++j) {
+        const int par = j & 1;
+        const int64_t jr = a.c0 + j;
+        const int owner = (int)((jr - a.c0) / R);
+        double bv = -1.0;
+        int64_t bi = INT64_MAX;
+        for (int r = tid; r < rows_here; r += LU_THREADS) {
+            int64_t ar = rbeg + r;
+            if (ar < jr) continue;
+            double v = fabs(sp[j * R + r]);
+            if (v > bv) { bv = v; bi = ar; }
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            double ov = __shfl_down_sync(0xffffffffu, bv, o);
+            int64_t oi = __shfl_down_sync(0xffffffffu, bi, o);
+            if (better(ov, oi, bv, bi)) { bv = ov; bi = oi; }
+        }
+        if (lane == 0) { red_v[warp] = bv; red_i[warp] = bi; }
+        __syncthreads();
+        double* myrec = rec + par * LUC_REC;
+        if (tid == 0) {
+            for (int wv = 1; wv < LU_THREADS / 32; ++wv)
+                if (better(red_v[wv], red_i[wv], bv, bi)) { bv = red_v[wv]; bi = red_i[wv]; }
+            myrec[0] = bv;
+            myrec[1] = __longlong_as_double((long long)bi);
+            s_piv = bi;
+        }
+        __syncthreads();
+        if (tid < jb) {
+            myrec[2 + tid] = (s_piv != INT64_MAX) ? sp[tid * R + (s_piv - rbeg)] : 0.0;
+            if (me == owner) myrec[2 + LU_JBMAX + tid] = sp[tid * R + (jr - rbeg)];
+        }
+        cluster.sync();
+        if (warp == 0) {
+            double v = -1.0;
+            int64_t i = INT64_MAX;
+            int wq = 0;
+            if (lane < CL) {
+                const double* pr = cluster.map_shared_rank(rec + par * LUC_REC, lane);
+                v = pr[0];
+                i = (int64_t)__double_as_longlong(pr[1]);
+                wq = lane;
+            }
+            for (int o = 16; o > 0; o >>= 1) {
+                double ov = __shfl_down_sync(0xffffffffu, v, o);
+                int64_t oi = __shfl_down_sync(0xffffffffu, i, o);
+                int ow = __shfl_down_sync(0xffffffffu, wq, o);
+                if (better(ov, oi, v, i)) { v = ov; i = oi; wq = ow; }
+            }
+            if (lane == 0) {
+                s_piv = i;
+                s_win = wq;
+                if (me == 0) a.ipiv[jr] = (int)i;
+            }
+        }
+        __syncthreads();
+        const int64_t piv = s_piv;
+        if (tid < jb) {
+            pivrow[tid] = cluster.map_shared_rank(rec + par * LUC_REC, s_win)[2 + tid];
+            oldrow[tid] = cluster.map_shared_rank(rec + par * LUC_REC, owner)[2 + LU_JBMAX + tid];
+        }
+        __syncthreads();
+        const double u = pivrow[j];
+        if (u != 0.0) {
+            if (piv != jr) {
+                if (piv >= rbeg && piv < rbeg + rows_here && tid < jb) sp[tid * R + (piv - rbeg)] = oldrow[tid];
+                if (jr >= rbeg && jr < rbeg + rows_here && tid < jb) sp[tid * R + (jr - rbeg)] = pivrow[tid];
+                for (int64_t e = gtid; e < n_out; e += gstride) {
+                    int64_t c = (e < a.c0) ? e : e + jb;
+                    double* pc = a.L + c * a.ld;
+                    double t = pc[jr];
+                    pc[jr] = pc[piv];
+                    pc[piv] = t;
+                }
+                if (gtid == 0) {
+                    int t = a.perm[jr];
+                    a.perm[jr] = a.perm[piv];
+                    a.perm[piv] = t;
+                }
+            }
+            __syncthreads();
+            for (int r = tid; r < rows_here; r += LU_THREADS) {
+                if (rbeg + r <= jr) continue;
+                double l = sp[j * R + r] / u;
+                sp[j * R + r] = l;
+                for (int c = j + 1; c < jb; ++c) sp[c * R + r] = fma(-l, pivrow[c], sp[c * R + r]);
+            }
+        }
+        __syncthreads();
+    }
+    for (int idx = tid; idx < R * jb; idx += LU_THREADS) {
+        int r = idx % R, c = idx / R;
+        if (r < rows_here) a.L[rbeg + r + (a.c0 + c) * a.ld] = sp[idx];
+    }
+    cluster.sync();  // peers may still read this CTA's last records
+}
+
+constexpr size_t LUC_SMEM_MAX = 196 * 1024;
+
+static bool lu_cluster_fits(int64_t rows, int jb, int* CLout, int* Rout)
+{
+    int CL = (int)imin(LUC_CLMAX, imax(1, cdiv(rows, 512)));
+    int R = (int)cdiv(rows, CL);
+    while ((size_t)R * jb * 8 + 2 * LUC_REC * 8 > LUC_SMEM_MAX && CL < LUC_CLMAX) {
+        ++CL;
+        R = (int)cdiv(rows, CL);
+    }
+    if ((size_t)R * jb * 8 + 2 * LUC_REC * 8 > LUC_SMEM_MAX) return false;
+    *CLout = CL;
+    *Rout = R;
+    return true;
+}
+
+static bool lu_panel_cluster(Ctx& cx, double* L, int64_t ld, int64_t w, int64_t d, int64_t c0, int jb, int* ipiv,
+                             int* perm)
+{
+    int CL, R;
+    if (!lu_cluster_fits(w - c0, jb, &CL, &R)) return false;
+    static bool attr = false;
+    if (!attr) {
+        BQ_CUDA(cudaFuncSetAttribute(lu_panel_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)LUC_SMEM_MAX));
+        BQ_CUDA(cudaFuncSetAttribute(lu_panel_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        attr = true;
+    }
+    LuPanelArgs a{L, ld, w, d, c0, jb, R, ipiv, perm, nullptr, nullptr};
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(CL);
+    cfg.blockDim = dim3(LU_THREADS);
+    cfg.dynamicSmemBytes = (size_t)R * jb * 8 + 2 * LUC_REC * 8;
+    cfg.stream = cx.stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = CL;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    BQ_CUDA(cudaLaunchKernelEx(&cfg, lu_panel_cluster_kernel, a));
+    ++g_launches;
+    return true;
+}
+
 static void lu_panel(Ctx& cx, double* L, int64_t ld, int64_t w, int64_t d, int64_t c0, int jb, int* ipiv, int* perm,
                      double* xbuf, double* rowj)
 {
+    if (lu_panel_cluster(cx, L, ld, w, d, c0, jb, ipiv, perm)) return;
     int64_t rows = w - c0;
     // few enough CTAs that the barrier stays cheap, enough that the slab fits shared memory
     int G = (int)imin(cx.num_sms, imax(1, cdiv(rows, 256)));
@@ -195,10 +370,13 @@ static void lu_panel(Ctx& cx, double* L, int64_t ld, int64_t w, int64_t d, int64
 
 static int lu_leaf_width(int64_t rows, int num_sms)
 {
-    // widest leaf whose per-CTA slab fits shared memory
-    int64_t R = cdiv(rows, num_sms);
-    if (R * 32 * 8 <= 200 * 1024) return 32;
-    if (R * 16 * 8 <= 200 * 1024) return 16;
+    // a leaf that one cluster can hold (32, else 16 columns), else the widest the grid kernel can hold
+    int CL, R;
+    if (lu_cluster_fits(rows, 32, &CL, &R)) return 32;
+    if (lu_cluster_fits(rows, 16, &CL, &R)) return 16;
+    int64_t Rg = cdiv(rows, num_sms);
+    if (Rg * 32 * 8 <= 200 * 1024) return 32;
+    if (Rg * 16 * 8 <= 200 * 1024) return 16;
     return 8;
 }
 

@@ -81,7 +81,7 @@ void my_gemm(int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, cons
     size_t sm = bqrrp::dgemm_smem_bytes<bqrrp::CfgWide, TA, TB>();
     static bool init = false;
     if (!init) { CK(cudaFuncSetAttribute(bqrrp::dgemm_kernel<bqrrp::CfgWide, TA, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)); init = true; }
-    dim3 grid((M + 127) / 128, (N + 63) / 64, 1);
+    dim3 grid(((M + 127) / 128) * ((N + 63) / 64), 1, 1);
     bqrrp::dgemm_kernel<bqrrp::CfgWide, TA, TB><<<grid, bqrrp::CfgWide::THREADS, sm, st>>>(g);
 }
 

@@ -40,7 +40,7 @@ float run(int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, const d
     GemmArgs g{M, N, K, alpha, beta, A, lda, B, ldb, C, M, nullptr, K, 0};
     size_t sm = dgemm_smem_bytes<Cfg, TA, TB>();
     cudaFuncSetAttribute(dgemm_kernel<Cfg, TA, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    dim3 grid((M + Cfg::BM - 1) / Cfg::BM, (N + Cfg::BN - 1) / Cfg::BN, 1);
+    dim3 grid(((M + Cfg::BM - 1) / Cfg::BM) * ((N + Cfg::BN - 1) / Cfg::BN), 1, 1);
     dgemm_kernel<Cfg, TA, TB><<<grid, Cfg::THREADS, sm>>>(g);
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0); cudaEventCreate(&e1);
