@@ -130,6 +130,25 @@ class ClockSampler:
         return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
 
 
+# ------------------------------------------------------------------------------------- multi-rank
+def max_over_ranks(value: float, device=None) -> float:
+    """The contract's multi-GPU timing rule: every rank times itself on its device; the job time is the
+    max over ranks (all_reduce MAX).  Works on any backend (NCCL on the GPU box, gloo in the CPU tests)."""
+    import torch
+    import torch.distributed as dist
+
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return float(value)
+    t = torch.tensor([float(value)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def aggregate_value(flops_per_step_per_rank: float, steps: int, world: int, t_ms_max: float) -> float:
+    """Whole-job TFLOP/s: the flops of all ranks over the max-over-ranks device time."""
+    return flops_per_step_per_rank * steps * world / (t_ms_max * 1e-3) / 1e12
+
+
 # ------------------------------------------------------------------------------------- oracle timing
 def oracle_sample(cfg_name: str, seed: int = 0):
     """Time the CPU oracle as it stands on a bounded sample of the workload; returns (TFLOP/s, seconds, desc)."""
@@ -241,13 +260,9 @@ def main():
         dist.barrier()
     launches = bq.launch_count() - launches0
     ranks_found = out[3]
-    t_ms = sum(s.elapsed_time(e) for s, e in ev)
-    t_max = torch.tensor([t_ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
-    t_ms = float(t_max.item())
+    t_ms = max_over_ranks(sum(s.elapsed_time(e) for s, e in ev), dev)
     flops_step = canonical_flops(m, n)
-    value = flops_step * args.steps * world / (t_ms * 1e-3) / 1e12
+    value = aggregate_value(flops_step, args.steps, world, t_ms)
     peak, peak_src = peak_fp64()
 
     # ---- roofline of the dominant kernel: the a5 trailing-update DMMA GEMMs (phase apply_trans_q)
@@ -288,12 +303,10 @@ def main():
             torch.cuda.synchronize()
             if i > 0:
                 tot += e0.elapsed_time(e1)
-        te = torch.tensor([tot / ks], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        e2e = {"value": flops_step * world / (float(te.item()) * 1e-3) / 1e12, "unit": "TFLOP/s",
+        te = max_over_ranks(tot / ks, dev)
+        e2e = {"value": aggregate_value(flops_step, 1, world, te), "unit": "TFLOP/s",
                "h2d_bytes_per_step": m * n * 8, "d2h_bytes_per_step": m * n * 8 + min(m, n) * 8 + n * 8,
-               "ms_per_step": float(te.item()), "api": "bqrrp_factor_host (pinned host buffers)"}
+               "ms_per_step": te, "api": "bqrrp_factor_host (pinned host buffers)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

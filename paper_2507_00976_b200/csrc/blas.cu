@@ -262,41 +262,47 @@ void trsm_left_lower_unit(Ctx& cx, int64_t n, int64_t cols, const double* L, int
 // ------------------------------------------------------------------------------------------- POTRF
 constexpr int FACT_NB = 64;
 
+// One CTA factors a <= 64 x 64 diagonal block, one barrier per column: with the column left unscaled,
+// step j updates A(i, c) -= A(i, j) A(c, j) / A(j, j) for i >= c > j (it reads only column j, final after
+// step j-1); the columns are scaled by 1/sqrt(A(j, j)) at the end.
 __global__ void __launch_bounds__(256) potrf_diag(int n, double* G, int64_t ldg, int j0, int* info)
 {
     __shared__ double A[FACT_NB][FACT_NB + 1];
-    __shared__ int failed;
+    __shared__ int bad;
     for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) {
         int i = idx % n, j = idx / n;
         A[i][j] = (i >= j) ? G[i + (int64_t)j * ldg] : 0.0;
     }
-    if (threadIdx.x == 0) failed = (*info != 0);
+    if (threadIdx.x == 0) bad = -1;
     __syncthreads();
-    for (int j = 0; j < n && !failed; ++j) {
-        if (threadIdx.x == 0) {
-            double a = A[j][j];
-            if (!(a > 0.0)) {
-                failed = 1;
-                atomicCAS(info, 0, j0 + j + 1);
-            } else {
-                A[j][j] = sqrt(a);
-            }
+    if (*info != 0) return;  // an earlier block already broke down
+    for (int j = 0; j < n; ++j) {
+        const double d = A[j][j];
+        if (!(d > 0.0)) {  // uniform: every thread sees the same pivot
+            if (threadIdx.x == 0) bad = j;
+            break;
         }
-        __syncthreads();
-        if (failed) break;
-        double djj = A[j][j];
-        for (int i = j + 1 + threadIdx.x; i < n; i += blockDim.x) A[i][j] = A[i][j] / djj;
-        __syncthreads();
-        int m = n - j - 1;
+        const int m = n - j - 1;
+        const double rd = 1.0 / d;
         for (int idx = threadIdx.x; idx < m * m; idx += blockDim.x) {
             int i = j + 1 + idx % m, c = j + 1 + idx / m;
-            if (c <= i) A[i][c] = fma(-A[i][j], A[c][j], A[i][c]);
+            if (c <= i) A[i][c] = fma(-A[i][j] * rd, A[c][j], A[i][c]);
         }
         __syncthreads();
     }
+    __syncthreads();
+    if (bad >= 0) {
+        if (threadIdx.x == 0) atomicCAS(info, 0, j0 + bad + 1);
+        return;
+    }
     for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) {
         int i = idx % n, j = idx / n;
-        G[i + (int64_t)j * ldg] = (i >= j) ? A[i][j] : 0.0;
+        double v = 0.0;
+        if (i >= j) {
+            double sj = sqrt(A[j][j]);
+            v = (i == j) ? sj : A[i][j] / sj;
+        }
+        G[i + (int64_t)j * ldg] = v;
     }
 }
 
@@ -318,35 +324,40 @@ void potrf_lower(Ctx& cx, int64_t n, double* G, int64_t ldg)
 }
 
 // ------------------------------------------------------------------------------------------- sign LU
+// Sign-choosing no-pivot LU of a <= 64 x 64 block, one barrier per column: at step j every thread reads
+// a = A(j, j) (final), S_j = -sgn(a), pivot p = a - S_j; A(i, c) -= A(i, j) A(j, c) / p for i, c > j.
+// The multipliers L(i, j) = A(i, j) / p_j are formed at the end.
 __global__ void __launch_bounds__(256) getrf_sign_diag(int n, double* Q, int64_t ldq, double* S)
 {
     __shared__ double A[FACT_NB][FACT_NB + 1];
+    __shared__ double piv[FACT_NB];
     for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) {
         int i = idx % n, j = idx / n;
         A[i][j] = Q[i + (int64_t)j * ldq];
     }
     __syncthreads();
     for (int j = 0; j < n; ++j) {
+        const double a = A[j][j];
+        const double sj = (a >= 0.0) ? -1.0 : 1.0;  // S_jj = -sgn(a), sgn(a) = a >= 0 ? +1 : -1 (Z20)
+        const double p = a - sj;
         if (threadIdx.x == 0) {
-            double a = A[j][j];
-            double s = (a >= 0.0) ? -1.0 : 1.0;  // S_jj = -sgn(a), sgn(a) = a >= 0 ? +1 : -1 (Z20)
-            S[j] = s;
-            A[j][j] = a - s;
+            S[j] = sj;
+            piv[j] = p;
         }
-        __syncthreads();
-        double piv = A[j][j];
-        for (int i = j + 1 + threadIdx.x; i < n; i += blockDim.x) A[i][j] = A[i][j] / piv;
-        __syncthreads();
-        int m = n - j - 1;
+        const int m = n - j - 1;
+        const double rp = 1.0 / p;
         for (int idx = threadIdx.x; idx < m * m; idx += blockDim.x) {
             int i = j + 1 + idx % m, c = j + 1 + idx / m;
-            A[i][c] = fma(-A[i][j], A[j][c], A[i][c]);
+            A[i][c] = fma(-A[i][j] * rp, A[j][c], A[i][c]);
         }
         __syncthreads();
     }
     for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) {
         int i = idx % n, j = idx / n;
-        Q[i + (int64_t)j * ldq] = A[i][j];
+        double v = A[i][j];
+        if (i == j) v = piv[j];
+        else if (i > j) v = v / piv[j];
+        Q[i + (int64_t)j * ldq] = v;
     }
 }
 
