@@ -269,11 +269,10 @@ __global__ void __launch_bounds__(256) potrf_diag(int n, double* G, int64_t ldg,
 {
     __shared__ double A[FACT_NB][FACT_NB + 1];
     __shared__ int bad;
-    for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) {
-        int i = idx % n, j = idx / n;
-        A[i][j] = (i >= j) ? G[i + (int64_t)j * ldg] : 0.0;
-    }
+    for (int j = 0; j < n; ++j)
+        for (int r = threadIdx.x; r < n; r += blockDim.x) cp_async8z(&A[r][j], G + r + (int64_t)j * ldg, r >= j);
     if (threadIdx.x == 0) bad = -1;
+    cp_async_wait_all();
     __syncthreads();
     if (*info != 0) return;  // an earlier block already broke down
     for (int j = 0; j < n; ++j) {
@@ -331,10 +330,9 @@ __global__ void __launch_bounds__(256) getrf_sign_diag(int n, double* Q, int64_t
 {
     __shared__ double A[FACT_NB][FACT_NB + 1];
     __shared__ double piv[FACT_NB];
-    for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) {
-        int i = idx % n, j = idx / n;
-        A[i][j] = Q[i + (int64_t)j * ldq];
-    }
+    for (int j = 0; j < n; ++j)
+        for (int r = threadIdx.x; r < n; r += blockDim.x) cp_async8z(&A[r][j], Q + r + (int64_t)j * ldq, true);
+    cp_async_wait_all();
     __syncthreads();
     for (int j = 0; j < n; ++j) {
         const double a = A[j][j];

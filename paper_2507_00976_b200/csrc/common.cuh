@@ -137,4 +137,32 @@ struct Ctx {
 // Device flag slots (int) written by kernels and read back once per iteration.
 enum Flags { F_K = 0, F_ZERO_COL = 1, F_POTRF_INFO = 2, F_NONFINITE = 3, F_NT = 4, F_NFLAGS = 8 };
 
+// ---- device helpers shared by the small kernels -------------------------------------------------
+// 8-byte global -> shared async copy; src-size 0 (zero-fill) when !pred
+__device__ __forceinline__ void cp_async8z(void* smem, const void* gmem, bool pred)
+{
+    unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    int sz = pred ? 8 : 0;
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
+}
+__device__ __forceinline__ void cp_async_wait_all()
+{
+    asm volatile("cp.async.commit_group;\n" ::);
+    asm volatile("cp.async.wait_group 0;\n" ::);
+}
+
+// Column-major slab -> shared, all copies in flight at once: dst[c*ldd + r] = src[r + c*lds] for
+// r < rows_valid, zero for rows_valid <= r < rows_pad; c < cols.  Ends with a block barrier.
+__device__ __forceinline__ void slab_load_async(double* dst, int ldd, const double* src, int64_t lds, int rows_valid,
+                                                int rows_pad, int cols)
+{
+    for (int c = 0; c < cols; ++c)
+        for (int r = threadIdx.x; r < rows_pad; r += blockDim.x) {
+            bool ok = r < rows_valid;
+            cp_async8z(dst + (size_t)c * ldd + r, ok ? (const void*)(src + r + c * lds) : (const void*)src, ok);
+        }
+    cp_async_wait_all();
+    __syncthreads();
+}
+
 }  // namespace bqrrp

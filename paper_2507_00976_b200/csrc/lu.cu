@@ -42,6 +42,60 @@ __device__ __forceinline__ bool better(double v, int64_t i, double bv, int64_t b
     return v > bv || (v == bv && i < bi);
 }
 
+// After a panel: apply its jb interchanges (row c0+j <-> spiv[j], in order) to the columns outside the
+// panel and to perm as ONE gather of the <= 2 jb rows they touch (independent loads, one latency round)
+// instead of jb dependent swaps inside the column loop.  Called by every CTA of the panel kernel with
+// its thread range [gtid, ., gstride) over the outside columns.
+__device__ void apply_panel_interchanges(const LuPanelArgs& a, const int64_t* spiv, int64_t* trow, int64_t* tsrc,
+                                         int* s_nt, int64_t gtid, int64_t gstride)
+{
+    const int jb = a.jb;
+    if (threadIdx.x == 0) {
+        int nt = 0;
+        for (int j = 0; j < jb; ++j) {
+            const int64_t jr = a.c0 + j, p = spiv[j];
+            if (p == jr) continue;
+            int ia = -1, ib = -1;
+            for (int t = 0; t < nt; ++t) {
+                if (trow[t] == jr) ia = t;
+                if (trow[t] == p) ib = t;
+            }
+            if (ia < 0) { trow[nt] = jr; tsrc[nt] = jr; ia = nt++; }
+            if (ib < 0) { trow[nt] = p; tsrc[nt] = p; ib = nt++; }
+            int64_t t = tsrc[ia];
+            tsrc[ia] = tsrc[ib];
+            tsrc[ib] = t;
+        }
+        *s_nt = nt;
+    }
+    __syncthreads();
+    const int nt = *s_nt;
+    if (nt == 0) return;
+    const int64_t n_out = a.d - jb;
+    for (int64_t e = gtid; e < n_out; e += gstride) {
+        const int64_t c = (e < a.c0) ? e : e + jb;
+        double* pc = a.L + c * a.ld;
+        // a gather is only safe if every source is read before any destination is written: the rows
+        // are the same set, so read all of them (16 loads in flight per chunk) before writing
+        double v[2 * LU_JBMAX];
+        for (int t0 = 0; t0 < nt; t0 += 16) {
+#pragma unroll
+            for (int t = 0; t < 16; ++t)
+                if (t0 + t < nt) v[t0 + t] = pc[tsrc[t0 + t]];
+        }
+        for (int t0 = 0; t0 < nt; t0 += 16) {
+#pragma unroll
+            for (int t = 0; t < 16; ++t)
+                if (t0 + t < nt) pc[trow[t0 + t]] = v[t0 + t];
+        }
+    }
+    if (gtid == 0) {
+        int pv[2 * LU_JBMAX];
+        for (int t = 0; t < nt; ++t) pv[t] = a.perm[tsrc[t]];
+        for (int t = 0; t < nt; ++t) a.perm[trow[t]] = pv[t];
+    }
+}
+
 __global__ void __launch_bounds__(LU_THREADS, 1) lu_panel_kernel(LuPanelArgs a)
 {
     cg::grid_group grid = cg::this_grid();
@@ -52,19 +106,16 @@ __global__ void __launch_bounds__(LU_THREADS, 1) lu_panel_kernel(LuPanelArgs a)
     __shared__ double pivrow[LU_JBMAX], oldrow[LU_JBMAX];
     __shared__ int64_t s_piv;
     __shared__ int s_win;
+    __shared__ int64_t spiv[LU_JBMAX], trow[2 * LU_JBMAX], tsrc[2 * LU_JBMAX];
+    __shared__ int s_nt;
 
     const int G = gridDim.x, cta = blockIdx.x, tid = threadIdx.x, R = a.R, jb = a.jb;
     const int lane = tid & 31, warp = tid >> 5;
     const int64_t rbeg = a.c0 + (int64_t)cta * R;  // absolute first row of this CTA
     const int64_t rows_here = (rbeg < a.w) ? ((a.w - rbeg < R) ? a.w - rbeg : R) : 0;
-    const int64_t n_out = a.d - jb;  // columns outside the panel
     const int64_t gtid = (int64_t)cta * LU_THREADS + tid, gstride = (int64_t)G * LU_THREADS;
 
-    for (int idx = tid; idx < R * jb; idx += LU_THREADS) {
-        int r = idx % R, c = idx / R;
-        sp[idx] = (r < rows_here) ? a.L[rbeg + r + (a.c0 + c) * a.ld] : 0.0;
-    }
-    __syncthreads();
+    slab_load_async(sp, R, a.L + rbeg + a.c0 * a.ld, a.ld, (int)rows_here, R, jb);
 
     for (int j = 0; j < jb; ++j) {
         const int par = j & 1;
@@ -135,23 +186,11 @@ __global__ void __launch_bounds__(LU_THREADS, 1) lu_panel_kernel(LuPanelArgs a)
         }
         __syncthreads();
         const double u = pivrow[j];
+        if (tid == 0) spiv[j] = (u != 0.0) ? piv : jr;
         if (u != 0.0) {
             if (piv != jr) {
                 if (piv >= rbeg && piv < rbeg + rows_here && tid < jb) sp[tid * R + (piv - rbeg)] = oldrow[tid];
                 if (jr >= rbeg && jr < rbeg + rows_here && tid < jb) sp[tid * R + (jr - rbeg)] = pivrow[tid];
-                // the same interchange on the rest of the row (columns outside the panel) and on perm
-                for (int64_t e = gtid; e < n_out; e += gstride) {
-                    int64_t c = (e < a.c0) ? e : e + jb;
-                    double* pc = a.L + c * a.ld;
-                    double t = pc[jr];
-                    pc[jr] = pc[piv];
-                    pc[piv] = t;
-                }
-                if (gtid == 0) {
-                    int t = a.perm[jr];
-                    a.perm[jr] = a.perm[piv];
-                    a.perm[piv] = t;
-                }
             }
             __syncthreads();
             for (int r = tid; r < rows_here; r += LU_THREADS) {
@@ -163,10 +202,10 @@ __global__ void __launch_bounds__(LU_THREADS, 1) lu_panel_kernel(LuPanelArgs a)
         }
         __syncthreads();
     }
-    for (int idx = tid; idx < R * jb; idx += LU_THREADS) {
-        int r = idx % R, c = idx / R;
-        if (r < rows_here) a.L[rbeg + r + (a.c0 + c) * a.ld] = sp[idx];
-    }
+    for (int c = 0; c < jb; ++c)
+        for (int r = tid; r < rows_here; r += LU_THREADS) a.L[rbeg + r + (a.c0 + c) * a.ld] = sp[c * R + r];
+    __syncthreads();
+    apply_panel_interchanges(a, spiv, trow, tsrc, &s_nt, gtid, gstride);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -189,17 +228,16 @@ __global__ void __launch_bounds__(LU_THREADS, 1) lu_panel_cluster_kernel(LuPanel
     __shared__ double pivrow[LU_JBMAX], oldrow[LU_JBMAX];
     __shared__ int64_t s_piv;
     __shared__ int s_win;
+    __shared__ int64_t spiv[LU_JBMAX], trow[2 * LU_JBMAX], tsrc[2 * LU_JBMAX];
+    __shared__ int s_nt;
     const int64_t rbeg = a.c0 + (int64_t)me * R;
     const int64_t rows_here = (rbeg < a.w) ? ((a.w - rbeg < R) ? a.w - rbeg : R) : 0;
-    const int64_t n_out = a.d - jb;
     const int64_t gtid = (int64_t)me * LU_THREADS + tid, gstride = (int64_t)CL * LU_THREADS;
 
-    for (int idx = tid; idx < R * jb; idx += LU_THREADS) {
-        int r = idx % R, c = idx / R;
-        sp[idx] = (r < rows_here) ? a.L[rbeg + r + (a.c0 + c) * a.ld] : 0.0;
-    }
-    __syncthreads();
+    slab_load_async(sp, R, a.L + rbeg + a.c0 * a.ld, a.ld, (int)rows_here, R, jb);
 
+    // Per column: 2 block barriers + 1 cluster barrier.  Every thread owns whole rows (r = tid + k 256);
+    // the interchange is folded into the row update, so rows are only ever touched by their owner.
     for (int j = 0; j < jb; ++j) {
         const int par = j & 1;
         const int64_t jr = a.c0 + j;
@@ -210,7 +248,7 @@ __global__ void __launch_bounds__(LU_THREADS, 1) lu_panel_cluster_kernel(LuPanel
             int64_t ar = rbeg + r;
             if (ar < jr) continue;
             double v = fabs(sp[j * R + r]);
-            if (v > bv) { bv = v; bi = ar; }
+            if (v > bv) { bv = v; bi = ar; }  // ascending rows per thread: first index kept on ties
         }
         for (int o = 16; o > 0; o >>= 1) {
             double ov = __shfl_down_sync(0xffffffffu, bv, o);
@@ -218,22 +256,28 @@ __global__ void __launch_bounds__(LU_THREADS, 1) lu_panel_cluster_kernel(LuPanel
             if (better(ov, oi, bv, bi)) { bv = ov; bi = oi; }
         }
         if (lane == 0) { red_v[warp] = bv; red_i[warp] = bi; }
-        __syncthreads();
+        __syncthreads();  // (1)
         double* myrec = rec + par * LUC_REC;
-        if (tid == 0) {
-            for (int wv = 1; wv < LU_THREADS / 32; ++wv)
-                if (better(red_v[wv], red_i[wv], bv, bi)) { bv = red_v[wv]; bi = red_i[wv]; }
-            myrec[0] = bv;
-            myrec[1] = __longlong_as_double((long long)bi);
-            s_piv = bi;
+        if (warp == 0) {  // this CTA's candidate: value, row and its full panel row
+            double v = (lane < LU_THREADS / 32) ? red_v[lane] : -1.0;
+            int64_t i = (lane < LU_THREADS / 32) ? red_i[lane] : INT64_MAX;
+            for (int o = 16; o > 0; o >>= 1) {
+                double ov = __shfl_down_sync(0xffffffffu, v, o);
+                int64_t oi = __shfl_down_sync(0xffffffffu, i, o);
+                if (better(ov, oi, v, i)) { v = ov; i = oi; }
+            }
+            v = __shfl_sync(0xffffffffu, v, 0);
+            i = __shfl_sync(0xffffffffu, i, 0);
+            if (lane == 0) {
+                myrec[0] = v;
+                myrec[1] = __longlong_as_double((long long)i);
+            }
+            if (lane < jb) myrec[2 + lane] = (i != INT64_MAX) ? sp[lane * R + (i - rbeg)] : 0.0;
+        } else if (warp == 1 && me == owner && lane < jb) {  // the current row j
+            myrec[2 + LU_JBMAX + lane] = sp[lane * R + (jr - rbeg)];
         }
-        __syncthreads();
-        if (tid < jb) {
-            myrec[2 + tid] = (s_piv != INT64_MAX) ? sp[tid * R + (s_piv - rbeg)] : 0.0;
-            if (me == owner) myrec[2 + LU_JBMAX + tid] = sp[tid * R + (jr - rbeg)];
-        }
-        cluster.sync();
-        if (warp == 0) {
+        cluster.sync();  // (C)
+        if (warp == 0) {  // every CTA picks the same winner
             double v = -1.0;
             int64_t i = INT64_MAX;
             int wq = 0;
@@ -249,52 +293,55 @@ __global__ void __launch_bounds__(LU_THREADS, 1) lu_panel_cluster_kernel(LuPanel
                 int ow = __shfl_down_sync(0xffffffffu, wq, o);
                 if (better(ov, oi, v, i)) { v = ov; i = oi; wq = ow; }
             }
+            i = __shfl_sync(0xffffffffu, i, 0);
+            wq = __shfl_sync(0xffffffffu, wq, 0);
+            if (lane < jb) {
+                pivrow[lane] = cluster.map_shared_rank(rec + par * LUC_REC, wq)[2 + lane];
+                oldrow[lane] = cluster.map_shared_rank(rec + par * LUC_REC, owner)[2 + LU_JBMAX + lane];
+            }
             if (lane == 0) {
                 s_piv = i;
-                s_win = wq;
                 if (me == 0) a.ipiv[jr] = (int)i;
             }
         }
-        __syncthreads();
+        __syncthreads();  // (2)
         const int64_t piv = s_piv;
-        if (tid < jb) {
-            pivrow[tid] = cluster.map_shared_rank(rec + par * LUC_REC, s_win)[2 + tid];
-            oldrow[tid] = cluster.map_shared_rank(rec + par * LUC_REC, owner)[2 + LU_JBMAX + tid];
-        }
-        __syncthreads();
         const double u = pivrow[j];
+        if (tid == 0) spiv[j] = (u != 0.0) ? piv : jr;
         if (u != 0.0) {
-            if (piv != jr) {
-                if (piv >= rbeg && piv < rbeg + rows_here && tid < jb) sp[tid * R + (piv - rbeg)] = oldrow[tid];
-                if (jr >= rbeg && jr < rbeg + rows_here && tid < jb) sp[tid * R + (jr - rbeg)] = pivrow[tid];
-                for (int64_t e = gtid; e < n_out; e += gstride) {
-                    int64_t c = (e < a.c0) ? e : e + jb;
-                    double* pc = a.L + c * a.ld;
-                    double t = pc[jr];
-                    pc[jr] = pc[piv];
-                    pc[piv] = t;
-                }
-                if (gtid == 0) {
-                    int t = a.perm[jr];
-                    a.perm[jr] = a.perm[piv];
-                    a.perm[piv] = t;
-                }
-            }
-            __syncthreads();
             for (int r = tid; r < rows_here; r += LU_THREADS) {
-                if (rbeg + r <= jr) continue;
-                double l = sp[j * R + r] / u;
+                const int64_t ar = rbeg + r;
+                if (ar < jr) continue;
+                if (ar == jr) {
+                    if (piv != jr)
+                        for (int c = 0; c < jb; ++c) sp[c * R + r] = pivrow[c];
+                    continue;
+                }
+                const bool swapped = (ar == piv);
+                if (swapped)
+                    for (int c = 0; c < j; ++c) sp[c * R + r] = oldrow[c];
+                const double l = (swapped ? oldrow[j] : sp[j * R + r]) / u;
                 sp[j * R + r] = l;
-                for (int c = j + 1; c < jb; ++c) sp[c * R + r] = fma(-l, pivrow[c], sp[c * R + r]);
+                for (int c0 = j + 1; c0 < jb; c0 += 8) {  // 8 independent loads in flight, then 8 FMAs
+                    double av[8], pv[8];
+#pragma unroll
+                    for (int uu = 0; uu < 8; ++uu)
+                        if (c0 + uu < jb) {
+                            av[uu] = swapped ? oldrow[c0 + uu] : sp[(c0 + uu) * R + r];
+                            pv[uu] = pivrow[c0 + uu];
+                        }
+#pragma unroll
+                    for (int uu = 0; uu < 8; ++uu)
+                        if (c0 + uu < jb) sp[(c0 + uu) * R + r] = fma(-l, pv[uu], av[uu]);
+                }
             }
         }
-        __syncthreads();
     }
-    for (int idx = tid; idx < R * jb; idx += LU_THREADS) {
-        int r = idx % R, c = idx / R;
-        if (r < rows_here) a.L[rbeg + r + (a.c0 + c) * a.ld] = sp[idx];
-    }
+    __syncthreads();
+    for (int c = 0; c < jb; ++c)
+        for (int r = tid; r < rows_here; r += LU_THREADS) a.L[rbeg + r + (a.c0 + c) * a.ld] = sp[c * R + r];
     cluster.sync();  // peers may still read this CTA's last records
+    apply_panel_interchanges(a, spiv, trow, tsrc, &s_nt, gtid, gstride);
 }
 
 constexpr size_t LUC_SMEM_MAX = 196 * 1024;

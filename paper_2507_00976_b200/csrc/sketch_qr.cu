@@ -53,11 +53,7 @@ __global__ void __launch_bounds__(QR_THREADS, 1) qr_panel_kernel(QrPanelArgs a)
     const int64_t rbeg = a.c0 + (int64_t)cta * R;
     const int64_t rows_here = (rbeg < a.m) ? ((a.m - rbeg < R) ? a.m - rbeg : R) : 0;
 
-    for (int idx = tid; idx < R * jb; idx += QR_THREADS) {
-        int r = idx % R, c = idx / R;
-        sp[idx] = (r < rows_here) ? a.A[rbeg + r + (a.c0 + c) * a.ld] : 0.0;
-    }
-    __syncthreads();
+    slab_load_async(sp, R, a.A + rbeg + a.c0 * a.ld, a.ld, (int)rows_here, R, jb);
 
     for (int j = 0; j < jb; ++j) {
         const int par = j & 1;
@@ -235,17 +231,15 @@ __global__ void __launch_bounds__(QC_THREADS, 1) qr_panel_cluster_kernel(QrClust
     double* rowjs = part + 64;         // [2][32] alpha, a_c (owner CTA of row jr)
     double* gram = rowjs + 64;         // [32 * 32] Gram partial
     __shared__ double red[QC_THREADS / 32][33];
-    __shared__ double wv[32], tot[32], s_taus[32];
-    __shared__ double s_tau, s_beta, s_denom;
+    __shared__ double coef[32], s_taus[32];
+    __shared__ double s_beta, s_denom, s_tau;
     const int64_t rbeg = a.c0 + (int64_t)me * R;
     const int64_t rows_here = (rbeg < a.m) ? ((a.m - rbeg < R) ? a.m - rbeg : R) : 0;
 
-    for (int idx = tid; idx < R * jb; idx += QC_THREADS) {
-        int r = idx % R, c = idx / R;
-        sp[idx] = (r < rows_here) ? a.A[rbeg + r + (a.c0 + c) * a.ld] : 0.0;
-    }
-    __syncthreads();
+    slab_load_async(sp, R, a.A + rbeg + a.c0 * a.ld, a.ld, (int)rows_here, R, jb);
 
+    // Per column: 2 block barriers + 1 cluster barrier.  Each thread updates and then reads only its own
+    // rows, so the update of step j and the partials of step j+1 need no barrier between them.
     for (int j = 0; j < jb; ++j) {
         const int par = j & 1;
         const int64_t jr = a.c0 + j;
@@ -262,64 +256,79 @@ __global__ void __launch_bounds__(QC_THREADS, 1) qr_panel_cluster_kernel(QrClust
                 if (j + c < jb) q[c] = fma(x, sp[(j + c) * R + r], q[c]);
         }
         red[warp][lane] = warp_transpose_reduce32(q, lane);
-        if (me == owner && tid < jb - j) rowjs[par * 32 + tid] = sp[(j + tid) * R + (jr - rbeg)];
         __syncthreads();
         if (tid < 32) {
             double v = 0.0;
 #pragma unroll
             for (int w = 0; w < QC_THREADS / 32; ++w) v += red[w][tid];
             part[par * 32 + tid] = v;
+        } else if (tid < 64 && me == owner && tid - 32 < jb - j) {
+            rowjs[par * 32 + (tid - 32)] = sp[(j + tid - 32) * R + (jr - rbeg)];
         }
         cluster.sync();
-        if (tid < 32) {
-            double v = 0.0;
-            for (int rk = 0; rk < CL; ++rk) v += *cluster.map_shared_rank(part + par * 32 + tid, rk);
-            tot[tid] = v;
-            wv[tid] = (tid < jb - j) ? *cluster.map_shared_rank(rowjs + par * 32 + tid, owner) : 0.0;
-        }
-        __syncthreads();
-        if (tid == 0) {
-            double alpha = wv[0];
-            double nrm = sqrt(fma(alpha, alpha, tot[0]));
-            if (nrm == 0.0) {
-                s_tau = 0.0; s_beta = 0.0; s_denom = 1.0;
-            } else {
-                double beta = (alpha >= 0.0) ? -nrm : nrm;  // convention H
-                s_beta = beta;
-                s_tau = (beta - alpha) / beta;
-                s_denom = alpha - beta;
+        if (warp == 0) {
+            double pv[QC_CLMAX];
+#pragma unroll
+            for (int rk = 0; rk < QC_CLMAX; ++rk)  // all DSMEM loads in flight before the (ordered) sum
+                pv[rk] = (rk < CL) ? *cluster.map_shared_rank(part + par * 32 + lane, rk) : 0.0;
+            const double ww = (lane < jb - j) ? *cluster.map_shared_rank(rowjs + par * 32 + lane, owner) : 0.0;
+            double tot = 0.0;
+#pragma unroll
+            for (int rk = 0; rk < QC_CLMAX; ++rk) tot += pv[rk];
+            const double alpha = __shfl_sync(0xffffffffu, ww, 0);
+            const double s2 = __shfl_sync(0xffffffffu, tot, 0);
+            const double nrm = sqrt(fma(alpha, alpha, s2));
+            double beta = 0.0, tau = 0.0, denom = 1.0;
+            if (nrm != 0.0) {
+                beta = (alpha >= 0.0) ? -nrm : nrm;  // convention H
+                tau = (beta - alpha) / beta;
+                denom = alpha - beta;
             }
-            s_taus[j] = s_tau;
-            if (me == 0) a.tau[jr] = s_tau;
+            coef[lane] = (lane > 0 && lane < jb - j) ? tau * (ww + tot / denom) : 0.0;  // tau w_c, w_c = v^T A(:, c)
+            if (lane == 0) {
+                s_beta = beta;
+                s_tau = tau;
+                s_denom = denom;
+                s_taus[j] = tau;
+                if (me == 0) a.tau[jr] = tau;
+            }
         }
         __syncthreads();
         const double tau = s_tau, denom = s_denom;
-        if (tid > 0 && tid < jb - j) wv[tid] = wv[tid] + tot[tid] / denom;  // w_c = v^T A(:, c)
-        __syncthreads();
         if (tau != 0.0) {
+            const int ncol = jb - j;
             for (int r = tid; r < rows_here; r += QC_THREADS) {
                 int64_t ar = rbeg + r;
                 if (ar < jr) continue;
+                double v;  // A(r, c) -= coef_c * v: v = 1 on the pivot row (v_0 = 1), x_r / denom below
                 if (ar == jr) {
                     sp[j * R + r] = s_beta;
-                    for (int c = 1; c < jb - j; ++c) sp[(j + c) * R + r] -= tau * wv[c];
+                    v = 1.0;
                 } else {
-                    double v = sp[j * R + r] / denom;
+                    v = sp[j * R + r] / denom;
                     sp[j * R + r] = v;
-                    for (int c = 1; c < jb - j; ++c) sp[(j + c) * R + r] = fma(-tau * wv[c], v, sp[(j + c) * R + r]);
+                }
+                for (int c0 = 1; c0 < ncol; c0 += 8) {  // 8 independent loads in flight, then 8 FMAs
+                    double av[8], cf[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u)
+                        if (c0 + u < ncol) { av[u] = sp[(j + c0 + u) * R + r]; cf[u] = coef[c0 + u]; }
+#pragma unroll
+                    for (int u = 0; u < 8; ++u)
+                        if (c0 + u < ncol) sp[(j + c0 + u) * R + r] = fma(-cf[u], v, av[u]);
                 }
             }
         }
-        __syncthreads();
     }
+    __syncthreads();
     // explicit V, write-back, Gram partial of V^T V over my rows
-    for (int idx = tid; idx < R * jb; idx += QC_THREADS) {
-        int r = idx % R, c = idx / R;
-        if (r >= rows_here) continue;
-        int64_t ar = rbeg + r, cr = a.c0 + c;
-        a.V[ar + cr * a.m] = (ar == cr) ? 1.0 : (ar > cr ? sp[idx] : 0.0);
-        a.A[ar + cr * a.ld] = sp[idx];
-    }
+    for (int c = 0; c < jb; ++c)
+        for (int r = tid; r < rows_here; r += QC_THREADS) {
+            int64_t ar = rbeg + r, cr = a.c0 + c;
+            double x = sp[c * R + r];
+            a.V[ar + cr * a.m] = (ar == cr) ? 1.0 : (ar > cr ? x : 0.0);
+            a.A[ar + cr * a.ld] = x;
+        }
     for (int pq = tid; pq < jb * jb; pq += QC_THREADS) {
         int p = pq % jb, qq = pq / jb;
         double s = 0.0;
