@@ -40,8 +40,9 @@ typedef struct bqrrp_options {
     /* tri_rank threshold relative to |R_sk^(0)(0,0)| (readings Z10/Z11).
      * <= 0 selects the default 10 * u * sqrt(max(m, n)). */
     double rank_tol;
-    /* Cholesky-QR passes in the panel (Alg. 3 step cholqr:cholqr): 2 = CholQR2 (default,
-     * DESIGN.md §7.3), 1 = the paper's single pass. */
+    /* Panel variant / Cholesky-QR passes (Alg. 3 step cholqr:cholqr): 2 = CholQR2 + Householder
+     * reconstruction (default), 1 = the paper's single CholQR pass, 0 = Householder QR of
+     * the panel (the paper's BQRRP_HQR variant).  Negative = default. */
     int cholqr_passes;
     /* reserved (0) */
     int reserved0;
@@ -107,7 +108,7 @@ int bqrrp_debug_sketch_qr(int64_t w, int64_t d, double* WT, int64_t ld, void* st
 int bqrrp_debug_permute(int64_t rows, int64_t w, double* X, int64_t ldx, int64_t nlu, const int64_t* ipiv,
                         int64_t* Jqr_out, void* stream);
 
-/* Panel: CholQR(passes) + Householder reconstruction of P (h x k, ld) preconditioned by Rsk11 (k x k
+/* Panel: CholQR(passes) + Householder reconstruction (passes 1..4) or Householder QR (passes 0) of P (h x k, ld) preconditioned by Rsk11 (k x k
  * upper, ld k), written in GEQP3 format in place (R11 on/above, V below) with tau (k), plus the
  * compact-WY update of the trailing C (h x t, ld) that follows P in memory (t may be 0). */
 int bqrrp_debug_panel(int64_t h, int64_t k, int64_t t, double* P, int64_t ld, const double* Rsk11, double* tau,

@@ -308,7 +308,7 @@ int bqrrp_factor_ex(int64_t m, int64_t n, double* A, int64_t lda, int64_t b, int
     int v = validate(m, n, A, lda, b, d, tau, J, rank);
     if (v != 0) return v;
     double rank_tol = (opts && opts->rank_tol > 0) ? opts->rank_tol : 10.0 * 0x1p-53 * sqrt((double)(m > n ? m : n));
-    int passes = (opts && opts->cholqr_passes >= 1 && opts->cholqr_passes <= 4) ? opts->cholqr_passes : 2;
+    int passes = (opts && opts->cholqr_passes >= 0 && opts->cholqr_passes <= 4) ? opts->cholqr_passes : 2;
     return guarded([&]() -> int {
         Ctx cx;
         setup_ctx(cx, stream);
@@ -591,6 +591,7 @@ int bqrrp_debug_panel(int64_t h, int64_t k, int64_t t, double* P, int64_t ld, co
     if (h < 1) return -1;
     if (k < 1 || k > h) return -2;
     if (t < 0) return -3;
+    if (cholqr_passes < 0 || cholqr_passes > 4) return -8;
     return guarded([&]() -> int {
         Ctx cx;
         setup_ctx(cx, stream);

@@ -21,6 +21,9 @@ void sketch_apply(Ctx& cx, int64_t m, int64_t n, const double* A, int64_t lda, i
 // a2: partial-pivot LU of the w x d matrix L (in place), ipiv[j] = 0-based pivot row, j < min(w,d);
 // perm (w) = the row permutation of piv_transform (J_qr - 1).
 void getrf_pivots(Ctx& cx, double* L, int64_t ld, int64_t w, int64_t d, int* ipiv, int* perm);
+// Householder QR (GEQRF semantics, convention H) of A (rows x cols, lda) in place: R on/above the
+// diagonal, reflectors below; V (rows x cols, ld rows) explicit, T (cols x cols) the compact-WY factor.
+void householder_panel(Ctx& cx, double* A, int64_t lda, int64_t rows, int64_t cols, double* tau, double* V, double* T);
 // a2: R_sk of the sketch window (transposed storage), in place.
 void sketch_qr(Ctx& cx, double* MskT, int64_t ldm, int64_t w, int64_t d);
 
@@ -31,7 +34,8 @@ void permute_columns(Ctx& cx, int64_t rows, double* X, int64_t ldx, const Touche
 void permute_rows(Ctx& cx, int64_t cols, double* X, int64_t ldx, const Touched& T, double* scratch);
 void permute_vector(Ctx& cx, int64_t* J, const Touched& T, int64_t* tmp);
 
-// a4: preconditioned CholQR(passes) + Householder reconstruction of the panel A(s:m, s:s+k) written in
+// a4: preconditioned CholQR(passes) + Householder reconstruction (passes >= 1) — or, passes == 0, the
+// Householder panel of the paper's BQRRP_HQR variant — of the panel A(s:m, s:s+k) written in
 // GEQP3 format in place (R11 on/above, V below, tau(s:s+k)); V (h x k, ld h, explicit: unit diagonal,
 // zeros above) and the compact-WY T (k x k, ld k) are returned in caller-owned buffers.
 void panel_factor(Ctx& cx, int64_t m, double* A, int64_t lda, int64_t s, int64_t k, const double* Rsk11, double* tau,

@@ -53,6 +53,10 @@ void panel_factor(Ctx& cx, int64_t m, double* A, int64_t lda, int64_t s, int64_t
                   int passes, double* V, double* T)
 {
     const int64_t h = m - s;
+    if (passes == 0) {  // BQRRP_HQR: Householder QR of the panel itself
+        householder_panel(cx, A + s + s * lda, lda, h, k, tau + s, V, T);
+        return;
+    }
     size_t mark = cx.ws_used;
     double* Q = V;  // h x k (ld h): M_pre -> Q_chol -> reconstruction L -> explicit V
     double* Cf[4];

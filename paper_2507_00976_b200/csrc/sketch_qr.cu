@@ -423,30 +423,47 @@ static void qr_panel(Ctx& cx, double* A, int64_t ld, int64_t m, int64_t c0, int 
 }
 
 // Recursive QR of columns [c0, c1) of Wq (rows [c0, m)); V (m x p explicit), Tf (p x p).
-static void geqrf_rec(Ctx& cx, double* Wq, int64_t m, int64_t c0, int64_t c1, double* tau, double* V, double* Tf,
-                      int64_t p, double* W1, double* W2, double* xbuf, double* rowj)
+// Recursive Householder QR of columns [c0, c1) of A (rows [c0, m), leading dimension lda); V (m x p
+// explicit, ld m, pre-zeroed), Tf (p x p, ld p).
+static void geqrf_rec(Ctx& cx, double* A, int64_t lda, int64_t m, int64_t c0, int64_t c1, double* tau, double* V,
+                      double* Tf, int64_t p, double* W1, double* W2, double* xbuf, double* rowj)
 {
     int64_t nc = c1 - c0;
     if (nc <= QR_JBMAX) {
-        qr_panel(cx, Wq, m, m, c0, (int)nc, tau, V, Tf, p, xbuf, rowj);
+        qr_panel(cx, A, lda, m, c0, (int)nc, tau, V, Tf, p, xbuf, rowj);
         return;
     }
     int64_t mid = c0 + cdiv(nc / 2, QR_JBMAX) * QR_JBMAX;
-    geqrf_rec(cx, Wq, m, c0, mid, tau, V, Tf, p, W1, W2, xbuf, rowj);
+    geqrf_rec(cx, A, lda, m, c0, mid, tau, V, Tf, p, W1, W2, xbuf, rowj);
     int64_t k1 = mid - c0, ncr = c1 - mid, h = m - c0;
     const double* V1 = V + c0 + c0 * m;    // h x k1
     const double* T11 = Tf + c0 + c0 * p;  // k1 x k1
-    double* A2 = Wq + c0 + mid * m;        // h x ncr
+    double* A2 = A + c0 + mid * lda;       // h x ncr
     // A2 <- (I - V1 T11 V1^T)^T A2 = A2 - V1 T11^T (V1^T A2)
-    gemm(cx, true, false, k1, ncr, h, 1.0, V1, m, A2, m, 0.0, W1, k1);
+    gemm(cx, true, false, k1, ncr, h, 1.0, V1, m, A2, lda, 0.0, W1, k1);
     gemm(cx, true, false, k1, ncr, k1, 1.0, T11, p, W1, k1, 0.0, W2, k1);
-    gemm(cx, false, false, h, ncr, k1, -1.0, V1, m, W2, k1, 1.0, A2, m);
-    geqrf_rec(cx, Wq, m, mid, c1, tau, V, Tf, p, W1, W2, xbuf, rowj);
+    gemm(cx, false, false, h, ncr, k1, -1.0, V1, m, W2, k1, 1.0, A2, lda);
+    geqrf_rec(cx, A, lda, m, mid, c1, tau, V, Tf, p, W1, W2, xbuf, rowj);
     // T12 = -T11 (V1^T V2) T22, V2 = V(c0:m, mid:c1) (zeros above row mid)
     const double* V2 = V + c0 + mid * m;
     gemm(cx, true, false, k1, ncr, h, 1.0, V1, m, V2, m, 0.0, W1, k1);
     gemm(cx, false, false, k1, ncr, k1, 1.0, T11, p, W1, k1, 0.0, W2, k1);
     gemm(cx, false, false, k1, ncr, ncr, -1.0, W2, k1, Tf + mid + mid * p, p, 0.0, Tf + c0 + mid * p, p);
+}
+
+void householder_panel(Ctx& cx, double* A, int64_t lda, int64_t rows, int64_t cols, double* tau, double* V, double* T)
+{
+    if (rows <= 0 || cols <= 0) return;
+    size_t mark = cx.ws_used;
+    double* W1 = cx.alloc((size_t)cols * cols);
+    double* W2 = cx.alloc((size_t)cols * cols);
+    int G = cx.num_sms;
+    double* xbuf = cx.alloc(2 * (size_t)G * QR_XSTRIDE + (size_t)G * QR_JBMAX * QR_JBMAX);
+    double* rowj = cx.alloc(2 * QR_JBMAX);
+    BQ_CUDA(cudaMemsetAsync(V, 0, sizeof(double) * rows * cols, cx.stream));
+    BQ_CUDA(cudaMemsetAsync(T, 0, sizeof(double) * cols * cols, cx.stream));
+    geqrf_rec(cx, A, lda, rows, 0, cols, tau, V, T, cols, W1, W2, xbuf, rowj);
+    cx.ws_used = mark;
 }
 
 __global__ void store_rsk_kernel(int64_t p, int64_t d, const double* Wq, double* MskT, int64_t ldm)
@@ -478,7 +495,7 @@ void sketch_qr(Ctx& cx, double* MskT, int64_t ldm, int64_t w, int64_t d)
     transpose_copy(cx, p, d, MskT, ldm, Wq, d);
     BQ_CUDA(cudaMemsetAsync(V, 0, sizeof(double) * d * p, cx.stream));
     BQ_CUDA(cudaMemsetAsync(Tf, 0, sizeof(double) * p * p, cx.stream));
-    geqrf_rec(cx, Wq, d, 0, p, tau, V, Tf, p, W1, W2, xbuf, rowj);
+    geqrf_rec(cx, Wq, d, d, 0, p, tau, V, Tf, p, W1, W2, xbuf, rowj);
     int64_t rest = w - p;
     if (rest > 0) {
         // p == d here.  Q_sk = H_1...H_p = I - V T V^T formed explicitly (d x d), then

@@ -138,7 +138,7 @@ def test_permute_bitexact(gpu, rows, w, nlu):
 
 # ----------------------------------------------------------------------------- a4/a5 panel
 @pytest.mark.parametrize("h,k,t", [(256, 32, 40), (1000, 100, 0), (3000, 128, 200), (129, 129, 3)])
-@pytest.mark.parametrize("passes", [1, 2])
+@pytest.mark.parametrize("passes", [0, 1, 2])
 def test_panel_matches_householder_oracle(gpu, h, k, t, passes):
     """c.1: CholQR + reconstruction gives the unique (V, tau, R) with tau in [1,2] = convention-H QR."""
     bq = _bq()
@@ -150,7 +150,7 @@ def test_panel_matches_householder_oracle(gpu, h, k, t, passes):
     F_o, tau_o = oracle.house_qr(P, kref=k)
     Pg, taug = bq.debug_panel(_dev(P), k, _dev(Rsk), cholqr_passes=passes)
     F_g = _host(Pg)
-    tol = 1e-12 if passes == 2 else 1e-9
+    tol = 1e-9 if passes == 1 else 1e-12  # 0 = Householder panel (BQRRP_HQR), 2 = CholQR2
     assert np.max(np.abs(_host(taug) - tau_o)) <= tol
     R_o, R_g = np.triu(F_o[:k, :k]), np.triu(F_g[:k, :k])
     assert np.linalg.norm(R_g - R_o) <= tol * np.linalg.norm(R_o)
@@ -161,10 +161,10 @@ def test_panel_matches_householder_oracle(gpu, h, k, t, passes):
 
 
 # ----------------------------------------------------------------------------- end to end
-def _run_both(A, b, d, seed=0, rank_tol=None):
+def _run_both(A, b, d, seed=0, rank_tol=None, passes=2):
     bq = _bq()
     out_o = oracle.bqrrp(A, b, d, seed=seed, rank_tol=rank_tol)
-    Ag, taug, Jg, rk = bq.factor(_dev(A), b, d, seed=seed, rank_tol=rank_tol)
+    Ag, taug, Jg, rk = bq.factor(_dev(A), b, d, seed=seed, rank_tol=rank_tol, cholqr_passes=passes)
     return out_o, (_host(Ag), _host(taug), _host(Jg), rk)
 
 
@@ -201,6 +201,15 @@ def test_factor_matches_oracle(gpu, shape, b, d):
     _compare(out_o, g)
     res = oracle.residual(A, oracle.OracleResult(g[0], g[1], g[2], g[3], None, 0, None))
     assert res <= 1e-13
+
+
+@pytest.mark.parametrize("shape,b,d", [((1024, 1024), 128, 160), ((2048, 512), 128, 160), ((700, 450), 64, 80)])
+def test_factor_hqr_variant_matches_oracle(gpu, shape, b, d):
+    """BQRRP_HQR: the Householder panel gives the same (V, tau, R) as the oracle."""
+    m, n = shape
+    A = inputs.gaussian(m, n, seed=m + n)
+    out_o, g = _run_both(A, b, d, seed=0, passes=0)
+    _compare(out_o, g)
 
 
 @pytest.mark.parametrize("seed", [1, 2, 3, 4])
