@@ -205,6 +205,10 @@ def main():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--backend", default="nccl", help="process-group backend for N > 1 (gloo: tests)")
+    ap.add_argument("--share-gpu", action="store_true", help="all ranks on cuda:0 (gloo tests on a 1-GPU box)")
+    ap.add_argument("--replicas", action="store_true",
+                    help="N > 1: independent replicas (weak scaling) instead of one distributed factorization")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -217,15 +221,20 @@ def main():
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = 0 if args.share_gpu else int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(args.backend)
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream()
 
     cfg = CONFIGS[args.config]
     m, n, b, d = cfg["m"], cfg["n"], cfg["b"], cfg["d"]
+    if world > 1 and not args.replicas:
+        return run_distributed(args, cfg, world, rank, local, dev)
     A0 = inputs.gaussian_cuda(m, n, seed=args.seed + rank, device=dev)  # column-major view
     A = torch.empty_like(A0.t()).t()
     ws = torch.empty(bq.workspace_query(m, n, b, d), dtype=torch.uint8, device=dev)
@@ -331,6 +340,95 @@ def main():
         print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()
+    return 0
+
+
+def run_distributed(args, cfg, world, rank, local, dev):
+    """N > 1: ONE factorization of the config's matrix, 1-D block-cyclic over the ranks (SURVEY §8(e),
+    paper_2507_00976_b200/dist.py; NCCL all-reduce / broadcast for the sketch, panel and column exchanges).
+    Strong scaling: value = canonical flops of the one matrix / max-over-ranks time."""
+    import torch
+    import torch.distributed as dist
+
+    import inputs
+    import paper_2507_00976_b200 as bq
+    from paper_2507_00976_b200.dist import factor_dist, local_columns
+
+    m, n, b, d = cfg["m"], cfg["n"], cfg["b"], cfg["d"]
+    stream = torch.cuda.current_stream()
+    A_full = inputs.gaussian_cuda(m, n, seed=args.seed, device=dev)  # identical on every rank
+    A_loc0, bc = local_columns(A_full, b, world, rank)
+    del A_full
+    torch.cuda.empty_cache()
+    A_loc = torch.empty_like(A_loc0.t()).t()
+
+    def step():
+        return factor_dist(A_loc, m, n, b, d, seed=args.seed)
+
+    for _ in range(args.warmup):
+        A_loc.copy_(A_loc0)
+        step()
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    launches0 = bq.launch_count()
+    dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            A_loc.copy_(A_loc0)
+            ev[i][0].record(stream)
+            out = step()
+            ev[i][1].record(stream)
+        torch.cuda.synchronize()
+    dist.barrier()
+    launches = bq.launch_count() - launches0
+    t_ms = max_over_ranks(sum(s_.elapsed_time(e_) for s_, e_ in ev), dev)
+    flops_step = canonical_flops(m, n)
+    value = aggregate_value(flops_step, args.steps, 1, t_ms)  # one matrix, all ranks
+    peak, peak_src = peak_fp64()
+    e2e = None
+    if not args.no_e2e:  # each rank: its columns host -> device, distributed factorization, back to host
+        Ah0 = torch.empty((A_loc0.shape[1], m), dtype=torch.float64).pin_memory()
+        Ah0.copy_(A_loc0.t())
+        Ah = torch.empty_like(Ah0).pin_memory()
+        tau_h = torch.empty(min(m, n), dtype=torch.float64).pin_memory()
+        J_h = torch.empty(n, dtype=torch.int64).pin_memory()
+        Ah.copy_(Ah0)
+        dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        A_loc.t().copy_(Ah, non_blocking=True)
+        _, tau, J, _ = step()
+        Ah.copy_(A_loc.t(), non_blocking=True)
+        tau_h.copy_(tau, non_blocking=True)
+        J_h.copy_(J, non_blocking=True)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        te = max_over_ranks(e0.elapsed_time(e1), dev)
+        e2e = {"value": aggregate_value(flops_step, 1, 1, te), "unit": "TFLOP/s",
+               "h2d_bytes_per_step": m * A_loc0.shape[1] * 8,
+               "d2h_bytes_per_step": m * A_loc0.shape[1] * 8 + min(m, n) * 8 + n * 8, "ms_per_step": te,
+               "api": "paper_2507_00976_b200.dist.factor_dist (per-rank pinned host columns)"}
+    if rank == 0:
+        per_gpu = value / world
+        line = {
+            "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{args.config} {cfg['desc']}", "m": m, "n": n, "b": b, "d": d,
+                       "parallelism": f"block-cyclic columns over {world} GPUs (dist_nb = b)",
+                       "l2": "inputs larger than L2", "rank_found": out[3],
+                       "timing": "per-step CUDA events around factor_dist, max over ranks"},
+            "pct_fp64_peak": 100.0 * per_gpu / peak,
+            "roofline": {"bound": "tensor", "achieved": per_gpu, "peak": peak, "unit": "TFLOP/s",
+                         "frac": per_gpu / peak, "traffic": None,
+                         "kernel": "whole distributed factorization, per GPU (canonical flops / time / N)",
+                         "peak_source": peak_src},
+            "cpu_baseline": None, "e2e": e2e, "gpu_launches": launches, "clocks": clk.summary(),
+        }
+        print(json.dumps(line))
+    dist.destroy_process_group()
     return 0
 
 

@@ -114,6 +114,40 @@ int bqrrp_debug_permute(int64_t rows, int64_t w, double* X, int64_t ldx, int64_t
 int bqrrp_debug_panel(int64_t h, int64_t k, int64_t t, double* P, int64_t ld, const double* Rsk11, double* tau,
                       int cholqr_passes, void* stream);
 
+/* ---- multi-GPU step entry points (driven by paper_2507_00976_b200/dist.py) ----
+ * A is distributed 1-D block-cyclically over column positions (block width dist_nb = b); the transposed
+ * sketch MskT (n x d) and J are replicated; the caller moves data between ranks (torch.distributed:
+ * NCCL all-reduce / broadcast on a multi-GPU node).  All pointers device, all calls stream-ordered. */
+
+/* a2 on the replicated sketch window MskT(s:n, :): LU pivots, J_qr touched set (tq[t] <- tsrc[t],
+ * positions relative to s, *nt entries, capacity 2 min(n-s, d)), sketch rows and J(s:n) permuted
+ * (J may be NULL), R_sk in place, k = tri_rank (ref = |R_sk(0,0)| stored when first).
+ * Synchronises the stream; *k_out host. */
+int bqrrp_step_pivots(int64_t n, int64_t d, int64_t s, int64_t kmax, double* MskT, int64_t ldm, int64_t* J,
+                      double rank_tol, double* ref, int first, int* tq, int* tsrc, int* nt, int64_t* k_out,
+                      void* stream);
+/* dst(:, t) = X(:, idx[t]) (rows x n_idx), slots with idx[t] < 0 untouched. */
+int bqrrp_step_gather_columns(int64_t rows, const double* X, int64_t ldx, const int* idx, int64_t nidx, double* dst,
+                              int64_t ldd, void* stream);
+/* X(:, idx[t]) = src(:, t), slots with idx[t] < 0 skipped. */
+int bqrrp_step_scatter_columns(int64_t rows, double* X, int64_t ldx, const int* idx, int64_t nidx, const double* src,
+                               int64_t lds, void* stream);
+/* *is_zero_host = 1 iff col(0:h) is all zeros (the P:1008 early exit).  Synchronises. */
+int bqrrp_step_zero_column_check(int64_t h, const double* col, int* is_zero_host, void* stream);
+/* a4 on the owner of the panel: P (h x k, ldp) in place in GEQP3 format, tau (k), explicit V (h x k, ld h)
+ * and T (k x k); R_sk11 read from the sketch window MskT_s (= MskT + s).  BQRRP_ENUMERIC on breakdown. */
+int bqrrp_step_panel(int64_t h, int64_t k, double* P, int64_t ldp, const double* MskT_s, int64_t ldm, double* tau,
+                     double* V, double* T, int cholqr_passes, void* stream);
+/* a5 on one rank's trailing columns: C (h x t, ldc) <- C - V T^T (V^T C). */
+int bqrrp_step_wy_update(int64_t h, int64_t k, int64_t t, const double* V, const double* T, double* C, int64_t ldc,
+                         void* stream);
+/* a6 on the replicated sketch: X = R_sk11 R11^{-1} (R_sk11 from MskT_s), MskT_s(b:b+t, 0:b) -= R12^T X^T with
+ * R11 (b x b, ldr) and R12 (b x t, ld12) gathered in position order. */
+int bqrrp_step_sample_update(int64_t b, int64_t t, const double* R11, int64_t ldr, const double* R12, int64_t ld12,
+                             double* MskT_s, int64_t ldm, void* stream);
+/* X(0:rows, 0:cols) = 0. */
+int bqrrp_step_zero(int64_t rows, int64_t cols, double* X, int64_t ldx, void* stream);
+
 /* Number of CUDA kernels this library has launched in the calling process (all threads). */
 unsigned long long bqrrp_launch_count(void);
 

@@ -1,0 +1,208 @@
+"""Multi-GPU BQRRP (phase 1): A is distributed 1-D block-cyclically over column POSITIONS
+(block width nb = b, so every panel lives on one rank); the transposed sketch MskT (n x d), J and tau are
+replicated.  Per iteration (Alg. 1):
+
+  a2  every rank runs the same pivot selection on the replicated sketch (deterministic kernels, identical
+      inputs -> identical pivots, k and R_sk on every rank)                      bqrrp_step_pivots
+  a3  X3: the <= 2 min(d, w) touched columns are packed by their owners into one buffer whose slots are
+      filled by exactly one rank, summed across ranks (exact: every other rank contributes zeros) and
+      unpacked by the new owners                                                 gather / all-reduce / scatter
+  a4  the panel owner factors it; X2: V, T, tau (and R11) broadcast               bqrrp_step_panel
+  a5  every rank updates its own trailing columns                                  bqrrp_step_wy_update
+  a6  X1: R12 (k x t) assembled in position order by an exact all-reduce, then the replicated sketch update
+                                                                                   bqrrp_step_sample_update
+
+Every arithmetic step runs in libbqrrp.so's kernels; torch.distributed (NCCL on a multi-GPU node, gloo in
+the single-GPU tests where two ranks share one device) only moves buffers.  The result equals the
+single-GPU factorization (J and rank identical, R / V / tau to rounding: the local GEMMs see different N
+and may choose different tilings, which does not change any element's K order, and split-K is only
+taken for small-MN shapes).
+"""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import BqrrpError, _check, _stream_ptr, default_rank_tol, lib
+
+__all__ = ["BlockCyclic", "factor_dist", "local_columns"]
+
+
+class BlockCyclic:
+    """1-D block-cyclic map of n column positions over G ranks with block width nb."""
+
+    def __init__(self, n: int, nb: int, G: int, rank: int):
+        self.n, self.nb, self.G, self.rank = n, nb, G, rank
+        p = np.arange(n)
+        self.owner_of = (p // nb) % G
+        self.pos = p[self.owner_of == rank]  # this rank's positions, ascending
+        self.loc_of = np.full(n, -1, dtype=np.int64)
+        self.loc_of[self.pos] = np.arange(len(self.pos))
+
+    @property
+    def n_loc(self) -> int:
+        return len(self.pos)
+
+    def first_local_at_or_after(self, p: int) -> int:
+        return int(np.searchsorted(self.pos, p))
+
+
+def local_columns(A, nb: int, G: int, rank: int):
+    """This rank's block-cyclic columns of a full column-major tensor (for tests and the bench)."""
+    import torch
+
+    bc = BlockCyclic(A.shape[1], nb, G, rank)
+    idx = torch.as_tensor(bc.pos, device=A.device)
+    loc = A.index_select(1, idx)
+    return loc.t().contiguous().t(), bc
+
+
+def _ptr(t):
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _declare():
+    L = lib()
+    if getattr(L, "_dist_declared", False):
+        return L
+    i64, d, P, i32 = ctypes.c_int64, ctypes.c_double, ctypes.c_void_p, ctypes.c_int
+    L.bqrrp_step_pivots.argtypes = [i64, i64, i64, i64, P, i64, P, d, P, i32, P, P, P, ctypes.POINTER(i64), P]
+    L.bqrrp_step_gather_columns.argtypes = [i64, P, i64, P, i64, P, i64, P]
+    L.bqrrp_step_scatter_columns.argtypes = [i64, P, i64, P, i64, P, i64, P]
+    L.bqrrp_step_zero_column_check.argtypes = [i64, P, ctypes.POINTER(i32), P]
+    L.bqrrp_step_panel.argtypes = [i64, i64, P, i64, P, i64, P, P, P, i32, P]
+    L.bqrrp_step_wy_update.argtypes = [i64, i64, i64, P, P, P, i64, P]
+    L.bqrrp_step_sample_update.argtypes = [i64, i64, P, i64, P, i64, P, i64, P]
+    L.bqrrp_step_zero.argtypes = [i64, i64, P, i64, P]
+    L.bqrrp_debug_sketch.argtypes = [i64, i64, P, i64, i64, ctypes.c_uint64, P, P, P]
+    L._dist_declared = True
+    return L
+
+
+def factor_dist(A_loc, m: int, n: int, b: int, d: int | None = None, seed: int = 0, rank_tol: float | None = None,
+                cholqr_passes: int = 2, group=None):
+    """Distributed BQRRP.  A_loc: this rank's block-cyclic columns (m x n_loc, column-major float64 CUDA).
+    Returns (A_loc, tau, J, rank) with A_loc overwritten in GEQP3 format (R above, V below, in this rank's
+    columns), tau (min(m,n)) and J (n, one-based gather) replicated."""
+    import torch
+    import torch.distributed as dist
+
+    L = _declare()
+    G = dist.get_world_size(group)
+    me = dist.get_rank(group)
+    dev = A_loc.device
+    st = _stream_ptr()
+    d = b if d is None else d
+    mn = min(m, n)
+    if rank_tol is None:
+        rank_tol = default_rank_tol(m, n)
+    bc = BlockCyclic(n, b, G, me)
+    assert A_loc.shape == (m, bc.n_loc) and (A_loc.stride(0) == 1 or m <= 1), "A_loc: m x n_loc column-major"
+    lda = max(A_loc.stride(1), m)
+    f64 = dict(dtype=torch.float64, device=dev)
+
+    def allreduce_sum(t):
+        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+
+    def colmaj(rows, cols):
+        return torch.zeros((cols, rows), **f64).t()
+
+    # ---- a1: local sketch rows, assembled into the replicated MskT (n x d) by an exact all-reduce
+    MskT = colmaj(n, d)
+    if bc.n_loc > 0:
+        MskT_loc = colmaj(bc.n_loc, d)
+        _check(L.bqrrp_debug_sketch(m, bc.n_loc, _ptr(A_loc), lda, d, seed, None, _ptr(MskT_loc), st),
+               "bqrrp_debug_sketch")
+        MskT[torch.as_tensor(bc.pos, device=dev)] = MskT_loc
+    allreduce_sum(MskT)
+    J = torch.arange(1, n + 1, dtype=torch.int64, device=dev)
+    tau = torch.zeros(max(mn, 1), **f64)
+    ref = torch.zeros(1, **f64)
+    tq = torch.zeros(2 * d, dtype=torch.int32, device=dev)
+    tsrc = torch.zeros(2 * d, dtype=torch.int32, device=dev)
+    nt = torch.zeros(1, dtype=torch.int32, device=dev)
+    ell = mn
+    i = 0
+    while True:
+        s = i * b
+        if s >= mn:
+            ell = mn
+            break
+        c, r, w, h = min(n, s + b), min(m, s + b), n - s, m - s
+        kmax = min(b, w, h)
+        # ---- a2 (replicated)
+        k = ctypes.c_int64(0)
+        _check(L.bqrrp_step_pivots(n, d, s, kmax, _ptr(MskT), n, _ptr(J), float(rank_tol), _ptr(ref), int(i == 0),
+                                   _ptr(tq), _ptr(tsrc), _ptr(nt), ctypes.byref(k), st), "bqrrp_step_pivots")
+        k = int(k.value)
+        ntv = int(nt.item())
+        # ---- a3: X3 column exchange through one exactly-summed buffer
+        if ntv > 0:
+            q = tq[:ntv].cpu().numpy().astype(np.int64) + s
+            p = tsrc[:ntv].cpu().numpy().astype(np.int64) + s
+            pack = np.where(bc.owner_of[p] == me, bc.loc_of[p], -1).astype(np.int32)
+            unpack = np.where(bc.owner_of[q] == me, bc.loc_of[q], -1).astype(np.int32)
+            buf = colmaj(m, ntv)
+            _check(L.bqrrp_step_gather_columns(m, _ptr(A_loc), lda, _ptr(torch.as_tensor(pack, device=dev)), ntv,
+                                               _ptr(buf), m, st), "gather")
+            allreduce_sum(buf)
+            _check(L.bqrrp_step_scatter_columns(m, _ptr(A_loc), lda, _ptr(torch.as_tensor(unpack, device=dev)), ntv,
+                                                _ptr(buf), m, st), "scatter")
+        # ---- a7 early exit: the owner of position s tests A(s:m, s)
+        owner = int(bc.owner_of[s])
+        flag = torch.zeros(1, **f64)
+        if owner == me:
+            z = ctypes.c_int(0)
+            _check(L.bqrrp_step_zero_column_check(h, _ptr(A_loc[s:, int(bc.loc_of[s])]), ctypes.byref(z), st), "zc")
+            flag.fill_(float(z.value))
+        allreduce_sum(flag)
+        if k == 0 or flag.item() != 0.0:
+            ell = s
+            break
+        # ---- a4 on the owner, X2 broadcast of V, T, tau (+ R11)
+        V = colmaj(h, k)
+        T = colmaj(k, k)
+        tk = torch.zeros(k, **f64)
+        R11 = colmaj(b, b)
+        status = torch.zeros(1, **f64)
+        if owner == me:
+            j0 = int(bc.loc_of[s])
+            st_panel = L.bqrrp_step_panel(h, k, _ptr(A_loc[s:, j0:]), lda, _ptr(MskT[s:]), n, _ptr(tk), _ptr(V),
+                                          _ptr(T), int(cholqr_passes), st)
+            status.fill_(float(st_panel))
+            if k == b:
+                R11.copy_(torch.triu(A_loc[s:s + b, j0:j0 + b]))
+        allreduce_sum(status)
+        if status.item() != 0.0:
+            raise BqrrpError(int(status.item()), "bqrrp_step_panel (distributed)")
+        for t_ in (V, T, tk):
+            dist.broadcast(t_, src=owner, group=group)
+        tau[s:s + k] = tk
+        # ---- a5 on every rank's own trailing columns (positions >= s + k)
+        j_tr = bc.first_local_at_or_after(s + k)
+        t_loc = bc.n_loc - j_tr
+        if t_loc > 0:
+            _check(L.bqrrp_step_wy_update(h, k, t_loc, _ptr(V), _ptr(T), _ptr(A_loc[s:, j_tr:]), lda, st), "wy")
+        if k < kmax or c == n or r == m:
+            ell = s + k
+            break
+        # ---- a6: R11 and R12 (k x t, position order) by exact all-reduce, replicated sketch update
+        dist.broadcast(R11, src=owner, group=group)
+        t = n - c
+        R12 = colmaj(k, t)
+        j_c = bc.first_local_at_or_after(c)
+        if bc.n_loc - j_c > 0:
+            slots = torch.as_tensor(bc.pos[j_c:] - c, device=dev)
+            R12[:, slots] = A_loc[s:s + k, j_c:]
+        allreduce_sum(R12)
+        _check(L.bqrrp_step_sample_update(b, t, _ptr(R11), b, _ptr(R12), k, _ptr(MskT[s:]), n, st), "sample_update")
+        i += 1
+    # ---- O4: tau(ell:) = 0, A(ell:m, ell:n) = 0 on the columns this rank owns
+    if ell < mn:
+        tau[ell:mn] = 0.0
+    j_l = bc.first_local_at_or_after(ell)
+    if ell < m and bc.n_loc - j_l > 0:
+        _check(L.bqrrp_step_zero(m - ell, bc.n_loc - j_l, _ptr(A_loc[ell:, j_l:]), lda, st), "zero")
+    torch.cuda.current_stream().synchronize()
+    return A_loc, tau[:mn], J, ell
