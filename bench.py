@@ -279,13 +279,16 @@ def main():
     # critical-stream part + the bulk GEMM timed on its own stream (it overlaps the next pivot selection)
     apply_ms = (phases_acc.get("apply_trans_q", 0.0) + phases_acc.get("apply_trans_q_bulk", 0.0)) / args.steps
     achieved = tr_flops / (apply_ms * 1e-3) / 1e12 if apply_ms > 0 else None
-    traffic = None
+    traffic, traffic_note = None, None
     try:
-        traffic = json.load(open(NCU_SUMMARY)).get("dgemm_trailing_dram_bytes_per_launch")
+        ns = json.load(open(NCU_SUMMARY))
+        traffic = ns.get("dgemm_trailing_dram_bytes_per_launch")
+        traffic_note = ("dram read+write bytes of ONE launch (the C3 iteration-0 bulk GEMM, ncu --set full); its "
+                        "algorithmic bytes: %.4g" % ns.get("algorithmic_bytes_per_launch", float("nan")))
     except Exception:
         pass
     roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                "frac": (achieved / peak) if achieved else None, "traffic": traffic, "traffic_note": traffic_note,
                 "kernel": "a5 compact-WY trailing update (dgemm_kernel: W=V^T C, W=T^T W, C-=V W) per factorization; "
                           "the bulk C-=V W rows are timed with events on their own (low-priority) stream",
                 "algorithmic_flops_per_step": tr_flops, "kernel_ms_per_step": apply_ms,

@@ -120,7 +120,7 @@ int bqrrp_debug_panel(int64_t h, int64_t k, int64_t t, double* P, int64_t ld, co
  * NCCL all-reduce / broadcast on a multi-GPU node).  All pointers device, all calls stream-ordered. */
 
 /* a2 on the replicated sketch window MskT(s:n, :): LU pivots, J_qr touched set (tq[t] <- tsrc[t],
- * positions relative to s, *nt entries, capacity 2 min(n-s, d)), sketch rows and J(s:n) permuted
+ * positions relative to s, *nt entries in unspecified order, capacity 2 min(n-s, d)), sketch rows and J(s:n) permuted
  * (J may be NULL), R_sk in place, k = tri_rank (ref = |R_sk(0,0)| stored when first).
  * Synchronises the stream; *k_out host. */
 int bqrrp_step_pivots(int64_t n, int64_t d, int64_t s, int64_t kmax, double* MskT, int64_t ldm, int64_t* J,

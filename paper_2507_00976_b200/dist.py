@@ -141,6 +141,10 @@ def factor_dist(A_loc, m: int, n: int, b: int, d: int | None = None, seed: int =
         if ntv > 0:
             q = tq[:ntv].cpu().numpy().astype(np.int64) + s
             p = tsrc[:ntv].cpu().numpy().astype(np.int64) + s
+            # the kernel emits the touched set in atomic (per-rank) order: sort by destination so that slot t of
+            # the exchange buffer names the same column on every rank
+            o = np.argsort(q, kind="stable")
+            q, p = q[o], p[o]
             pack = np.where(bc.owner_of[p] == me, bc.loc_of[p], -1).astype(np.int32)
             unpack = np.where(bc.owner_of[q] == me, bc.loc_of[q], -1).astype(np.int32)
             buf = colmaj(m, ntv)
