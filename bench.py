@@ -10,9 +10,10 @@ config's synthetic matrix, inputs resident in HBM.  A is restored from a pristin
 every step OUTSIDE the timed events (the factorization is in place); each step is timed with CUDA events
 on the library's stream; the K step times are summed.  Inputs (34 GB at C3) are larger than L2.
 
-N > 1 (torchrun): each rank factors its own independent matrix (replicas, "scaling": "weak"); the
-distributed block-column factorization is the NEXT row of SURVEY §8(e).  value = total flops of all
-ranks / max-over-ranks time.
+N > 1 (torchrun): ONE distributed factorization of the same matrix (dist.py: 1-D block-cyclic columns,
+replicated sketch, NCCL exchanges; "scaling": "strong" — the N = 1 line is the same fixed workload, so it
+says "strong" too).  value = canonical flops of the one matrix / max-over-ranks time.  --replicas: each
+rank factors its own matrix instead ("scaling": "weak", value = flops of all ranks / max-over-ranks time).
 
 --impl reference: the reference arm of this tier is the plain CPU oracle (oracle/), timed on the host
 cores, each step a bounded sample of the workload (rank 0 only).
@@ -185,7 +186,7 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / max(len(times), 1),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": args.config + " " + CONFIGS[args.config]["desc"], "sample": f"{sm}x{sn}"},
         "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": cores, "kind": "oracle", "sample": desc},
         "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -329,7 +330,8 @@ def main():
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak" if args.replicas else "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"{args.config} {cfg['desc']}", "m": m, "n": n, "b": b, "d": d,
                        "parallelism": "replicas" if world > 1 else "single",

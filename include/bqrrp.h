@@ -44,8 +44,11 @@ typedef struct bqrrp_options {
      * reconstruction (default), 1 = the paper's single CholQR pass, 0 = Householder QR of
      * the panel (the paper's BQRRP_HQR variant).  Negative = default. */
     int cholqr_passes;
-    /* reserved (0) */
-    int reserved0;
+    /* 0 (default): a panel whose Cholesky QR breaks down (POTRF meets a non-positive pivot, e.g. a rank_tol
+     * far below the default) is re-factored by Householder QR (the BQRRP_HQR panel; SURVEY
+     * §8(f) N2) instead of failing; costs one host sync per panel.  1: no fallback, breakdown returns
+     * BQRRP_ENUMERIC. */
+    int no_hqr_fallback;
     /* optional host float[9] out: per-phase milliseconds in the order of SPEC's profile keys
      * {qrcp_wide, tri_rank, col_perm, qr_tall, apply_trans_q, sample_update, other, total} (a sequential
      * partition of the critical stream's timeline) followed by apply_trans_q_bulk, the duration of the
@@ -94,6 +97,13 @@ int bqrrp_debug_sketch(int64_t m, int64_t n, const double* A, int64_t lda, int64
 /* C = alpha op(A) op(B) + beta C with the DMMA engine; ta/tb: 0 = N, 1 = T. */
 int bqrrp_debug_gemm(int ta, int tb, int64_t M, int64_t N, int64_t K, double alpha, const double* A, int64_t lda,
                      const double* B, int64_t ldb, double beta, double* C, int64_t ldc, void* stream);
+
+/* X op(T) = B in place (B rows x n, ldb), op(T) upper triangular n x n: t_lower = 0 -> op(T) = T (upper
+ * part read), 1 -> op(T) = T^T (lower part read); unit = 1: unit diagonal assumed.  inverse = 0:
+ * blocked substitution (backward stable); 1: 64 x 64 diagonal blocks inverted and applied by DMMA (used by
+ * the panel on its well-conditioned triangles).  The panel's TRSM building block. */
+int bqrrp_debug_trsm(int64_t rows, int64_t n, const double* T, int64_t ldt, int t_lower, int unit, int inverse,
+                     double* B, int64_t ldb, void* stream);
 
 /* Partial-pivot LU of the w x d matrix L (in place): ipiv (device int64, min(w,d)) one-based LAPACK swap
  * list. */
@@ -150,6 +160,9 @@ int bqrrp_step_zero(int64_t rows, int64_t cols, double* X, int64_t ldx, void* st
 
 /* Number of CUDA kernels this library has launched in the calling process (all threads). */
 unsigned long long bqrrp_launch_count(void);
+/* Panels re-factored by Householder QR after a CholQR breakdown in the last bqrrp_factor* call on this
+ * thread (plus bqrrp_step_panel calls since). */
+long long bqrrp_panel_fallbacks(void);
 
 const char* bqrrp_strerror(int status);
 const char* bqrrp_last_error(void);

@@ -31,7 +31,7 @@ class BqrrpError(RuntimeError):
 
 
 class Options(ctypes.Structure):
-    _fields_ = [("rank_tol", ctypes.c_double), ("cholqr_passes", ctypes.c_int), ("reserved0", ctypes.c_int),
+    _fields_ = [("rank_tol", ctypes.c_double), ("cholqr_passes", ctypes.c_int), ("no_hqr_fallback", ctypes.c_int),
                 ("phase_ms", ctypes.POINTER(ctypes.c_float))]
 
 
@@ -59,6 +59,7 @@ def lib() -> ctypes.CDLL:
         L.bqrrp_last_error.restype = ctypes.c_char_p
         L.bqrrp_version.restype = ctypes.c_char_p
         L.bqrrp_launch_count.restype = ctypes.c_ulonglong
+        L.bqrrp_panel_fallbacks.restype = ctypes.c_longlong
         _lib = L
     return _lib
 
@@ -66,6 +67,11 @@ def lib() -> ctypes.CDLL:
 def launch_count() -> int:
     """Kernels launched by libbqrrp.so in this process so far."""
     return int(lib().bqrrp_launch_count())
+
+
+def panel_fallbacks() -> int:
+    """Panels of the last factor call (this thread) re-factored by Householder QR after a CholQR breakdown."""
+    return int(lib().bqrrp_panel_fallbacks())
 
 
 def default_rank_tol(m: int, n: int) -> float:
@@ -101,21 +107,23 @@ def workspace_query(m: int, n: int, b: int, d: int) -> int:
     return int(out.value)
 
 
-def _options(rank_tol, cholqr_passes, phases):
+def _options(rank_tol, cholqr_passes, phases, hqr_fallback=True):
     o = Options()
     o.rank_tol = float(rank_tol) if rank_tol else 0.0
     o.cholqr_passes = int(cholqr_passes)
-    o.reserved0 = 0
+    o.no_hqr_fallback = 0 if hqr_fallback else 1
     o.phase_ms = ctypes.cast(phases, ctypes.POINTER(ctypes.c_float)) if phases is not None else None
     return o
 
 
 def factor(A, b: int, d: int | None = None, seed: int = 0, rank_tol: float | None = None, cholqr_passes: int = 2,
-           workspace=None, tau=None, J=None, stream=None, phase_times: bool = False):
+           workspace=None, tau=None, J=None, stream=None, phase_times: bool = False, hqr_fallback: bool = True):
     """BQRRP of A in place (Alg. 1); returns (A, tau, J, rank[, phase_ms dict]).
 
     A: float64 CUDA tensor in column-major layout (m x n); overwritten in GEQP3 format.
     d: sketch rows (default b, gamma = 1 as in the paper's experiments).
+    hqr_fallback: a panel whose Cholesky QR breaks down is re-factored by Householder QR (else
+    BqrrpError status 1); panel_fallbacks() counts them.
     """
     import torch
 
@@ -132,7 +140,7 @@ def factor(A, b: int, d: int | None = None, seed: int = 0, rank_tol: float | Non
         ws_ptr, ws_bytes = ctypes.c_void_p(workspace.data_ptr()), workspace.numel() * workspace.element_size()
     rank = ctypes.c_int64(0)
     phases = (ctypes.c_float * len(PHASES))() if phase_times else None
-    opts = _options(rank_tol, cholqr_passes, phases)
+    opts = _options(rank_tol, cholqr_passes, phases, hqr_fallback)
     st = lib().bqrrp_factor_ex(m, n, ctypes.c_void_p(A.data_ptr()), lda, b, d, seed, ctypes.c_void_p(tau.data_ptr()),
                                ctypes.c_void_p(J.data_ptr()), ctypes.byref(rank), ws_ptr, ws_bytes,
                                _stream_ptr(stream), ctypes.byref(opts))
@@ -192,6 +200,18 @@ def debug_gemm(ta: bool, tb: bool, alpha, A, B, beta, C):
                                   _require_fortran_f64_cuda(B), float(beta), ctypes.c_void_p(C.data_ptr()),
                                   _require_fortran_f64_cuda(C), _stream_ptr()), "bqrrp_debug_gemm")
     return C
+
+
+def debug_trsm(T, B, t_lower: bool = False, unit: bool = False, inverse: bool = False):
+    """B <- B op(T)^{-1} in place (bqrrp_debug_trsm)."""
+    rows, n = B.shape
+    L = lib()
+    L.bqrrp_debug_trsm.argtypes = [ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int,
+                                   ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p]
+    _check(L.bqrrp_debug_trsm(rows, n, ctypes.c_void_p(T.data_ptr()), _require_fortran_f64_cuda(T), int(t_lower),
+                              int(unit), int(inverse), ctypes.c_void_p(B.data_ptr()), _require_fortran_f64_cuda(B),
+                              _stream_ptr()), "bqrrp_debug_trsm")
+    return B
 
 
 def debug_lu_pivots(L):

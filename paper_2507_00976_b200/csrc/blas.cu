@@ -227,22 +227,155 @@ static void trsm_base(Ctx& cx, int n, int64_t nr, const double* T, int64_t ldt, 
     BQ_LAUNCH_CHECK();
 }
 
-void trsm_right_upper(Ctx& cx, int64_t rows, int64_t n, const double* T, int64_t ldt, bool t_lower, bool unit,
-                      double* B, int64_t ldb)
+// ---- inverse-based base case (well-conditioned triangles only: CholQR / reconstruction factors)
+// The 64-wide diagonal blocks of op(T) are inverted once per TRSM call (one CTA per block, all blocks in
+// parallel); each base case is then X = B * inv(D), a 64-row x 64 x 64 DMMA product per CTA, in place,
+// with no per-unknown barrier.  Error ~ kappa(D) u per element (vs backward-stable substitution), hence
+// only used where op(T) is known to be well conditioned.
+
+// Dinv (64 x 64 per block, ld 64, zero-padded) = inv(op(T)(b0:b0+64, b0:b0+64)), op(T) upper.
+// Thread group (4 lanes) per column j of the inverse: back substitution x_i = (e_ij - sum U_il x_l) / U_ii,
+// i = j .. 0, the sum split over the 4 lanes and combined by shuffles.
+__global__ void __launch_bounds__(256) tri_inv_diag_kernel(int n, const double* __restrict__ T, int64_t ldt, int mode,
+                                                           int unit, double* __restrict__ Dinv)
 {
-    if (rows <= 0 || n <= 0) return;
+    extern __shared__ double ism[];
+    double(*U)[TRSM_NB + 1] = reinterpret_cast<double(*)[TRSM_NB + 1]>(ism);
+    double(*X)[TRSM_NB + 1] = reinterpret_cast<double(*)[TRSM_NB + 1]>(ism + TRSM_NB * (TRSM_NB + 1));
+    const int tid = threadIdx.x;
+    const int b0 = blockIdx.x * TRSM_NB, bn = (n - b0 < TRSM_NB) ? n - b0 : TRSM_NB;
+    const double* Tb = T + b0 + (int64_t)b0 * ldt;
+    for (int idx = tid; idx < TRSM_NB * TRSM_NB; idx += 256) {
+        int l = idx % TRSM_NB, t = idx / TRSM_NB;
+        double v = 0.0;
+        if (l < bn && t < bn && l <= t) {
+            v = (mode == 0) ? Tb[l + (int64_t)t * ldt] : Tb[t + (int64_t)l * ldt];
+            if (unit && l == t) v = 1.0;
+        }
+        U[l][t] = v;
+        X[l][t] = 0.0;
+    }
+    __syncthreads();
+    const int j = tid >> 2, q = tid & 3;
+    const bool col = j < bn;
+    for (int i = TRSM_NB - 1; i >= 0; --i) {
+        double part = 0.0;
+        if (col && i <= j)
+            for (int l = i + 1 + q; l <= j; l += 4) part = fma(U[i][l], X[l][j], part);
+        part += __shfl_xor_sync(0xffffffffu, part, 1);
+        part += __shfl_xor_sync(0xffffffffu, part, 2);
+        if (col && q == 0 && i <= j) X[i][j] = ((i == j ? 1.0 : 0.0) - part) / U[i][i];
+        __syncwarp();
+    }
+    __syncthreads();
+    double* D = Dinv + (int64_t)blockIdx.x * TRSM_NB * TRSM_NB;
+    for (int idx = tid; idx < TRSM_NB * TRSM_NB; idx += 256) D[idx] = X[idx % TRSM_NB][idx / TRSM_NB];
+}
+
+constexpr size_t TINV_SMEM = sizeof(double) * 2 * TRSM_NB * (TRSM_NB + 1);
+constexpr int TI_LD = TRSM_NB + 4;  // 4 mod 16 doubles: conflict-free DMMA fragment loads
+constexpr size_t TI_SMEM = sizeof(double) * 2 * TRSM_NB * TI_LD;
+
+// B(r0:r0+64, 0:n) <- B(r0:r0+64, 0:n) * Dinv (n <= 64), in place; 4 warps, each 32 x 32 (4 x 4 DMMA tiles).
+__global__ void __launch_bounds__(128) trsm_inv_apply_kernel(int n, int64_t nr, const double* __restrict__ Dinv,
+                                                             double* B, int64_t ldb)
+{
+    extern __shared__ __align__(16) double tsm[];
+    double* sB = tsm;                   // [k][r]
+    double* sD = tsm + TRSM_NB * TI_LD;  // [t][k]
+    const int tid = threadIdx.x;
+    const int64_t r0 = (int64_t)blockIdx.x * TRSM_NB;
+    for (int idx = tid; idx < TRSM_NB * TRSM_NB; idx += 128) {
+        int r = idx % TRSM_NB, k = idx / TRSM_NB;
+        bool ok = (k < n) && (r0 + r < nr);
+        cp_async8z(&sB[k * TI_LD + r], ok ? B + (r0 + r) + (int64_t)k * ldb : B, ok);
+        cp_async8z(&sD[k * TI_LD + r], Dinv + idx, true);  // Dinv[r + k*64] = D(r, k): sD[t = k][k' = r]
+    }
+    cp_async_wait_all();
+    __syncthreads();
+    const int lane = tid & 31, warp = tid >> 5, wm = warp & 1, wn = warp >> 1, gid = lane >> 2, tig = lane & 3;
+    double acc[4][4][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) acc[i][jj][0] = acc[i][jj][1] = 0.0;
+    const int kn = (n + 3) & ~3;
+    for (int kk = 0; kk < kn; kk += 4) {
+        double af[4], bf[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) af[i] = sB[(kk + tig) * TI_LD + wm * 32 + i * 8 + gid];
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) bf[jj] = sD[(wn * 32 + jj * 8 + gid) * TI_LD + kk + tig];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int jj = 0; jj < 4; ++jj) dmma_884(acc[i][jj][0], acc[i][jj][1], af[i], bf[jj]);
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                int64_t r = r0 + wm * 32 + i * 8 + gid;
+                int c = wn * 32 + jj * 8 + 2 * tig + h;
+                if (r < nr && c < n) B[r + (int64_t)c * ldb] = acc[i][jj][h];
+            }
+}
+
+constexpr int64_t TRSM_INV_MIN_ROWS = 4096;
+
+static void trsm_ru_rec(Ctx& cx, int64_t rows, int64_t n, const double* T, int64_t ldt, bool t_lower, bool unit,
+                        double* B, int64_t ldb, const double* Dinv)
+{
     if (n <= TRSM_NB) {
-        trsm_base(cx, (int)n, rows, T, ldt, t_lower ? 1 : 0, unit ? 1 : 0, B, ldb, 1);
+        if (Dinv) {
+            trsm_inv_apply_kernel<<<(unsigned)cdiv(rows, TRSM_NB), 128, TI_SMEM, cx.stream>>>((int)n, rows, Dinv, B,
+                                                                                               ldb);
+            BQ_LAUNCH_CHECK();
+        } else {
+            trsm_base(cx, (int)n, rows, T, ldt, t_lower ? 1 : 0, unit ? 1 : 0, B, ldb, 1);
+        }
         return;
     }
     int64_t n1 = cdiv(n / 2, TRSM_NB) * TRSM_NB;
     int64_t n2 = n - n1;
-    trsm_right_upper(cx, rows, n1, T, ldt, t_lower, unit, B, ldb);
+    trsm_ru_rec(cx, rows, n1, T, ldt, t_lower, unit, B, ldb, Dinv);
     if (!t_lower)  // op(T)(0:n1, n1:n) = T(0:n1, n1:n)
         gemm(cx, false, false, rows, n2, n1, -1.0, B, ldb, T + n1 * ldt, ldt, 1.0, B + n1 * ldb, ldb);
     else  // op(T)(0:n1, n1:n) = T(n1:n, 0:n1)^T
         gemm(cx, false, true, rows, n2, n1, -1.0, B, ldb, T + n1, ldt, 1.0, B + n1 * ldb, ldb);
-    trsm_right_upper(cx, rows, n2, T + n1 + n1 * ldt, ldt, t_lower, unit, B + n1 * ldb, ldb);
+    trsm_ru_rec(cx, rows, n2, T + n1 + n1 * ldt, ldt, t_lower, unit, B + n1 * ldb, ldb,
+                Dinv ? Dinv + (n1 / TRSM_NB) * TRSM_NB * TRSM_NB : nullptr);
+}
+
+void trsm_right_upper(Ctx& cx, int64_t rows, int64_t n, const double* T, int64_t ldt, bool t_lower, bool unit,
+                      double* B, int64_t ldb, bool well_conditioned)
+{
+    if (rows <= 0 || n <= 0) return;
+    static int inv_mode = -1;
+    if (inv_mode < 0) {
+        const char* e = std::getenv("BQRRP_TRSM_INV");  // 0: substitution everywhere (A/B experiments)
+        inv_mode = (e && e[0] == '0') ? 0 : 1;
+    }
+    // the inversion launch pays off only when the apply kernels are wide (tall B: the CholQR passes and Y2)
+    if (!well_conditioned || !inv_mode || rows < TRSM_INV_MIN_ROWS) {
+        trsm_ru_rec(cx, rows, n, T, ldt, t_lower, unit, B, ldb, nullptr);
+        return;
+    }
+    static bool attr = false;
+    if (!attr) {
+        BQ_CUDA(cudaFuncSetAttribute(trsm_inv_apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TI_SMEM));
+        BQ_CUDA(cudaFuncSetAttribute(tri_inv_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TINV_SMEM));
+        attr = true;
+    }
+    const size_t mark = cx.ws_used;
+    const int64_t nblk = cdiv(n, TRSM_NB);
+    double* Dinv = cx.alloc((size_t)nblk * TRSM_NB * TRSM_NB);
+    tri_inv_diag_kernel<<<(unsigned)nblk, 256, TINV_SMEM, cx.stream>>>((int)n, T, ldt, t_lower ? 1 : 0, unit ? 1 : 0, Dinv);
+    BQ_LAUNCH_CHECK();
+    trsm_ru_rec(cx, rows, n, T, ldt, t_lower, unit, B, ldb, Dinv);
+    cx.ws_used = mark;
 }
 
 void trsm_left_lower_unit(Ctx& cx, int64_t n, int64_t cols, const double* L, int64_t ldl, double* B, int64_t ldb)
@@ -315,7 +448,7 @@ void potrf_lower(Ctx& cx, int64_t n, double* G, int64_t ldg)
         int64_t rest = n - j0 - jb;
         if (rest > 0) {
             double* G21 = Gjj + jb;
-            trsm_right_upper(cx, rest, jb, Gjj, ldg, /*t_lower=*/true, /*unit=*/false, G21, ldg);
+            trsm_right_upper(cx, rest, jb, Gjj, ldg, /*t_lower=*/true, /*unit=*/false, G21, ldg, true);
             gemm(cx, false, true, rest, rest, jb, -1.0, G21, ldg, G21, ldg, 1.0, G21 + jb * ldg, ldg, /*tri=*/true);
         }
     }
@@ -370,7 +503,7 @@ void getrf_nopiv_sign(Ctx& cx, int64_t n, double* Q, int64_t ldq, double* S)
         if (rest > 0) {
             // U12 = L11^{-1} A12 ; L21 = A21 U11^{-1} ; A22 -= L21 U12
             trsm_left_lower_unit(cx, jb, rest, Qjj, ldq, Qjj + jb * ldq, ldq);
-            trsm_right_upper(cx, rest, jb, Qjj, ldq, false, false, Qjj + jb, ldq);
+            trsm_right_upper(cx, rest, jb, Qjj, ldq, false, false, Qjj + jb, ldq, true);
             gemm(cx, false, false, rest, rest, jb, -1.0, Qjj + jb, ldq, Qjj + jb * ldq, ldq, 1.0, Qjj + jb + jb * ldq,
                  ldq);
         }

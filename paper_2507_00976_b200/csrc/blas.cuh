@@ -10,8 +10,11 @@ void gemm(Ctx& cx, bool ta, bool tb, int64_t M, int64_t N, int64_t K, double alp
 
 // X op(T) = B, right side, op(T) upper triangular (n x n), in place on B (rows x n).
 //   t_lower = false: T stored upper, op(T) = T;  t_lower = true: T stored lower, op(T) = T^T.
+//   well_conditioned: op(T) is known to be well conditioned (Cholesky factors of CholQR Gram matrices,
+//   the reconstruction's U and unit-lower L): base cases multiply by inverted 64 x 64 diagonal blocks
+//   (DMMA) instead of substituting; workspace: ceil(n/64) * 4096 doubles.
 void trsm_right_upper(Ctx& cx, int64_t rows, int64_t n, const double* T, int64_t ldt, bool t_lower, bool unit,
-                      double* B, int64_t ldb);
+                      double* B, int64_t ldb, bool well_conditioned = false);
 
 // L X = B, left side, L unit lower (n x n), in place on B (n x cols).
 void trsm_left_lower_unit(Ctx& cx, int64_t n, int64_t cols, const double* L, int64_t ldl, double* B, int64_t ldb);

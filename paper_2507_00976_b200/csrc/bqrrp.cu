@@ -22,6 +22,7 @@
 namespace bqrrp {
 
 static thread_local std::string g_last_error;
+thread_local long long g_panel_fallbacks = 0;
 unsigned long long g_launches = 0;
 
 // ----------------------------------------------------------------------------------- small kernels
@@ -118,7 +119,7 @@ static Layout layout(int64_t m, int64_t n, int64_t b, int64_t d)
     size_t p = (size_t)d;
     size_t sq = r(p * p) * 7 + r(p) + r(2 * 160 * 33 + 160 * 32 * 32) + r(64) + r((size_t)n * p);
     size_t lu = r(2 * 160 * 34) + r(64);
-    size_t pn = r(bb * bb) * 8 + r(bb);
+    size_t pn = r(bb * bb) * 8 + r(bb) + r((size_t)cdiv((int64_t)bb, 64) * 4096 + 4096);  // + TRSM Dinv
     size_t T = sq > pn ? sq : pn;
     T = T > lu ? T : lu;
     size_t sk = r((size_t)16 * (p > bb ? p * p : bb * bb) + (size_t)4 * 1024 * 1024);
@@ -144,7 +145,7 @@ static int validate(int64_t m, int64_t n, const void* A, int64_t lda, int64_t b,
 // ----------------------------------------------------------------------------------- the driver
 static int64_t factor_impl(Ctx& cx, Ctx* cxb, cudaEvent_t ev_top, cudaEvent_t ev_bulk, int64_t m, int64_t n, double* A,
                            int64_t lda, int64_t b, int64_t d, uint64_t seed, double* tau, int64_t* J, double rank_tol,
-                           int passes, int* host_flags)
+                           int passes, bool hqr_fallback, int* host_flags)
 {
     const int64_t mn = imin(m, n);
     double* MskT = cx.alloc((size_t)n * d);
@@ -216,7 +217,7 @@ static int64_t factor_impl(Ctx& cx, Ctx* cxb, cudaEvent_t ev_top, cudaEvent_t ev
         extract_rsk11_kernel<<<(unsigned)imin(cdiv(k * k, 256), 4 * cx.num_sms), 256, 0, cx.stream>>>(k, MskT + s, n,
                                                                                                         Rsk11);
         BQ_LAUNCH_CHECK();
-        panel_factor(cx, m, A, lda, s, k, Rsk11, tau, passes, Vp, Tp);
+        g_panel_fallbacks += panel_factor(cx, m, A, lda, s, k, Rsk11, tau, passes, Vp, Tp, hqr_fallback);
         // ---- a5 (the bulk rows overlap the sketch update and the next a2) and a7
         cx.mark(PH_APPLY_QT);
         const bool terminal = (k < kmax || c == n || r == m);
@@ -309,6 +310,7 @@ int bqrrp_factor_ex(int64_t m, int64_t n, double* A, int64_t lda, int64_t b, int
     if (v != 0) return v;
     double rank_tol = (opts && opts->rank_tol > 0) ? opts->rank_tol : 10.0 * 0x1p-53 * sqrt((double)(m > n ? m : n));
     int passes = (opts && opts->cholqr_passes >= 0 && opts->cholqr_passes <= 4) ? opts->cholqr_passes : 2;
+    g_panel_fallbacks = 0;
     return guarded([&]() -> int {
         Ctx cx;
         setup_ctx(cx, stream);
@@ -376,7 +378,7 @@ int bqrrp_factor_ex(int64_t m, int64_t n, double* A, int64_t lda, int64_t b, int
         };
         try {
             ell = factor_impl(cx, &cxb, ev_top, ev_bulk, m, n, A, lda, b, d, seed, tau, J, rank_tol, passes,
-                              pinned_flags());
+                              !(opts && opts->no_hqr_fallback), pinned_flags());
         } catch (...) {
             cleanup();
             if (own) cudaFreeAsync(ws, user);
@@ -481,6 +483,27 @@ int bqrrp_debug_gemm(int ta, int tb, int64_t M, int64_t N, int64_t K, double alp
         Layout L{0, 0, sk * 8, 0};
         carve(cx, ws, sk * 8 + 4096, L);
         gemm(cx, ta != 0, tb != 0, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+        cudaFreeAsync(ws, cx.stream);
+        BQ_CUDA(cudaStreamSynchronize(cx.stream));
+        return 0;
+    });
+}
+
+int bqrrp_debug_trsm(int64_t rows, int64_t n, const double* T, int64_t ldt, int t_lower, int unit, int inverse,
+                     double* B, int64_t ldb, void* stream)
+{
+    if (rows < 0) return -1;
+    if (n < 0) return -2;
+    return guarded([&]() -> int {
+        Ctx cx;
+        setup_ctx(cx, stream);
+        size_t sk = (size_t)16 * 64 * 64 + (4u << 20) / 8;
+        size_t bytes = (sk + (size_t)cdiv(imax(n, 1), 64) * 4096 + 8192) * 8;
+        void* ws = nullptr;
+        BQ_CUDA(cudaMallocAsync(&ws, bytes, cx.stream));
+        Layout L{0, 0, sk * 8, 0};
+        carve(cx, ws, bytes, L);
+        trsm_right_upper(cx, rows, n, T, ldt, t_lower != 0, unit != 0, B, ldb, inverse != 0);
         cudaFreeAsync(ws, cx.stream);
         BQ_CUDA(cudaStreamSynchronize(cx.stream));
         return 0;
@@ -595,7 +618,7 @@ int bqrrp_debug_panel(int64_t h, int64_t k, int64_t t, double* P, int64_t ld, co
     return guarded([&]() -> int {
         Ctx cx;
         setup_ctx(cx, stream);
-        size_t wsb = (size_t)(64u << 20) + ((size_t)h * k + (size_t)8 * k * k + (size_t)2 * k * (t + 1)) * 8 +
+        size_t wsb = (size_t)(64u << 20) + ((size_t)h * k + (size_t)9 * k * k + (size_t)2 * k * (t + 1)) * 8 +
                      (size_t)16 * k * k * 8;
         void* ws = nullptr;
         BQ_CUDA(cudaMallocAsync(&ws, wsb, cx.stream));
@@ -631,6 +654,8 @@ const char* bqrrp_strerror(int status)
 const char* bqrrp_last_error(void) { return g_last_error.c_str(); }
 
 unsigned long long bqrrp_launch_count(void) { return g_launches; }
+
+long long bqrrp_panel_fallbacks(void) { return g_panel_fallbacks; }
 
 const char* bqrrp_version(void) { return "bqrrp-b200 0.1 (sm_100a, DMMA f64)"; }
 

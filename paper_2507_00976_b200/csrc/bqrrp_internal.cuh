@@ -38,8 +38,12 @@ void permute_vector(Ctx& cx, int64_t* J, const Touched& T, int64_t* tmp);
 // Householder panel of the paper's BQRRP_HQR variant — of the panel A(s:m, s:s+k) written in
 // GEQP3 format in place (R11 on/above, V below, tau(s:s+k)); V (h x k, ld h, explicit: unit diagonal,
 // zeros above) and the compact-WY T (k x k, ld k) are returned in caller-owned buffers.
-void panel_factor(Ctx& cx, int64_t m, double* A, int64_t lda, int64_t s, int64_t k, const double* Rsk11, double* tau,
-                  int passes, double* V, double* T);
+// Panels re-factored by Householder QR after a CholQR breakdown (bqrrp_panel_fallbacks()).
+extern thread_local long long g_panel_fallbacks;
+// hqr_fallback: after the Cholesky passes, read the POTRF breakdown flag (one host sync) and on a breakdown
+// factor this panel with Householder QR instead (returns 1; 0 otherwise; the flag is cleared).
+int panel_factor(Ctx& cx, int64_t m, double* A, int64_t lda, int64_t s, int64_t k, const double* Rsk11, double* tau,
+                 int passes, double* V, double* T, bool hqr_fallback = false);
 // a5: C = A(s:m, s+k:n) <- C - V T^T (V^T C).  With cx_bulk, rows k:h of the last GEMM run on
 // cx_bulk->stream after ev_top (recorded on cx.stream), and ev_bulk marks their completion.
 void wy_update(Ctx& cx, Ctx* cx_bulk, int64_t m, int64_t n, double* A, int64_t lda, int64_t s, int64_t k,

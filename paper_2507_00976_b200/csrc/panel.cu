@@ -4,7 +4,8 @@
 //
 //   M_pre  = P(:, 0:k) R_sk11^{-1}                               (Alg. 3 step cholqr:precond)
 //   for pass in 1..passes:  G = Q^T Q, G = C C^T, Q <- Q C^{-T}   (cholqr; passes = 2 is CholQR2,
-//                                                                  DESIGN.md §7.3)
+//                                                                  DESIGN.md §7.3, SURVEY App. B1;
+//                                                                  a breakdown falls back to HQR)
 //   Q - [S; 0] = L U (no pivoting, S_jj = -sgn(Q'_jj) on the fly)   (cholqr:orhr_col, BD2015 Alg. 5/6;
 //   V = L, T = -U S Y1^{-T}, tau = diag(T)                           P:697-701)
 //   R11 = diag(S) C_last^T ... C_1^T R_sk11                        (cholqr:undo_precond, reading Z7)
@@ -49,13 +50,13 @@ __global__ void write_panel_kernel(int64_t h, int64_t k, double* Q, int64_t ldq,
     }
 }
 
-void panel_factor(Ctx& cx, int64_t m, double* A, int64_t lda, int64_t s, int64_t k, const double* Rsk11, double* tau,
-                  int passes, double* V, double* T)
+int panel_factor(Ctx& cx, int64_t m, double* A, int64_t lda, int64_t s, int64_t k, const double* Rsk11, double* tau,
+                 int passes, double* V, double* T, bool hqr_fallback)
 {
     const int64_t h = m - s;
     if (passes == 0) {  // BQRRP_HQR: Householder QR of the panel itself
         householder_panel(cx, A + s + s * lda, lda, h, k, tau + s, V, T);
-        return;
+        return 0;
     }
     size_t mark = cx.ws_used;
     double* Q = V;  // h x k (ld h): M_pre -> Q_chol -> reconstruction L -> explicit V
@@ -64,24 +65,46 @@ void panel_factor(Ctx& cx, int64_t m, double* A, int64_t lda, int64_t s, int64_t
     double* S = cx.alloc((size_t)k);
     double* Wr = cx.alloc((size_t)k * k);
     double* Wr2 = cx.alloc((size_t)k * k);
+    double* Mb = cx.alloc((size_t)k * k);
     double* Ap = A + s + s * lda;
     unsigned eb = (unsigned)imin(cdiv(h * k, 256), 8 * cx.num_sms);
 
     // M_pre = P(:, 0:k) R_sk11^{-1}
     copy_matrix(cx, h, k, Ap, lda, Q, h);
     trsm_right_upper(cx, h, k, Rsk11, k, false, false, Q, h);
-    // Cholesky QR passes
+    // Cholesky QR passes; the last pass's TRSM is applied only to the top k rows here and folded into the
+    // reconstruction's TRSM below (Y2 = Q_prev,2 C^{-T} U^{-1} = Q_prev,2 (U C^T)^{-1})
     for (int p = 0; p < passes; ++p) {
         gemm(cx, true, false, k, k, h, 1.0, Q, h, Q, h, 0.0, Cf[p], k, /*tri=*/true);
         potrf_lower(cx, k, Cf[p], k);
-        trsm_right_upper(cx, h, k, Cf[p], k, /*t_lower=*/true, false, Q, h);
+        if (p + 1 < passes) trsm_right_upper(cx, h, k, Cf[p], k, /*t_lower=*/true, false, Q, h, true);
     }
-    // Householder reconstruction
-    getrf_nopiv_sign(cx, k, Q, h, S);
-    if (h > k) trsm_right_upper(cx, h - k, k, Q, h, false, false, Q + k, h);  // Y2 = Q2 U^{-1}
+    if (hqr_fallback) {  // CholQR breakdown (POTRF non-positive pivot): this panel by Householder QR instead
+        int info = 0;
+        BQ_CUDA(cudaMemcpyAsync(&info, cx.flags + F_POTRF_INFO, sizeof(int), cudaMemcpyDeviceToHost, cx.stream));
+        BQ_CUDA(cudaStreamSynchronize(cx.stream));
+        if (info) {
+            BQ_CUDA(cudaMemsetAsync(cx.flags + F_POTRF_INFO, 0, sizeof(int), cx.stream));
+            cx.ws_used = mark;
+            householder_panel(cx, Ap, lda, h, k, tau + s, V, T);
+            return 1;
+        }
+    }
+    const double* Cl = Cf[passes - 1];
+    // Householder reconstruction on the top k x k of Q_last = Q C^{-T}
+    copy_matrix(cx, k, k, Q, h, Wr, k);
+    trsm_right_upper(cx, k, k, Cl, k, /*t_lower=*/true, false, Wr, k, true);
+    getrf_nopiv_sign(cx, k, Wr, k, S);
+    if (h > k) {
+        copy_matrix(cx, k, k, Wr, k, Wr2, k);
+        zero_triangle(cx, 'U', k, k, Wr2, k);                                       // U
+        gemm(cx, false, true, k, k, k, 1.0, Wr2, k, Cl, k, 0.0, Mb, k);             // U C^T (upper)
+        trsm_right_upper(cx, h - k, k, Mb, k, false, false, Q + k, h, true);         // Y2
+    }
+    copy_matrix(cx, k, k, Wr, k, Q, h);  // L \ U on top
     build_t_rhs_kernel<<<(unsigned)imin(cdiv(k * k, 256), 4 * cx.num_sms), 256, 0, cx.stream>>>(k, Q, h, S, T);
     BQ_LAUNCH_CHECK();
-    trsm_right_upper(cx, k, k, Q, h, /*t_lower=*/true, /*unit=*/true, T, k);  // T Y1^T = -U S
+    trsm_right_upper(cx, k, k, Q, h, /*t_lower=*/true, /*unit=*/true, T, k, true);  // T Y1^T = -U S
     zero_triangle(cx, 'U', k, k, T, k);
     diag_to_tau_kernel<<<(unsigned)cdiv(k, 128), 128, 0, cx.stream>>>(k, T, tau + s);
     BQ_LAUNCH_CHECK();
@@ -94,6 +117,7 @@ void panel_factor(Ctx& cx, int64_t m, double* A, int64_t lda, int64_t s, int64_t
     write_panel_kernel<<<eb, 256, 0, cx.stream>>>(h, k, Q, h, Wr, S, Ap, lda);
     BQ_LAUNCH_CHECK();
     cx.ws_used = mark;
+    return 0;
 }
 
 void wy_update(Ctx& cx, Ctx* cx_bulk, int64_t m, int64_t n, double* A, int64_t lda, int64_t s, int64_t k,

@@ -213,14 +213,14 @@ int bqrrp_step_panel(int64_t h, int64_t k, double* P, int64_t ldp, const double*
     if (k < 1 || k > h) return -2;
     if (cholqr_passes < 0 || cholqr_passes > 4) return -10;
     return step_guard([&]() -> int {
-        size_t bytes = ((size_t)k * k * 12 + (size_t)k + 2 * 160 * 33 + 160 * 32 * 32 + 4096) * 8;
+        size_t bytes = ((size_t)k * k * 12 + (size_t)k + 2 * 160 * 33 + 160 * 32 * 32 + 4096 + 64 * (size_t)k + 8192) * 8;
         StepWs sw(stream, bytes, (size_t)16 * k * k * 8 + (4u << 20));
         Ctx& cx = sw.cx;
         double* Rsk11 = cx.alloc((size_t)k * k);
         extract_rsk_kernel<<<(unsigned)imin(cdiv(k * k, 256), 4 * cx.num_sms), 256, 0, cx.stream>>>(k, MskT_s, ldm,
                                                                                                     Rsk11);
         BQ_LAUNCH_CHECK();
-        panel_factor(cx, h, P, ldp, 0, k, Rsk11, tau, cholqr_passes, V, T);
+        g_panel_fallbacks += panel_factor(cx, h, P, ldp, 0, k, Rsk11, tau, cholqr_passes, V, T, /*hqr_fallback=*/true);
         int info = 0;
         BQ_CUDA(cudaMemcpyAsync(&info, cx.flags + F_POTRF_INFO, sizeof(int), cudaMemcpyDeviceToHost, cx.stream));
         BQ_CUDA(cudaStreamSynchronize(cx.stream));
