@@ -55,6 +55,10 @@ typedef struct bqrrp_options {
      * bulk trailing-update GEMM that runs concurrently on the low-priority stream;
      * NULL = no timing (timing adds one event pair per phase). */
     float* phase_ms;
+    /* 0 (default): the bulk rows of the trailing update run on a low-priority stream, overlapping the sketch
+     * update and the next pivot selection.  1: everything on one stream, serialised (the
+     * per-phase times then partition the whole step; used to measure each phase alone). */
+    int no_lookahead;
 } bqrrp_options;
 
 /* Bytes of device workspace bqrrp_factor needs for an m x n matrix with block b and sketch d. */

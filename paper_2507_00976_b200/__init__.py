@@ -32,7 +32,7 @@ class BqrrpError(RuntimeError):
 
 class Options(ctypes.Structure):
     _fields_ = [("rank_tol", ctypes.c_double), ("cholqr_passes", ctypes.c_int), ("no_hqr_fallback", ctypes.c_int),
-                ("phase_ms", ctypes.POINTER(ctypes.c_float))]
+                ("phase_ms", ctypes.POINTER(ctypes.c_float)), ("no_lookahead", ctypes.c_int)]
 
 
 def lib() -> ctypes.CDLL:
@@ -107,8 +107,9 @@ def workspace_query(m: int, n: int, b: int, d: int) -> int:
     return int(out.value)
 
 
-def _options(rank_tol, cholqr_passes, phases, hqr_fallback=True):
+def _options(rank_tol, cholqr_passes, phases, hqr_fallback=True, lookahead=True):
     o = Options()
+    o.no_lookahead = 0 if lookahead else 1
     o.rank_tol = float(rank_tol) if rank_tol else 0.0
     o.cholqr_passes = int(cholqr_passes)
     o.no_hqr_fallback = 0 if hqr_fallback else 1
@@ -117,13 +118,14 @@ def _options(rank_tol, cholqr_passes, phases, hqr_fallback=True):
 
 
 def factor(A, b: int, d: int | None = None, seed: int = 0, rank_tol: float | None = None, cholqr_passes: int = 2,
-           workspace=None, tau=None, J=None, stream=None, phase_times: bool = False, hqr_fallback: bool = True):
+           workspace=None, tau=None, J=None, stream=None, phase_times: bool = False, hqr_fallback: bool = True, lookahead: bool = True):
     """BQRRP of A in place (Alg. 1); returns (A, tau, J, rank[, phase_ms dict]).
 
     A: float64 CUDA tensor in column-major layout (m x n); overwritten in GEQP3 format.
     d: sketch rows (default b, gamma = 1 as in the paper's experiments).
     hqr_fallback: a panel whose Cholesky QR breaks down is re-factored by Householder QR (else
     BqrrpError status 1); panel_fallbacks() counts them.
+    lookahead: False runs every step on one stream (phase times then measure each step alone).
     """
     import torch
 
@@ -140,7 +142,7 @@ def factor(A, b: int, d: int | None = None, seed: int = 0, rank_tol: float | Non
         ws_ptr, ws_bytes = ctypes.c_void_p(workspace.data_ptr()), workspace.numel() * workspace.element_size()
     rank = ctypes.c_int64(0)
     phases = (ctypes.c_float * len(PHASES))() if phase_times else None
-    opts = _options(rank_tol, cholqr_passes, phases, hqr_fallback)
+    opts = _options(rank_tol, cholqr_passes, phases, hqr_fallback, lookahead)
     st = lib().bqrrp_factor_ex(m, n, ctypes.c_void_p(A.data_ptr()), lda, b, d, seed, ctypes.c_void_p(tau.data_ptr()),
                                ctypes.c_void_p(J.data_ptr()), ctypes.byref(rank), ws_ptr, ws_bytes,
                                _stream_ptr(stream), ctypes.byref(opts))

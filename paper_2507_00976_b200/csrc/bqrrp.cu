@@ -377,7 +377,7 @@ int bqrrp_factor_ex(int64_t m, int64_t n, double* A, int64_t lda, int64_t b, int
             cx.stream = user;
         };
         try {
-            ell = factor_impl(cx, &cxb, ev_top, ev_bulk, m, n, A, lda, b, d, seed, tau, J, rank_tol, passes,
+            ell = factor_impl(cx, (opts && opts->no_lookahead) ? nullptr : &cxb, ev_top, ev_bulk, m, n, A, lda, b, d, seed, tau, J, rank_tol, passes,
                               !(opts && opts->no_hqr_fallback), pinned_flags());
         } catch (...) {
             cleanup();

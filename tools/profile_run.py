@@ -15,6 +15,7 @@ import paper_2507_00976_b200 as bq  # noqa: E402
 name = sys.argv[1] if len(sys.argv) > 1 else "C2"
 warm = int(sys.argv[sys.argv.index("--warm") + 1]) if "--warm" in sys.argv else 1
 passes = int(sys.argv[sys.argv.index("--passes") + 1]) if "--passes" in sys.argv else 2
+lookahead = "--no-lookahead" not in sys.argv
 cfg = bench.CONFIGS[name]
 m, n, b, d = cfg["m"], cfg["n"], cfg["b"], cfg["d"]
 A0 = inputs.gaussian_cuda(m, n, seed=0)
@@ -25,6 +26,7 @@ for i in range(warm + 1):
     torch.cuda.synchronize()
     if i == warm:
         torch.cuda.nvtx.range_push("timed")
-    out = bq.factor(A, b, d, seed=0, workspace=ws, phase_times=True, cholqr_passes=passes)
+    out = bq.factor(A, b, d, seed=0, workspace=ws, phase_times=True, cholqr_passes=passes,
+                    lookahead=lookahead)
     torch.cuda.synchronize()
-print(name, "passes", passes, "rank", out[3], "phases(ms)", {k: round(v, 2) for k, v in out[4].items()})
+print(name, "passes", passes, "lookahead", lookahead, "rank", out[3], "phases(ms)", {k: round(v, 2) for k, v in out[4].items()})
