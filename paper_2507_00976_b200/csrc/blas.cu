@@ -45,19 +45,21 @@ template <class Cfg, bool TA, bool TB>
 static void launch_gemm_t(Ctx& cx, const GemmArgs& g, dim3 grid)
 {
     static bool attr_set = false;
-    constexpr size_t sm = dgemm_smem_bytes<Cfg, TA, TB>();
+    constexpr size_t sm = dgemm2_smem_bytes<Cfg, TA, TB>();
     if (!attr_set) {
-        BQ_CUDA(cudaFuncSetAttribute(dgemm_kernel<Cfg, TA, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        BQ_CUDA(cudaFuncSetAttribute(dgemm2_kernel<Cfg, TA, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
         attr_set = true;
     }
-    dgemm_kernel<Cfg, TA, TB><<<grid, Cfg::THREADS, sm, cx.stream>>>(g);
+    dgemm2_kernel<Cfg, TA, TB><<<grid, Cfg::THREADS, sm, cx.stream>>>(g, dgemm2_vec_ok(g));
     BQ_LAUNCH_CHECK();
 }
 
 template <class Cfg>
-static void launch_gemm(Ctx& cx, bool ta, bool tb, const GemmArgs& g, int nsplit)
+static void launch_gemm(Ctx& cx, bool ta, bool tb, const GemmArgs& g, int nsplit, int ctas_per_sm)
 {
-    dim3 grid((unsigned)(cdiv(g.M, Cfg::BM) * cdiv(g.N, Cfg::BN)), 1, (unsigned)nsplit);
+    int64_t tiles = cdiv(g.M, Cfg::BM) * cdiv(g.N, Cfg::BN);
+    if (ctas_per_sm > 0) tiles = imin(tiles, (int64_t)ctas_per_sm * cx.num_sms);  // persistent
+    dim3 grid((unsigned)tiles, 1, (unsigned)nsplit);
     if (!ta && !tb) launch_gemm_t<Cfg, false, false>(cx, g, grid);
     else if (ta && !tb) launch_gemm_t<Cfg, true, false>(cx, g, grid);
     else if (!ta && tb) launch_gemm_t<Cfg, false, true>(cx, g, grid);
@@ -68,30 +70,30 @@ static void launch_gemm(Ctx& cx, bool ta, bool tb, const GemmArgs& g, int nsplit
 // small and skinny GEMMs of the recursions).  Split-K (fixed slices, fixed-order sum) when even the
 // chosen tiling leaves the SMs idle and K is long.
 void gemm(Ctx& cx, bool ta, bool tb, int64_t M, int64_t N, int64_t K, double alpha, const double* A, int64_t lda,
-          const double* B, int64_t ldb, double beta, double* C, int64_t ldc, bool tri)
+          const double* B, int64_t ldb, double beta, double* C, int64_t ldc, bool tri, int ctas_per_sm)
 {
     if (M <= 0 || N <= 0) return;
     auto ntiles = [&](int bm, int bn) {
         int64_t tm = cdiv(M, bm), tn = cdiv(N, bn);
         return tri ? (tm * tn + tm) / 2 : tm * tn;
     };
-    // 64x64 / 3 stages / grouped rasterisation is the best tile on every large shape and operand order
-    // (33.3-34.3 TFLOP/s, profiles/gemm_tune_r01c_raster.json); 64x32 gives more CTAs to small GEMMs.
+    // v2 64x64 / BK 16 / 3 stages / grouped rasterisation is the best tile on every large shape and operand
+    // order (35.3-36.0 TFLOP/s, profiles/gemm_tune_r01d_v2.json); 64x32 gives more CTAs to small GEMMs.
     int cfg;  // 1 mid (64x64), 2 small (64x32)
     int bm, bn;
-    if (N > 32 && ntiles(CfgMid::BM, CfgMid::BN) >= cx.num_sms) { cfg = 1; bm = CfgMid::BM; bn = CfgMid::BN; }
-    else { cfg = 2; bm = CfgSmall::BM; bn = CfgSmall::BN; }
+    if (N > 32 && ntiles(Cfg2Mid::BM, Cfg2Mid::BN) >= cx.num_sms) { cfg = 1; bm = Cfg2Mid::BM; bn = Cfg2Mid::BN; }
+    else { cfg = 2; bm = Cfg2Small::BM; bn = Cfg2Small::BN; }
     int64_t tiles = ntiles(bm, bn);
     int nsplit = 1;
     int64_t kchunk = K > 0 ? K : 1;
-    if (K >= 256 && tiles < 2 * cx.num_sms && cx.splitk) {
+    if (K >= 256 && tiles < 2 * cx.num_sms && cx.splitk && ctas_per_sm == 0) {
         int64_t want = cdiv(2 * cx.num_sms, tiles);
         want = imin(want, 32);
         want = imin(want, K / 128);
         int64_t cap = (int64_t)(cx.splitk_elems / (size_t)(M * N));
         want = imin(want, cap);
         if (want >= 2) {
-            kchunk = cdiv(cdiv(K, want), GEMM_BK) * GEMM_BK;
+            kchunk = cdiv(cdiv(K, want), Cfg2Mid::BK) * Cfg2Mid::BK;
             nsplit = (int)cdiv(K, kchunk);
         }
     }
@@ -103,8 +105,8 @@ void gemm(Ctx& cx, bool ta, bool tb, int64_t M, int64_t N, int64_t K, double alp
         cudaEventCreate(&rec.e1);
         cudaEventRecord(rec.e0, cx.stream);
     }
-    if (cfg == 1) launch_gemm<CfgMid>(cx, ta, tb, g, nsplit);
-    else launch_gemm<CfgSmall>(cx, ta, tb, g, nsplit);
+    if (cfg == 1) launch_gemm<Cfg2Mid>(cx, ta, tb, g, nsplit, ctas_per_sm);
+    else launch_gemm<Cfg2Small>(cx, ta, tb, g, nsplit, ctas_per_sm);
     if (nsplit > 1) {
         int64_t total = M * N;
         int blocks = (int)imin(cdiv(total, 256), 4 * cx.num_sms);

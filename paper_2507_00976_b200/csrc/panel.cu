@@ -138,6 +138,9 @@ void wy_update(Ctx& cx, Ctx* cx_bulk, int64_t m, int64_t n, double* A, int64_t l
     BQ_CUDA(cudaEventRecord(ev_top, cx.stream));
     BQ_CUDA(cudaStreamWaitEvent(cx_bulk->stream, ev_top, 0));
     if (cx_bulk->timer) cx_bulk->timer->begin_interval(cx_bulk->stream, PH_APPLY_QT_BULK);
+    // one CTA per tile: the high-priority GEMMs of the sketch update and the next pivot selection take SMs
+    // as the bulk's CTAs retire (a persistent bulk with 2-4 CTAs/SM starved them: C3 +0.5-0.8 s,
+    // profiles/bulk_persistent_r01.json)
     gemm(*cx_bulk, false, false, h - k, t, k, -1.0, V + k, h, W2, k, 1.0, C + k, lda);
     if (cx_bulk->timer) cx_bulk->timer->end_interval(cx_bulk->stream);
     BQ_CUDA(cudaEventRecord(ev_bulk, cx_bulk->stream));

@@ -9,13 +9,14 @@
 #include "../paper_2507_00976_b200/csrc/dgemm.cuh"
 
 using namespace bqrrp;
-using C128x64 = GemmCfg<128, 64, 2, 2, 3>;
-using C64x64s3 = GemmCfg<64, 64, 2, 2, 4>;
-using C64x32s3 = GemmCfg<64, 32, 2, 2, 3>;
-using C64x32w2 = GemmCfg<64, 32, 2, 1, 4>;
-using C32x64 = GemmCfg<32, 64, 1, 2, 4>;
-using C128w16 = GemmCfg<128, 128, 4, 4, 3>;
-using C64x128 = GemmCfg<64, 128, 2, 4, 4>;
+// v2 candidates: BM, BN, BK, WARPS_M, WARPS_N, STAGES, MIN_BLOCKS
+using V64k16 = Gemm2Cfg<64, 64, 16, 2, 2, 3, 4>;
+using V64k16s4 = Gemm2Cfg<64, 64, 16, 2, 2, 4, 3>;
+using V64k32 = Gemm2Cfg<64, 64, 32, 2, 2, 3, 2>;
+using V128x64 = Gemm2Cfg<128, 64, 16, 4, 2, 3, 2>;
+using V128x128 = Gemm2Cfg<128, 128, 16, 2, 4, 3, 1>;
+using V128x128w16 = Gemm2Cfg<128, 128, 16, 4, 4, 3, 1>;
+using V64x32 = Gemm2Cfg<64, 32, 16, 2, 2, 3, 4>;
 
 __global__ void fill(double* p, size_t n, unsigned seed)
 {
@@ -54,6 +55,33 @@ float run(int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, const d
         cudaEventElapsedTime(&ms, e0, e1);
         if (ms < best) best = ms;
     }
+    return best;
+}
+
+template <class Cfg, bool TA, bool TB>
+float run2(int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, const double* B, int64_t ldb, double* C,
+           int reps, double alpha = 1.0, double beta = 0.0)
+{
+    GemmArgs g{M, N, K, alpha, beta, A, lda, B, ldb, C, M, nullptr, K, 0};
+    size_t sm = dgemm2_smem_bytes<Cfg, TA, TB>();
+    cudaFuncSetAttribute(dgemm2_kernel<Cfg, TA, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    dim3 grid(((M + Cfg::BM - 1) / Cfg::BM) * ((N + Cfg::BN - 1) / Cfg::BN), 1, 1);
+    int vec = dgemm2_vec_ok(g);
+    dgemm2_kernel<Cfg, TA, TB><<<grid, Cfg::THREADS, sm>>>(g, vec);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0); cudaEventCreate(&e1);
+    float best = 1e30f;
+    for (int r = 0; r < reps; ++r) {
+        cudaEventRecord(e0);
+        dgemm2_kernel<Cfg, TA, TB><<<grid, Cfg::THREADS, sm>>>(g, vec);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms;
+        cudaEventElapsedTime(&ms, e0, e1);
+        if (ms < best) best = ms;
+    }
+    cudaError_t err = cudaGetLastError();
+    if (err != cudaSuccess) { fprintf(stderr, "cuda error %s\n", cudaGetErrorString(err)); exit(1); }
     return best;
 }
 
@@ -112,16 +140,19 @@ int main()
     if (!s.ta && !s.tb) report(NM, run<CFG, false, false>(s.M, s.N, s.K, A, lda, B, ldb, C, 5, s.alpha, s.beta)); \
     else if (s.ta && !s.tb) report(NM, run<CFG, true, false>(s.M, s.N, s.K, A, lda, B, ldb, C, 5, s.alpha, s.beta)); \
     else report(NM, run<CFG, false, true>(s.M, s.N, s.K, A, lda, B, ldb, C, 5, s.alpha, s.beta));
-        RUNV(CfgWide, "wide128x64");
-        RUNV(CfgMid, "mid64x64");
-        RUNV(CfgSmall, "small64x32");
-        RUNV(C128x64, "w128x64s3");
-        RUNV(C64x64s3, "mid64x64s4");
-        RUNV(C64x32s3, "small64x32s3");
-        RUNV(C64x32w2, "small64x32w2");
-        RUNV(C32x64, "s32x64");
-        RUNV(C128w16, "big128x128w16");
-        RUNV(C64x128, "w64x128w8");
+#define RUNV2(CFG, NM)                                                                                       \
+    cudaMemset(C, 0, (size_t)s.M * s.N * 8);                                                                        \
+    if (!s.ta && !s.tb) report(NM, run2<CFG, false, false>(s.M, s.N, s.K, A, lda, B, ldb, C, 5, s.alpha, s.beta)); \
+    else if (s.ta && !s.tb) report(NM, run2<CFG, true, false>(s.M, s.N, s.K, A, lda, B, ldb, C, 5, s.alpha, s.beta)); \
+    else report(NM, run2<CFG, false, true>(s.M, s.N, s.K, A, lda, B, ldb, C, 5, s.alpha, s.beta));
+        RUNV(CfgMid, "v1_64x64");
+        RUNV2(V64k16, "v2_64x64k16");
+        RUNV2(V64k16s4, "v2_64x64k16s4");
+        RUNV2(V64k32, "v2_64x64k32");
+        RUNV2(V128x64, "v2_128x64");
+        RUNV2(V128x128, "v2_128x128");
+        RUNV2(V128x128w16, "v2_128x128w16");
+        RUNV2(V64x32, "v2_64x32");
         printf("},\n");
         fflush(stdout);
     }
