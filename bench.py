@@ -290,7 +290,7 @@ def main():
         pass
     roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": (achieved / peak) if achieved else None, "traffic": traffic, "traffic_note": traffic_note,
-                "kernel": "a5 compact-WY trailing update (dgemm_kernel: W=V^T C, W=T^T W, C-=V W) per factorization; "
+                "kernel": "a5 compact-WY trailing update (dgemm2_kernel: W=V^T C, W=T^T W, C-=V W) per factorization; "
                           "the bulk C-=V W rows are timed with events on their own (low-priority) stream",
                 "algorithmic_flops_per_step": tr_flops, "kernel_ms_per_step": apply_ms,
                 "peak_source": peak_src, "share_of_step": apply_ms / (t_ms / args.steps)}

@@ -168,6 +168,11 @@ unsigned long long bqrrp_launch_count(void);
  * thread (plus bqrrp_step_panel calls since). */
 long long bqrrp_panel_fallbacks(void);
 
+/* Device memory the library allocates itself (the workspace when none is passed, bqrrp_factor_host's device
+ * copies, debug scratch) comes from a library-owned stream-ordered pool that keeps freed blocks mapped for
+ * the next call.  This returns them to the driver (synchronises the current device).  0 or BQRRP_ECUDA. */
+int bqrrp_trim_memory(void);
+
 const char* bqrrp_strerror(int status);
 const char* bqrrp_last_error(void);
 /* Library version string. */

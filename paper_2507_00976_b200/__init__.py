@@ -11,7 +11,7 @@ import ctypes
 import math
 import os
 
-__all__ = ["lib", "factor", "factor_host", "workspace_query", "BqrrpError", "default_rank_tol", "PHASES"]
+__all__ = ["lib", "factor", "factor_host", "workspace_query", "trim_memory", "BqrrpError", "default_rank_tol", "PHASES"]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(_HERE, "libbqrrp.so")
@@ -67,6 +67,11 @@ def lib() -> ctypes.CDLL:
 def launch_count() -> int:
     """Kernels launched by libbqrrp.so in this process so far."""
     return int(lib().bqrrp_launch_count())
+
+
+def trim_memory() -> None:
+    """Return the device memory cached by the library's own pool to the driver (bqrrp_trim_memory)."""
+    _check(lib().bqrrp_trim_memory(), "bqrrp_trim_memory")
 
 
 def panel_fallbacks() -> int:

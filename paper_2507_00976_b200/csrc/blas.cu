@@ -129,9 +129,13 @@ constexpr int TRSM_NB = 64;
 // pivot:  x_t = (b_t - sum_{l<t} coef(l, t) x_l) / diag(t).
 //   right side, X op(T) = B:  st = ldb, sr = 1,   coef(l, t) = op(T)(l, t), diag = op(T)(t, t)
 //   left side,  L X = B:      st = 1,   sr = ldb, coef(l, t) = L(t, l),     diag = 1 (unit)
-// A CTA owns 64 independent indices; thread (r = tid % 64, g = tid / 64) keeps x_t for t = g mod 4
-// in registers; the solved x_t is broadcast through shared memory (one barrier per t).
-constexpr int TB_R = 64, TB_G = 4, TB_THREADS = TB_R * TB_G;
+// One THREAD per independent index r: its 64 unknowns live in registers and are eliminated column by
+// column (x_t = b_t / diag(t), then b_tt -= coef(t, tt) x_t for tt > t: 63 independent FMAs per step),
+// the coefficients are broadcast reads from shared memory — no barrier inside the solve.  Rows are
+// read / written straight from global memory when r is the contiguous axis (right side), else through a
+// shared transpose.  Coefficients outside n x n are zero and 1/diag = 1 there, so ragged n needs no
+// branches.
+constexpr int TB_R = 128, TB_THREADS = TB_R;
 
 __global__ void __launch_bounds__(TB_THREADS) trsm_base_kernel(int n, int64_t nr, const double* __restrict__ T,
                                                                 int64_t ldt, int mode, int unit, double* __restrict__ B,
@@ -140,82 +144,62 @@ __global__ void __launch_bounds__(TB_THREADS) trsm_base_kernel(int n, int64_t nr
     // mode 0: right, T stored upper (op(T) = T); mode 1: right, T stored lower (op(T) = T^T);
     // mode 2: left, T stored lower (unit)
     extern __shared__ double dsm[];
-    double(*C)[TRSM_NB + 1] = reinterpret_cast<double(*)[TRSM_NB + 1]>(dsm);                        // C[l][t]
-    double(*Bs)[TB_R + 1] = reinterpret_cast<double(*)[TB_R + 1]>(dsm + TRSM_NB * (TRSM_NB + 1));  // Bs[t][r]
-    double(*xs)[TB_R] = reinterpret_cast<double(*)[TB_R]>(dsm + TRSM_NB * (TRSM_NB + 1) + TRSM_NB * (TB_R + 1));
+    double(*C)[TRSM_NB + 1] = reinterpret_cast<double(*)[TRSM_NB + 1]>(dsm);  // C[l][t] = coef(l, t)
+    double* rdiag = dsm + TRSM_NB * (TRSM_NB + 1);                               // 1 / diag(t)
+    double(*Bs)[TB_R + 1] = reinterpret_cast<double(*)[TB_R + 1]>(rdiag + TRSM_NB);  // Bs[t][r] (sr != 1)
     const int tid = threadIdx.x;
-    for (int idx = tid; idx < n * n; idx += TB_THREADS) {
-        int l = idx % n, t = idx / n;
+    for (int idx = tid; idx < TRSM_NB * TRSM_NB; idx += TB_THREADS) {
+        const int l = idx % TRSM_NB, t = idx / TRSM_NB;
         double v = 0.0;
-        if (l <= t) {
+        if (l < t && t < n) {
             if (mode == 0) v = T[l + (int64_t)t * ldt];
-            else if (mode == 1) v = T[t + (int64_t)l * ldt];
-            else v = (l < t) ? T[t + (int64_t)l * ldt] : 1.0;
+            else v = T[t + (int64_t)l * ldt];  // mode 1: op(T)(l, t) = T(t, l); mode 2: L(t, l)
         }
         C[l][t] = v;
     }
+    if (tid < TRSM_NB) rdiag[tid] = (unit || tid >= n) ? 1.0 : 1.0 / T[tid + (int64_t)tid * ldt];
     const int64_t r0 = (int64_t)blockIdx.x * TB_R;
     const int nloc = (int)((nr - r0 < TB_R) ? nr - r0 : TB_R);
-    // coalesced load of the n x 64 tile along whichever axis is contiguous
-    if (sr == 1) {
-        for (int idx = tid; idx < n * TB_R; idx += TB_THREADS) {
-            int r = idx % TB_R, t = idx / TB_R;
-            Bs[t][r] = (r < nloc) ? B[t * st + (r0 + r)] : 0.0;
-        }
-    } else {
-        for (int idx = tid; idx < n * TB_R; idx += TB_THREADS) {
-            int t = idx % n, r = idx / n;
-            Bs[t][r] = (r < nloc) ? B[t + (r0 + r) * sr] : 0.0;
+    double x[TRSM_NB];
+    if (sr != 1) {  // left side: stage the n x TB_R tile through shared memory (coalesced along t)
+        for (int idx = tid; idx < TRSM_NB * TB_R; idx += TB_THREADS) {
+            const int t = idx % TRSM_NB, r = idx / TRSM_NB;
+            Bs[t][r] = (t < n && r < nloc) ? B[t + (r0 + r) * sr] : 0.0;
         }
     }
     __syncthreads();
-    const int r = tid % TB_R, g = tid / TB_R;
-    constexpr int PER = TRSM_NB / TB_G;
-    double x[PER];
+    const bool mine = tid < nloc;
+    if (sr == 1) {
 #pragma unroll
-    for (int q = 0; q < PER; ++q) {
-        int t = g + q * TB_G;
-        x[q] = (t < n) ? Bs[t][r] : 0.0;
+        for (int t = 0; t < TRSM_NB; ++t) x[t] = (mine && t < n) ? B[t * st + (r0 + tid)] : 0.0;
+    } else {
+#pragma unroll
+        for (int t = 0; t < TRSM_NB; ++t) x[t] = Bs[t][tid];
     }
 #pragma unroll
     for (int t = 0; t < TRSM_NB; ++t) {
-        if (t < n) {
-            const int q = t / TB_G;
-            if (g == t % TB_G) {
-                double v = x[q];
-                if (!unit) v = v / C[t][t];
-                x[q] = v;
-                xs[t & 1][r] = v;
-            }
-            __syncthreads();
-            const double xt = xs[t & 1][r];
+        x[t] *= rdiag[t];
 #pragma unroll
-            for (int qq = q; qq < PER; ++qq) {
-                int tt = g + qq * TB_G;
-                if (tt > t && tt < n) x[qq] = fma(-xt, C[t][tt], x[qq]);
-            }
-        }
+        for (int tt = t + 1; tt < TRSM_NB; ++tt) x[tt] = fma(-x[t], C[t][tt], x[tt]);
     }
-#pragma unroll
-    for (int q = 0; q < PER; ++q) {
-        int t = g + q * TB_G;
-        if (t < n) Bs[t][r] = x[q];
-    }
-    __syncthreads();
     if (sr == 1) {
-        for (int idx = tid; idx < n * TB_R; idx += TB_THREADS) {
-            int rr = idx % TB_R, t = idx / TB_R;
-            if (rr < nloc) B[t * st + (r0 + rr)] = Bs[t][rr];
+        if (mine) {
+#pragma unroll
+            for (int t = 0; t < TRSM_NB; ++t)
+                if (t < n) B[t * st + (r0 + tid)] = x[t];
         }
     } else {
-        for (int idx = tid; idx < n * TB_R; idx += TB_THREADS) {
-            int t = idx % n, rr = idx / n;
-            if (rr < nloc) B[t + (r0 + rr) * sr] = Bs[t][rr];
+#pragma unroll
+        for (int t = 0; t < TRSM_NB; ++t) Bs[t][tid] = x[t];
+        __syncthreads();
+        for (int idx = tid; idx < TRSM_NB * TB_R; idx += TB_THREADS) {
+            const int t = idx % TRSM_NB, r = idx / TRSM_NB;
+            if (t < n && r < nloc) B[t + (r0 + r) * sr] = Bs[t][r];
         }
     }
 }
 
-constexpr size_t TB_SMEM = sizeof(double) * (TRSM_NB * (TRSM_NB + 1) + TRSM_NB * (TB_R + 1) + 2 * TB_R);
+constexpr size_t TB_SMEM = sizeof(double) * (TRSM_NB * (TRSM_NB + 1) + TRSM_NB + TRSM_NB * (TB_R + 1));
 
 static void trsm_base(Ctx& cx, int n, int64_t nr, const double* T, int64_t ldt, int mode, int unit, double* B,
                       int64_t st, int64_t sr)
@@ -397,46 +381,69 @@ void trsm_left_lower_unit(Ctx& cx, int64_t n, int64_t cols, const double* L, int
 // ------------------------------------------------------------------------------------------- POTRF
 constexpr int FACT_NB = 64;
 
-// One CTA factors a <= 64 x 64 diagonal block, one barrier per column: with the column left unscaled,
-// step j updates A(i, c) -= A(i, j) A(c, j) / A(j, j) for i >= c > j (it reads only column j, final after
-// step j-1); the columns are scaled by 1/sqrt(A(j, j)) at the end.
+// One CTA factors a <= 64 x 64 diagonal block with the block in REGISTERS: thread (i = tid % 64,
+// g = tid / 64) owns row i, columns c = g + 4q (q < 16).  Step j (right-looking, column left unscaled):
+// the owners of column j publish it to shared memory (double-buffered), ONE barrier, then every thread
+// updates A(i, c) -= A(i, j) A(c, j) / A(j, j) for its c > j, c <= i.  Columns are scaled by
+// 1/sqrt(A(j, j)) at the end.  (A shared-memory version with one (i, c) pair per loop trip ran
+// ~1 us per column; this one is a handful of FMAs + 17 shared reads per column.)
 __global__ void __launch_bounds__(256) potrf_diag(int n, double* G, int64_t ldg, int j0, int* info)
 {
-    __shared__ double A[FACT_NB][FACT_NB + 1];
-    __shared__ int bad;
-    for (int j = 0; j < n; ++j)
-        for (int r = threadIdx.x; r < n; r += blockDim.x) cp_async8z(&A[r][j], G + r + (int64_t)j * ldg, r >= j);
-    if (threadIdx.x == 0) bad = -1;
-    cp_async_wait_all();
-    __syncthreads();
-    if (*info != 0) return;  // an earlier block already broke down
-    for (int j = 0; j < n; ++j) {
-        const double d = A[j][j];
-        if (!(d > 0.0)) {  // uniform: every thread sees the same pivot
-            if (threadIdx.x == 0) bad = j;
-            break;
-        }
-        const int m = n - j - 1;
-        const double rd = 1.0 / d;
-        for (int idx = threadIdx.x; idx < m * m; idx += blockDim.x) {
-            int i = j + 1 + idx % m, c = j + 1 + idx / m;
-            if (c <= i) A[i][c] = fma(-A[i][j] * rd, A[c][j], A[i][c]);
-        }
-        __syncthreads();
+    __shared__ double colj[2][FACT_NB];
+    __shared__ double piv[FACT_NB];
+    const int tid = threadIdx.x, i = tid & 63, g = tid >> 6;
+    constexpr int Q = FACT_NB / 4;
+    double a[Q];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+        const int c = g + 4 * q;
+        a[q] = (i < n && c < n && c <= i) ? G[i + (int64_t)c * ldg] : 0.0;
     }
-    __syncthreads();
+    if (*info != 0) return;  // an earlier block already broke down (uniform)
+    int bad = -1;
+    // j = 4 jq + jr with jq unrolled, so the owned column a[jq] is a compile-time register index
+#pragma unroll
+    for (int jq = 0; jq < Q; ++jq) {
+        for (int jr = 0; jr < 4; ++jr) {
+            const int j = 4 * jq + jr;
+            if (j >= n || bad >= 0) break;
+            const int par = j & 1;
+            if (g == jr) colj[par][i] = a[jq];
+            __syncthreads();
+            const double d = colj[par][j];
+            if (!(d > 0.0)) {  // uniform: every thread sees the same pivot
+                bad = j;
+                break;
+            }
+            if (tid == 0) piv[j] = d;
+            const double lij = colj[par][i] * (1.0 / d);
+            if (i > j) {
+#pragma unroll
+                for (int q = jq; q < Q; ++q) {
+                    const int c = g + 4 * q;
+                    if (c > j && c <= i) a[q] = fma(-lij, colj[par][c], a[q]);
+                }
+            }
+        }
+    }
     if (bad >= 0) {
-        if (threadIdx.x == 0) atomicCAS(info, 0, j0 + bad + 1);
+        if (tid == 0) atomicCAS(info, 0, j0 + bad + 1);
         return;
     }
-    for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) {
-        int i = idx % n, j = idx / n;
-        double v = 0.0;
-        if (i >= j) {
-            double sj = sqrt(A[j][j]);
-            v = (i == j) ? sj : A[i][j] / sj;
+    __syncthreads();
+    if (i < n) {
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+            const int c = g + 4 * q;
+            if (c < n) {
+                double v = 0.0;
+                if (i >= c) {
+                    const double sc = sqrt(piv[c]);
+                    v = (i == c) ? sc : a[q] / sc;
+                }
+                G[i + (int64_t)c * ldg] = v;
+            }
         }
-        G[i + (int64_t)j * ldg] = v;
     }
 }
 
@@ -458,39 +465,63 @@ void potrf_lower(Ctx& cx, int64_t n, double* G, int64_t ldg)
 }
 
 // ------------------------------------------------------------------------------------------- sign LU
-// Sign-choosing no-pivot LU of a <= 64 x 64 block, one barrier per column: at step j every thread reads
-// a = A(j, j) (final), S_j = -sgn(a), pivot p = a - S_j; A(i, c) -= A(i, j) A(j, c) / p for i, c > j.
-// The multipliers L(i, j) = A(i, j) / p_j are formed at the end.
-__global__ void __launch_bounds__(256) getrf_sign_diag(int n, double* Q, int64_t ldq, double* S)
+// Sign-choosing no-pivot LU of a <= 64 x 64 block, registers as in potrf_diag (thread (i, g) owns row i,
+// columns g + 4q), one barrier per column: at step j the owners publish column j and row j, every thread
+// reads a = A(j, j) (final), S_j = -sgn(a), pivot p = a - S_j, and updates A(i, c) -= A(i, j) A(j, c) / p
+// for i, c > j.  The multipliers L(i, j) = A(i, j) / p_j are formed at the end.
+__global__ void __launch_bounds__(256) getrf_sign_diag(int n, double* Qm, int64_t ldq, double* S)
 {
-    __shared__ double A[FACT_NB][FACT_NB + 1];
+    __shared__ double colj[2][FACT_NB], rowj[2][FACT_NB];
     __shared__ double piv[FACT_NB];
-    for (int j = 0; j < n; ++j)
-        for (int r = threadIdx.x; r < n; r += blockDim.x) cp_async8z(&A[r][j], Q + r + (int64_t)j * ldq, true);
-    cp_async_wait_all();
-    __syncthreads();
-    for (int j = 0; j < n; ++j) {
-        const double a = A[j][j];
-        const double sj = (a >= 0.0) ? -1.0 : 1.0;  // S_jj = -sgn(a), sgn(a) = a >= 0 ? +1 : -1 (Z20)
-        const double p = a - sj;
-        if (threadIdx.x == 0) {
-            S[j] = sj;
-            piv[j] = p;
-        }
-        const int m = n - j - 1;
-        const double rp = 1.0 / p;
-        for (int idx = threadIdx.x; idx < m * m; idx += blockDim.x) {
-            int i = j + 1 + idx % m, c = j + 1 + idx / m;
-            A[i][c] = fma(-A[i][j] * rp, A[j][c], A[i][c]);
-        }
-        __syncthreads();
+    const int tid = threadIdx.x, i = tid & 63, g = tid >> 6;
+    constexpr int Q = FACT_NB / 4;
+    double a[Q];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+        const int c = g + 4 * q;
+        a[q] = (i < n && c < n) ? Qm[i + (int64_t)c * ldq] : 0.0;
     }
-    for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) {
-        int i = idx % n, j = idx / n;
-        double v = A[i][j];
-        if (i == j) v = piv[j];
-        else if (i > j) v = v / piv[j];
-        Q[i + (int64_t)j * ldq] = v;
+#pragma unroll
+    for (int jq = 0; jq < Q; ++jq) {
+        for (int jr = 0; jr < 4; ++jr) {
+            const int j = 4 * jq + jr;
+            if (j >= n) break;
+            const int par = j & 1;
+            if (g == jr) colj[par][i] = a[jq];
+            if (i == j) {
+#pragma unroll
+                for (int q = 0; q < Q; ++q) rowj[par][g + 4 * q] = a[q];
+            }
+            __syncthreads();
+            const double av = rowj[par][j];
+            const double sj = (av >= 0.0) ? -1.0 : 1.0;  // S_jj = -sgn(a), sgn(a) = a >= 0 ? +1 : -1 (Z20)
+            const double p = av - sj;
+            if (tid == 0) {
+                S[j] = sj;
+                piv[j] = p;
+            }
+            if (i > j) {
+                const double lij = colj[par][i] * (1.0 / p);
+#pragma unroll
+                for (int q = jq; q < Q; ++q) {
+                    const int c = g + 4 * q;
+                    if (c > j) a[q] = fma(-lij, rowj[par][c], a[q]);
+                }
+            }
+        }
+    }
+    __syncthreads();
+    if (i < n) {
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+            const int c = g + 4 * q;
+            if (c < n) {
+                double v = a[q];
+                if (i == c) v = piv[c];
+                else if (i > c) v = v / piv[c];
+                Qm[i + (int64_t)c * ldq] = v;
+            }
+        }
     }
 }
 

@@ -12,6 +12,7 @@
 //   a7  termination (step bqrrp:termination)
 //   a6  sketch update MskT(c:n, 0:b) -= R12^T (R_sk11 R11^{-1})^T  (step bqrrp:update_sample)
 #include <cstring>
+#include <mutex>
 #include <string>
 
 #include "../../include/bqrrp.h"
@@ -22,6 +23,25 @@
 namespace bqrrp {
 
 static thread_local std::string g_last_error;
+
+cudaMemPool_t lib_pool()
+{
+    static std::mutex mu;
+    static cudaMemPool_t pools[64] = {};
+    int dev = 0;
+    BQ_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(mu);
+    if (!pools[dev]) {
+        cudaMemPoolProps props = {};
+        props.allocType = cudaMemAllocationTypePinned;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = dev;
+        BQ_CUDA(cudaMemPoolCreate(&pools[dev], &props));
+        uint64_t thr = UINT64_MAX;
+        BQ_CUDA(cudaMemPoolSetAttribute(pools[dev], cudaMemPoolAttrReleaseThreshold, &thr));
+    }
+    return pools[dev];
+}
 thread_local long long g_panel_fallbacks = 0;
 unsigned long long g_launches = 0;
 
@@ -326,7 +346,7 @@ int bqrrp_factor_ex(int64_t m, int64_t n, double* A, int64_t lda, int64_t b, int
         void* ws = workspace;
         bool own = false;
         if (!ws) {
-            BQ_CUDA(cudaMallocAsync(&ws, L.total, cx.stream));
+            BQ_CUDA(lib_malloc_async(&ws, L.total, cx.stream));
             ws_bytes = L.total;
             own = true;
         } else if (ws_bytes < L.total) {
@@ -417,10 +437,10 @@ int bqrrp_factor_host(int64_t m, int64_t n, double* A_host, int64_t lda, int64_t
         size_t wsb = 0;
         bqrrp_workspace_query(m, n, b, d, &wsb);
         void* ws = nullptr;
-        BQ_CUDA(cudaMallocAsync((void**)&dA, sizeof(double) * (size_t)imax(1, m * n), st));
-        BQ_CUDA(cudaMallocAsync((void**)&dtau, sizeof(double) * (size_t)imax(1, mn), st));
-        BQ_CUDA(cudaMallocAsync((void**)&dJ, sizeof(int64_t) * (size_t)imax(1, n), st));
-        BQ_CUDA(cudaMallocAsync(&ws, wsb, st));
+        BQ_CUDA(lib_malloc_async(&dA, sizeof(double) * (size_t)imax(1, m * n), st));
+        BQ_CUDA(lib_malloc_async(&dtau, sizeof(double) * (size_t)imax(1, mn), st));
+        BQ_CUDA(lib_malloc_async(&dJ, sizeof(int64_t) * (size_t)imax(1, n), st));
+        BQ_CUDA(lib_malloc_async(&ws, wsb, st));
         if (m > 0 && n > 0)
             BQ_CUDA(cudaMemcpy2DAsync(dA, m * sizeof(double), A_host, lda * sizeof(double), m * sizeof(double), n,
                                       cudaMemcpyHostToDevice, st));
@@ -454,10 +474,10 @@ int bqrrp_debug_sketch(int64_t m, int64_t n, const double* A, int64_t lda, int64
         Ctx cx;
         setup_ctx(cx, stream);
         double* St = nullptr;
-        BQ_CUDA(cudaMallocAsync((void**)&St, sizeof(double) * m * d, cx.stream));
+        BQ_CUDA(lib_malloc_async(&St, sizeof(double) * m * d, cx.stream));
         Layout L{0, 0, (size_t)16 * 1024 * 1024, 0};
         void* ws = nullptr;
-        BQ_CUDA(cudaMallocAsync(&ws, L.splitk + 4096, cx.stream));
+        BQ_CUDA(lib_malloc_async(&ws, L.splitk + 4096, cx.stream));
         carve(cx, ws, L.splitk + 4096, L);
         sketch_apply(cx, m, n, A, lda, d, seed, MskT_out, n, St);
         if (S_out) transpose_copy(cx, m, d, St, m, S_out, d);
@@ -479,7 +499,7 @@ int bqrrp_debug_gemm(int ta, int tb, int64_t M, int64_t N, int64_t K, double alp
         setup_ctx(cx, stream);
         size_t sk = (size_t)32 * (size_t)imax(1, M * N);
         void* ws = nullptr;
-        BQ_CUDA(cudaMallocAsync(&ws, sk * 8 + 4096, cx.stream));
+        BQ_CUDA(lib_malloc_async(&ws, sk * 8 + 4096, cx.stream));
         Layout L{0, 0, sk * 8, 0};
         carve(cx, ws, sk * 8 + 4096, L);
         gemm(cx, ta != 0, tb != 0, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
@@ -500,7 +520,7 @@ int bqrrp_debug_trsm(int64_t rows, int64_t n, const double* T, int64_t ldt, int 
         size_t sk = (size_t)16 * 64 * 64 + (4u << 20) / 8;
         size_t bytes = (sk + (size_t)cdiv(imax(n, 1), 64) * 4096 + 8192) * 8;
         void* ws = nullptr;
-        BQ_CUDA(cudaMallocAsync(&ws, bytes, cx.stream));
+        BQ_CUDA(lib_malloc_async(&ws, bytes, cx.stream));
         Layout L{0, 0, sk * 8, 0};
         carve(cx, ws, bytes, L);
         trsm_right_upper(cx, rows, n, T, ldt, t_lower != 0, unit != 0, B, ldb, inverse != 0);
@@ -512,7 +532,8 @@ int bqrrp_debug_trsm(int64_t rows, int64_t n, const double* T, int64_t ldt, int 
 
 static size_t debug_ws_bytes(int64_t rows, int64_t d)
 {
-    return (size_t)(64ull << 20) + (size_t)rows * (size_t)d * 8 * 6 + (size_t)d * d * 8 * 8;
+    // scratch (rows x d panels, d x d factors) + the split-K slices carved first (16 d^2 + 4 MiB)
+    return (size_t)(64ull << 20) + (size_t)rows * (size_t)d * 8 * 6 + (size_t)d * d * 8 * (8 + 16);
 }
 
 int bqrrp_debug_lu_pivots(int64_t w, int64_t d, double* L, int64_t ld, int64_t* ipiv, void* stream)
@@ -524,7 +545,7 @@ int bqrrp_debug_lu_pivots(int64_t w, int64_t d, double* L, int64_t ld, int64_t* 
         setup_ctx(cx, stream);
         size_t wsb = debug_ws_bytes(w, d);
         void* ws = nullptr;
-        BQ_CUDA(cudaMallocAsync(&ws, wsb, cx.stream));
+        BQ_CUDA(lib_malloc_async(&ws, wsb, cx.stream));
         Layout Ly{0, 0, (size_t)16 * imax(1, d * d) * 8 + (4u << 20), 0};
         carve(cx, ws, wsb, Ly);
         int* ip = cx.alloc_as<int>((size_t)imax(1, d));
@@ -550,7 +571,7 @@ int bqrrp_debug_sketch_qr(int64_t w, int64_t d, double* WT, int64_t ld, void* st
         setup_ctx(cx, stream);
         size_t wsb = debug_ws_bytes(w, d);
         void* ws = nullptr;
-        BQ_CUDA(cudaMallocAsync(&ws, wsb, cx.stream));
+        BQ_CUDA(lib_malloc_async(&ws, wsb, cx.stream));
         Layout Ly{0, 0, (size_t)16 * d * d * 8 + (4u << 20), 0};
         carve(cx, ws, wsb, Ly);
         sketch_qr(cx, WT, ld, w, d);
@@ -583,7 +604,7 @@ int bqrrp_debug_permute(int64_t rows, int64_t w, double* X, int64_t ldx, int64_t
         setup_ctx(cx, stream);
         size_t wsb = (size_t)(8u << 20) + (size_t)2 * imax(1, nlu) * imax(1, rows) * 8 + (size_t)w * 4;
         void* ws = nullptr;
-        BQ_CUDA(cudaMallocAsync(&ws, wsb, cx.stream));
+        BQ_CUDA(lib_malloc_async(&ws, wsb, cx.stream));
         Layout Ly{0, 0, 4096, 0};
         carve(cx, ws, wsb, Ly);
         Touched T;
@@ -621,7 +642,7 @@ int bqrrp_debug_panel(int64_t h, int64_t k, int64_t t, double* P, int64_t ld, co
         size_t wsb = (size_t)(64u << 20) + ((size_t)h * k + (size_t)9 * k * k + (size_t)2 * k * (t + 1)) * 8 +
                      (size_t)16 * k * k * 8;
         void* ws = nullptr;
-        BQ_CUDA(cudaMallocAsync(&ws, wsb, cx.stream));
+        BQ_CUDA(lib_malloc_async(&ws, wsb, cx.stream));
         Layout Ly{0, 0, (size_t)16 * k * k * 8 + (4u << 20), 0};
         carve(cx, ws, wsb, Ly);
         BQ_CUDA(cudaMemsetAsync(cx.flags, 0, sizeof(int) * F_NFLAGS, cx.stream));
@@ -656,6 +677,15 @@ const char* bqrrp_last_error(void) { return g_last_error.c_str(); }
 unsigned long long bqrrp_launch_count(void) { return g_launches; }
 
 long long bqrrp_panel_fallbacks(void) { return g_panel_fallbacks; }
+
+int bqrrp_trim_memory(void)
+{
+    return guarded([&]() -> int {
+        BQ_CUDA(cudaDeviceSynchronize());
+        BQ_CUDA(cudaMemPoolTrimTo(lib_pool(), 0));
+        return 0;
+    });
+}
 
 const char* bqrrp_version(void) { return "bqrrp-b200 0.1 (sm_100a, DMMA f64)"; }
 

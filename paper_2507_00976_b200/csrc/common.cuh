@@ -108,6 +108,22 @@ struct Timer {
 };
 
 // Execution context: stream + a bump allocator over one workspace buffer + split-K scratch.
+// Device memory the library allocates itself (workspace when the caller passes none, the host entry's
+// device copies, debug scratch) comes from a library-owned stream-ordered pool per device whose release
+// threshold is unlimited: freed blocks stay mapped for the next call instead of being unmapped at every
+// synchronisation (the default pool's threshold is 0, which made each bqrrp_factor_host call re-map ~40 GB
+// at C3).  bqrrp_trim_memory() returns the cached blocks to the driver.
+cudaMemPool_t lib_pool();
+inline cudaError_t lib_malloc_async(void** p, size_t bytes, cudaStream_t st)
+{
+    return cudaMallocFromPoolAsync(p, bytes, lib_pool(), st);
+}
+template <typename T>
+inline cudaError_t lib_malloc_async(T** p, size_t bytes, cudaStream_t st)
+{
+    return lib_malloc_async(reinterpret_cast<void**>(p), bytes, st);
+}
+
 struct Ctx {
     cudaStream_t stream = 0;
     int num_sms = 148;

@@ -10,6 +10,8 @@
 //   V = L, T = -U S Y1^{-T}, tau = diag(T)                           P:697-701)
 //   R11 = diag(S) C_last^T ... C_1^T R_sk11                        (cholqr:undo_precond, reading Z7)
 //   C <- C - V T^T (V^T C) on C = A(s:m, s+k:n)                    (apply_trans_q, compact WY)
+#include <cstdlib>
+
 #include "blas.cuh"
 #include "bqrrp_internal.cuh"
 
@@ -78,6 +80,11 @@ int panel_factor(Ctx& cx, int64_t m, double* A, int64_t lda, int64_t s, int64_t 
         gemm(cx, true, false, k, k, h, 1.0, Q, h, Q, h, 0.0, Cf[p], k, /*tri=*/true);
         potrf_lower(cx, k, Cf[p], k);
         if (p + 1 < passes) trsm_right_upper(cx, h, k, Cf[p], k, /*t_lower=*/true, false, Q, h, true);
+    }
+    {   // test hook: BQRRP_DEBUG_FORCE_BREAKDOWN=1 reports a POTRF breakdown on every panel, so the fallback /
+        // error path is exercised deterministically (a real breakdown depends on rounding)
+        const char* f = std::getenv("BQRRP_DEBUG_FORCE_BREAKDOWN");
+        if (f && f[0] == '1') BQ_CUDA(cudaMemsetAsync(cx.flags + F_POTRF_INFO, 1, 1, cx.stream));
     }
     if (hqr_fallback) {  // CholQR breakdown (POTRF non-positive pivot): this panel by Householder QR instead
         int info = 0;

@@ -100,7 +100,7 @@ struct StepWs {
         BQ_CUDA(cudaGetDevice(&dev));
         BQ_CUDA(cudaDeviceGetAttribute(&cx.num_sms, cudaDevAttrMultiProcessorCount, dev));
         size_t total = bytes + splitk_bytes + 4096;
-        BQ_CUDA(cudaMallocAsync(&ws, total, cx.stream));
+        BQ_CUDA(lib_malloc_async(&ws, total, cx.stream));
         cx.ws = (char*)ws;
         cx.ws_bytes = total;
         cx.ws_used = 0;

@@ -345,21 +345,33 @@ def test_factor_kahan_matches_oracle(gpu):
     _compare_ill_conditioned(A, out_o, g)
 
 
-def test_cholqr_breakdown_falls_back_to_householder(gpu):
+def test_cholqr_breakdown_falls_back_to_householder(gpu, monkeypatch):
+    """CholQR breakdown handling: a panel whose POTRF reports a non-positive pivot is
+    re-factored by Householder QR and the factorization stays backward stable — with the same pivots and
+    R as the oracle, since the HQR panel and CholQR2 + reconstruction give the same (V, tau, R) (SURVEY
+    c.1).  Without the fallback the call reports BQRRP_ENUMERIC.  Whether a given ill-conditioned input
+    breaks POTRF down depends on rounding, so the breakdown is forced through the library's test hook."""
+    bq = _bq()
+    A = np.asfortranarray(inputs.gaussian(1000, 1000, seed=4))
+    monkeypatch.setenv("BQRRP_DEBUG_FORCE_BREAKDOWN", "1")
+    out_o, g = _run_both(A, 128, 160, seed=0)
+    assert bq.panel_fallbacks() == 8  # every panel of the 8 iterations
+    _compare(out_o, g)
+    with pytest.raises(bq.BqrrpError) as e:
+        bq.factor(_dev(A), 128, 160, seed=0, hqr_fallback=False)
+    assert e.value.status == 1
+    monkeypatch.delenv("BQRRP_DEBUG_FORCE_BREAKDOWN")
+    bq.factor(_dev(A), 128, 160, seed=0)
+    assert bq.panel_fallbacks() == 0
+
+
+def test_numerically_singular_panels_stay_backward_stable(gpu):
     """A Kahan matrix (kappa ~ 1e20 at n = 4096) with rank_tol far below the default keeps numerically
-    dependent columns in the blocks: the preconditioned Gram matrix is numerically singular and POTRF breaks
-    down.  With the fallback the panel is re-factored by Householder QR and the
-    factorization stays backward stable; without it the call reports BQRRP_ENUMERIC."""
+    dependent columns in the blocks; whether or not POTRF then breaks down (rounding-dependent; the
+    fallback takes over if it does), the factorization is backward stable and Q orthonormal."""
     bq = _bq()
     A = np.asfortranarray(inputs.kahan(4096))
     Ag, taug, Jg, rk = bq.factor(_dev(A), 1024, 1024, seed=0, rank_tol=1e-300)
-    assert bq.panel_fallbacks() >= 1
     res = oracle.OracleResult(_host(Ag), _host(taug), _host(Jg), rk, None, 0, None)
     assert oracle.residual(A, res) <= 1e-13
     assert oracle.orthogonality(res) <= 1e-12
-    with pytest.raises(bq.BqrrpError) as e:
-        bq.factor(_dev(A), 1024, 1024, seed=0, rank_tol=1e-300, hqr_fallback=False)
-    assert e.value.status == 1
-    # the default tolerance never needs the fallback here
-    bq.factor(_dev(A), 1024, 1024, seed=0)
-    assert bq.panel_fallbacks() == 0

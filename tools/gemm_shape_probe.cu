@@ -1,5 +1,5 @@
 // gemm_shape_probe.cu — one launch of the library's DMMA GEMM on a given shape through the same tile
-// choice as blas.cu's large-GEMM path (64x64, 3 stages, rasterised), e.g. the C3 bulk trailing GEMM at
+// choice as blas.cu's large-GEMM path (v2 64x64, BK 16, 3 stages, rasterised), e.g. the C3 bulk trailing GEMM at
 // iteration 0: M = N = 63488, K = 2048, alpha = -1, beta = 1 (NN) — for an `ncu --set full` capture
 // of dram bytes per launch (bench.py roofline.traffic).
 // Build: nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -lineinfo tools/gemm_shape_probe.cu
@@ -31,15 +31,17 @@ int main(int argc, char** argv)
     fill<<<2048, 256>>>(B, (size_t)K * N, 2);
     fill<<<2048, 256>>>(C, (size_t)M * N, 3);
     GemmArgs g{M, N, K, -1.0, 1.0, A, M, B, K, C, M, nullptr, K, 0};
-    constexpr size_t sm = dgemm_smem_bytes<CfgMid, false, false>();
-    cudaFuncSetAttribute(dgemm_kernel<CfgMid, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    using Cfg = Cfg2Mid;  // the library's large-GEMM configuration (blas.cu)
+    constexpr size_t sm = dgemm2_smem_bytes<Cfg, false, false>();
+    cudaFuncSetAttribute(dgemm2_kernel<Cfg, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    const int vec = dgemm2_vec_ok(g);
     dim3 grid((unsigned)(((M + 63) / 64) * ((N + 63) / 64)));
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
-    dgemm_kernel<CfgMid, false, false><<<grid, CfgMid::THREADS, sm>>>(g);  // warm
+    dgemm2_kernel<Cfg, false, false><<<grid, Cfg::THREADS, sm>>>(g, vec);  // warm
     cudaEventRecord(e0);
-    dgemm_kernel<CfgMid, false, false><<<grid, CfgMid::THREADS, sm>>>(g);
+    dgemm2_kernel<Cfg, false, false><<<grid, Cfg::THREADS, sm>>>(g, vec);
     cudaEventRecord(e1);
     cudaEventSynchronize(e1);
     float ms;
