@@ -155,6 +155,14 @@ int bqrrp_step_panel(int64_t h, int64_t k, double* P, int64_t ldp, const double*
 /* a5 on one rank's trailing columns: C (h x t, ldc) <- C - V T^T (V^T C). */
 int bqrrp_step_wy_update(int64_t h, int64_t k, int64_t t, const double* V, const double* T, double* C, int64_t ldc,
                          void* stream);
+/* a5 split for the lookahead (DESIGN.md §7.5 / §8.1): bqrrp_step_wy_top computes W2 = T^T (V^T C) into the
+ * caller's W2 (k x t, ldw >= k; it must stay alive until the bulk call has run) and applies C -= V W2 to rows
+ * 0:k (R12) only; bqrrp_step_wy_bulk applies rows k:h, typically on a second stream ordered after the top call.
+ * Together they equal bqrrp_step_wy_update. */
+int bqrrp_step_wy_top(int64_t h, int64_t k, int64_t t, const double* V, const double* T, double* C, int64_t ldc,
+                      double* W2, int64_t ldw, void* stream);
+int bqrrp_step_wy_bulk(int64_t h, int64_t k, int64_t t, const double* V, const double* W2, int64_t ldw, double* C,
+                       int64_t ldc, void* stream);
 /* a6 on the replicated sketch: X = R_sk11 R11^{-1} (R_sk11 from MskT_s), MskT_s(b:b+t, 0:b) -= R12^T X^T with
  * R11 (b x b, ldr) and R12 (b x t, ld12) gathered in position order. */
 int bqrrp_step_sample_update(int64_t b, int64_t t, const double* R11, int64_t ldr, const double* R12, int64_t ld12,

@@ -11,6 +11,7 @@
 // vector perm (perm = J_qr - 1 of piv_transform), so no separate laswp pass exists and the
 // touched set of the permutation is read straight off perm.
 #include <cooperative_groups.h>
+#include <cstdlib>
 
 #include "blas.cuh"
 #include "bqrrp_internal.cuh"
@@ -346,6 +347,298 @@ __global__ void __launch_bounds__(LU_THREADS, 1) lu_panel_cluster_kernel(LuPanel
 
 constexpr size_t LUC_SMEM_MAX = 196 * 1024;
 
+// ---------------------------------------------------------------------------------------------
+// Register-resident leaf (rows <= 148 x 512): each thread owns RPT rows of the 32-column panel in
+// registers (the smem slab kernels above spend most of a column step moving the slab through shared
+// memory).  Per column: local first-max -> warp shuffles -> ONE block barrier -> every thread derives
+// the CTA candidate; the thread owning it publishes (|value|, row, its full panel row), the owner of row
+// jr (always CTA 0: rows c0 .. c0+31 are its first rows) publishes row jr; then warp 0 picks the global
+// winner (IDAMAX order, Z19) and fetches the two rows, one more block barrier, and every thread swaps /
+// scales / updates its own rows.  The exchange is
+//   CLUSTER: records in each CTA's shared memory, one barrier.cluster, DSMEM reads;
+//   grid   : records in global memory tagged with a per-launch sequence number (st.release after the
+//            data; readers spin on ld.acquire), so no grid-wide barrier is needed; co-residency of the
+//            polling CTAs is guaranteed by the cooperative launch.
+// Records are double-buffered by column parity (a CTA can only publish column j+2 after reading every
+// CTA's column j+1 record, which each CTA publishes only after finishing its column-j reads).
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p)
+{
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned long long v)
+{
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ double select32(const double (&v)[32], int j)
+{
+    double l1[16], l2[8], l3[4], l4[2];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) l1[i] = (j & 1) ? v[2 * i + 1] : v[2 * i];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) l2[i] = (j & 2) ? l1[2 * i + 1] : l1[2 * i];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) l3[i] = (j & 4) ? l2[2 * i + 1] : l2[2 * i];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) l4[i] = (j & 8) ? l3[2 * i + 1] : l3[2 * i];
+    return (j & 16) ? l4[1] : l4[0];
+}
+
+constexpr int LR_REC = 2 + LU_JBMAX;  // |value|, row, panel row
+
+template <int RPT, bool CLUSTER>
+__global__ void __launch_bounds__(LU_THREADS, 1) lu_leaf_reg_kernel(LuPanelArgs a, unsigned long long tag0,
+                                                                    unsigned long long* tags)
+{
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, jb = a.jb;
+    int G, me;
+    if (CLUSTER) {
+        cg::cluster_group cl = cg::this_cluster();
+        G = (int)cl.num_blocks();
+        me = (int)cl.block_rank();
+    } else {
+        G = gridDim.x;
+        me = blockIdx.x;
+    }
+    constexpr int RC = LU_THREADS * RPT;  // rows per CTA
+    const int64_t rbeg = a.c0 + (int64_t)me * RC;
+    __shared__ double red_v[LU_THREADS / 32];
+    __shared__ int64_t red_i[LU_THREADS / 32];
+    __shared__ double pivrow[LU_JBMAX], oldrow[LU_JBMAX];
+    __shared__ int64_t s_piv;
+    __shared__ int64_t spiv[LU_JBMAX], trow[2 * LU_JBMAX], tsrc[2 * LU_JBMAX];
+    __shared__ int s_nt;
+    __shared__ double crec[2][LR_REC + LU_JBMAX];  // CLUSTER records: candidate + row jr (CTA 0)
+
+    double av[RPT][32];
+    int64_t rr[RPT];
+#pragma unroll
+    for (int i = 0; i < RPT; ++i) {
+        rr[i] = rbeg + tid + (int64_t)i * LU_THREADS;
+        const bool ok = rr[i] < a.w;
+#pragma unroll
+        for (int c = 0; c < 32; ++c) av[i][c] = (ok && c < jb) ? a.L[rr[i] + (a.c0 + c) * a.ld] : 0.0;
+    }
+
+#pragma unroll 1
+    for (int j = 0; j < jb; ++j) {
+        const int par = j & 1;
+        const int64_t jr = a.c0 + j;
+        const unsigned long long tag = tag0 + (unsigned long long)j + 1ull;
+        // local first-max of |L(r, j)| over my active rows (ascending rows: first index kept on ties)
+        double bv = -1.0;
+        int64_t bi = INT64_MAX;
+        double xj[RPT];
+#pragma unroll
+        for (int i = 0; i < RPT; ++i) {
+            xj[i] = select32(av[i], j);
+            if (rr[i] < a.w && rr[i] >= jr) {
+                const double v = fabs(xj[i]);
+                if (v > bv) { bv = v; bi = rr[i]; }
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double ov = __shfl_down_sync(0xffffffffu, bv, o);
+            const int64_t oi = __shfl_down_sync(0xffffffffu, bi, o);
+            if (better(ov, oi, bv, bi)) { bv = ov; bi = oi; }
+        }
+        if (lane == 0) { red_v[warp] = bv; red_i[warp] = bi; }
+        __syncthreads();  // (1)
+        double cv = red_v[0];
+        int64_t ci = red_i[0];
+#pragma unroll
+        for (int wv = 1; wv < LU_THREADS / 32; ++wv)
+            if (better(red_v[wv], red_i[wv], cv, ci)) { cv = red_v[wv]; ci = red_i[wv]; }
+        // publish this CTA's candidate (by the thread owning its row) and, in CTA 0, row jr
+        double* rec = CLUSTER ? crec[par] : a.xbuf + ((int64_t)par * G + me) * LR_REC;
+        double* recj = CLUSTER ? crec[par] + LR_REC : a.rowj + par * LU_JBMAX;
+#pragma unroll
+        for (int i = 0; i < RPT; ++i) {
+            if (rr[i] == ci) {
+                rec[0] = cv;
+                rec[1] = __longlong_as_double((long long)ci);
+#pragma unroll
+                for (int c = 0; c < 32; ++c)
+                    if (c < jb) rec[2 + c] = av[i][c];
+                if (!CLUSTER) st_release_u64(tags + (int64_t)par * G + me, tag);
+            }
+            if (rr[i] == jr) {
+#pragma unroll
+                for (int c = 0; c < 32; ++c)
+                    if (c < jb) recj[c] = av[i][c];
+                if (!CLUSTER) st_release_u64(tags + 2 * (int64_t)G + par, tag);
+            }
+        }
+        if (ci == INT64_MAX && tid == 0) {  // no active row here
+            rec[0] = -1.0;
+            rec[1] = __longlong_as_double((long long)INT64_MAX);
+            if (!CLUSTER) st_release_u64(tags + (int64_t)par * G + me, tag);
+        }
+        if (CLUSTER) cg::this_cluster().sync();
+        if (warp == 0) {  // every CTA picks the same winner and fetches its row and row jr
+            double v = -1.0;
+            int64_t idx = INT64_MAX;
+            int wq = 0;
+            if (!CLUSTER) {
+                // wait for every CTA's record: relaxed (volatile) polls of all of this lane's tags in flight
+                // together, then one acquire fence before the data reads
+                bool ready;
+                do {
+                    ready = true;
+                    for (int q = lane; q < G; q += 32)
+                        ready &= (*(volatile const unsigned long long*)(tags + (int64_t)par * G + q) == tag);
+                    if (!__all_sync(0xffffffffu, ready)) __nanosleep(20);
+                    else break;
+                } while (true);
+                __threadfence();
+            }
+            for (int q = lane; q < G; q += 32) {
+                double qv;
+                int64_t qi;
+                if (CLUSTER) {
+                    const double* pr = cg::this_cluster().map_shared_rank(crec[par], q);
+                    qv = pr[0];
+                    qi = (int64_t)__double_as_longlong(pr[1]);
+                } else {
+                    const double* pr = a.xbuf + ((int64_t)par * G + q) * LR_REC;
+                    qv = __ldcg(pr);
+                    qi = (int64_t)__double_as_longlong(__ldcg(pr + 1));
+                }
+                if (better(qv, qi, v, idx)) { v = qv; idx = qi; wq = q; }
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const double ov = __shfl_down_sync(0xffffffffu, v, o);
+                const int64_t oi = __shfl_down_sync(0xffffffffu, idx, o);
+                const int ow = __shfl_down_sync(0xffffffffu, wq, o);
+                if (better(ov, oi, v, idx)) { v = ov; idx = oi; wq = ow; }
+            }
+            idx = __shfl_sync(0xffffffffu, idx, 0);
+            wq = __shfl_sync(0xffffffffu, wq, 0);
+            if (CLUSTER) {
+                if (lane < jb) {
+                    pivrow[lane] = cg::this_cluster().map_shared_rank(crec[par], wq)[2 + lane];
+                    oldrow[lane] = cg::this_cluster().map_shared_rank(crec[par], 0)[LR_REC + lane];
+                }
+            } else {
+                if (lane < jb) pivrow[lane] = __ldcg(a.xbuf + ((int64_t)par * G + wq) * LR_REC + 2 + lane);
+                while (ld_acquire_u64(tags + 2 * (int64_t)G + par) != tag) __nanosleep(32);
+                if (lane < jb) oldrow[lane] = __ldcg(a.rowj + par * LU_JBMAX + lane);
+            }
+            if (lane == 0) {
+                s_piv = idx;
+                if (me == 0) a.ipiv[jr] = (int)idx;
+            }
+        }
+        __syncthreads();  // (2)
+        const int64_t piv = s_piv;
+        const double u = pivrow[j];
+        if (tid == 0) spiv[j] = (u != 0.0) ? piv : jr;
+        if (u != 0.0) {  // (an exactly zero pivot column: no swap, no scaling, Z18)
+#pragma unroll
+            for (int i = 0; i < RPT; ++i) {
+                const int64_t r = rr[i];
+                if (r >= a.w || r < jr) continue;
+                if (r == jr) {
+                    if (piv != jr) {
+#pragma unroll
+                        for (int c = 0; c < 32; ++c)
+                            if (c < jb) av[i][c] = pivrow[c];
+                    }
+                    continue;
+                }
+                const bool swapped = (r == piv);
+                const double l = (swapped ? oldrow[j] : xj[i]) / u;
+#pragma unroll
+                for (int c = 0; c < 32; ++c) {
+                    const double base = swapped ? oldrow[c < jb ? c : 0] : av[i][c];
+                    av[i][c] = (c < j) ? base : ((c == j) ? l : fma(-l, pivrow[c < jb ? c : 0], base));
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < RPT; ++i)
+        if (rr[i] < a.w) {
+#pragma unroll
+            for (int c = 0; c < 32; ++c)
+                if (c < jb) a.L[rr[i] + (a.c0 + c) * a.ld] = av[i][c];
+        }
+    if (CLUSTER) cg::this_cluster().sync();  // peers may still read this CTA's last records
+    __syncthreads();
+    const int64_t gtid = (int64_t)me * LU_THREADS + tid, gstride = (int64_t)G * LU_THREADS;
+    apply_panel_interchanges(a, spiv, trow, tsrc, &s_nt, gtid, gstride);
+}
+
+static int lu_reg_mode()
+{
+    static int use = -1;
+    if (use < 0) {  // BQRRP_LU_LEAF=0: the shared-memory slab kernels only; 2: register leaf in grid form too
+        const char* e = std::getenv("BQRRP_LU_LEAF");
+        use = (e && e[0] == '0') ? 0 : ((e && e[0] == '2') ? 2 : 1);
+    }
+    return use;
+}
+
+// The register leaf is used in its one-row-per-thread cluster form only (rows <= 16 CTAs x 256 threads:
+// 5.8 vs 6.4 us per column).  With two rows per thread it only ties the shared-memory cluster kernel
+// (8192 rows), and its grid form (global-memory records with release/acquire tags, cooperative launch) is
+// correct but ~1.8x SLOWER than the shared-memory grid kernel at C3 sizes (w = 16384 .. 63488: 8.4-13.9
+// vs 6.6-7.6 us per column, profiles/lu_leaf_r01.json), so those panels keep the slab kernels; the other
+// forms stay selectable (BQRRP_LU_LEAF=2) for further work.
+static bool lu_reg_fits(int64_t rows, int num_sms)
+{
+    const int mode = lu_reg_mode();
+    if (mode == 0) return false;
+    if (mode == 2) return rows <= (int64_t)num_sms * LU_THREADS * 2;
+    return rows <= 16 * LU_THREADS;
+}
+
+static bool lu_panel_reg(Ctx& cx, double* L, int64_t ld, int64_t w, int64_t d, int64_t c0, int jb, int* ipiv, int* perm,
+                         double* xbuf, double* rowj, unsigned long long* tags, unsigned long long* seq)
+{
+    const int64_t rows = w - c0;
+    if (!lu_reg_fits(rows, cx.num_sms) || jb > 32) return false;
+    const bool cluster = rows <= 16 * LU_THREADS * 2;
+    const int rpt = cluster ? (rows <= 16 * LU_THREADS ? 1 : 2) : (rows <= (int64_t)cx.num_sms * LU_THREADS ? 1 : 2);
+    const int G = (int)cdiv(rows, (int64_t)LU_THREADS * rpt);
+    LuPanelArgs a{L, ld, w, d, c0, jb, LU_THREADS * rpt, ipiv, perm, xbuf, rowj};
+    const unsigned long long tag0 = (++*seq) << 6;
+    if (cluster) {
+        static bool attr = false;
+        if (!attr) {
+            BQ_CUDA(cudaFuncSetAttribute(lu_leaf_reg_kernel<1, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+            BQ_CUDA(cudaFuncSetAttribute(lu_leaf_reg_kernel<2, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+            attr = true;
+        }
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(G);
+        cfg.blockDim = dim3(LU_THREADS);
+        cfg.stream = cx.stream;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = G;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        if (rpt == 1) BQ_CUDA(cudaLaunchKernelEx(&cfg, lu_leaf_reg_kernel<1, true>, a, tag0, tags));
+        else BQ_CUDA(cudaLaunchKernelEx(&cfg, lu_leaf_reg_kernel<2, true>, a, tag0, tags));
+    } else {
+        void* args[] = {&a, (void*)&tag0, &tags};
+        if (rpt == 1)
+            BQ_CUDA(cudaLaunchCooperativeKernel((void*)lu_leaf_reg_kernel<1, false>, dim3(G), dim3(LU_THREADS), args, 0,
+                                                cx.stream));
+        else
+            BQ_CUDA(cudaLaunchCooperativeKernel((void*)lu_leaf_reg_kernel<2, false>, dim3(G), dim3(LU_THREADS), args, 0,
+                                                cx.stream));
+    }
+    ++g_launches;
+    return true;
+}
+
 static bool lu_cluster_fits(int64_t rows, int jb, int* CLout, int* Rout)
 {
     int CL = (int)imin(LUC_CLMAX, imax(1, cdiv(rows, 512)));
@@ -390,9 +683,19 @@ static bool lu_panel_cluster(Ctx& cx, double* L, int64_t ld, int64_t w, int64_t 
     return true;
 }
 
+struct LuExchange {
+    double* xbuf;
+    double* rowj;
+    unsigned long long* tags;  // [2][G] candidate tags + [2] row-jr tags (register leaf, grid mode)
+    unsigned long long seq;    // launches so far in this getrf (tags are zeroed per getrf)
+};
+
 static void lu_panel(Ctx& cx, double* L, int64_t ld, int64_t w, int64_t d, int64_t c0, int jb, int* ipiv, int* perm,
-                     double* xbuf, double* rowj)
+                     LuExchange& ex)
 {
+    if (lu_panel_reg(cx, L, ld, w, d, c0, jb, ipiv, perm, ex.xbuf, ex.rowj, ex.tags, &ex.seq)) return;
+    double* xbuf = ex.xbuf;
+    double* rowj = ex.rowj;
     if (lu_panel_cluster(cx, L, ld, w, d, c0, jb, ipiv, perm)) return;
     int64_t rows = w - c0;
     // few enough CTAs that the barrier stays cheap, enough that the slab fits shared memory
@@ -417,6 +720,7 @@ static void lu_panel(Ctx& cx, double* L, int64_t ld, int64_t w, int64_t d, int64
 
 static int lu_leaf_width(int64_t rows, int num_sms)
 {
+    if (lu_reg_fits(rows, num_sms)) return 32;  // the register leaf holds any row count up to 148 x 512
     // a leaf that one cluster can hold (32, else 16 columns), else the widest the grid kernel can hold
     int CL, R;
     if (lu_cluster_fits(rows, 32, &CL, &R)) return 32;
@@ -428,15 +732,15 @@ static int lu_leaf_width(int64_t rows, int num_sms)
 }
 
 static void getrf_rec(Ctx& cx, double* L, int64_t ld, int64_t w, int64_t d, int64_t c0, int64_t c1, int* ipiv,
-                      int* perm, double* xbuf, double* rowj, int leaf)
+                      int* perm, LuExchange& ex, int leaf)
 {
     int64_t nc = c1 - c0;
     if (nc <= leaf) {
-        lu_panel(cx, L, ld, w, d, c0, (int)nc, ipiv, perm, xbuf, rowj);
+        lu_panel(cx, L, ld, w, d, c0, (int)nc, ipiv, perm, ex);
         return;
     }
     int64_t mid = c0 + cdiv(nc / 2, leaf) * leaf;
-    getrf_rec(cx, L, ld, w, d, c0, mid, ipiv, perm, xbuf, rowj, leaf);
+    getrf_rec(cx, L, ld, w, d, c0, mid, ipiv, perm, ex, leaf);
     // (the left half's interchanges were applied to whole rows inside its panels)
     // U12 = L11^{-1} A12 ; A22 -= L21 U12
     int64_t ncr = c1 - mid;
@@ -444,7 +748,7 @@ static void getrf_rec(Ctx& cx, double* L, int64_t ld, int64_t w, int64_t d, int6
     double* A12 = L + c0 + mid * ld;
     trsm_left_lower_unit(cx, mid - c0, ncr, L11, ld, A12, ld);
     gemm(cx, false, false, w - mid, ncr, mid - c0, -1.0, L + mid + c0 * ld, ld, A12, ld, 1.0, L + mid + mid * ld, ld);
-    getrf_rec(cx, L, ld, w, d, mid, c1, ipiv, perm, xbuf, rowj, leaf);
+    getrf_rec(cx, L, ld, w, d, mid, c1, ipiv, perm, ex, leaf);
 }
 
 __global__ void iota_kernel(int64_t n, int* p)
@@ -460,10 +764,14 @@ void getrf_pivots(Ctx& cx, double* L, int64_t ld, int64_t w, int64_t d, int* ipi
     BQ_LAUNCH_CHECK();
     if (nlu <= 0) return;
     size_t mark = cx.ws_used;
-    double* xbuf = cx.alloc(2 * (size_t)cx.num_sms * LU_XSTRIDE);
-    double* rowj = cx.alloc(2 * LU_JBMAX);
+    LuExchange ex;
+    ex.xbuf = cx.alloc(2 * (size_t)cx.num_sms * LU_XSTRIDE);
+    ex.rowj = cx.alloc(2 * LU_JBMAX);
+    ex.tags = cx.alloc_as<unsigned long long>(2 * (size_t)cx.num_sms + 2);
+    ex.seq = 0;
+    BQ_CUDA(cudaMemsetAsync(ex.tags, 0, sizeof(unsigned long long) * (2 * (size_t)cx.num_sms + 2), cx.stream));
     int leaf = lu_leaf_width(w, cx.num_sms);
-    getrf_rec(cx, L, ld, w, nlu, 0, nlu, ipiv, perm, xbuf, rowj, leaf);
+    getrf_rec(cx, L, ld, w, nlu, 0, nlu, ipiv, perm, ex, leaf);
     cx.ws_used = mark;
 }
 

@@ -13,6 +13,7 @@
 //      MskT(s+p:n, :) <- MskT(s+p:n, :) - ((MskT(s+p:n, :) V) T) V^T  (three DMMA GEMMs).
 //   3. R_sk(:, 0:p)^T (upper trapezoidal, explicit zeros) is written back to MskT(s:s+p, :).
 #include <cooperative_groups.h>
+#include <cstdlib>
 
 #include "blas.cuh"
 #include "bqrrp_internal.cuh"
@@ -371,6 +372,207 @@ __global__ void __launch_bounds__(QC_THREADS, 1) qr_panel_cluster_kernel(QrClust
     cluster.sync();  // keep every CTA's shared memory alive until CTA 0 has read it
 }
 
+// ---------------------------------------------------------------------------------------------
+// Register-resident cluster leaf (rows <= 16 x 256): one panel row per thread, its <= 32 entries in
+// registers, and ONE cluster barrier per column with push-style exchange:
+//   1. every thread with row r > jr forms q[c] = x_r a_r[c] for all 32 c (q[j] = x_r^2); a 31-shuffle
+//      transpose-reduction leaves the warp sum of q[c] in lane c, which stores it into slot (warp) of
+//      EVERY CTA's shared memory (DSMEM); warp 0 of CTA 0 (which owns the leaf's 32 pivot rows) also
+//      pushes the pivot row a_jr[:];
+//   2. barrier.cluster;
+//   3. every warp sums the slots in a fixed order (lane c: coefficient c), forms beta, tau, denom
+//      (convention H, reading Z9/Z20) and coef_c = tau (a_jr[c] + sum_c / denom) for c > j; for c < j the
+//      same sums give V(:, c)^T v_j, the column of the larft recurrence for T (no separate Gram pass);
+//   4. each thread updates its own row (coef_c broadcast by shuffles).
+// The slots are double-buffered by column parity: a CTA can only reach column j+2's stores after the
+// barrier of column j+1, which every thread passes only after finishing column j's reads.
+constexpr int QL_THREADS = 256, QL_WARPS = QL_THREADS / 32, QL_CLMAX = 16;
+
+// v[j] for a runtime j < 32 from a register array: a 5-level select tree (31 independent-per-level selects,
+// depth 5) instead of a 32-long dependent select chain or a local-memory indexed load.
+__device__ __forceinline__ double select32(const double (&v)[32], int j)
+{
+    double l1[16], l2[8], l3[4], l4[2];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) l1[i] = (j & 1) ? v[2 * i + 1] : v[2 * i];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) l2[i] = (j & 2) ? l1[2 * i + 1] : l1[2 * i];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) l3[i] = (j & 4) ? l2[2 * i + 1] : l2[2 * i];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) l4[i] = (j & 8) ? l3[2 * i + 1] : l3[2 * i];
+    return (j & 16) ? l4[1] : l4[0];
+}
+
+struct QrLeafArgs {
+    double* A;
+    int64_t ld;
+    int64_t m;
+    int64_t c0;
+    int jb;
+    double* tau;
+    double* V;
+    double* T;
+    int64_t ldt;
+};
+
+__global__ void __launch_bounds__(QL_THREADS, 1) qr_leaf_reg_kernel(QrLeafArgs a)
+{
+    cg::cluster_group cluster = cg::this_cluster();
+    const int CL = (int)cluster.num_blocks(), me = (int)cluster.block_rank();
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, jb = a.jb;
+    const int NS = CL * QL_WARPS;  // slot sources
+    extern __shared__ double dyn[];
+    double* slot = dyn;                    // [2][NS][32]
+    double* prow = slot + 2 * NS * 32;     // [2][32]
+    __shared__ double TcS[32][33];         // TcS[j][l] = V(:, l)^T v_j (CTA 0)
+    __shared__ double taus[32];
+    const int64_t r = a.c0 + (int64_t)me * QL_THREADS + tid;  // this thread's row
+    const bool has = r < a.m;
+    double av[32];
+#pragma unroll
+    for (int c = 0; c < 32; ++c) av[c] = (has && c < jb) ? a.A[r + (a.c0 + c) * a.ld] : 0.0;
+    const int src = me * QL_WARPS + warp;
+
+    // The column loop is NOT unrolled (a 32-way unrolled body overflows the instruction cache: ~30 % of
+    // the samples were no-instruction stalls); av[j] is read / written through unrolled selects so the
+    // row stays in registers.
+#pragma unroll 1
+    for (int j = 0; j < jb; ++j) {
+        const int par = j & 1;
+        const int64_t jr = a.c0 + j;
+        double q[32];
+        const double xj = select32(av, j);
+        const double x = (has && r > jr) ? xj : 0.0;
+#pragma unroll
+        for (int c = 0; c < 32; ++c) q[c] = x * av[c];  // q[j] = x^2
+        const double ws = warp_transpose_reduce32(q, lane);
+        double* my = slot + (par * NS + src) * 32 + lane;
+        for (int rk = 0; rk < CL; ++rk) *cluster.map_shared_rank(my, rk) = ws;
+        if (me == 0 && warp == 0) {  // pivot row jr = row of lane j: broadcast its entries, lane c pushes a_jr[c]
+            // lane l holds row c0 + l, so a_jr[c] is lane j's av[c]: lane c keeps it
+            double pv = 0.0;
+#pragma unroll
+            for (int c = 0; c < 32; ++c) {
+                const double t = __shfl_sync(0xffffffffu, av[c], j);
+                pv = (lane == c) ? t : pv;
+            }
+            for (int rk = 0; rk < CL; ++rk) *cluster.map_shared_rank(prow + par * 32 + lane, rk) = pv;
+        }
+        cluster.sync();
+        // fixed-order sum of the NS slot values: 4 interleaved partial sums (short dependency chains)
+        double t4[4] = {0.0, 0.0, 0.0, 0.0};
+        for (int sidx = 0; sidx < NS; sidx += 4) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (sidx + u < NS) t4[u] += slot[(par * NS + sidx + u) * 32 + lane];
+        }
+        const double tot = (t4[0] + t4[1]) + (t4[2] + t4[3]);
+        const double ww = prow[par * 32 + lane];
+        const double alpha = __shfl_sync(0xffffffffu, ww, j);
+        const double s2 = __shfl_sync(0xffffffffu, tot, j);
+        const double nrm = sqrt(fma(alpha, alpha, s2));
+        double beta = 0.0, tau = 0.0, denom = 1.0;
+        if (nrm != 0.0) {
+            beta = (alpha >= 0.0) ? -nrm : nrm;  // convention H
+            tau = (beta - alpha) / beta;
+            denom = alpha - beta;
+        }
+        const double vdot = ww + tot / denom;  // lane c: V(:, c)^T v_j (c < j) / w_c = v_j^T A(:, c) (c > j)
+        const double coef = (lane > j && lane < jb) ? tau * vdot : 0.0;
+        if (me == 0 && warp == 0) {
+            if (lane < j) TcS[j][lane] = vdot;
+            if (lane == 0) {
+                taus[j] = tau;
+                a.tau[jr] = tau;
+            }
+        }
+        // update this thread's row (the shuffles stay outside the divergent part)
+        const bool upd = has && r >= jr;
+        double v = 0.0;
+        double newj = xj;
+        if (upd) {
+            if (r == jr) {
+                newj = beta;
+                v = 1.0;
+            } else {
+                v = xj / denom;
+                newj = v;
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < 32; ++c) {
+            const double cf = __shfl_sync(0xffffffffu, coef, c);
+            const double upd_c = fma(-cf, v, av[c]);
+            av[c] = (c == j) ? newj : ((upd && c > j) ? upd_c : av[c]);
+        }
+    }
+    // write back: R / reflectors in A, explicit V
+    if (has) {
+#pragma unroll
+        for (int c = 0; c < 32; ++c) {
+            if (c < jb) {
+                const int64_t cr = a.c0 + c;
+                a.A[r + cr * a.ld] = av[c];
+                a.V[r + cr * a.m] = (r == cr) ? 1.0 : (r > cr ? av[c] : 0.0);
+            }
+        }
+    }
+    // T (larft): T_jj = tau_j, T(0:j, j) = -tau_j T(0:j, 0:j) (V(:, 0:j)^T v_j)
+    if (me == 0 && warp == 0) {
+        __shared__ double Ts[32][33];
+        for (int j = 0; j < jb; ++j) {
+            double t = 0.0;
+            if (lane < j)
+                for (int l = lane; l < j; ++l) t = fma(Ts[lane][l], TcS[j][l], t);
+            __syncwarp();
+            if (lane < j) Ts[lane][j] = -taus[j] * t;
+            if (lane == j) Ts[j][j] = taus[j];
+            if (lane > j) Ts[lane][j] = 0.0;
+            __syncwarp();
+        }
+        for (int j = 0; j < jb; ++j)
+            if (lane < jb) a.T[(a.c0 + lane) + (a.c0 + j) * a.ldt] = Ts[lane][j];
+    }
+    cluster.sync();  // peers may still be reading this CTA's slots
+}
+
+static bool qr_leaf_reg(Ctx& cx, double* A, int64_t ld, int64_t m, int64_t c0, int jb, double* tau, double* V,
+                        double* T, int64_t ldt)
+{
+    static int use = -1;
+    if (use < 0) {  // BQRRP_QR_LEAF=0: the shared-memory cluster kernel (A/B)
+        const char* e = std::getenv("BQRRP_QR_LEAF");
+        use = (e && e[0] == '0') ? 0 : 1;
+    }
+    const int64_t rows = m - c0;
+    const int CL = (int)cdiv(rows, QL_THREADS);
+    if (!use || CL > QL_CLMAX || jb > 32) return false;
+    const size_t smem = ((size_t)2 * CL * QL_WARPS * 32 + 64) * sizeof(double);
+    static bool attr = false;
+    if (!attr) {
+        BQ_CUDA(cudaFuncSetAttribute(qr_leaf_reg_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
+        BQ_CUDA(cudaFuncSetAttribute(qr_leaf_reg_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        attr = true;
+    }
+    QrLeafArgs args{A, ld, m, c0, jb, tau, V, T, ldt};
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(CL);
+    cfg.blockDim = dim3(QL_THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = cx.stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = CL;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    BQ_CUDA(cudaLaunchKernelEx(&cfg, qr_leaf_reg_kernel, args));
+    ++g_launches;
+    return true;
+}
+
 static bool qr_panel_cluster(Ctx& cx, double* A, int64_t ld, int64_t m, int64_t c0, int jb, double* tau, double* V,
                              double* T, int64_t ldt)
 {
@@ -405,6 +607,7 @@ static bool qr_panel_cluster(Ctx& cx, double* A, int64_t ld, int64_t m, int64_t 
 static void qr_panel(Ctx& cx, double* A, int64_t ld, int64_t m, int64_t c0, int jb, double* tau, double* V, double* T,
                      int64_t ldt, double* xbuf, double* rowj)
 {
+    if (qr_leaf_reg(cx, A, ld, m, c0, jb, tau, V, T, ldt)) return;
     if (qr_panel_cluster(cx, A, ld, m, c0, jb, tau, V, T, ldt)) return;
     int64_t rows = m - c0;
     int G = (int)imin(cx.num_sms, imax(1, cdiv(rows, 64)));

@@ -248,6 +248,43 @@ int bqrrp_step_wy_update(int64_t h, int64_t k, int64_t t, const double* V, const
     });
 }
 
+int bqrrp_step_wy_top(int64_t h, int64_t k, int64_t t, const double* V, const double* T, double* C, int64_t ldc,
+                      double* W2, int64_t ldw, void* stream)
+{
+    if (h < 1) return -1;
+    if (k < 1) return -2;
+    if (t < 0) return -3;
+    if (!W2 || ldw < k) return -9;
+    if (t == 0) return 0;
+    return step_guard([&]() -> int {
+        StepWs sw(stream, ((size_t)k * t + 4096) * 8, (size_t)16 * k * k * 8 + (4u << 20));
+        Ctx& cx = sw.cx;
+        double* W = cx.alloc((size_t)k * t);
+        gemm(cx, true, false, k, t, h, 1.0, V, h, C, ldc, 0.0, W, k);      // W  = V^T C
+        gemm(cx, true, false, k, t, k, 1.0, T, k, W, k, 0.0, W2, ldw);     // W2 = T^T W
+        gemm(cx, false, false, imin(k, h), t, k, -1.0, V, h, W2, ldw, 1.0, C, ldc);  // rows 0:k (R12)
+        return 0;
+    });
+}
+
+int bqrrp_step_wy_bulk(int64_t h, int64_t k, int64_t t, const double* V, const double* W2, int64_t ldw, double* C,
+                       int64_t ldc, void* stream)
+{
+    if (h < 1) return -1;
+    if (k < 1) return -2;
+    if (t < 0) return -3;
+    if (!W2 || ldw < k) return -6;
+    if (t == 0 || h <= k) return 0;
+    return step_guard([&]() -> int {
+        StepWs sw(stream, 4096 * 8, (size_t)16 * 8 + (4u << 20));
+        Ctx& cx = sw.cx;
+        cx.splitk = nullptr;  // one CTA per tile, no split-K scratch shared with the critical stream
+        cx.splitk_elems = 0;
+        gemm(cx, false, false, h - k, t, k, -1.0, V + k, h, W2, ldw, 1.0, C + k, ldc);  // rows k:h
+        return 0;
+    });
+}
+
 int bqrrp_step_sample_update(int64_t b, int64_t t, const double* R11, int64_t ldr, const double* R12, int64_t ld12,
                              double* MskT_s, int64_t ldm, void* stream)
 {

@@ -73,6 +73,8 @@ def _declare():
     L.bqrrp_step_zero_column_check.argtypes = [i64, P, ctypes.POINTER(i32), P]
     L.bqrrp_step_panel.argtypes = [i64, i64, P, i64, P, i64, P, P, P, i32, P]
     L.bqrrp_step_wy_update.argtypes = [i64, i64, i64, P, P, P, i64, P]
+    L.bqrrp_step_wy_top.argtypes = [i64, i64, i64, P, P, P, i64, P, i64, P]
+    L.bqrrp_step_wy_bulk.argtypes = [i64, i64, i64, P, P, i64, P, i64, P]
     L.bqrrp_step_sample_update.argtypes = [i64, i64, P, i64, P, i64, P, i64, P]
     L.bqrrp_step_zero.argtypes = [i64, i64, P, i64, P]
     L.bqrrp_debug_sketch.argtypes = [i64, i64, P, i64, i64, ctypes.c_uint64, P, P, P]
@@ -81,10 +83,31 @@ def _declare():
 
 
 def factor_dist(A_loc, m: int, n: int, b: int, d: int | None = None, seed: int = 0, rank_tol: float | None = None,
-                cholqr_passes: int = 2, group=None):
+                cholqr_passes: int = 2, group=None, lookahead: bool = True):
     """Distributed BQRRP.  A_loc: this rank's block-cyclic columns (m x n_loc, column-major float64 CUDA).
     Returns (A_loc, tau, J, rank) with A_loc overwritten in GEQP3 format (R above, V below, in this rank's
-    columns), tau (min(m,n)) and J (n, one-based gather) replicated."""
+    columns), tau (min(m,n)) and J (n, one-based gather) replicated.
+
+    lookahead: the critical chain runs on a high-priority stream and each rank's bulk trailing rows (rows k:h
+    of C -= V W2, bqrrp_step_wy_bulk) on a low-priority one, overlapping the R12 exchange, the replicated
+    sample update and the next pivot selection; the next column exchange waits for it."""
+    import torch
+
+    caller = torch.cuda.current_stream(A_loc.device)
+    crit = torch.cuda.Stream(device=A_loc.device, priority=-1)
+    bulk = torch.cuda.Stream(device=A_loc.device, priority=0) if lookahead else None
+    crit.wait_stream(caller)
+    if bulk is not None:
+        bulk.wait_stream(caller)
+    with torch.cuda.stream(crit):
+        out = _factor_dist_impl(A_loc, m, n, b, d, seed, rank_tol, cholqr_passes, group, bulk)
+    caller.wait_stream(crit)
+    if bulk is not None:
+        caller.wait_stream(bulk)
+    return out
+
+
+def _factor_dist_impl(A_loc, m, n, b, d, seed, rank_tol, cholqr_passes, group, bulk):
     import torch
     import torch.distributed as dist
 
@@ -124,6 +147,7 @@ def factor_dist(A_loc, m: int, n: int, b: int, d: int | None = None, seed: int =
     nt = torch.zeros(1, dtype=torch.int32, device=dev)
     ell = mn
     i = 0
+    pending = None  # bulk trailing update of the previous iteration (lookahead)
     while True:
         s = i * b
         if s >= mn:
@@ -137,7 +161,10 @@ def factor_dist(A_loc, m: int, n: int, b: int, d: int | None = None, seed: int =
                                    _ptr(tq), _ptr(tsrc), _ptr(nt), ctypes.byref(k), st), "bqrrp_step_pivots")
         k = int(k.value)
         ntv = int(nt.item())
-        # ---- a3: X3 column exchange through one exactly-summed buffer
+        # ---- a3: X3 column exchange through one exactly-summed buffer (after this rank's bulk update landed)
+        if pending is not None:
+            torch.cuda.current_stream().wait_event(pending)
+            pending = None
         if ntv > 0:
             q = tq[:ntv].cpu().numpy().astype(np.int64) + s
             p = tsrc[:ntv].cpu().numpy().astype(np.int64) + s
@@ -187,7 +214,22 @@ def factor_dist(A_loc, m: int, n: int, b: int, d: int | None = None, seed: int =
         j_tr = bc.first_local_at_or_after(s + k)
         t_loc = bc.n_loc - j_tr
         if t_loc > 0:
-            _check(L.bqrrp_step_wy_update(h, k, t_loc, _ptr(V), _ptr(T), _ptr(A_loc[s:, j_tr:]), lda, st), "wy")
+            C = A_loc[s:, j_tr:]
+            terminal = k < kmax or c == n or r == m
+            if bulk is None or terminal or h <= k:
+                _check(L.bqrrp_step_wy_update(h, k, t_loc, _ptr(V), _ptr(T), _ptr(C), lda, st), "wy")
+            else:
+                W2 = colmaj(k, t_loc)
+                _check(L.bqrrp_step_wy_top(h, k, t_loc, _ptr(V), _ptr(T), _ptr(C), lda, _ptr(W2), k, st), "wy_top")
+                ev_top = torch.cuda.Event()
+                ev_top.record()
+                bulk.wait_event(ev_top)
+                _check(L.bqrrp_step_wy_bulk(h, k, t_loc, _ptr(V), _ptr(W2), k, _ptr(C), lda,
+                                            ctypes.c_void_p(bulk.cuda_stream)), "wy_bulk")
+                V.record_stream(bulk)
+                W2.record_stream(bulk)
+                pending = torch.cuda.Event()
+                pending.record(bulk)
         if k < kmax or c == n or r == m:
             ell = s + k
             break
@@ -202,6 +244,8 @@ def factor_dist(A_loc, m: int, n: int, b: int, d: int | None = None, seed: int =
         allreduce_sum(R12)
         _check(L.bqrrp_step_sample_update(b, t, _ptr(R11), b, _ptr(R12), k, _ptr(MskT[s:]), n, st), "sample_update")
         i += 1
+    if pending is not None:
+        torch.cuda.current_stream().wait_event(pending)
     # ---- O4: tau(ell:) = 0, A(ell:m, ell:n) = 0 on the columns this rank owns
     if ell < mn:
         tau[ell:mn] = 0.0

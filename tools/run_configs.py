@@ -112,6 +112,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--only", default="")
     ap.add_argument("--tols", default="1e-13,3e-14,1e-14")
+    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "configs_r01.json"))
     args = ap.parse_args()
     res = {}
     if args.only in ("", "C4"):
@@ -120,7 +121,7 @@ def main():
         torch.cuda.empty_cache()
     if args.only in ("", "C5"):
         res["C5"] = run_c5([float(x) for x in args.tols.split(",")])
-    json.dump(res, open(os.path.join(ROOT, "profiles", "configs_r01.json"), "w"), indent=1)
+    json.dump(res, open(args.out, "w"), indent=1)
 
 
 if __name__ == "__main__":
