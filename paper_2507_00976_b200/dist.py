@@ -83,14 +83,16 @@ def _declare():
 
 
 def factor_dist(A_loc, m: int, n: int, b: int, d: int | None = None, seed: int = 0, rank_tol: float | None = None,
-                cholqr_passes: int = 2, group=None, lookahead: bool = True):
+                cholqr_passes: int = 2, group=None, lookahead: bool = True, exchange: str = "auto"):
     """Distributed BQRRP.  A_loc: this rank's block-cyclic columns (m x n_loc, column-major float64 CUDA).
     Returns (A_loc, tau, J, rank) with A_loc overwritten in GEQP3 format (R above, V below, in this rank's
     columns), tau (min(m,n)) and J (n, one-based gather) replicated.
 
     lookahead: the critical chain runs on a high-priority stream and each rank's bulk trailing rows (rows k:h
     of C -= V W2, bqrrp_step_wy_bulk) on a low-priority one, overlapping the R12 exchange, the replicated
-    sample update and the next pivot selection; the next column exchange waits for it."""
+    sample update and the next pivot selection; the next column exchange waits for it.
+    exchange: "a2a" (point-to-point column moves), "allreduce" (exact-sum of the touched set) or "auto"
+    (a2a on NCCL)."""
     import torch
 
     caller = torch.cuda.current_stream(A_loc.device)
@@ -100,14 +102,46 @@ def factor_dist(A_loc, m: int, n: int, b: int, d: int | None = None, seed: int =
     if bulk is not None:
         bulk.wait_stream(caller)
     with torch.cuda.stream(crit):
-        out = _factor_dist_impl(A_loc, m, n, b, d, seed, rank_tol, cholqr_passes, group, bulk)
+        out = _factor_dist_impl(A_loc, m, n, b, d, seed, rank_tol, cholqr_passes, group, bulk, exchange)
     caller.wait_stream(crit)
     if bulk is not None:
         caller.wait_stream(bulk)
     return out
 
 
-def _factor_dist_impl(A_loc, m, n, b, d, seed, rank_tol, cholqr_passes, group, bulk):
+def _exchange_a2a(L, A_loc, lda, m, q, p, bc, me, G, group, st, dev, colmaj):
+    """X3 (a3): move column position p[t] -> q[t] for every touched slot t (q sorted).  Every source column is
+    gathered (sends in (destination rank, slot) order, then this rank's local moves) before any destination is
+    written; one all_to_all_single carries the cross-rank columns; receives arrive in (source rank, slot) order."""
+    import torch
+    import torch.distributed as dist
+
+    src, dst = bc.owner_of[p], bc.owner_of[q]
+    s_idx = np.nonzero((src == me) & (dst != me))[0]
+    s_idx = s_idx[np.argsort(dst[s_idx], kind="stable")]
+    r_idx = np.nonzero((dst == me) & (src != me))[0]
+    r_idx = r_idx[np.argsort(src[r_idx], kind="stable")]
+    l_idx = np.nonzero((src == me) & (dst == me))[0]
+    ns, nr, nl = len(s_idx), len(r_idx), len(l_idx)
+    pack = np.concatenate([bc.loc_of[p[s_idx]], bc.loc_of[p[l_idx]]]).astype(np.int32)
+    buf = colmaj(m, max(ns + nl, 1))
+    if ns + nl > 0:
+        _check(L.bqrrp_step_gather_columns(m, _ptr(A_loc), lda, _ptr(torch.as_tensor(pack, device=dev)), ns + nl,
+                                           _ptr(buf), m, st), "gather")
+    recv = colmaj(m, max(nr, 1))
+    send_counts = (np.bincount(dst[s_idx], minlength=G) * m).tolist()
+    recv_counts = (np.bincount(src[r_idx], minlength=G) * m).tolist()
+    dist.all_to_all_single(recv.t().reshape(-1)[: nr * m], buf.t().reshape(-1)[: ns * m], recv_counts, send_counts,
+                           group=group)
+    if nr > 0:
+        idx = torch.as_tensor(bc.loc_of[q[r_idx]].astype(np.int32), device=dev)
+        _check(L.bqrrp_step_scatter_columns(m, _ptr(A_loc), lda, _ptr(idx), nr, _ptr(recv), m, st), "scatter")
+    if nl > 0:
+        idx = torch.as_tensor(bc.loc_of[q[l_idx]].astype(np.int32), device=dev)
+        _check(L.bqrrp_step_scatter_columns(m, _ptr(A_loc), lda, _ptr(idx), nl, _ptr(buf[:, ns:]), m, st), "scatter")
+
+
+def _factor_dist_impl(A_loc, m, n, b, d, seed, rank_tol, cholqr_passes, group, bulk, exchange):
     import torch
     import torch.distributed as dist
 
@@ -127,6 +161,10 @@ def _factor_dist_impl(A_loc, m, n, b, d, seed, rank_tol, cholqr_passes, group, b
 
     def allreduce_sum(t):
         dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+
+    # X3 as point-to-point moves (all_to_all_single: each moved column crosses the fabric once) on NCCL; the
+    # exact-sum all-reduce of the whole touched set (2x the volume, every column to every rank) otherwise
+    use_a2a = exchange == "a2a" or (exchange == "auto" and dist.get_backend(group) == "nccl")
 
     def colmaj(rows, cols):
         return torch.zeros((cols, rows), **f64).t()
@@ -172,14 +210,17 @@ def _factor_dist_impl(A_loc, m, n, b, d, seed, rank_tol, cholqr_passes, group, b
             # the exchange buffer names the same column on every rank
             o = np.argsort(q, kind="stable")
             q, p = q[o], p[o]
-            pack = np.where(bc.owner_of[p] == me, bc.loc_of[p], -1).astype(np.int32)
-            unpack = np.where(bc.owner_of[q] == me, bc.loc_of[q], -1).astype(np.int32)
-            buf = colmaj(m, ntv)
-            _check(L.bqrrp_step_gather_columns(m, _ptr(A_loc), lda, _ptr(torch.as_tensor(pack, device=dev)), ntv,
-                                               _ptr(buf), m, st), "gather")
-            allreduce_sum(buf)
-            _check(L.bqrrp_step_scatter_columns(m, _ptr(A_loc), lda, _ptr(torch.as_tensor(unpack, device=dev)), ntv,
-                                                _ptr(buf), m, st), "scatter")
+            if use_a2a:
+                _exchange_a2a(L, A_loc, lda, m, q, p, bc, me, G, group, st, dev, colmaj)
+            else:
+                pack = np.where(bc.owner_of[p] == me, bc.loc_of[p], -1).astype(np.int32)
+                unpack = np.where(bc.owner_of[q] == me, bc.loc_of[q], -1).astype(np.int32)
+                buf = colmaj(m, ntv)
+                _check(L.bqrrp_step_gather_columns(m, _ptr(A_loc), lda, _ptr(torch.as_tensor(pack, device=dev)), ntv,
+                                                   _ptr(buf), m, st), "gather")
+                allreduce_sum(buf)
+                _check(L.bqrrp_step_scatter_columns(m, _ptr(A_loc), lda, _ptr(torch.as_tensor(unpack, device=dev)),
+                                                    ntv, _ptr(buf), m, st), "scatter")
         # ---- a7 early exit: the owner of position s tests A(s:m, s)
         owner = int(bc.owner_of[s])
         flag = torch.zeros(1, **f64)
@@ -233,15 +274,35 @@ def _factor_dist_impl(A_loc, m, n, b, d, seed, rank_tol, cholqr_passes, group, b
         if k < kmax or c == n or r == m:
             ell = s + k
             break
-        # ---- a6: R11 and R12 (k x t, position order) by exact all-reduce, replicated sketch update
+        # ---- a6: R11 and R12 (k x t, position order) assembled on every rank, replicated sketch update
         dist.broadcast(R11, src=owner, group=group)
         t = n - c
-        R12 = colmaj(k, t)
         j_c = bc.first_local_at_or_after(c)
-        if bc.n_loc - j_c > 0:
-            slots = torch.as_tensor(bc.pos[j_c:] - c, device=dev)
-            R12[:, slots] = A_loc[s:s + k, j_c:]
-        allreduce_sum(R12)
+        if use_a2a:
+            # X1 as an all-gather of every rank's own R12 columns (padded to the largest share), then one
+            # gather into position order: each column crosses the fabric once (the exact-sum all-reduce
+            # moves the whole k x t block twice)
+            q_own = bc.owner_of[c:n]
+            counts = np.bincount(q_own, minlength=G)
+            cmax = int(counts.max())
+            loc = colmaj(k, cmax)
+            if bc.n_loc - j_c > 0:
+                loc[:, : bc.n_loc - j_c] = A_loc[s:s + k, j_c:]
+            gathered = colmaj(k, G * cmax)
+            dist.all_gather_into_tensor(gathered.t().reshape(-1), loc.t().reshape(-1), group=group)
+            rank_in = np.zeros(n - c, dtype=np.int64)  # index of position c+u among its owner's positions >= c
+            for g_ in range(G):
+                sel = q_own == g_
+                rank_in[sel] = np.arange(int(sel.sum()))
+            idx = torch.as_tensor((q_own * cmax + rank_in).astype(np.int32), device=dev)
+            R12 = colmaj(k, t)
+            _check(L.bqrrp_step_gather_columns(k, _ptr(gathered), k, _ptr(idx), t, _ptr(R12), k, st), "gather R12")
+        else:
+            R12 = colmaj(k, t)
+            if bc.n_loc - j_c > 0:
+                slots = torch.as_tensor(bc.pos[j_c:] - c, device=dev)
+                R12[:, slots] = A_loc[s:s + k, j_c:]
+            allreduce_sum(R12)
         _check(L.bqrrp_step_sample_update(b, t, _ptr(R11), b, _ptr(R12), k, _ptr(MskT[s:]), n, st), "sample_update")
         i += 1
     if pending is not None:
