@@ -155,6 +155,33 @@ int bqrrp_step_panel(int64_t h, int64_t k, double* P, int64_t ldp, const double*
 /* a5 on one rank's trailing columns: C (h x t, ldc) <- C - V T^T (V^T C). */
 int bqrrp_step_wy_update(int64_t h, int64_t k, int64_t t, const double* V, const double* T, double* C, int64_t ldc,
                          void* stream);
+/* a4 row-sharded (SURVEY §8(e) phase 2 item 3): each rank holds a block of the panel's rows
+ * (column-major, rows x k); the k x k pieces are computed redundantly from all-reduced Gram matrices.
+ * Preconditioning + first Gram (Alg. 3 cholqr:precond): Q = P R_sk11^{-1} (R_sk11 = R_sk(0:k,0:k) read
+ * from MskT_s), G = Q^T Q (lower, k x k, ld k; zero when rows == 0).  P may equal Q (ldp == ldq). */
+int bqrrp_step_cholqr_pre(int64_t rows, int64_t k, const double* P, int64_t ldp, const double* MskT_s, int64_t ldm,
+                          double* Q, int64_t ldq, double* G, void* stream);
+/* Lower Cholesky of the (all-reduced) Gram G in place, upper part zeroed.  Synchronises; BQRRP_ENUMERIC on a
+ * non-positive pivot (the caller then factors the panel with the Householder variant). */
+int bqrrp_step_potrf(int64_t k, double* G, int64_t ldg, void* stream);
+/* Second CholQR pass on a row block: Q <- Q C^{-T}, G = Q^T Q (lower; zero when rows == 0). */
+int bqrrp_step_cholqr_pass(int64_t rows, int64_t k, double* Q, int64_t ldq, const double* C, double* G, void* stream);
+/* Householder reconstruction (Alg. 3 cholqr:orhr_col) on the block holding the panel's top k rows:
+ * Wr = Q_top C^{-T} (k x k, ld k) factored in place as L \ U with S_jj = -sgn (S: k values). */
+int bqrrp_step_recon_top(int64_t k, const double* Qtop, int64_t ldq, const double* C, double* Wr, double* S,
+                         void* stream);
+/* Y2 rows: Q <- Q (U C^T)^{-1} for a block of rows below the top k (U from Wr). */
+int bqrrp_step_recon_rows(int64_t rows, int64_t k, double* Q, int64_t ldq, const double* Wr, const double* C,
+                          void* stream);
+/* k x k results: T = -U S L^{-T} (compact WY), tau = diag(T), R = C2^T C1^T R_sk11 (C2 may be NULL for one
+ * pass; R11 = S R). */
+int bqrrp_step_recon_finish(int64_t k, const double* Wr, const double* S, const double* C1, const double* C2,
+                            const double* MskT_s, int64_t ldm, double* T, double* tau, double* R, void* stream);
+/* top != 0: the first k rows of the block become the explicit unit-lower V rows of L (from Wr). */
+int bqrrp_step_v_rows(int64_t rows, int64_t k, double* Q, int64_t ldq, const double* Wr, int top, void* stream);
+/* GEQP3 write of the panel A (h x k, lda): S R on and above the diagonal, V (explicit, h x k, ldv) below. */
+int bqrrp_step_write_panel(int64_t h, int64_t k, double* V, int64_t ldv, const double* R, const double* S, double* A,
+                           int64_t lda, void* stream);
 /* a5 split for the lookahead (DESIGN.md §7.5 / §8.1): bqrrp_step_wy_top computes W2 = T^T (V^T C) into the
  * caller's W2 (k x t, ldw >= k; it must stay alive until the bulk call has run) and applies C -= V W2 to rows
  * 0:k (R12) only; bqrrp_step_wy_bulk applies rows k:h, typically on a second stream ordered after the top call.

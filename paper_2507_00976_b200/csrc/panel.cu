@@ -52,6 +52,89 @@ __global__ void write_panel_kernel(int64_t h, int64_t k, double* Q, int64_t ldq,
     }
 }
 
+// ---- phases of the CholQR panel, shared by the one-GPU panel below and the row-sharded multi-GPU panel
+// (steps.cu): every phase works on a block of panel ROWS except the k x k ones.
+
+void cholqr_precondition_gram(Ctx& cx, int64_t rows, int64_t k, const double* P, int64_t ldp, const double* Rsk11,
+                              double* Q, int64_t ldq, double* G)
+{
+    if (rows > 0) {
+        if (P != Q) copy_matrix(cx, rows, k, P, ldp, Q, ldq);
+        trsm_right_upper(cx, rows, k, Rsk11, k, false, false, Q, ldq);  // M_pre = P R_sk11^{-1}
+        gemm(cx, true, false, k, k, rows, 1.0, Q, ldq, Q, ldq, 0.0, G, k, /*tri=*/true);
+    } else {
+        BQ_CUDA(cudaMemsetAsync(G, 0, sizeof(double) * k * k, cx.stream));
+    }
+}
+
+void cholqr_pass_gram(Ctx& cx, int64_t rows, int64_t k, double* Q, int64_t ldq, const double* C, double* G)
+{
+    if (rows > 0) {
+        trsm_right_upper(cx, rows, k, C, k, /*t_lower=*/true, false, Q, ldq, true);  // Q <- Q C^{-T}
+        gemm(cx, true, false, k, k, rows, 1.0, Q, ldq, Q, ldq, 0.0, G, k, /*tri=*/true);
+    } else {
+        BQ_CUDA(cudaMemsetAsync(G, 0, sizeof(double) * k * k, cx.stream));
+    }
+}
+
+void recon_top_lu(Ctx& cx, int64_t k, const double* Qtop, int64_t ldq, const double* C, double* Wr, double* S)
+{
+    copy_matrix(cx, k, k, Qtop, ldq, Wr, k);
+    trsm_right_upper(cx, k, k, C, k, /*t_lower=*/true, false, Wr, k, true);  // top rows of Q_last = Q C^{-T}
+    getrf_nopiv_sign(cx, k, Wr, k, S);                                       // Q_last,1 - S = L U
+}
+
+void recon_rows(Ctx& cx, int64_t rows, int64_t k, double* Q, int64_t ldq, const double* Wr, const double* C)
+{
+    if (rows <= 0) return;
+    const size_t mark = cx.ws_used;
+    double* U = cx.alloc((size_t)k * k);
+    double* Mb = cx.alloc((size_t)k * k);
+    copy_matrix(cx, k, k, Wr, k, U, k);
+    zero_triangle(cx, 'U', k, k, U, k);                                    // U
+    gemm(cx, false, true, k, k, k, 1.0, U, k, C, k, 0.0, Mb, k);            // U C^T (upper)
+    trsm_right_upper(cx, rows, k, Mb, k, false, false, Q, ldq, true);      // Y2 = Q_prev,2 (U C^T)^{-1}
+    cx.ws_used = mark;
+}
+
+void recon_finish(Ctx& cx, int64_t k, const double* Wr, const double* S, const double* const* Cf, int passes,
+                  const double* Rsk11, double* T, double* tau, double* R)
+{
+    build_t_rhs_kernel<<<(unsigned)imin(cdiv(k * k, 256), 4 * cx.num_sms), 256, 0, cx.stream>>>(k, Wr, k, S, T);
+    BQ_LAUNCH_CHECK();
+    trsm_right_upper(cx, k, k, Wr, k, /*t_lower=*/true, /*unit=*/true, T, k, true);  // T Y1^T = -U S
+    zero_triangle(cx, 'U', k, k, T, k);
+    diag_to_tau_kernel<<<(unsigned)cdiv(k, 128), 128, 0, cx.stream>>>(k, T, tau);
+    BQ_LAUNCH_CHECK();
+    // R = C_last^T ... C_1^T R_sk11 (the caller applies S: R11 = S R)
+    const size_t mark = cx.ws_used;
+    double* Wa = cx.alloc((size_t)k * k);
+    double* Wb = cx.alloc((size_t)k * k);
+    copy_matrix(cx, k, k, Rsk11, k, Wa, k);
+    for (int p = 0; p < passes; ++p) {
+        gemm(cx, true, false, k, k, k, 1.0, Cf[p], k, Wa, k, 0.0, Wb, k);
+        double* t = Wa; Wa = Wb; Wb = t;
+    }
+    copy_matrix(cx, k, k, Wa, k, R, k);
+    cx.ws_used = mark;
+}
+
+void write_panel(Ctx& cx, int64_t h, int64_t k, double* Q, int64_t ldq, const double* R, const double* S, double* Ap,
+                 int64_t lda)
+{
+    unsigned eb = (unsigned)imin(cdiv(h * k, 256), 8 * cx.num_sms);
+    write_panel_kernel<<<eb, 256, 0, cx.stream>>>(h, k, Q, ldq, R, S, Ap, lda);
+    BQ_LAUNCH_CHECK();
+}
+
+void force_breakdown_hook(Ctx& cx)
+{
+    // test hook: BQRRP_DEBUG_FORCE_BREAKDOWN=1 reports a POTRF breakdown on every panel, so the fallback /
+    // error path is exercised deterministically (a real breakdown depends on rounding)
+    const char* f = std::getenv("BQRRP_DEBUG_FORCE_BREAKDOWN");
+    if (f && f[0] == '1') BQ_CUDA(cudaMemsetAsync(cx.flags + F_POTRF_INFO, 1, 1, cx.stream));
+}
+
 int panel_factor(Ctx& cx, int64_t m, double* A, int64_t lda, int64_t s, int64_t k, const double* Rsk11, double* tau,
                  int passes, double* V, double* T, bool hqr_fallback)
 {
@@ -66,26 +149,18 @@ int panel_factor(Ctx& cx, int64_t m, double* A, int64_t lda, int64_t s, int64_t 
     for (int p = 0; p < passes; ++p) Cf[p] = cx.alloc((size_t)k * k);
     double* S = cx.alloc((size_t)k);
     double* Wr = cx.alloc((size_t)k * k);
-    double* Wr2 = cx.alloc((size_t)k * k);
-    double* Mb = cx.alloc((size_t)k * k);
+    double* R = cx.alloc((size_t)k * k);
     double* Ap = A + s + s * lda;
-    unsigned eb = (unsigned)imin(cdiv(h * k, 256), 8 * cx.num_sms);
 
-    // M_pre = P(:, 0:k) R_sk11^{-1}
-    copy_matrix(cx, h, k, Ap, lda, Q, h);
-    trsm_right_upper(cx, h, k, Rsk11, k, false, false, Q, h);
-    // Cholesky QR passes; the last pass's TRSM is applied only to the top k rows here and folded into the
-    // reconstruction's TRSM below (Y2 = Q_prev,2 C^{-T} U^{-1} = Q_prev,2 (U C^T)^{-1})
-    for (int p = 0; p < passes; ++p) {
-        gemm(cx, true, false, k, k, h, 1.0, Q, h, Q, h, 0.0, Cf[p], k, /*tri=*/true);
+    // Cholesky QR passes; the last pass's TRSM is applied only to the top k rows (recon_top_lu) and folded into
+    // the reconstruction's TRSM (Y2 = Q_prev,2 C^{-T} U^{-1} = Q_prev,2 (U C^T)^{-1}, recon_rows)
+    cholqr_precondition_gram(cx, h, k, Ap, lda, Rsk11, Q, h, Cf[0]);
+    potrf_lower(cx, k, Cf[0], k);
+    for (int p = 1; p < passes; ++p) {
+        cholqr_pass_gram(cx, h, k, Q, h, Cf[p - 1], Cf[p]);
         potrf_lower(cx, k, Cf[p], k);
-        if (p + 1 < passes) trsm_right_upper(cx, h, k, Cf[p], k, /*t_lower=*/true, false, Q, h, true);
     }
-    {   // test hook: BQRRP_DEBUG_FORCE_BREAKDOWN=1 reports a POTRF breakdown on every panel, so the fallback /
-        // error path is exercised deterministically (a real breakdown depends on rounding)
-        const char* f = std::getenv("BQRRP_DEBUG_FORCE_BREAKDOWN");
-        if (f && f[0] == '1') BQ_CUDA(cudaMemsetAsync(cx.flags + F_POTRF_INFO, 1, 1, cx.stream));
-    }
+    force_breakdown_hook(cx);
     if (hqr_fallback) {  // CholQR breakdown (POTRF non-positive pivot): this panel by Householder QR instead
         int info = 0;
         BQ_CUDA(cudaMemcpyAsync(&info, cx.flags + F_POTRF_INFO, sizeof(int), cudaMemcpyDeviceToHost, cx.stream));
@@ -98,31 +173,11 @@ int panel_factor(Ctx& cx, int64_t m, double* A, int64_t lda, int64_t s, int64_t 
         }
     }
     const double* Cl = Cf[passes - 1];
-    // Householder reconstruction on the top k x k of Q_last = Q C^{-T}
-    copy_matrix(cx, k, k, Q, h, Wr, k);
-    trsm_right_upper(cx, k, k, Cl, k, /*t_lower=*/true, false, Wr, k, true);
-    getrf_nopiv_sign(cx, k, Wr, k, S);
-    if (h > k) {
-        copy_matrix(cx, k, k, Wr, k, Wr2, k);
-        zero_triangle(cx, 'U', k, k, Wr2, k);                                       // U
-        gemm(cx, false, true, k, k, k, 1.0, Wr2, k, Cl, k, 0.0, Mb, k);             // U C^T (upper)
-        trsm_right_upper(cx, h - k, k, Mb, k, false, false, Q + k, h, true);         // Y2
-    }
+    recon_top_lu(cx, k, Q, h, Cl, Wr, S);
+    if (h > k) recon_rows(cx, h - k, k, Q + k, h, Wr, Cl);
     copy_matrix(cx, k, k, Wr, k, Q, h);  // L \ U on top
-    build_t_rhs_kernel<<<(unsigned)imin(cdiv(k * k, 256), 4 * cx.num_sms), 256, 0, cx.stream>>>(k, Q, h, S, T);
-    BQ_LAUNCH_CHECK();
-    trsm_right_upper(cx, k, k, Q, h, /*t_lower=*/true, /*unit=*/true, T, k, true);  // T Y1^T = -U S
-    zero_triangle(cx, 'U', k, k, T, k);
-    diag_to_tau_kernel<<<(unsigned)cdiv(k, 128), 128, 0, cx.stream>>>(k, T, tau + s);
-    BQ_LAUNCH_CHECK();
-    // R11 = S * C_last^T ... C_1^T * R_sk11
-    copy_matrix(cx, k, k, Rsk11, k, Wr, k);
-    for (int p = 0; p < passes; ++p) {
-        gemm(cx, true, false, k, k, k, 1.0, Cf[p], k, Wr, k, 0.0, Wr2, k);
-        double* t = Wr; Wr = Wr2; Wr2 = t;
-    }
-    write_panel_kernel<<<eb, 256, 0, cx.stream>>>(h, k, Q, h, Wr, S, Ap, lda);
-    BQ_LAUNCH_CHECK();
+    recon_finish(cx, k, Wr, S, Cf, passes, Rsk11, T, tau + s, R);
+    write_panel(cx, h, k, Q, h, R, S, Ap, lda);
     cx.ws_used = mark;
     return 0;
 }

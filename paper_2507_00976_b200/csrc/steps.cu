@@ -228,6 +228,131 @@ int bqrrp_step_panel(int64_t h, int64_t k, double* P, int64_t ldp, const double*
     });
 }
 
+// ---- row-sharded CholQR panel (SURVEY §8(e) phase 2 item 3): the phases of panel_factor on
+// one rank's block of panel rows, the k x k pieces replicated; the caller all-reduces the Gram matrices.
+int bqrrp_step_cholqr_pre(int64_t rows, int64_t k, const double* P, int64_t ldp, const double* MskT_s, int64_t ldm,
+                          double* Q, int64_t ldq, double* G, void* stream)
+{
+    if (rows < 0) return -1;
+    if (k < 1) return -2;
+    if (rows > 0 && (ldp < rows || ldq < rows)) return -4;
+    return step_guard([&]() -> int {
+        StepWs sw(stream, ((size_t)k * k + 8192) * 8, (size_t)16 * k * k * 8 + (4u << 20));
+        Ctx& cx = sw.cx;
+        double* Rsk11 = cx.alloc((size_t)k * k);
+        extract_rsk_kernel<<<(unsigned)imin(cdiv(k * k, 256), 4 * cx.num_sms), 256, 0, cx.stream>>>(k, MskT_s, ldm,
+                                                                                                    Rsk11);
+        BQ_LAUNCH_CHECK();
+        cholqr_precondition_gram(cx, rows, k, P, ldp, Rsk11, Q, ldq, G);
+        return 0;
+    });
+}
+
+int bqrrp_step_potrf(int64_t k, double* G, int64_t ldg, void* stream)
+{
+    if (k < 1) return -1;
+    if (ldg < k) return -3;
+    return step_guard([&]() -> int {
+        StepWs sw(stream, 8192 * 8, (size_t)16 * k * k * 8 + (4u << 20));
+        Ctx& cx = sw.cx;
+        potrf_lower(cx, k, G, ldg);
+        force_breakdown_hook(cx);
+        int info = 0;
+        BQ_CUDA(cudaMemcpyAsync(&info, cx.flags + F_POTRF_INFO, sizeof(int), cudaMemcpyDeviceToHost, cx.stream));
+        BQ_CUDA(cudaStreamSynchronize(cx.stream));
+        return info ? BQRRP_ENUMERIC : 0;
+    });
+}
+
+int bqrrp_step_cholqr_pass(int64_t rows, int64_t k, double* Q, int64_t ldq, const double* C, double* G, void* stream)
+{
+    if (rows < 0) return -1;
+    if (k < 1) return -2;
+    return step_guard([&]() -> int {
+        StepWs sw(stream, ((size_t)k * 64 + 8192) * 8, (size_t)16 * k * k * 8 + (4u << 20));
+        cholqr_pass_gram(sw.cx, rows, k, Q, ldq, C, G);
+        return 0;
+    });
+}
+
+int bqrrp_step_recon_top(int64_t k, const double* Qtop, int64_t ldq, const double* C, double* Wr, double* S,
+                         void* stream)
+{
+    if (k < 1) return -1;
+    return step_guard([&]() -> int {
+        StepWs sw(stream, ((size_t)k * 64 + 8192) * 8, (size_t)16 * k * k * 8 + (4u << 20));
+        recon_top_lu(sw.cx, k, Qtop, ldq, C, Wr, S);
+        return 0;
+    });
+}
+
+int bqrrp_step_recon_rows(int64_t rows, int64_t k, double* Q, int64_t ldq, const double* Wr, const double* C,
+                          void* stream)
+{
+    if (rows < 0) return -1;
+    if (k < 1) return -2;
+    if (rows == 0) return 0;
+    return step_guard([&]() -> int {
+        StepWs sw(stream, ((size_t)2 * k * k + (size_t)k * 64 + 8192) * 8, (size_t)16 * k * k * 8 + (4u << 20));
+        recon_rows(sw.cx, rows, k, Q, ldq, Wr, C);
+        return 0;
+    });
+}
+
+// explicit V rows of a row block: top block (row0 == 0) gets the unit-lower L of Wr in its first k rows
+__global__ void v_rows_kernel(int64_t rows, int64_t k, double* Q, int64_t ldq, const double* Wr, int top)
+{
+    int64_t total = rows * k;
+    for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += (int64_t)gridDim.x * blockDim.x) {
+        int64_t i = idx % rows, j = idx / rows;
+        if (top && i < k) Q[i + j * ldq] = (i > j) ? Wr[i + j * k] : (i == j ? 1.0 : 0.0);
+    }
+}
+
+int bqrrp_step_recon_finish(int64_t k, const double* Wr, const double* S, const double* C1, const double* C2,
+                            const double* MskT_s, int64_t ldm, double* T, double* tau, double* R, void* stream)
+{
+    if (k < 1) return -1;
+    return step_guard([&]() -> int {
+        StepWs sw(stream, ((size_t)4 * k * k + (size_t)k * 64 + 8192) * 8, (size_t)16 * k * k * 8 + (4u << 20));
+        Ctx& cx = sw.cx;
+        double* Rsk11 = cx.alloc((size_t)k * k);
+        extract_rsk_kernel<<<(unsigned)imin(cdiv(k * k, 256), 4 * cx.num_sms), 256, 0, cx.stream>>>(k, MskT_s, ldm,
+                                                                                                    Rsk11);
+        BQ_LAUNCH_CHECK();
+        const double* Cf[2] = {C1, C2};
+        recon_finish(cx, k, Wr, S, Cf, C2 ? 2 : 1, Rsk11, T, tau, R);
+        return 0;
+    });
+}
+
+int bqrrp_step_v_rows(int64_t rows, int64_t k, double* Q, int64_t ldq, const double* Wr, int top, void* stream)
+{
+    if (rows < 0) return -1;
+    if (rows == 0 || !top) return 0;
+    return step_guard([&]() -> int {
+        cudaStream_t st = (cudaStream_t)stream;
+        int dev = 0, nsm = 1;
+        BQ_CUDA(cudaGetDevice(&dev));
+        BQ_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+        v_rows_kernel<<<(unsigned)imin(cdiv(rows * k, 256), 8 * nsm), 256, 0, st>>>(rows, k, Q, ldq, Wr, 1);
+        BQ_LAUNCH_CHECK();
+        return 0;
+    });
+}
+
+int bqrrp_step_write_panel(int64_t h, int64_t k, double* V, int64_t ldv, const double* R, const double* S, double* A,
+                           int64_t lda, void* stream)
+{
+    if (h < 1) return -1;
+    if (k < 1 || k > h) return -2;
+    return step_guard([&]() -> int {
+        StepWs sw(stream, 8192 * 8, 4096);
+        write_panel(sw.cx, h, k, V, ldv, R, S, A, lda);
+        return 0;
+    });
+}
+
 int bqrrp_step_wy_update(int64_t h, int64_t k, int64_t t, const double* V, const double* T, double* C, int64_t ldc,
                          void* stream)
 {

@@ -73,6 +73,14 @@ def _declare():
     L.bqrrp_step_zero_column_check.argtypes = [i64, P, ctypes.POINTER(i32), P]
     L.bqrrp_step_panel.argtypes = [i64, i64, P, i64, P, i64, P, P, P, i32, P]
     L.bqrrp_step_wy_update.argtypes = [i64, i64, i64, P, P, P, i64, P]
+    L.bqrrp_step_cholqr_pre.argtypes = [i64, i64, P, i64, P, i64, P, i64, P, P]
+    L.bqrrp_step_potrf.argtypes = [i64, P, i64, P]
+    L.bqrrp_step_cholqr_pass.argtypes = [i64, i64, P, i64, P, P, P]
+    L.bqrrp_step_recon_top.argtypes = [i64, P, i64, P, P, P, P]
+    L.bqrrp_step_recon_rows.argtypes = [i64, i64, P, i64, P, P, P]
+    L.bqrrp_step_recon_finish.argtypes = [i64, P, P, P, P, P, i64, P, P, P, P]
+    L.bqrrp_step_v_rows.argtypes = [i64, i64, P, i64, P, i32, P]
+    L.bqrrp_step_write_panel.argtypes = [i64, i64, P, i64, P, P, P, i64, P]
     L.bqrrp_step_wy_top.argtypes = [i64, i64, i64, P, P, P, i64, P, i64, P]
     L.bqrrp_step_wy_bulk.argtypes = [i64, i64, i64, P, P, i64, P, i64, P]
     L.bqrrp_step_sample_update.argtypes = [i64, i64, P, i64, P, i64, P, i64, P]
@@ -83,7 +91,8 @@ def _declare():
 
 
 def factor_dist(A_loc, m: int, n: int, b: int, d: int | None = None, seed: int = 0, rank_tol: float | None = None,
-                cholqr_passes: int = 2, group=None, lookahead: bool = True, exchange: str = "auto"):
+                cholqr_passes: int = 2, group=None, lookahead: bool = True, exchange: str = "auto",
+                shard_panel: bool = True):
     """Distributed BQRRP.  A_loc: this rank's block-cyclic columns (m x n_loc, column-major float64 CUDA).
     Returns (A_loc, tau, J, rank) with A_loc overwritten in GEQP3 format (R above, V below, in this rank's
     columns), tau (min(m,n)) and J (n, one-based gather) replicated.
@@ -92,7 +101,10 @@ def factor_dist(A_loc, m: int, n: int, b: int, d: int | None = None, seed: int =
     of C -= V W2, bqrrp_step_wy_bulk) on a low-priority one, overlapping the R12 exchange, the replicated
     sample update and the next pivot selection; the next column exchange waits for it.
     exchange: "a2a" (point-to-point column moves), "allreduce" (exact-sum of the touched set) or "auto"
-    (a2a on NCCL)."""
+    (a2a on NCCL).
+    shard_panel: the CholQR panel's row work (preconditioning TRSM, both Gram SYRKs, the pass-1 TRSM and the
+    Y2 TRSM) is split over the ranks by rows, the k x k factorizations are replicated (bqrrp_step_cholqr_pre /
+    potrf / cholqr_pass / recon_*); a POTRF breakdown falls back to the owner's Householder panel."""
     import torch
 
     caller = torch.cuda.current_stream(A_loc.device)
@@ -102,7 +114,7 @@ def factor_dist(A_loc, m: int, n: int, b: int, d: int | None = None, seed: int =
     if bulk is not None:
         bulk.wait_stream(caller)
     with torch.cuda.stream(crit):
-        out = _factor_dist_impl(A_loc, m, n, b, d, seed, rank_tol, cholqr_passes, group, bulk, exchange)
+        out = _factor_dist_impl(A_loc, m, n, b, d, seed, rank_tol, cholqr_passes, group, bulk, exchange, shard_panel)
     caller.wait_stream(crit)
     if bulk is not None:
         caller.wait_stream(bulk)
@@ -141,7 +153,73 @@ def _exchange_a2a(L, A_loc, lda, m, q, p, bc, me, G, group, st, dev, colmaj):
         _check(L.bqrrp_step_scatter_columns(m, _ptr(A_loc), lda, _ptr(idx), nl, _ptr(buf[:, ns:]), m, st), "scatter")
 
 
-def _factor_dist_impl(A_loc, m, n, b, d, seed, rank_tol, cholqr_passes, group, bulk, exchange):
+def _panel_sharded(L, A_loc, lda, m, s, h, k, b, n, MskT, bc, me, G, owner, group, st, dev, colmaj, passes, V, T, tk,
+                   R11):
+    """a4 with the panel's rows split over Gp = min(G, h // k) ranks (rank 0 holds the top k rows).  Returns
+    False (nothing written) if a replicated POTRF breaks down: the caller then runs the owner's panel, whose
+    Householder fallback handles it.  On success V (h x k explicit), T, tk and, on the owner, the panel columns
+    of A_loc (GEQP3 format) and R11 are set."""
+    import torch
+    import torch.distributed as dist
+
+    f64 = dict(dtype=torch.float64, device=dev)
+    P = colmaj(h, k)
+    j0 = int(bc.loc_of[s]) if owner == me else 0
+    if owner == me:
+        P.copy_(A_loc[s:, j0:j0 + k])
+    dist.broadcast(P, src=owner, group=group)
+    Gp = min(G, h // k)
+    hc = -(-h // Gp)
+    r0 = me * hc
+    rows = max(0, min(h, r0 + hc) - r0) if me < Gp else 0
+    ldq = max(rows, 1)
+    Q = colmaj(ldq, k)
+    C1 = colmaj(k, k)
+    _check(L.bqrrp_step_cholqr_pre(rows, k, _ptr(P[min(r0, h - 1):]), h, _ptr(MskT[s:]), n, _ptr(Q), ldq, _ptr(C1), st),
+           "cholqr_pre")
+    dist.all_reduce(C1, group=group)
+    if L.bqrrp_step_potrf(k, _ptr(C1), k, st) != 0:
+        return False
+    C2 = None
+    if passes == 2:
+        C2 = colmaj(k, k)
+        _check(L.bqrrp_step_cholqr_pass(rows, k, _ptr(Q), ldq, _ptr(C1), _ptr(C2), st), "cholqr_pass")
+        dist.all_reduce(C2, group=group)
+        if L.bqrrp_step_potrf(k, _ptr(C2), k, st) != 0:
+            return False
+    Cl = C2 if C2 is not None else C1
+    Wr = colmaj(k, k)
+    Sv = torch.zeros(k, **f64)
+    if me == 0:
+        _check(L.bqrrp_step_recon_top(k, _ptr(Q), ldq, _ptr(Cl), _ptr(Wr), _ptr(Sv), st), "recon_top")
+    dist.broadcast(Wr, src=0, group=group)
+    dist.broadcast(Sv, src=0, group=group)
+    if me == 0:
+        _check(L.bqrrp_step_recon_rows(rows - k, k, _ptr(Q[k:]), ldq, _ptr(Wr), _ptr(Cl), st), "recon_rows")
+        _check(L.bqrrp_step_v_rows(rows, k, _ptr(Q), ldq, _ptr(Wr), 1, st), "v_rows")
+    elif rows > 0:
+        _check(L.bqrrp_step_recon_rows(rows, k, _ptr(Q), ldq, _ptr(Wr), _ptr(Cl), st), "recon_rows")
+    Rm = colmaj(k, k)
+    _check(L.bqrrp_step_recon_finish(k, _ptr(Wr), _ptr(Sv), _ptr(C1), _ptr(C2) if C2 is not None else None,
+                                     _ptr(MskT[s:]), n, _ptr(T), _ptr(tk), _ptr(Rm), st), "recon_finish")
+    # V rows: every rank's block (padded to hc rows) all-gathered, then stacked in row order
+    Vb = colmaj(hc, k)
+    if rows > 0:
+        Vb[:rows].copy_(Q[:rows])
+    gathered = torch.empty(G * hc * k, **f64)
+    dist.all_gather_into_tensor(gathered, Vb.t().reshape(-1), group=group)
+    for g_ in range(Gp):
+        rg = max(0, min(h, (g_ + 1) * hc) - g_ * hc)
+        blk = gathered[g_ * hc * k:(g_ + 1) * hc * k].view(k, hc).t()
+        V[g_ * hc:g_ * hc + rg].copy_(blk[:rg])
+    if owner == me:
+        _check(L.bqrrp_step_write_panel(h, k, _ptr(V), h, _ptr(Rm), _ptr(Sv), _ptr(A_loc[s:, j0:]), lda, st), "write")
+        if k == b:
+            R11.copy_(torch.triu(A_loc[s:s + b, j0:j0 + b]))
+    return True
+
+
+def _factor_dist_impl(A_loc, m, n, b, d, seed, rank_tol, cholqr_passes, group, bulk, exchange, shard_panel):
     import torch
     import torch.distributed as dist
 
@@ -232,24 +310,31 @@ def _factor_dist_impl(A_loc, m, n, b, d, seed, rank_tol, cholqr_passes, group, b
         if k == 0 or flag.item() != 0.0:
             ell = s
             break
-        # ---- a4 on the owner, X2 broadcast of V, T, tau (+ R11)
+        # ---- a4: row-sharded CholQR panel (every rank factors a block of the panel's rows; V all-gathered) or
+        #      on the owner with an X2 broadcast of V, T, tau (+ R11)
         V = colmaj(h, k)
         T = colmaj(k, k)
         tk = torch.zeros(k, **f64)
         R11 = colmaj(b, b)
         status = torch.zeros(1, **f64)
-        if owner == me:
+        sharded = (shard_panel and G > 1 and cholqr_passes in (1, 2) and h // k >= 2
+                   and _panel_sharded(L, A_loc, lda, m, s, h, k, b, n, MskT, bc, me, G, owner, group, st, dev, colmaj,
+                                      cholqr_passes, V, T, tk, R11))
+        if sharded:
+            pass
+        elif owner == me:
             j0 = int(bc.loc_of[s])
             st_panel = L.bqrrp_step_panel(h, k, _ptr(A_loc[s:, j0:]), lda, _ptr(MskT[s:]), n, _ptr(tk), _ptr(V),
                                           _ptr(T), int(cholqr_passes), st)
             status.fill_(float(st_panel))
             if k == b:
                 R11.copy_(torch.triu(A_loc[s:s + b, j0:j0 + b]))
-        allreduce_sum(status)
-        if status.item() != 0.0:
-            raise BqrrpError(int(status.item()), "bqrrp_step_panel (distributed)")
-        for t_ in (V, T, tk):
-            dist.broadcast(t_, src=owner, group=group)
+        if not sharded:
+            allreduce_sum(status)
+            if status.item() != 0.0:
+                raise BqrrpError(int(status.item()), "bqrrp_step_panel (distributed)")
+            for t_ in (V, T, tk):
+                dist.broadcast(t_, src=owner, group=group)
         tau[s:s + k] = tk
         # ---- a5 on every rank's own trailing columns (positions >= s + k)
         j_tr = bc.first_local_at_or_after(s + k)

@@ -37,7 +37,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, m, n, b, d, seed, gen, out, exchange="allreduce", lookahead=True):
+def _worker(rank, world, port, m, n, b, d, seed, gen, out, exchange="allreduce", lookahead=True, shard=True):
     import torch.distributed as dist
 
     import inputs
@@ -52,7 +52,8 @@ def _worker(rank, world, port, m, n, b, d, seed, gen, out, exchange="allreduce",
         A = inputs.low_rank(m, n, gen, seed=seed) if gen else inputs.gaussian(m, n, seed=seed)
         Ad = torch.tensor(np.ascontiguousarray(A.T), device="cuda").t()
         A_loc, bc = local_columns(Ad, b, world, rank)
-        A_loc, tau, J, ell = factor_dist(A_loc, m, n, b, d, seed=seed + 1, exchange=exchange, lookahead=lookahead)
+        A_loc, tau, J, ell = factor_dist(A_loc, m, n, b, d, seed=seed + 1, exchange=exchange, lookahead=lookahead,
+                                         shard_panel=shard)
         full = torch.zeros((n, m), dtype=torch.float64, device="cuda").t()
         full[:, torch.as_tensor(bc.pos, device="cuda")] = A_loc
         dist.all_reduce(full)
@@ -81,15 +82,17 @@ def _worker(rank, world, port, m, n, b, d, seed, gen, out, exchange="allreduce",
 @pytest.mark.parametrize("m,n,b,d,gen", [(1024, 1024, 128, 160, 0), (700, 450, 64, 80, 0), (512, 768, 64, 64, 0),
                                          (512, 512, 64, 80, 150)])
 @pytest.mark.parametrize("world", [2, 3])
-@pytest.mark.parametrize("exchange,lookahead", [("allreduce", True), ("a2a", True), ("a2a", False)])
-def test_dist_matches_single_gpu(gpu, m, n, b, d, gen, world, exchange, lookahead):
+@pytest.mark.parametrize("exchange,lookahead,shard", [("allreduce", True, False), ("a2a", True, True),
+                                                     ("a2a", False, True), ("allreduce", False, False)])
+def test_dist_matches_single_gpu(gpu, m, n, b, d, gen, world, exchange, lookahead, shard):
     """The distributed factorization equals the single-GPU one, for both column-exchange forms (X3 as an
-    exact-sum all-reduce, or point-to-point all_to_all moves as used on NCCL) and with / without the
-    lookahead."""
+    exact-sum all-reduce, or point-to-point all_to_all moves as used on NCCL), with / without the lookahead,
+    and with the panel on its owner or row-sharded over the ranks."""
     port = _free_port()
     mgr = mp.Manager()
     out = mgr.dict()
-    mp.spawn(_worker, args=(world, port, m, n, b, d, 5, gen, out, exchange, lookahead), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, port, m, n, b, d, 5, gen, out, exchange, lookahead, shard), nprocs=world,
+             join=True)
     r = out["res"]
     assert r["ell"] == r["ellr"]
     assert r["same_j"] if not gen else r["prefix_j"]
