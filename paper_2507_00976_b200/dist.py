@@ -62,6 +62,18 @@ def _ptr(t):
     return ctypes.c_void_p(t.data_ptr())
 
 
+def _dense(t):
+    """The contiguous tensor behind a column-major view (colmaj(r, c) is a transposed row-major (c, r) block):
+    NCCL collectives reject non-contiguous tensors ("Tensors must be contiguous"), and a collective acts on
+    the same bytes either way."""
+    if t.is_contiguous():
+        return t
+    tt = t.t()
+    if tt.is_contiguous():
+        return tt
+    raise ValueError("collective buffer is neither row- nor column-major contiguous")
+
+
 def _declare():
     L = lib()
     if getattr(L, "_dist_declared", False):
@@ -167,7 +179,7 @@ def _panel_sharded(L, A_loc, lda, m, s, h, k, b, n, MskT, bc, me, G, owner, grou
     j0 = int(bc.loc_of[s]) if owner == me else 0
     if owner == me:
         P.copy_(A_loc[s:, j0:j0 + k])
-    dist.broadcast(P, src=owner, group=group)
+    dist.broadcast(_dense(P), src=owner, group=group)
     Gp = min(G, h // k)
     hc = -(-h // Gp)
     r0 = me * hc
@@ -177,14 +189,14 @@ def _panel_sharded(L, A_loc, lda, m, s, h, k, b, n, MskT, bc, me, G, owner, grou
     C1 = colmaj(k, k)
     _check(L.bqrrp_step_cholqr_pre(rows, k, _ptr(P[min(r0, h - 1):]), h, _ptr(MskT[s:]), n, _ptr(Q), ldq, _ptr(C1), st),
            "cholqr_pre")
-    dist.all_reduce(C1, group=group)
+    dist.all_reduce(_dense(C1), group=group)
     if L.bqrrp_step_potrf(k, _ptr(C1), k, st) != 0:
         return False
     C2 = None
     if passes == 2:
         C2 = colmaj(k, k)
         _check(L.bqrrp_step_cholqr_pass(rows, k, _ptr(Q), ldq, _ptr(C1), _ptr(C2), st), "cholqr_pass")
-        dist.all_reduce(C2, group=group)
+        dist.all_reduce(_dense(C2), group=group)
         if L.bqrrp_step_potrf(k, _ptr(C2), k, st) != 0:
             return False
     Cl = C2 if C2 is not None else C1
@@ -192,8 +204,8 @@ def _panel_sharded(L, A_loc, lda, m, s, h, k, b, n, MskT, bc, me, G, owner, grou
     Sv = torch.zeros(k, **f64)
     if me == 0:
         _check(L.bqrrp_step_recon_top(k, _ptr(Q), ldq, _ptr(Cl), _ptr(Wr), _ptr(Sv), st), "recon_top")
-    dist.broadcast(Wr, src=0, group=group)
-    dist.broadcast(Sv, src=0, group=group)
+    dist.broadcast(_dense(Wr), src=0, group=group)
+    dist.broadcast(_dense(Sv), src=0, group=group)
     if me == 0:
         _check(L.bqrrp_step_recon_rows(rows - k, k, _ptr(Q[k:]), ldq, _ptr(Wr), _ptr(Cl), st), "recon_rows")
         _check(L.bqrrp_step_v_rows(rows, k, _ptr(Q), ldq, _ptr(Wr), 1, st), "v_rows")
@@ -238,7 +250,7 @@ def _factor_dist_impl(A_loc, m, n, b, d, seed, rank_tol, cholqr_passes, group, b
     f64 = dict(dtype=torch.float64, device=dev)
 
     def allreduce_sum(t):
-        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+        dist.all_reduce(_dense(t), op=dist.ReduceOp.SUM, group=group)
 
     # X3 as point-to-point moves (all_to_all_single: each moved column crosses the fabric once) on NCCL; the
     # exact-sum all-reduce of the whole touched set (2x the volume, every column to every rank) otherwise
@@ -334,7 +346,7 @@ def _factor_dist_impl(A_loc, m, n, b, d, seed, rank_tol, cholqr_passes, group, b
             if status.item() != 0.0:
                 raise BqrrpError(int(status.item()), "bqrrp_step_panel (distributed)")
             for t_ in (V, T, tk):
-                dist.broadcast(t_, src=owner, group=group)
+                dist.broadcast(_dense(t_), src=owner, group=group)
         tau[s:s + k] = tk
         # ---- a5 on every rank's own trailing columns (positions >= s + k)
         j_tr = bc.first_local_at_or_after(s + k)
@@ -360,7 +372,7 @@ def _factor_dist_impl(A_loc, m, n, b, d, seed, rank_tol, cholqr_passes, group, b
             ell = s + k
             break
         # ---- a6: R11 and R12 (k x t, position order) assembled on every rank, replicated sketch update
-        dist.broadcast(R11, src=owner, group=group)
+        dist.broadcast(_dense(R11), src=owner, group=group)
         t = n - c
         j_c = bc.first_local_at_or_after(c)
         if use_a2a:

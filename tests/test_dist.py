@@ -37,6 +37,21 @@ def _free_port():
     return p
 
 
+def _require_contiguous_collectives(dist):
+    """NCCL rejects non-contiguous tensors ("Tensors must be contiguous"); gloo does not.  The tests run on gloo,
+    so make every collective the driver issues check it, as NCCL would."""
+    def wrap(fn):
+        def checked(*args, **kw):
+            for a in list(args) + list(kw.values()):
+                if hasattr(a, "is_contiguous") and hasattr(a, "is_cuda"):
+                    assert a.is_contiguous(), f"{fn.__name__}: non-contiguous tensor {tuple(a.shape)} {a.stride()}"
+            return fn(*args, **kw)
+        return checked
+
+    for name in ("broadcast", "all_reduce", "all_gather_into_tensor", "all_to_all_single"):
+        setattr(dist, name, wrap(getattr(dist, name)))
+
+
 def _worker(rank, world, port, m, n, b, d, seed, gen, out, exchange="allreduce", lookahead=True, shard=True):
     import torch.distributed as dist
 
@@ -48,6 +63,7 @@ def _worker(rank, world, port, m, n, b, d, seed, gen, out, exchange="allreduce",
     os.environ["MASTER_PORT"] = str(port)
     torch.cuda.set_device(0)
     dist.init_process_group("gloo", rank=rank, world_size=world)
+    _require_contiguous_collectives(dist)
     try:
         A = inputs.low_rank(m, n, gen, seed=seed) if gen else inputs.gaussian(m, n, seed=seed)
         Ad = torch.tensor(np.ascontiguousarray(A.T), device="cuda").t()
@@ -56,7 +72,7 @@ def _worker(rank, world, port, m, n, b, d, seed, gen, out, exchange="allreduce",
                                          shard_panel=shard)
         full = torch.zeros((n, m), dtype=torch.float64, device="cuda").t()
         full[:, torch.as_tensor(bc.pos, device="cuda")] = A_loc
-        dist.all_reduce(full)
+        dist.all_reduce(full.t())  # the contiguous storage behind the column-major view
         if rank == 0:
             Ar, taur, Jr, ellr = bq.factor(Ad.clone().t().contiguous().t(), b, d, seed=seed + 1)
             same_j = bool(torch.equal(J, Jr))
