@@ -155,6 +155,18 @@ int bqrrp_step_panel(int64_t h, int64_t k, double* P, int64_t ldp, const double*
 /* a5 on one rank's trailing columns: C (h x t, ldc) <- C - V T^T (V^T C). */
 int bqrrp_step_wy_update(int64_t h, int64_t k, int64_t t, const double* V, const double* T, double* C, int64_t ldc,
                          void* stream);
+/* Row-distributed sketch: as bqrrp_step_pivots, but the rows of R_sk(:, d:w) (the d x d
+ * QR's GEMM part) are computed only for the row blocks listed (host arrays; offsets counted from
+ * window row min(d, w), i.e. position s + d): this rank's positions.  The other rows of MskT are left stale and
+ * must be refreshed (all-gather) before the next pivot selection reads them. */
+int bqrrp_step_pivots_rows(int64_t n, int64_t d, int64_t s, int64_t kmax, double* MskT, int64_t ldm, int64_t* J,
+                           double rank_tol, double* ref, int first, int* tq, int* tsrc, int* nt, int64_t* k_out,
+                           const int64_t* row_off, const int64_t* row_len, int64_t n_rows, void* stream);
+/* a6 on this rank's positions only: X = R_sk11 R11^{-1}; for block j: MskT_s(b + pos_off[j] .. + len[j], 0:b)
+ * -= R12(:, col_off[j] ..)^T X^T with R12 this rank's k x t_loc top rows (host arrays). */
+int bqrrp_step_sample_update_rows(int64_t b, const double* R11, int64_t ldr, const double* R12, int64_t ld12,
+                                  double* MskT_s, int64_t ldm, const int64_t* pos_off, const int64_t* col_off,
+                                  const int64_t* len, int64_t nblk, void* stream);
 /* a4 row-sharded (SURVEY §8(e) phase 2 item 3): each rank holds a block of the panel's rows
  * (column-major, rows x k); the k x k pieces are computed redundantly from all-reduced Gram matrices.
  * Preconditioning + first Gram (Alg. 3 cholqr:precond): Q = P R_sk11^{-1} (R_sk11 = R_sk(0:k,0:k) read

@@ -25,7 +25,15 @@ void getrf_pivots(Ctx& cx, double* L, int64_t ld, int64_t w, int64_t d, int* ipi
 // diagonal, reflectors below; V (rows x cols, ld rows) explicit, T (cols x cols) the compact-WY factor.
 void householder_panel(Ctx& cx, double* A, int64_t lda, int64_t rows, int64_t cols, double* tau, double* V, double* T);
 // a2: R_sk of the sketch window (transposed storage), in place.
-void sketch_qr(Ctx& cx, double* MskT, int64_t ldm, int64_t w, int64_t d);
+// rows: optional restriction of the R_sk(:, d:w) rows computed (multi-GPU: only the rows of this rank's
+// positions; the others are left stale and refreshed by the caller's all-gather): n_rows blocks, block j =
+// rows [row_off[j], row_off[j] + row_len[j]) counted from window row p = min(d, w) (host arrays).
+struct RowBlocks {
+    const int64_t* off = nullptr;
+    const int64_t* len = nullptr;
+    int64_t n = -1;  // < 0: all rows
+};
+void sketch_qr(Ctx& cx, double* MskT, int64_t ldm, int64_t w, int64_t d, const RowBlocks& rows = RowBlocks());
 
 // a3: touched set and gathers
 void touched_from_perm(Ctx& cx, int64_t w, int64_t nlu, const int* perm, Touched& T);

@@ -680,7 +680,7 @@ __global__ void store_rsk_kernel(int64_t p, int64_t d, const double* Wq, double*
 }
 
 // R_sk of the d x w sketch window MskT(0:w, 0:d)^T (MskT points at row s, ld ldm); in place.
-void sketch_qr(Ctx& cx, double* MskT, int64_t ldm, int64_t w, int64_t d)
+void sketch_qr(Ctx& cx, double* MskT, int64_t ldm, int64_t w, int64_t d, const RowBlocks& rows)
 {
     int64_t p = imin(d, w);
     if (p <= 0) return;
@@ -711,8 +711,17 @@ void sketch_qr(Ctx& cx, double* MskT, int64_t ldm, int64_t w, int64_t d)
         BQ_CUDA(cudaMemsetAsync(Q, 0, sizeof(double) * d * d, cx.stream));
         zero_triangle(cx, 'L', d, d, Q, d, /*unit_diag=*/true);
         gemm(cx, false, false, d, d, p, -1.0, V, d, Wt, p, 1.0, Q, d);  // Q = I - V Wt
-        gemm(cx, false, false, rest, d, d, 1.0, Xt, ldm, Q, d, 0.0, Y, rest);
-        copy_matrix(cx, rest, d, Y, rest, Xt, ldm);
+        if (rows.n < 0) {
+            gemm(cx, false, false, rest, d, d, 1.0, Xt, ldm, Q, d, 0.0, Y, rest);
+            copy_matrix(cx, rest, d, Y, rest, Xt, ldm);
+        } else {
+            for (int64_t j = 0; j < rows.n; ++j) {
+                const int64_t o = rows.off[j], l = imin(rows.len[j], rest - o);
+                if (o < 0 || l <= 0) continue;
+                gemm(cx, false, false, l, d, d, 1.0, Xt + o, ldm, Q, d, 0.0, Y, l);
+                copy_matrix(cx, l, d, Y, l, Xt + o, ldm);
+            }
+        }
     }
     store_rsk_kernel<<<(unsigned)imin(cdiv(p * d, 256), 4 * cx.num_sms), 256, 0, cx.stream>>>(p, d, Wq, MskT, ldm);
     BQ_LAUNCH_CHECK();

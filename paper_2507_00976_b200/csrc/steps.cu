@@ -121,9 +121,33 @@ using namespace bqrrp;
 
 extern "C" {
 
+static int step_pivots_impl(int64_t n, int64_t d, int64_t s, int64_t kmax, double* MskT, int64_t ldm, int64_t* J,
+                            double rank_tol, double* ref, int first, int* tq, int* tsrc, int* nt, int64_t* k_out,
+                            const RowBlocks& rows, void* stream);
+
 int bqrrp_step_pivots(int64_t n, int64_t d, int64_t s, int64_t kmax, double* MskT, int64_t ldm, int64_t* J,
                       double rank_tol, double* ref, int first, int* tq, int* tsrc, int* nt, int64_t* k_out,
                       void* stream)
+{
+    return step_pivots_impl(n, d, s, kmax, MskT, ldm, J, rank_tol, ref, first, tq, tsrc, nt, k_out, RowBlocks(),
+                            stream);
+}
+
+int bqrrp_step_pivots_rows(int64_t n, int64_t d, int64_t s, int64_t kmax, double* MskT, int64_t ldm, int64_t* J,
+                           double rank_tol, double* ref, int first, int* tq, int* tsrc, int* nt, int64_t* k_out,
+                           const int64_t* row_off, const int64_t* row_len, int64_t n_rows, void* stream)
+{
+    if (n_rows < 0 || (n_rows > 0 && (!row_off || !row_len))) return -17;
+    RowBlocks rb;
+    rb.off = row_off;
+    rb.len = row_len;
+    rb.n = n_rows;
+    return step_pivots_impl(n, d, s, kmax, MskT, ldm, J, rank_tol, ref, first, tq, tsrc, nt, k_out, rb, stream);
+}
+
+static int step_pivots_impl(int64_t n, int64_t d, int64_t s, int64_t kmax, double* MskT, int64_t ldm, int64_t* J,
+                            double rank_tol, double* ref, int first, int* tq, int* tsrc, int* nt, int64_t* k_out,
+                            const RowBlocks& rows, void* stream)
 {
     if (n < 1) return -1;
     if (d < 1) return -2;
@@ -150,7 +174,7 @@ int bqrrp_step_pivots(int64_t n, int64_t d, int64_t s, int64_t kmax, double* Msk
         touched_from_perm(cx, w, nlu, perm, T);
         permute_rows(cx, d, MskT + s, ldm, T, rowscr);
         if (J) permute_vector(cx, J + s, T, vtmp);
-        sketch_qr(cx, MskT + s, ldm, w, d);
+        sketch_qr(cx, MskT + s, ldm, w, d, rows);
         tri_rank_step_kernel<<<1, 1024, 0, cx.stream>>>(MskT + s, ldm, kmax, first, rank_tol, ref, kdev);
         BQ_LAUNCH_CHECK();
         int kh = 0;
@@ -424,6 +448,28 @@ int bqrrp_step_sample_update(int64_t b, int64_t t, const double* R11, int64_t ld
         trsm_right_upper(cx, b, b, R11, ldr, false, false, X, b);  // X = R_sk11 R11^{-1}
         zero_triangle(cx, 'U', b, b, X, b);
         if (t > 0) gemm(cx, true, true, t, b, b, -1.0, R12, ld12, X, b, 1.0, MskT_s + b, ldm);
+        return 0;
+    });
+}
+
+int bqrrp_step_sample_update_rows(int64_t b, const double* R11, int64_t ldr, const double* R12, int64_t ld12,
+                                  double* MskT_s, int64_t ldm, const int64_t* pos_off, const int64_t* col_off,
+                                  const int64_t* len, int64_t nblk, void* stream)
+{
+    if (b < 1) return -1;
+    if (nblk < 0 || (nblk > 0 && (!pos_off || !col_off || !len))) return -12;
+    return step_guard([&]() -> int {
+        StepWs sw(stream, ((size_t)2 * b * b + 4096) * 8, (size_t)16 * b * b * 8 + (4u << 20));
+        Ctx& cx = sw.cx;
+        double* X = cx.alloc((size_t)b * b);
+        extract_rsk_kernel<<<(unsigned)imin(cdiv(b * b, 256), 4 * cx.num_sms), 256, 0, cx.stream>>>(b, MskT_s, ldm, X);
+        BQ_LAUNCH_CHECK();
+        trsm_right_upper(cx, b, b, R11, ldr, false, false, X, b);  // X = R_sk11 R11^{-1}
+        zero_triangle(cx, 'U', b, b, X, b);
+        for (int64_t j = 0; j < nblk; ++j)  // this rank's positions: MskT(c + pos_off, 0:b) -= R12(:, col_off)^T X^T
+            if (len[j] > 0)
+                gemm(cx, true, true, len[j], b, b, -1.0, R12 + col_off[j] * ld12, ld12, X, b, 1.0,
+                     MskT_s + b + pos_off[j], ldm);
         return 0;
     });
 }

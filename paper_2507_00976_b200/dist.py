@@ -47,6 +47,14 @@ class BlockCyclic:
     def first_local_at_or_after(self, p: int) -> int:
         return int(np.searchsorted(self.pos, p))
 
+    def blocks_of_from(self, r: int, p: int):
+        """First positions of rank r's nb-blocks that end after position p (p is a multiple of nb in use)."""
+        first = (p // self.nb) * self.nb
+        return [q0 for q0 in range(first, self.n, self.nb) if (q0 // self.nb) % self.G == r]
+
+    def own_blocks_from(self, p: int):
+        return self.blocks_of_from(self.rank, p)
+
 
 def local_columns(A, nb: int, G: int, rank: int):
     """This rank's block-cyclic columns of a full column-major tensor (for tests and the bench)."""
@@ -85,6 +93,9 @@ def _declare():
     L.bqrrp_step_zero_column_check.argtypes = [i64, P, ctypes.POINTER(i32), P]
     L.bqrrp_step_panel.argtypes = [i64, i64, P, i64, P, i64, P, P, P, i32, P]
     L.bqrrp_step_wy_update.argtypes = [i64, i64, i64, P, P, P, i64, P]
+    L.bqrrp_step_pivots_rows.argtypes = [i64, i64, i64, i64, P, i64, P, d, P, i32, P, P, P, ctypes.POINTER(i64), P,
+                                         P, i64, P]
+    L.bqrrp_step_sample_update_rows.argtypes = [i64, P, i64, P, i64, P, i64, P, P, P, i64, P]
     L.bqrrp_step_cholqr_pre.argtypes = [i64, i64, P, i64, P, i64, P, i64, P, P]
     L.bqrrp_step_potrf.argtypes = [i64, P, i64, P]
     L.bqrrp_step_cholqr_pass.argtypes = [i64, i64, P, i64, P, P, P]
@@ -104,7 +115,7 @@ def _declare():
 
 def factor_dist(A_loc, m: int, n: int, b: int, d: int | None = None, seed: int = 0, rank_tol: float | None = None,
                 cholqr_passes: int = 2, group=None, lookahead: bool = True, exchange: str = "auto",
-                shard_panel: bool = True):
+                shard_panel: bool = True, shard_sketch: bool = True):
     """Distributed BQRRP.  A_loc: this rank's block-cyclic columns (m x n_loc, column-major float64 CUDA).
     Returns (A_loc, tau, J, rank) with A_loc overwritten in GEQP3 format (R above, V below, in this rank's
     columns), tau (min(m,n)) and J (n, one-based gather) replicated.
@@ -116,7 +127,10 @@ def factor_dist(A_loc, m: int, n: int, b: int, d: int | None = None, seed: int =
     (a2a on NCCL).
     shard_panel: the CholQR panel's row work (preconditioning TRSM, both Gram SYRKs, the pass-1 TRSM and the
     Y2 TRSM) is split over the ranks by rows, the k x k factorizations are replicated (bqrrp_step_cholqr_pre /
-    potrf / cholqr_pass / recon_*); a POTRF breakdown falls back to the owner's Householder panel."""
+    potrf / cholqr_pass / recon_*); a POTRF breakdown falls back to the owner's Householder panel.
+    shard_sketch: the R_sk(:, d:) GEMM of the pivot selection and the sample update run on this rank's
+    positions only, and one all-gather of the updated sketch rows per iteration (instead of the R12 exchange)
+    keeps the replicated pivot selection whole."""
     import torch
 
     caller = torch.cuda.current_stream(A_loc.device)
@@ -126,11 +140,37 @@ def factor_dist(A_loc, m: int, n: int, b: int, d: int | None = None, seed: int =
     if bulk is not None:
         bulk.wait_stream(caller)
     with torch.cuda.stream(crit):
-        out = _factor_dist_impl(A_loc, m, n, b, d, seed, rank_tol, cholqr_passes, group, bulk, exchange, shard_panel)
+        out = _factor_dist_impl(A_loc, m, n, b, d, seed, rank_tol, cholqr_passes, group, bulk, exchange, shard_panel,
+                                shard_sketch)
     caller.wait_stream(crit)
     if bulk is not None:
         caller.wait_stream(bulk)
     return out
+
+
+def _allgather_sketch_rows(MskT, c, n, d, b, bc, me, G, group, colmaj, dev):
+    """Every rank contributes the sketch rows of its own positions >= c (b-row blocks, stacked and padded to
+    the largest block count); after one all-gather each rank copies the other ranks' blocks into MskT."""
+    import torch
+    import torch.distributed as dist
+
+    blocks = [bc.blocks_of_from(r, c) for r in range(G)]
+    nmax = max(len(x) for x in blocks)
+    if nmax == 0:
+        return
+    buf = colmaj(nmax * b, d)
+    for j, q0 in enumerate(blocks[me]):
+        ln = min(b, n - q0)
+        buf[j * b:j * b + ln].copy_(MskT[q0:q0 + ln])
+    gathered = torch.empty(G * nmax * b * d, dtype=torch.float64, device=dev)
+    dist.all_gather_into_tensor(gathered, _dense(buf).reshape(-1), group=group)
+    for r in range(G):
+        if r == me:
+            continue
+        blk = gathered[r * nmax * b * d:(r + 1) * nmax * b * d].view(d, nmax * b).t()
+        for j, q0 in enumerate(blocks[r]):
+            ln = min(b, n - q0)
+            MskT[q0:q0 + ln].copy_(blk[j * b:j * b + ln])
 
 
 def _exchange_a2a(L, A_loc, lda, m, q, p, bc, me, G, group, st, dev, colmaj):
@@ -231,7 +271,8 @@ def _panel_sharded(L, A_loc, lda, m, s, h, k, b, n, MskT, bc, me, G, owner, grou
     return True
 
 
-def _factor_dist_impl(A_loc, m, n, b, d, seed, rank_tol, cholqr_passes, group, bulk, exchange, shard_panel):
+def _factor_dist_impl(A_loc, m, n, b, d, seed, rank_tol, cholqr_passes, group, bulk, exchange, shard_panel,
+                      shard_sketch):
     import torch
     import torch.distributed as dist
 
@@ -255,6 +296,7 @@ def _factor_dist_impl(A_loc, m, n, b, d, seed, rank_tol, cholqr_passes, group, b
     # X3 as point-to-point moves (all_to_all_single: each moved column crosses the fabric once) on NCCL; the
     # exact-sum all-reduce of the whole touched set (2x the volume, every column to every rank) otherwise
     use_a2a = exchange == "a2a" or (exchange == "auto" and dist.get_backend(group) == "nccl")
+    shard_sketch = shard_sketch and G > 1
 
     def colmaj(rows, cols):
         return torch.zeros((cols, rows), **f64).t()
@@ -285,8 +327,27 @@ def _factor_dist_impl(A_loc, m, n, b, d, seed, rank_tol, cholqr_passes, group, b
         kmax = min(b, w, h)
         # ---- a2 (replicated)
         k = ctypes.c_int64(0)
-        _check(L.bqrrp_step_pivots(n, d, s, kmax, _ptr(MskT), n, _ptr(J), float(rank_tol), _ptr(ref), int(i == 0),
-                                   _ptr(tq), _ptr(tsrc), _ptr(nt), ctypes.byref(k), st), "bqrrp_step_pivots")
+        if shard_sketch:
+            # R_sk(:, d:w) only for this rank's positions (the rest of MskT is refreshed by the row all-gather
+            # after the sample update)
+            p0 = s + min(d, n - s)
+            offs, lens = [], []
+            for q0 in bc.own_blocks_from(s):
+                lo, hi = max(q0, p0), min(q0 + b, n)
+                if hi > lo:
+                    offs.append(lo - p0)
+                    lens.append(hi - lo)
+            offs_a = np.ascontiguousarray(offs, dtype=np.int64)
+            lens_a = np.ascontiguousarray(lens, dtype=np.int64)
+            _check(L.bqrrp_step_pivots_rows(n, d, s, kmax, _ptr(MskT), n, _ptr(J), float(rank_tol), _ptr(ref),
+                                            int(i == 0), _ptr(tq), _ptr(tsrc), _ptr(nt), ctypes.byref(k),
+                                            offs_a.ctypes.data_as(ctypes.c_void_p),
+                                            lens_a.ctypes.data_as(ctypes.c_void_p), len(offs), st),
+                   "bqrrp_step_pivots_rows")
+        else:
+            _check(L.bqrrp_step_pivots(n, d, s, kmax, _ptr(MskT), n, _ptr(J), float(rank_tol), _ptr(ref),
+                                       int(i == 0), _ptr(tq), _ptr(tsrc), _ptr(nt), ctypes.byref(k), st),
+                   "bqrrp_step_pivots")
         k = int(k.value)
         ntv = int(nt.item())
         # ---- a3: X3 column exchange through one exactly-summed buffer (after this rank's bulk update landed)
@@ -375,6 +436,22 @@ def _factor_dist_impl(A_loc, m, n, b, d, seed, rank_tol, cholqr_passes, group, b
         dist.broadcast(_dense(R11), src=owner, group=group)
         t = n - c
         j_c = bc.first_local_at_or_after(c)
+        if shard_sketch:
+            # this rank's sketch rows only (its own R12 columns are local), then every rank's rows all-gathered
+            # so the next (replicated) pivot selection sees the whole updated sketch
+            pos_off, col_off, lens = [], [], []
+            for q0 in bc.own_blocks_from(c):
+                pos_off.append(q0 - c)
+                col_off.append(int(bc.loc_of[q0]) - j_c)
+                lens.append(min(b, n - q0))
+            arrs = [np.ascontiguousarray(x, dtype=np.int64) for x in (pos_off, col_off, lens)]
+            _check(L.bqrrp_step_sample_update_rows(b, _ptr(R11), b, _ptr(A_loc[s:s + k, j_c:] if bc.n_loc > j_c
+                                                                          else A_loc), lda, _ptr(MskT[s:]), n,
+                                                   *[a_.ctypes.data_as(ctypes.c_void_p) for a_ in arrs], len(lens),
+                                                   st), "sample_update_rows")
+            _allgather_sketch_rows(MskT, c, n, d, b, bc, me, G, group, colmaj, dev)
+            i += 1
+            continue
         if use_a2a:
             # X1 as an all-gather of every rank's own R12 columns (padded to the largest share), then one
             # gather into position order: each column crosses the fabric once (the exact-sum all-reduce

@@ -69,7 +69,7 @@ def _worker(rank, world, port, m, n, b, d, seed, gen, out, exchange="allreduce",
         Ad = torch.tensor(np.ascontiguousarray(A.T), device="cuda").t()
         A_loc, bc = local_columns(Ad, b, world, rank)
         A_loc, tau, J, ell = factor_dist(A_loc, m, n, b, d, seed=seed + 1, exchange=exchange, lookahead=lookahead,
-                                         shard_panel=shard)
+                                         shard_panel=shard, shard_sketch=shard)
         full = torch.zeros((n, m), dtype=torch.float64, device="cuda").t()
         full[:, torch.as_tensor(bc.pos, device="cuda")] = A_loc
         dist.all_reduce(full.t())  # the contiguous storage behind the column-major view
@@ -103,7 +103,8 @@ def _worker(rank, world, port, m, n, b, d, seed, gen, out, exchange="allreduce",
 def test_dist_matches_single_gpu(gpu, m, n, b, d, gen, world, exchange, lookahead, shard):
     """The distributed factorization equals the single-GPU one, for both column-exchange forms (X3 as an
     exact-sum all-reduce, or point-to-point all_to_all moves as used on NCCL), with / without the lookahead,
-    and with the panel on its owner or row-sharded over the ranks."""
+    and with the panel on its owner or row-sharded over the ranks (shard also restricts the R_sk GEMM and the
+    sample update to each rank's positions, with the sketch rows all-gathered)."""
     port = _free_port()
     mgr = mp.Manager()
     out = mgr.dict()
