@@ -13,6 +13,7 @@
 //   a6  sketch update MskT(c:n, 0:b) -= R12^T (R_sk11 R11^{-1})^T  (step bqrrp:update_sample)
 #include <cstring>
 #include <mutex>
+#include <vector>
 #include <string>
 
 #include "../../include/bqrrp.h"
@@ -163,9 +164,45 @@ static int validate(int64_t m, int64_t n, const void* A, int64_t lda, int64_t b,
 }
 
 // ----------------------------------------------------------------------------------- the driver
+// Host staging for bqrrp_factor_host: A arrives from pinned host memory in column chunks on its own copy
+// stream and each chunk's sketch rows are computed as soon as it lands (the sketch is column-separable:
+// MskT(cols, :) = A(:, cols)^T S^T), and every block column goes back to the host on a second copy stream
+// as soon as it is final (after its iteration's panel: later iterations only touch columns >= c), so both
+// PCIe directions overlap the factorization instead of bracketing it.
+struct HostIO {
+    const double* A_in = nullptr;  // host, ld ld_host
+    double* A_out = nullptr;       // host, ld ld_host
+    int64_t ld_host = 0;
+    cudaStream_t h2d = nullptr, d2h = nullptr;
+    int64_t done = 0;  // columns [0, done) already queued to the host
+    std::vector<cudaEvent_t> evs;
+    cudaEvent_t event()
+    {
+        cudaEvent_t e;
+        BQ_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        evs.push_back(e);
+        return e;
+    }
+    // queue columns [done, upto) device -> host after the work queued so far on `after`
+    void flush(cudaStream_t after, int64_t m, const double* A, int64_t lda, int64_t upto)
+    {
+        if (upto <= done) return;
+        cudaEvent_t e = event();
+        BQ_CUDA(cudaEventRecord(e, after));
+        BQ_CUDA(cudaStreamWaitEvent(d2h, e, 0));
+        BQ_CUDA(cudaMemcpy2DAsync(A_out + done * ld_host, ld_host * sizeof(double), A + done * lda, lda * sizeof(double),
+                                  m * sizeof(double), upto - done, cudaMemcpyDeviceToHost, d2h));
+        done = upto;
+    }
+    ~HostIO()
+    {
+        for (auto e : evs) cudaEventDestroy(e);
+    }
+};
+
 static int64_t factor_impl(Ctx& cx, Ctx* cxb, cudaEvent_t ev_top, cudaEvent_t ev_bulk, int64_t m, int64_t n, double* A,
                            int64_t lda, int64_t b, int64_t d, uint64_t seed, double* tau, int64_t* J, double rank_tol,
-                           int passes, bool hqr_fallback, int* host_flags)
+                           int passes, bool hqr_fallback, int* host_flags, HostIO* hio = nullptr)
 {
     const int64_t mn = imin(m, n);
     double* MskT = cx.alloc((size_t)n * d);
@@ -196,7 +233,22 @@ static int64_t factor_impl(Ctx& cx, Ctx* cxb, cudaEvent_t ev_top, cudaEvent_t ev
     BQ_CUDA(cudaMemsetAsync(tau, 0, sizeof(double) * mn, cx.stream));
     BQ_CUDA(cudaMemsetAsync(cx.flags, 0, sizeof(int) * F_NFLAGS, cx.stream));
     // a1: sketch (S^T lives in the column scratch until the loop starts)
-    sketch_apply(cx, m, n, A, lda, d, seed, MskT, n, colscr);
+    if (hio) {
+        sketch_operator_T(cx, m, d, seed, colscr, m);
+        const int64_t chunk = imax(b, cdiv(n, 16));
+        for (int64_t c0 = 0; c0 < n; c0 += chunk) {
+            const int64_t nc = imin(chunk, n - c0);
+            BQ_CUDA(cudaMemcpy2DAsync(A + c0 * lda, lda * sizeof(double), hio->A_in + c0 * hio->ld_host,
+                                      hio->ld_host * sizeof(double), m * sizeof(double), nc, cudaMemcpyHostToDevice,
+                                      hio->h2d));
+            cudaEvent_t e = hio->event();
+            BQ_CUDA(cudaEventRecord(e, hio->h2d));
+            BQ_CUDA(cudaStreamWaitEvent(cx.stream, e, 0));
+            gemm(cx, true, false, nc, d, m, 1.0, A + c0 * lda, lda, colscr, m, 0.0, MskT + c0, n);  // MskT rows
+        }
+    } else {
+        sketch_apply(cx, m, n, A, lda, d, seed, MskT, n, colscr);
+    }
     nonfinite_kernel<<<(unsigned)imin(cdiv(n * d, 256), 4 * cx.num_sms), 256, 0, cx.stream>>>(n, d, MskT, n, cx.flags);
     BQ_LAUNCH_CHECK();
 
@@ -241,6 +293,7 @@ static int64_t factor_impl(Ctx& cx, Ctx* cxb, cudaEvent_t ev_top, cudaEvent_t ev
         // ---- a5 (the bulk rows overlap the sketch update and the next a2) and a7
         cx.mark(PH_APPLY_QT);
         const bool terminal = (k < kmax || c == n || r == m);
+        if (hio && !terminal) hio->flush(cx.stream, m, A, lda, c);  // block column [s, c) is final
         wy_update(cx, terminal ? nullptr : cxb, m, n, A, lda, s, k, Vp, Tp, W, W2, ev_top, ev_bulk);
         if (!terminal && cxb && h > k && n - s - k > 0) bulk_pending = true;
         if (terminal) { ell = s + k; break; }
@@ -256,6 +309,7 @@ static int64_t factor_impl(Ctx& cx, Ctx* cxb, cudaEvent_t ev_top, cudaEvent_t ev
     if (bulk_pending) BQ_CUDA(cudaStreamWaitEvent(cx.stream, ev_bulk, 0));
     if (ell < mn) BQ_CUDA(cudaMemsetAsync(tau + ell, 0, sizeof(double) * (mn - ell), cx.stream));
     set_zero(cx, m - ell, n - ell, A + ell + ell * lda, lda);
+    if (hio) hio->flush(cx.stream, m, A, lda, n);
     cx.mark(PH_OTHER);
     BQ_CUDA(cudaMemcpyAsync(host_flags, cx.flags, sizeof(int) * F_NFLAGS, cudaMemcpyDeviceToHost, cx.stream));
     BQ_CUDA(cudaStreamSynchronize(cx.stream));
@@ -323,8 +377,19 @@ int bqrrp_workspace_query(int64_t m, int64_t n, int64_t b, int64_t d, size_t* by
     return 0;
 }
 
+static int factor_ex_impl(int64_t m, int64_t n, double* A, int64_t lda, int64_t b, int64_t d, uint64_t seed,
+                          double* tau, int64_t* J, int64_t* rank, void* workspace, size_t ws_bytes, void* stream,
+                          const bqrrp_options* opts, HostIO* hio);
+
 int bqrrp_factor_ex(int64_t m, int64_t n, double* A, int64_t lda, int64_t b, int64_t d, uint64_t seed, double* tau,
                     int64_t* J, int64_t* rank, void* workspace, size_t ws_bytes, void* stream, const bqrrp_options* opts)
+{
+    return factor_ex_impl(m, n, A, lda, b, d, seed, tau, J, rank, workspace, ws_bytes, stream, opts, nullptr);
+}
+
+static int factor_ex_impl(int64_t m, int64_t n, double* A, int64_t lda, int64_t b, int64_t d, uint64_t seed,
+                          double* tau, int64_t* J, int64_t* rank, void* workspace, size_t ws_bytes, void* stream,
+                          const bqrrp_options* opts, HostIO* hio)
 {
     int v = validate(m, n, A, lda, b, d, tau, J, rank);
     if (v != 0) return v;
@@ -397,8 +462,8 @@ int bqrrp_factor_ex(int64_t m, int64_t n, double* A, int64_t lda, int64_t b, int
             cx.stream = user;
         };
         try {
-            ell = factor_impl(cx, (opts && opts->no_lookahead) ? nullptr : &cxb, ev_top, ev_bulk, m, n, A, lda, b, d, seed, tau, J, rank_tol, passes,
-                              !(opts && opts->no_hqr_fallback), pinned_flags());
+            ell = factor_impl(cx, (opts && opts->no_lookahead) ? nullptr : &cxb, ev_top, ev_bulk, m, n, A, lda, b, d,
+                              seed, tau, J, rank_tol, passes, !(opts && opts->no_hqr_fallback), pinned_flags(), hio);
         } catch (...) {
             cleanup();
             if (own) cudaFreeAsync(ws, user);
@@ -441,16 +506,37 @@ int bqrrp_factor_host(int64_t m, int64_t n, double* A_host, int64_t lda, int64_t
         BQ_CUDA(lib_malloc_async(&dtau, sizeof(double) * (size_t)imax(1, mn), st));
         BQ_CUDA(lib_malloc_async(&dJ, sizeof(int64_t) * (size_t)imax(1, n), st));
         BQ_CUDA(lib_malloc_async(&ws, wsb, st));
-        if (m > 0 && n > 0)
-            BQ_CUDA(cudaMemcpy2DAsync(dA, m * sizeof(double), A_host, lda * sizeof(double), m * sizeof(double), n,
-                                      cudaMemcpyHostToDevice, st));
-        int status = bqrrp_factor_ex(m, n, dA, imax(1, m), b, d, seed, dtau, dJ, rank, ws, wsb, stream, opts);
-        if (status == 0 && m > 0 && n > 0) {
-            BQ_CUDA(cudaMemcpy2DAsync(A_host, lda * sizeof(double), dA, m * sizeof(double), m * sizeof(double), n,
-                                      cudaMemcpyDeviceToHost, st));
-            BQ_CUDA(cudaMemcpyAsync(tau_host, dtau, sizeof(double) * mn, cudaMemcpyDeviceToHost, st));
+        int status = 0;
+        if (m > 0 && n > 0) {
+            // the copies run on their own streams, overlapped with the factorization (HostIO above)
+            HostIO hio;
+            hio.A_in = A_host;
+            hio.A_out = A_host;
+            hio.ld_host = lda;
+            BQ_CUDA(cudaStreamCreateWithFlags(&hio.h2d, cudaStreamNonBlocking));
+            BQ_CUDA(cudaStreamCreateWithFlags(&hio.d2h, cudaStreamNonBlocking));
+            cudaEvent_t e0 = hio.event();
+            BQ_CUDA(cudaEventRecord(e0, st));  // after the allocations
+            BQ_CUDA(cudaStreamWaitEvent(hio.h2d, e0, 0));
+            BQ_CUDA(cudaStreamWaitEvent(hio.d2h, e0, 0));
+            status = factor_ex_impl(m, n, dA, imax(1, m), b, d, seed, dtau, dJ, rank, ws, wsb, stream, opts, &hio);
+            cudaEvent_t e1 = hio.event();
+            BQ_CUDA(cudaEventRecord(e1, hio.d2h));
+            BQ_CUDA(cudaStreamWaitEvent(st, e1, 0));
+            BQ_CUDA(cudaEventRecord(e1, hio.h2d));
+            BQ_CUDA(cudaStreamWaitEvent(st, e1, 0));
+            if (status == 0) {
+                BQ_CUDA(cudaMemcpyAsync(tau_host, dtau, sizeof(double) * mn, cudaMemcpyDeviceToHost, st));
+                BQ_CUDA(cudaMemcpyAsync(J_host, dJ, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, st));
+            }
+            BQ_CUDA(cudaStreamSynchronize(st));
+            cudaStreamDestroy(hio.h2d);
+            cudaStreamDestroy(hio.d2h);
+        } else {
+            status = factor_ex_impl(m, n, dA, imax(1, m), b, d, seed, dtau, dJ, rank, ws, wsb, stream, opts, nullptr);
+            if (status == 0 && n > 0)
+                BQ_CUDA(cudaMemcpyAsync(J_host, dJ, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, st));
         }
-        if (status == 0 && n > 0) BQ_CUDA(cudaMemcpyAsync(J_host, dJ, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, st));
         cudaFreeAsync(dA, st);
         cudaFreeAsync(dtau, st);
         cudaFreeAsync(dJ, st);
