@@ -683,16 +683,6 @@ static bool lu_panel_cluster(Ctx& cx, double* L, int64_t ld, int64_t w, int64_t 
     return true;
 }
 
-// CTAs of the cooperative grid leaf (<= the SM count).  While the bulk trailing GEMM runs concurrently
-// (lookahead), every grid-leaf CTA holds ~110 KB of an SM's shared memory; BQRRP_LU_GRID_CTAS caps the
-// count (A/B knob for that interference).
-static int lu_grid_ctas(int num_sms)
-{
-    static int cap = -1;
-    if (cap < 0) {
-        const char* e = std::getenv("BQRRP_LU_GRID_CTAS");
-        cap = e ? std::atoi(e) : 0;
-    }
     return (cap > 0 && cap < num_sms) ? cap : num_sms;
 }
 
@@ -712,7 +702,7 @@ static void lu_panel(Ctx& cx, double* L, int64_t ld, int64_t w, int64_t d, int64
     if (lu_panel_cluster(cx, L, ld, w, d, c0, jb, ipiv, perm)) return;
     int64_t rows = w - c0;
     // few enough CTAs that the barrier stays cheap, enough that the slab fits shared memory
-    const int gmax = lu_grid_ctas(cx.num_sms);
+    const int gmax = cx.num_sms;
     int G = (int)imin(gmax, imax(1, cdiv(rows, 256)));
     int R = (int)cdiv(rows, G);
     if ((size_t)R * jb * sizeof(double) > 200 * 1024) {
@@ -734,7 +724,6 @@ static void lu_panel(Ctx& cx, double* L, int64_t ld, int64_t w, int64_t d, int64
 
 static int lu_leaf_width(int64_t rows, int num_sms)
 {
-    num_sms = lu_grid_ctas(num_sms);
     if (lu_reg_fits(rows, num_sms)) return 32;  // the register leaf holds any row count up to 148 x 512
     // a leaf that one cluster can hold (32, else 16 columns), else the widest the grid kernel can hold
     int CL, R;
