@@ -683,9 +683,6 @@ static bool lu_panel_cluster(Ctx& cx, double* L, int64_t ld, int64_t w, int64_t 
     return true;
 }
 
-    return (cap > 0 && cap < num_sms) ? cap : num_sms;
-}
-
 struct LuExchange {
     double* xbuf;
     double* rowj;
