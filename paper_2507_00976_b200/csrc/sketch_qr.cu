@@ -416,6 +416,40 @@ struct QrLeafArgs {
     int64_t ldt;
 };
 
+// DSMEM push with transaction counting: st.async writes 8 bytes into a peer CTA's shared memory and
+// decrements that CTA's mbarrier tx-count by 8 when the write has landed; the receiver arms its mbarrier
+// with the bytes it expects per phase and waits on the phase parity (no cluster-wide barrier, no fence).
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ unsigned mapa_u32(unsigned addr, int rank)
+{
+    unsigned r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void st_async_f64(unsigned remote_addr, double v, unsigned remote_mbar)
+{
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];"
+                 ::"r"(remote_addr), "l"(__double_as_longlong(v)), "r"(remote_mbar) : "memory");
+}
+__device__ __forceinline__ void mbar_init(unsigned mbar, unsigned count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(mbar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(unsigned mbar, unsigned bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_parity(unsigned mbar, unsigned parity)
+{
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(mbar), "r"(parity) : "memory");
+}
+
 __global__ void __launch_bounds__(QL_THREADS, 1) qr_leaf_reg_kernel(QrLeafArgs a)
 {
     cg::cluster_group cluster = cg::this_cluster();
@@ -427,6 +461,13 @@ __global__ void __launch_bounds__(QL_THREADS, 1) qr_leaf_reg_kernel(QrLeafArgs a
     double* prow = slot + 2 * NS * 32;     // [2][32]
     __shared__ double TcS[32][33];         // TcS[j][l] = V(:, l)^T v_j (CTA 0)
     __shared__ double taus[32];
+    __shared__ __align__(8) unsigned long long mbar[2];  // one per slot parity
+    if (tid == 0) {
+        mbar_init(smem_u32(&mbar[0]), 1);
+        mbar_init(smem_u32(&mbar[1]), 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    cluster.sync();  // every peer's mbarriers are initialised before the first push
     const int64_t r = a.c0 + (int64_t)me * QL_THREADS + tid;  // this thread's row
     const bool has = r < a.m;
     double av[32];
@@ -447,8 +488,8 @@ __global__ void __launch_bounds__(QL_THREADS, 1) qr_leaf_reg_kernel(QrLeafArgs a
 #pragma unroll
         for (int c = 0; c < 32; ++c) q[c] = x * av[c];  // q[j] = x^2
         const double ws = warp_transpose_reduce32(q, lane);
-        double* my = slot + (par * NS + src) * 32 + lane;
-        for (int rk = 0; rk < CL; ++rk) *cluster.map_shared_rank(my, rk) = ws;
+        const unsigned my = smem_u32(slot + (par * NS + src) * 32 + lane), mb = smem_u32(&mbar[par]);
+        for (int rk = 0; rk < CL; ++rk) st_async_f64(mapa_u32(my, rk), ws, mapa_u32(mb, rk));
         if (me == 0 && warp == 0) {  // pivot row jr = row of lane j: broadcast its entries, lane c pushes a_jr[c]
             // lane l holds row c0 + l, so a_jr[c] is lane j's av[c]: lane c keeps it
             double pv = 0.0;
@@ -457,9 +498,14 @@ __global__ void __launch_bounds__(QL_THREADS, 1) qr_leaf_reg_kernel(QrLeafArgs a
                 const double t = __shfl_sync(0xffffffffu, av[c], j);
                 pv = (lane == c) ? t : pv;
             }
-            for (int rk = 0; rk < CL; ++rk) *cluster.map_shared_rank(prow + par * 32 + lane, rk) = pv;
+            const unsigned pr = smem_u32(prow + par * 32 + lane);
+            for (int rk = 0; rk < CL; ++rk) st_async_f64(mapa_u32(pr, rk), pv, mapa_u32(mb, rk));
         }
-        cluster.sync();
+        // this CTA expects NS x 32 slot values and the 32 pivot-row values per column; phase (j / 2) of the
+        // parity's mbarrier completes when all have landed (a peer can only push column j + 2 after this CTA
+        // pushed column j + 1, i.e. after it finished reading column j: double buffering suffices)
+        if (tid == 0) mbar_arrive_expect_tx(mb, (unsigned)((NS * 32 + 32) * sizeof(double)));
+        mbar_wait_parity(mb, (unsigned)((j >> 1) & 1));
         // fixed-order sum of the NS slot values: 4 interleaved partial sums (short dependency chains)
         double t4[4] = {0.0, 0.0, 0.0, 0.0};
         for (int sidx = 0; sidx < NS; sidx += 4) {
