@@ -27,6 +27,13 @@ def test_block_cyclic_map():
         for p in range(n + 1):  # local suffix of positions >= p is contiguous
             j = bc.first_local_at_or_after(p)
             assert np.all(bc.pos[j:] >= p) and np.all(bc.pos[:j] < p)
+        for p in range(0, n, nb):  # the row blocks the row-distributed sketch computes and all-gathers
+            blocks = bc.own_blocks_from(p)
+            covered = np.concatenate([np.arange(q0, min(q0 + nb, n)) for q0 in blocks]) if blocks else np.arange(0)
+            assert np.array_equal(covered, bc.pos[bc.first_local_at_or_after(p):])
+    for p in range(0, n, nb):  # every position >= p is in exactly one rank's blocks
+        union = np.sort(np.concatenate([np.arange(q0, min(q0 + nb, n)) for bc in maps for q0 in bc.own_blocks_from(p)]))
+        assert np.array_equal(union, np.arange(p, n))
 
 
 def _free_port():
