@@ -30,6 +30,8 @@ void potrf_lower(Ctx& cx, int64_t n, double* G, int64_t ldg);
 // On return: strict lower = L (unit), upper = U; S[j] = S_jj (+-1).
 void getrf_nopiv_sign(Ctx& cx, int64_t n, double* Q, int64_t ldq, double* S);
 
+constexpr int FACT_NB = 64;  // diagonal block of the blocked / persistent k x k factorizations
+
 // small element-wise kernels
 void copy_matrix(Ctx& cx, int64_t rows, int64_t cols, const double* src, int64_t lds, double* dst, int64_t ldd);
 void transpose_copy(Ctx& cx, int64_t rows, int64_t cols, const double* src, int64_t lds, double* dst, int64_t ldd);

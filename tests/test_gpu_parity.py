@@ -375,3 +375,43 @@ def test_numerically_singular_panels_stay_backward_stable(gpu):
     res = oracle.OracleResult(_host(Ag), _host(taug), _host(Jg), rk, None, 0, None)
     assert oracle.residual(A, res) <= 1e-13
     assert oracle.orthogonality(res) <= 1e-12
+
+
+@pytest.mark.parametrize("n", [200, 1000, 2048])
+def test_kxk_cholesky_and_sign_lu(gpu, n):
+    """The k x k factorizations of the panel (persistent kernel for n >= 256, blocked below): POTRF of an SPD
+    Gram matrix against LAPACK's Cholesky (numpy), and the sign-choosing no-pivot LU of the reconstruction
+    (bqrrp_step_recon_top with C = I): L U = W - diag(S), S_j = -sgn of the running pivot (reading Z20),
+    unit-lower L with |L| <= 1 (the pivots |a - S| >= 1 for orthonormal columns, BD2015)."""
+    import ctypes
+
+    import torch
+
+    from paper_2507_00976_b200.dist import _declare
+
+    L = _declare()
+    rng = np.random.default_rng(n)
+    X = rng.standard_normal((3 * n, n))
+    G = X.T @ X
+    Gd = _dev(G)
+    st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    assert L.bqrrp_step_potrf(n, ctypes.c_void_p(Gd.data_ptr()), n, st) == 0
+    Lg = np.tril(_host(Gd))
+    Lref = np.linalg.cholesky(G)
+    assert np.linalg.norm(Lg - Lref) <= 1e-12 * np.linalg.norm(Lref)
+    assert np.all(np.triu(_host(Gd), 1) == 0)
+    # sign LU of the top n x n of an orthonormal Q (C = I)
+    Q, _ = np.linalg.qr(rng.standard_normal((2 * n, n)))
+    Qd = _dev(Q)
+    C = _dev(np.eye(n))
+    Wr = torch.empty((n, n), dtype=torch.float64, device="cuda").t()
+    S = torch.empty(n, dtype=torch.float64, device="cuda")
+    assert L.bqrrp_step_recon_top(n, ctypes.c_void_p(Qd.data_ptr()), 2 * n, ctypes.c_void_p(C.data_ptr()),
+                                  ctypes.c_void_p(Wr.data_ptr()), ctypes.c_void_p(S.data_ptr()), st) == 0
+    W, s_ = _host(Wr), _host(S)
+    Lw = np.tril(W, -1) + np.eye(n)
+    Uw = np.triu(W)
+    A = Q[:n] - np.diag(s_)
+    assert np.linalg.norm(Lw @ Uw - A) <= 1e-12 * np.linalg.norm(A)
+    assert np.all(np.abs(Lw) <= 1 + 1e-12)
+    assert np.all(np.isin(s_, [-1.0, 1.0]))
