@@ -103,10 +103,8 @@ __global__ void __launch_bounds__(LU_THREADS, 1) lu_panel_kernel(LuPanelArgs a)
     extern __shared__ double sp[];  // sp[c * R + r]
     __shared__ double red_v[LU_THREADS / 32];
     __shared__ int64_t red_i[LU_THREADS / 32];
-    __shared__ int red_w[LU_THREADS / 32];
     __shared__ double pivrow[LU_JBMAX], oldrow[LU_JBMAX];
     __shared__ int64_t s_piv;
-    __shared__ int s_win;
     __shared__ int64_t spiv[LU_JBMAX], trow[2 * LU_JBMAX], tsrc[2 * LU_JBMAX];
     __shared__ int s_nt;
 
@@ -152,12 +150,14 @@ __global__ void __launch_bounds__(LU_THREADS, 1) lu_panel_kernel(LuPanelArgs a)
             if (jr >= rbeg && jr < rbeg + rows_here) a.rowj[par * LU_JBMAX + tid] = sp[tid * R + (jr - rbeg)];
         }
         grid.sync();
-        // every CTA picks the same winner: parallel first-max over the G candidates
-        {
+        // every CTA picks the same winner: warp 0 alone reads the G candidates (lane-strided), reduces them
+        // with shuffles (first-max, IDAMAX order) and fetches the winner's row and row jr — one block barrier
+        // instead of three
+        if (warp == 0) {
             double v = -1.0;
             int64_t i = INT64_MAX;
             int wq = 0;
-            for (int q = tid; q < G; q += LU_THREADS) {
+            for (int q = lane; q < G; q += 32) {
                 const double* slot = a.xbuf + ((int64_t)par * G + q) * LU_XSTRIDE;
                 double cv = __ldcg(slot);
                 int64_t ci = (int64_t)__double_as_longlong(__ldcg(slot + 1));
@@ -169,23 +169,19 @@ __global__ void __launch_bounds__(LU_THREADS, 1) lu_panel_kernel(LuPanelArgs a)
                 int ow = __shfl_down_sync(0xffffffffu, wq, o);
                 if (better(ov, oi, v, i)) { v = ov; i = oi; wq = ow; }
             }
-            if (lane == 0) { red_v[warp] = v; red_i[warp] = i; red_w[warp] = wq; }
-            __syncthreads();
-            if (tid == 0) {
-                for (int wv = 1; wv < LU_THREADS / 32; ++wv)
-                    if (better(red_v[wv], red_i[wv], v, i)) { v = red_v[wv]; i = red_i[wv]; wq = red_w[wv]; }
+            i = __shfl_sync(0xffffffffu, i, 0);
+            wq = __shfl_sync(0xffffffffu, wq, 0);
+            if (lane < jb) {
+                pivrow[lane] = __ldcg(a.xbuf + ((int64_t)par * G + wq) * LU_XSTRIDE + 2 + lane);
+                oldrow[lane] = __ldcg(a.rowj + par * LU_JBMAX + lane);
+            }
+            if (lane == 0) {
                 s_piv = i;
-                s_win = wq;
                 if (cta == 0) a.ipiv[jr] = (int)i;
             }
-            __syncthreads();
-        }
-        const int64_t piv = s_piv;
-        if (tid < jb) {
-            pivrow[tid] = __ldcg(a.xbuf + ((int64_t)par * G + s_win) * LU_XSTRIDE + 2 + tid);
-            oldrow[tid] = __ldcg(a.rowj + par * LU_JBMAX + tid);
         }
         __syncthreads();
+        const int64_t piv = s_piv;
         const double u = pivrow[j];
         if (tid == 0) spiv[j] = (u != 0.0) ? piv : jr;
         if (u != 0.0) {
