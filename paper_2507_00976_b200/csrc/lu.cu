@@ -14,6 +14,7 @@
 #include <cstdlib>
 
 #include "blas.cuh"
+#include "dsmem.cuh"
 #include "bqrrp_internal.cuh"
 
 namespace cg = cooperative_groups;
@@ -210,7 +211,7 @@ __global__ void __launch_bounds__(LU_THREADS, 1) lu_panel_kernel(LuPanelArgs a)
 // the exchange in distributed shared memory and one barrier.cluster per column instead of a grid
 // barrier through L2.  Records are double-buffered by column parity (see the QR panel for the argument).
 constexpr int LUC_CLMAX = 16;
-constexpr int LUC_REC = 2 + 2 * LU_JBMAX;  // val, idx, candidate row, current row j (owner only)
+constexpr int LUC_SLOT = 2 + LU_JBMAX;  // val, idx, candidate row
 
 __global__ void __launch_bounds__(LU_THREADS, 1) lu_panel_cluster_kernel(LuPanelArgs a)
 {
@@ -219,7 +220,11 @@ __global__ void __launch_bounds__(LU_THREADS, 1) lu_panel_cluster_kernel(LuPanel
     extern __shared__ double dyn[];
     const int R = a.R, jb = a.jb, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     double* sp = dyn;                       // sp[c * R + r]
-    double* rec = dyn + (size_t)R * jb;     // [2][LUC_REC]
+    // exchange: slot[par][src] = (|value|, row, candidate row[32]) pushed by every CTA of the cluster;
+    // rowj[par] = row jr pushed by its owner — all into THIS CTA's memory (st.async + mbarrier tx-count)
+    double* slot = dyn + (size_t)R * jb;             // [2][CL][LUC_SLOT]
+    double* rowjs = slot + 2 * (size_t)CL * LUC_SLOT;  // [2][LU_JBMAX]
+    __shared__ __align__(8) unsigned long long mbar[2];
     __shared__ double red_v[LU_THREADS / 32];
     __shared__ int64_t red_i[LU_THREADS / 32];
     __shared__ double pivrow[LU_JBMAX], oldrow[LU_JBMAX];
@@ -231,10 +236,20 @@ __global__ void __launch_bounds__(LU_THREADS, 1) lu_panel_cluster_kernel(LuPanel
     const int64_t rows_here = (rbeg < a.w) ? ((a.w - rbeg < R) ? a.w - rbeg : R) : 0;
     const int64_t gtid = (int64_t)me * LU_THREADS + tid, gstride = (int64_t)CL * LU_THREADS;
 
+    if (tid == 0) {
+        mbar_init(smem_u32(&mbar[0]), 1);
+        mbar_init(smem_u32(&mbar[1]), 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
     slab_load_async(sp, R, a.L + rbeg + a.c0 * a.ld, a.ld, (int)rows_here, R, jb);
+    cluster.sync();  // every peer's mbarriers are initialised before the first push
 
-    // Per column: 2 block barriers + 1 cluster barrier.  Every thread owns whole rows (r = tid + k 256);
-    // the interchange is folded into the row update, so rows are only ever touched by their owner.
+    // Per column: 2 block barriers and one mbarrier wait: every CTA pushes its candidate record into every
+    // CTA's slot and the owner of row jr pushes that row (st.async), so after the wait each CTA picks the
+    // winner from its OWN shared memory (no cluster barrier, no fence, no remote reads).  Slots are
+    // double-buffered by parity: a CTA pushes column j+2 only after its column-(j+1) wait, i.e. after every
+    // peer pushed column j+1, which each peer does only after reading its column-j slots.  Every thread owns
+    // whole rows (r = tid + k 256); the interchange is folded into the row update.
     for (int j = 0; j < jb; ++j) {
         const int par = j & 1;
         const int64_t jr = a.c0 + j;
@@ -254,8 +269,8 @@ __global__ void __launch_bounds__(LU_THREADS, 1) lu_panel_cluster_kernel(LuPanel
         }
         if (lane == 0) { red_v[warp] = bv; red_i[warp] = bi; }
         __syncthreads();  // (1)
-        double* myrec = rec + par * LUC_REC;
-        if (warp == 0) {  // this CTA's candidate: value, row and its full panel row
+        const unsigned mb = smem_u32(&mbar[par]);
+        if (warp == 0) {  // this CTA's candidate: value, row and its full panel row, pushed to every CTA
             double v = (lane < LU_THREADS / 32) ? red_v[lane] : -1.0;
             int64_t i = (lane < LU_THREADS / 32) ? red_i[lane] : INT64_MAX;
             for (int o = 16; o > 0; o >>= 1) {
@@ -265,21 +280,29 @@ __global__ void __launch_bounds__(LU_THREADS, 1) lu_panel_cluster_kernel(LuPanel
             }
             v = __shfl_sync(0xffffffffu, v, 0);
             i = __shfl_sync(0xffffffffu, i, 0);
-            if (lane == 0) {
-                myrec[0] = v;
-                myrec[1] = __longlong_as_double((long long)i);
+            const unsigned dst = smem_u32(slot + ((size_t)par * CL + me) * LUC_SLOT);
+            const double rowv = (lane < jb && i != INT64_MAX) ? sp[lane * R + (i - rbeg)] : 0.0;
+            for (int rk = 0; rk < CL; ++rk) {
+                const unsigned rm = mapa_u32(mb, rk), rd = mapa_u32(dst, rk);
+                if (lane == 0) {
+                    st_async_f64(rd, v, rm);
+                    st_async_f64(rd + 8, __longlong_as_double((long long)i), rm);
+                }
+                if (lane < jb) st_async_f64(rd + 8 * (2 + lane), rowv, rm);
             }
-            if (lane < jb) myrec[2 + lane] = (i != INT64_MAX) ? sp[lane * R + (i - rbeg)] : 0.0;
-        } else if (warp == 1 && me == owner && lane < jb) {  // the current row j
-            myrec[2 + LU_JBMAX + lane] = sp[lane * R + (jr - rbeg)];
+        } else if (warp == 1 && me == owner && lane < jb) {  // the current row j, pushed to every CTA
+            const double rv = sp[lane * R + (jr - rbeg)];
+            const unsigned dst = smem_u32(rowjs + par * LU_JBMAX + lane);
+            for (int rk = 0; rk < CL; ++rk) st_async_f64(mapa_u32(dst, rk), rv, mapa_u32(mb, rk));
         }
-        cluster.sync();  // (C)
-        if (warp == 0) {  // every CTA picks the same winner
+        if (tid == 0) mbar_arrive_expect_tx(mb, (unsigned)((CL * (2 + jb) + jb) * sizeof(double)));
+        mbar_wait_parity(mb, (unsigned)((j >> 1) & 1));
+        if (warp == 0) {  // every CTA picks the same winner, from its own copy of the records
             double v = -1.0;
             int64_t i = INT64_MAX;
             int wq = 0;
             if (lane < CL) {
-                const double* pr = cluster.map_shared_rank(rec + par * LUC_REC, lane);
+                const double* pr = slot + ((size_t)par * CL + lane) * LUC_SLOT;
                 v = pr[0];
                 i = (int64_t)__double_as_longlong(pr[1]);
                 wq = lane;
@@ -293,8 +316,8 @@ __global__ void __launch_bounds__(LU_THREADS, 1) lu_panel_cluster_kernel(LuPanel
             i = __shfl_sync(0xffffffffu, i, 0);
             wq = __shfl_sync(0xffffffffu, wq, 0);
             if (lane < jb) {
-                pivrow[lane] = cluster.map_shared_rank(rec + par * LUC_REC, wq)[2 + lane];
-                oldrow[lane] = cluster.map_shared_rank(rec + par * LUC_REC, owner)[2 + LU_JBMAX + lane];
+                pivrow[lane] = slot[((size_t)par * CL + wq) * LUC_SLOT + 2 + lane];
+                oldrow[lane] = rowjs[par * LU_JBMAX + lane];
             }
             if (lane == 0) {
                 s_piv = i;
@@ -639,11 +662,12 @@ static bool lu_cluster_fits(int64_t rows, int jb, int* CLout, int* Rout)
 {
     int CL = (int)imin(LUC_CLMAX, imax(1, cdiv(rows, 512)));
     int R = (int)cdiv(rows, CL);
-    while ((size_t)R * jb * 8 + 2 * LUC_REC * 8 > LUC_SMEM_MAX && CL < LUC_CLMAX) {
+    auto bytes = [&](int cl, int r) { return (size_t)r * jb * 8 + ((size_t)2 * cl * LUC_SLOT + 2 * LU_JBMAX) * 8; };
+    while (bytes(CL, R) > LUC_SMEM_MAX && CL < LUC_CLMAX) {
         ++CL;
         R = (int)cdiv(rows, CL);
     }
-    if ((size_t)R * jb * 8 + 2 * LUC_REC * 8 > LUC_SMEM_MAX) return false;
+    if (bytes(CL, R) > LUC_SMEM_MAX) return false;
     *CLout = CL;
     *Rout = R;
     return true;
@@ -665,7 +689,7 @@ static bool lu_panel_cluster(Ctx& cx, double* L, int64_t ld, int64_t w, int64_t 
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(CL);
     cfg.blockDim = dim3(LU_THREADS);
-    cfg.dynamicSmemBytes = (size_t)R * jb * 8 + 2 * LUC_REC * 8;
+    cfg.dynamicSmemBytes = (size_t)R * jb * 8 + ((size_t)2 * CL * LUC_SLOT + 2 * LU_JBMAX) * 8;
     cfg.stream = cx.stream;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
