@@ -169,6 +169,17 @@ def oracle_sample(cfg_name: str, seed: int = 0):
     return canonical_flops(sm, sn) / dt / 1e12, dt, desc
 
 
+def cpu_model() -> str:
+    """The host CPU model (for the cpu_baseline record)."""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -188,7 +199,8 @@ def run_reference(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / max(len(times), 1),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": args.config + " " + CONFIGS[args.config]["desc"], "sample": f"{sm}x{sn}"},
-        "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": cores, "kind": "oracle", "sample": desc},
+        "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": cores, "kind": "oracle", "sample": desc,
+                         "cpu": cpu_model()},
         "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
@@ -325,6 +337,7 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, dt, desc = oracle_sample(args.config)
         cpu = {"value": v, "unit": "TFLOP/s", "cores": os.cpu_count(), "kind": "oracle", "sample": desc,
+               "cpu": cpu_model(),
                "seconds": dt}
 
     if rank == 0:

@@ -97,6 +97,23 @@ void gemm(Ctx& cx, bool ta, bool tb, int64_t M, int64_t N, int64_t K, double alp
             kchunk = cdiv(cdiv(K, want), Cfg2Mid::BK) * Cfg2Mid::BK;
             nsplit = (int)cdiv(K, kchunk);
         }
+    } else if (K >= 4096 && tiles < 8 * 4 * cx.num_sms && cx.splitk && ctas_per_sm == 0 && cfg == 1) {
+        // a few waves of long-K tiles (the panel's Gram SYRKs, late-iteration GEMM1): pick the split whose
+        // last wave is fullest (4 resident 64x64 CTAs per SM), if it beats no split by > 4 %
+        const int64_t slots = 4 * (int64_t)cx.num_sms;
+        auto eff = [&](int64_t sp) {
+            const int64_t w = tiles * sp;
+            return (double)w / (double)(cdiv(w, slots) * slots);
+        };
+        const int64_t cap = imin(16, imin(K / 1024, (int64_t)(cx.splitk_elems / (size_t)(M * N))));
+        int64_t best = 1;
+        double beff = eff(1);
+        for (int64_t sp = 2; sp <= cap; ++sp)
+            if (eff(sp) > beff + 0.04 + 0.002 * (double)sp) { best = sp; beff = eff(sp); }
+        if (best >= 2) {
+            kchunk = cdiv(cdiv(K, best), Cfg2Mid::BK) * Cfg2Mid::BK;
+            nsplit = (int)cdiv(K, kchunk);
+        }
     }
     GemmArgs g{M, N, K, alpha, beta, A, lda, B, ldb, C, ldc, nsplit > 1 ? cx.splitk : nullptr, kchunk, tri ? 1 : 0};
     GemmTraceRec rec{};
