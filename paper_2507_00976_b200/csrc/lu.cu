@@ -367,29 +367,16 @@ __global__ void __launch_bounds__(LU_THREADS, 1) lu_panel_cluster_kernel(LuPanel
 constexpr size_t LUC_SMEM_MAX = 196 * 1024;
 
 // ---------------------------------------------------------------------------------------------
-// Register-resident leaf (rows <= 148 x 512): each thread owns RPT rows of the 32-column panel in
-// registers (the smem slab kernels above spend most of a column step moving the slab through shared
-// memory).  Per column: local first-max -> warp shuffles -> ONE block barrier -> every thread derives
-// the CTA candidate; the thread owning it publishes (|value|, row, its full panel row), the owner of row
-// jr (always CTA 0: rows c0 .. c0+31 are its first rows) publishes row jr; then warp 0 picks the global
-// winner (IDAMAX order, Z19) and fetches the two rows, one more block barrier, and every thread swaps /
-// scales / updates its own rows.  The exchange is
-//   CLUSTER: records in each CTA's shared memory, one barrier.cluster, DSMEM reads;
-//   grid   : records in global memory tagged with a per-launch sequence number (st.release after the
-//            data; readers spin on ld.acquire), so no grid-wide barrier is needed; co-residency of the
-//            polling CTAs is guaranteed by the cooperative launch.
-// Records are double-buffered by column parity (a CTA can only publish column j+2 after reading every
-// CTA's column j+1 record, which each CTA publishes only after finishing its column-j reads).
-__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p)
-{
-    unsigned long long v;
-    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned long long v)
-{
-    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
+// Register-resident cluster leaf (rows <= 16 CTAs x 256 threads x RPT, RPT <= 2): each thread owns RPT rows
+// of the 32-column panel in registers (no shared-memory slab traffic).  Per column: local first-max ->
+// warp shuffles -> ONE block barrier -> every thread derives the CTA candidate; the warp owning it pushes
+// (|value|, row, its panel row) into every CTA's slot with st.async (mbarrier tx-count), CTA 0's warp 0
+// pushes row jr (rows c0 .. c0+31 are its lanes); after the mbarrier wait, warp 0 picks the winner (IDAMAX
+// order, Z19) from LOCAL shared memory, one more block barrier, every thread swaps / scales / updates its
+// own rows.  Slots are double-buffered by column parity (a CTA pushes column j+2 only after its column-
+// (j+1) wait, i.e. after every peer pushed column j+1, which each does after its column-j reads).  (A grid
+// form exchanging through global records with release/acquire tags was ~1.8x slower than the
+// shared-memory grid kernel and was removed.)
 __device__ __forceinline__ double select32(const double (&v)[32], int j)
 {
     double l1[16], l2[8], l3[4], l4[2];
@@ -405,21 +392,14 @@ __device__ __forceinline__ double select32(const double (&v)[32], int j)
 }
 
 constexpr int LR_REC = 2 + LU_JBMAX;  // |value|, row, panel row
+constexpr int LR_CLMAX = 16;
 
-template <int RPT, bool CLUSTER>
-__global__ void __launch_bounds__(LU_THREADS, 1) lu_leaf_reg_kernel(LuPanelArgs a, unsigned long long tag0,
-                                                                    unsigned long long* tags)
+template <int RPT>
+__global__ void __launch_bounds__(LU_THREADS, 1) lu_leaf_reg_kernel(LuPanelArgs a)
 {
+    cg::cluster_group cluster = cg::this_cluster();
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, jb = a.jb;
-    int G, me;
-    if (CLUSTER) {
-        cg::cluster_group cl = cg::this_cluster();
-        G = (int)cl.num_blocks();
-        me = (int)cl.block_rank();
-    } else {
-        G = gridDim.x;
-        me = blockIdx.x;
-    }
+    const int G = (int)cluster.num_blocks(), me = (int)cluster.block_rank();
     constexpr int RC = LU_THREADS * RPT;  // rows per CTA
     const int64_t rbeg = a.c0 + (int64_t)me * RC;
     __shared__ double red_v[LU_THREADS / 32];
@@ -428,7 +408,14 @@ __global__ void __launch_bounds__(LU_THREADS, 1) lu_leaf_reg_kernel(LuPanelArgs 
     __shared__ int64_t s_piv;
     __shared__ int64_t spiv[LU_JBMAX], trow[2 * LU_JBMAX], tsrc[2 * LU_JBMAX];
     __shared__ int s_nt;
-    __shared__ double crec[2][LR_REC + LU_JBMAX];  // CLUSTER records: candidate + row jr (CTA 0)
+    __shared__ double slot[2][LR_CLMAX][LR_REC];  // records pushed by every CTA of the cluster
+    __shared__ double rowjs[2][LU_JBMAX];         // row jr, pushed by CTA 0
+    __shared__ __align__(8) unsigned long long mbar[2];
+    if (tid == 0) {
+        mbar_init(smem_u32(&mbar[0]), 1);
+        mbar_init(smem_u32(&mbar[1]), 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
 
     double av[RPT][32];
     int64_t rr[RPT];
@@ -439,12 +426,13 @@ __global__ void __launch_bounds__(LU_THREADS, 1) lu_leaf_reg_kernel(LuPanelArgs 
 #pragma unroll
         for (int c = 0; c < 32; ++c) av[i][c] = (ok && c < jb) ? a.L[rr[i] + (a.c0 + c) * a.ld] : 0.0;
     }
+    cluster.sync();  // every peer's mbarriers are initialised before the first push
 
 #pragma unroll 1
     for (int j = 0; j < jb; ++j) {
         const int par = j & 1;
         const int64_t jr = a.c0 + j;
-        const unsigned long long tag = tag0 + (unsigned long long)j + 1ull;
+        const unsigned mb = smem_u32(&mbar[par]);
         // local first-max of |L(r, j)| over my active rows (ascending rows: first index kept on ties)
         double bv = -1.0;
         int64_t bi = INT64_MAX;
@@ -470,62 +458,50 @@ __global__ void __launch_bounds__(LU_THREADS, 1) lu_leaf_reg_kernel(LuPanelArgs 
 #pragma unroll
         for (int wv = 1; wv < LU_THREADS / 32; ++wv)
             if (better(red_v[wv], red_i[wv], cv, ci)) { cv = red_v[wv]; ci = red_i[wv]; }
-        // publish this CTA's candidate (by the thread owning its row) and, in CTA 0, row jr
-        double* rec = CLUSTER ? crec[par] : a.xbuf + ((int64_t)par * G + me) * LR_REC;
-        double* recj = CLUSTER ? crec[par] + LR_REC : a.rowj + par * LU_JBMAX;
+        // push this CTA's candidate: the warp owning row ci gathers it by shuffles (lane c takes entry c)
+        const int owner_t = (ci == INT64_MAX) ? 0 : (int)((ci - rbeg) % LU_THREADS);
+        const int owner_i = (ci == INT64_MAX) ? 0 : (int)((ci - rbeg) / LU_THREADS);
+        if (warp == (owner_t >> 5)) {
+            double mine = 0.0;
 #pragma unroll
-        for (int i = 0; i < RPT; ++i) {
-            if (rr[i] == ci) {
-                rec[0] = cv;
-                rec[1] = __longlong_as_double((long long)ci);
+            for (int c = 0; c < 32; ++c) {
+                double src = 0.0;
 #pragma unroll
-                for (int c = 0; c < 32; ++c)
-                    if (c < jb) rec[2 + c] = av[i][c];
-                if (!CLUSTER) st_release_u64(tags + (int64_t)par * G + me, tag);
+                for (int i = 0; i < RPT; ++i) src = (i == owner_i) ? av[i][c] : src;
+                const double t = __shfl_sync(0xffffffffu, src, owner_t & 31);
+                mine = (lane == c) ? t : mine;
             }
-            if (rr[i] == jr) {
-#pragma unroll
-                for (int c = 0; c < 32; ++c)
-                    if (c < jb) recj[c] = av[i][c];
-                if (!CLUSTER) st_release_u64(tags + 2 * (int64_t)G + par, tag);
+            if (ci == INT64_MAX) mine = 0.0;
+            const unsigned dst = smem_u32(&slot[par][me][0]);
+            for (int rk = 0; rk < G; ++rk) {
+                const unsigned rm = mapa_u32(mb, rk), rd = mapa_u32(dst, rk);
+                if (lane == 0) {
+                    st_async_f64(rd, (ci == INT64_MAX) ? -1.0 : cv, rm);
+                    st_async_f64(rd + 8, __longlong_as_double((long long)ci), rm);
+                }
+                st_async_f64(rd + 8 * (2 + lane), mine, rm);
             }
         }
-        if (ci == INT64_MAX && tid == 0) {  // no active row here
-            rec[0] = -1.0;
-            rec[1] = __longlong_as_double((long long)INT64_MAX);
-            if (!CLUSTER) st_release_u64(tags + (int64_t)par * G + me, tag);
+        if (me == 0 && warp == 0) {  // row jr = row c0 + j = lane j's first row
+            double rj = 0.0;
+#pragma unroll
+            for (int c = 0; c < 32; ++c) {
+                const double t = __shfl_sync(0xffffffffu, av[0][c], j);
+                rj = (lane == c) ? t : rj;
+            }
+            const unsigned dst = smem_u32(&rowjs[par][lane]);
+            for (int rk = 0; rk < G; ++rk) st_async_f64(mapa_u32(dst, rk), rj, mapa_u32(mb, rk));
         }
-        if (CLUSTER) cg::this_cluster().sync();
-        if (warp == 0) {  // every CTA picks the same winner and fetches its row and row jr
+        if (tid == 0) mbar_arrive_expect_tx(mb, (unsigned)((G * LR_REC + LU_JBMAX) * sizeof(double)));
+        mbar_wait_parity(mb, (unsigned)((j >> 1) & 1));
+        if (warp == 0) {  // every CTA picks the same winner from its own copy of the records
             double v = -1.0;
             int64_t idx = INT64_MAX;
             int wq = 0;
-            if (!CLUSTER) {
-                // wait for every CTA's record: relaxed (volatile) polls of all of this lane's tags in flight
-                // together, then one acquire fence before the data reads
-                bool ready;
-                do {
-                    ready = true;
-                    for (int q = lane; q < G; q += 32)
-                        ready &= (*(volatile const unsigned long long*)(tags + (int64_t)par * G + q) == tag);
-                    if (!__all_sync(0xffffffffu, ready)) __nanosleep(20);
-                    else break;
-                } while (true);
-                __threadfence();
-            }
-            for (int q = lane; q < G; q += 32) {
-                double qv;
-                int64_t qi;
-                if (CLUSTER) {
-                    const double* pr = cg::this_cluster().map_shared_rank(crec[par], q);
-                    qv = pr[0];
-                    qi = (int64_t)__double_as_longlong(pr[1]);
-                } else {
-                    const double* pr = a.xbuf + ((int64_t)par * G + q) * LR_REC;
-                    qv = __ldcg(pr);
-                    qi = (int64_t)__double_as_longlong(__ldcg(pr + 1));
-                }
-                if (better(qv, qi, v, idx)) { v = qv; idx = qi; wq = q; }
+            if (lane < G) {
+                v = slot[par][lane][0];
+                idx = (int64_t)__double_as_longlong(slot[par][lane][1]);
+                wq = lane;
             }
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) {
@@ -536,15 +512,9 @@ __global__ void __launch_bounds__(LU_THREADS, 1) lu_leaf_reg_kernel(LuPanelArgs 
             }
             idx = __shfl_sync(0xffffffffu, idx, 0);
             wq = __shfl_sync(0xffffffffu, wq, 0);
-            if (CLUSTER) {
-                if (lane < jb) {
-                    pivrow[lane] = cg::this_cluster().map_shared_rank(crec[par], wq)[2 + lane];
-                    oldrow[lane] = cg::this_cluster().map_shared_rank(crec[par], 0)[LR_REC + lane];
-                }
-            } else {
-                if (lane < jb) pivrow[lane] = __ldcg(a.xbuf + ((int64_t)par * G + wq) * LR_REC + 2 + lane);
-                while (ld_acquire_u64(tags + 2 * (int64_t)G + par) != tag) __nanosleep(32);
-                if (lane < jb) oldrow[lane] = __ldcg(a.rowj + par * LU_JBMAX + lane);
+            if (lane < jb) {
+                pivrow[lane] = slot[par][wq][2 + lane];
+                oldrow[lane] = rowjs[par][lane];
             }
             if (lane == 0) {
                 s_piv = idx;
@@ -585,75 +555,49 @@ __global__ void __launch_bounds__(LU_THREADS, 1) lu_leaf_reg_kernel(LuPanelArgs 
             for (int c = 0; c < 32; ++c)
                 if (c < jb) a.L[rr[i] + (a.c0 + c) * a.ld] = av[i][c];
         }
-    if (CLUSTER) cg::this_cluster().sync();  // peers may still read this CTA's last records
-    __syncthreads();
+    cluster.sync();  // no CTA exits while peers may still push into it
     const int64_t gtid = (int64_t)me * LU_THREADS + tid, gstride = (int64_t)G * LU_THREADS;
     apply_panel_interchanges(a, spiv, trow, tsrc, &s_nt, gtid, gstride);
 }
 
-static int lu_reg_mode()
+static bool lu_reg_fits(int64_t rows)
 {
     static int use = -1;
-    if (use < 0) {  // BQRRP_LU_LEAF=0: the shared-memory slab kernels only; 2: register leaf in grid form too
+    if (use < 0) {  // BQRRP_LU_LEAF=0: the shared-memory slab kernels only (A/B)
         const char* e = std::getenv("BQRRP_LU_LEAF");
-        use = (e && e[0] == '0') ? 0 : ((e && e[0] == '2') ? 2 : 1);
+        use = (e && e[0] == '0') ? 0 : 1;
     }
-    return use;
+    // one row per thread: with two rows per thread it measured slower than the shared-memory cluster kernel
+    // (8192 rows: 8.5 vs 6.5 us per column), at <= 4096 rows slightly faster (5.7-5.9 vs 5.9-6.1)
+    return use && rows <= (int64_t)LR_CLMAX * LU_THREADS;
 }
 
-// The register leaf is used in its one-row-per-thread cluster form only (rows <= 16 CTAs x 256 threads:
-// 5.8 vs 6.4 us per column).  With two rows per thread it only ties the shared-memory cluster kernel
-// (8192 rows), and its grid form (global-memory records with release/acquire tags, cooperative launch) is
-// correct but ~1.8x SLOWER than the shared-memory grid kernel at C3 sizes (w = 16384 .. 63488: 8.4-13.9
-// vs 6.6-7.6 us per column, profiles/lu_leaf_r01.json), so those panels keep the slab kernels; the other
-// forms stay selectable (BQRRP_LU_LEAF=2) for further work.
-static bool lu_reg_fits(int64_t rows, int num_sms)
-{
-    const int mode = lu_reg_mode();
-    if (mode == 0) return false;
-    if (mode == 2) return rows <= (int64_t)num_sms * LU_THREADS * 2;
-    return rows <= 16 * LU_THREADS;
-}
-
-static bool lu_panel_reg(Ctx& cx, double* L, int64_t ld, int64_t w, int64_t d, int64_t c0, int jb, int* ipiv, int* perm,
-                         double* xbuf, double* rowj, unsigned long long* tags, unsigned long long* seq)
+static bool lu_panel_reg(Ctx& cx, double* L, int64_t ld, int64_t w, int64_t d, int64_t c0, int jb, int* ipiv, int* perm)
 {
     const int64_t rows = w - c0;
-    if (!lu_reg_fits(rows, cx.num_sms) || jb > 32) return false;
-    const bool cluster = rows <= 16 * LU_THREADS * 2;
-    const int rpt = cluster ? (rows <= 16 * LU_THREADS ? 1 : 2) : (rows <= (int64_t)cx.num_sms * LU_THREADS ? 1 : 2);
+    if (!lu_reg_fits(rows) || jb > 32) return false;
+    const int rpt = rows <= (int64_t)LR_CLMAX * LU_THREADS ? 1 : 2;
     const int G = (int)cdiv(rows, (int64_t)LU_THREADS * rpt);
-    LuPanelArgs a{L, ld, w, d, c0, jb, LU_THREADS * rpt, ipiv, perm, xbuf, rowj};
-    const unsigned long long tag0 = (++*seq) << 6;
-    if (cluster) {
-        static bool attr = false;
-        if (!attr) {
-            BQ_CUDA(cudaFuncSetAttribute(lu_leaf_reg_kernel<1, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-            BQ_CUDA(cudaFuncSetAttribute(lu_leaf_reg_kernel<2, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-            attr = true;
-        }
-        cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3(G);
-        cfg.blockDim = dim3(LU_THREADS);
-        cfg.stream = cx.stream;
-        cudaLaunchAttribute at[1];
-        at[0].id = cudaLaunchAttributeClusterDimension;
-        at[0].val.clusterDim.x = G;
-        at[0].val.clusterDim.y = 1;
-        at[0].val.clusterDim.z = 1;
-        cfg.attrs = at;
-        cfg.numAttrs = 1;
-        if (rpt == 1) BQ_CUDA(cudaLaunchKernelEx(&cfg, lu_leaf_reg_kernel<1, true>, a, tag0, tags));
-        else BQ_CUDA(cudaLaunchKernelEx(&cfg, lu_leaf_reg_kernel<2, true>, a, tag0, tags));
-    } else {
-        void* args[] = {&a, (void*)&tag0, &tags};
-        if (rpt == 1)
-            BQ_CUDA(cudaLaunchCooperativeKernel((void*)lu_leaf_reg_kernel<1, false>, dim3(G), dim3(LU_THREADS), args, 0,
-                                                cx.stream));
-        else
-            BQ_CUDA(cudaLaunchCooperativeKernel((void*)lu_leaf_reg_kernel<2, false>, dim3(G), dim3(LU_THREADS), args, 0,
-                                                cx.stream));
+    LuPanelArgs a{L, ld, w, d, c0, jb, LU_THREADS * rpt, ipiv, perm, nullptr, nullptr};
+    static bool attr = false;
+    if (!attr) {
+        BQ_CUDA(cudaFuncSetAttribute(lu_leaf_reg_kernel<1>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        BQ_CUDA(cudaFuncSetAttribute(lu_leaf_reg_kernel<2>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        attr = true;
     }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(G);
+    cfg.blockDim = dim3(LU_THREADS);
+    cfg.stream = cx.stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = G;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    if (rpt == 1) BQ_CUDA(cudaLaunchKernelEx(&cfg, lu_leaf_reg_kernel<1>, a));
+    else BQ_CUDA(cudaLaunchKernelEx(&cfg, lu_leaf_reg_kernel<2>, a));
     ++g_launches;
     return true;
 }
@@ -703,17 +647,15 @@ static bool lu_panel_cluster(Ctx& cx, double* L, int64_t ld, int64_t w, int64_t 
     return true;
 }
 
-struct LuExchange {
+struct LuExchange {  // global exchange buffers of the cooperative grid leaf
     double* xbuf;
     double* rowj;
-    unsigned long long* tags;  // [2][G] candidate tags + [2] row-jr tags (register leaf, grid mode)
-    unsigned long long seq;    // launches so far in this getrf (tags are zeroed per getrf)
 };
 
 static void lu_panel(Ctx& cx, double* L, int64_t ld, int64_t w, int64_t d, int64_t c0, int jb, int* ipiv, int* perm,
                      LuExchange& ex)
 {
-    if (lu_panel_reg(cx, L, ld, w, d, c0, jb, ipiv, perm, ex.xbuf, ex.rowj, ex.tags, &ex.seq)) return;
+    if (lu_panel_reg(cx, L, ld, w, d, c0, jb, ipiv, perm)) return;
     double* xbuf = ex.xbuf;
     double* rowj = ex.rowj;
     if (lu_panel_cluster(cx, L, ld, w, d, c0, jb, ipiv, perm)) return;
@@ -741,7 +683,7 @@ static void lu_panel(Ctx& cx, double* L, int64_t ld, int64_t w, int64_t d, int64
 
 static int lu_leaf_width(int64_t rows, int num_sms)
 {
-    if (lu_reg_fits(rows, num_sms)) return 32;  // the register leaf holds any row count up to 148 x 512
+    if (lu_reg_fits(rows)) return 32;  // the register cluster leaf (<= 16 x 512 rows)
     // a leaf that one cluster can hold (32, else 16 columns), else the widest the grid kernel can hold
     int CL, R;
     if (lu_cluster_fits(rows, 32, &CL, &R)) return 32;
@@ -788,9 +730,6 @@ void getrf_pivots(Ctx& cx, double* L, int64_t ld, int64_t w, int64_t d, int* ipi
     LuExchange ex;
     ex.xbuf = cx.alloc(2 * (size_t)cx.num_sms * LU_XSTRIDE);
     ex.rowj = cx.alloc(2 * LU_JBMAX);
-    ex.tags = cx.alloc_as<unsigned long long>(2 * (size_t)cx.num_sms + 2);
-    ex.seq = 0;
-    BQ_CUDA(cudaMemsetAsync(ex.tags, 0, sizeof(unsigned long long) * (2 * (size_t)cx.num_sms + 2), cx.stream));
     int leaf = lu_leaf_width(w, cx.num_sms);
     getrf_rec(cx, L, ld, w, nlu, 0, nlu, ipiv, perm, ex, leaf);
     cx.ws_used = mark;
