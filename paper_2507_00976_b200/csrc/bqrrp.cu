@@ -289,7 +289,7 @@ static int64_t factor_impl(Ctx& cx, Ctx* cxb, cudaEvent_t ev_top, cudaEvent_t ev
         extract_rsk11_kernel<<<(unsigned)imin(cdiv(k * k, 256), 4 * cx.num_sms), 256, 0, cx.stream>>>(k, MskT + s, n,
                                                                                                         Rsk11);
         BQ_LAUNCH_CHECK();
-        g_panel_fallbacks += panel_factor(cx, m, A, lda, s, k, Rsk11, tau, passes, Vp, Tp, hqr_fallback);
+        g_panel_fallbacks += panel_factor(cx, m, A, lda, s, k, Rsk11, tau, passes, Vp, Tp, hqr_fallback, cxb);
         // ---- a5 (the bulk rows overlap the sketch update and the next a2) and a7
         cx.mark(PH_APPLY_QT);
         const bool terminal = (k < kmax || c == n || r == m);

@@ -51,7 +51,7 @@ extern thread_local long long g_panel_fallbacks;
 // hqr_fallback: after the Cholesky passes, read the POTRF breakdown flag (one host sync) and on a breakdown
 // factor this panel with Householder QR instead (returns 1; 0 otherwise; the flag is cleared).
 int panel_factor(Ctx& cx, int64_t m, double* A, int64_t lda, int64_t s, int64_t k, const double* Rsk11, double* tau,
-                 int passes, double* V, double* T, bool hqr_fallback = false);
+                 int passes, double* V, double* T, bool hqr_fallback = false, Ctx* side = nullptr);
 // Phases of the CholQR panel (panel.cu), on a block of panel rows unless k x k:
 //   M_pre = P R_sk11^{-1} -> Q (ld ldq), G = M_pre^T M_pre (lower; zero if rows == 0)
 void cholqr_precondition_gram(Ctx& cx, int64_t rows, int64_t k, const double* P, int64_t ldp, const double* Rsk11,
@@ -64,7 +64,7 @@ void recon_top_lu(Ctx& cx, int64_t k, const double* Qtop, int64_t ldq, const dou
 void recon_rows(Ctx& cx, int64_t rows, int64_t k, double* Q, int64_t ldq, const double* Wr, const double* C);
 //   T = -U S L^{-T}, tau = diag(T), R = C_passes^T ... C_1^T R_sk11 (R11 = S R)
 void recon_finish(Ctx& cx, int64_t k, const double* Wr, const double* S, const double* const* Cf, int passes,
-                  const double* Rsk11, double* T, double* tau, double* R);
+                  const double* Rsk11, double* T, double* tau, double* R, double* scratch = nullptr);
 //   GEQP3 write of the panel (S R on/above, V below) and Q (L \ U on top, Y2 below) -> explicit V in place
 void write_panel(Ctx& cx, int64_t h, int64_t k, double* Q, int64_t ldq, const double* R, const double* S, double* Ap,
                  int64_t lda);

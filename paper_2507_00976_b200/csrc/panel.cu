@@ -98,7 +98,7 @@ void recon_rows(Ctx& cx, int64_t rows, int64_t k, double* Q, int64_t ldq, const 
 }
 
 void recon_finish(Ctx& cx, int64_t k, const double* Wr, const double* S, const double* const* Cf, int passes,
-                  const double* Rsk11, double* T, double* tau, double* R)
+                  const double* Rsk11, double* T, double* tau, double* R, double* scratch)
 {
     build_t_rhs_kernel<<<(unsigned)imin(cdiv(k * k, 256), 4 * cx.num_sms), 256, 0, cx.stream>>>(k, Wr, k, S, T);
     BQ_LAUNCH_CHECK();
@@ -108,8 +108,8 @@ void recon_finish(Ctx& cx, int64_t k, const double* Wr, const double* S, const d
     BQ_LAUNCH_CHECK();
     // R = C_last^T ... C_1^T R_sk11 (the caller applies S: R11 = S R)
     const size_t mark = cx.ws_used;
-    double* Wa = cx.alloc((size_t)k * k);
-    double* Wb = cx.alloc((size_t)k * k);
+    double* Wa = scratch ? scratch : cx.alloc((size_t)k * k);
+    double* Wb = scratch ? scratch + (size_t)k * k : cx.alloc((size_t)k * k);
     copy_matrix(cx, k, k, Rsk11, k, Wa, k);
     for (int p = 0; p < passes; ++p) {
         gemm(cx, true, false, k, k, k, 1.0, Cf[p], k, Wa, k, 0.0, Wb, k);
@@ -136,7 +136,7 @@ void force_breakdown_hook(Ctx& cx)
 }
 
 int panel_factor(Ctx& cx, int64_t m, double* A, int64_t lda, int64_t s, int64_t k, const double* Rsk11, double* tau,
-                 int passes, double* V, double* T, bool hqr_fallback)
+                 int passes, double* V, double* T, bool hqr_fallback, Ctx* side)
 {
     const int64_t h = m - s;
     if (passes == 0) {  // BQRRP_HQR: Householder QR of the panel itself
@@ -174,9 +174,32 @@ int panel_factor(Ctx& cx, int64_t m, double* A, int64_t lda, int64_t s, int64_t 
     }
     const double* Cl = Cf[passes - 1];
     recon_top_lu(cx, k, Q, h, Cl, Wr, S);
-    if (h > k) recon_rows(cx, h - k, k, Q + k, h, Wr, Cl);
-    copy_matrix(cx, k, k, Wr, k, Q, h);  // L \ U on top
-    recon_finish(cx, k, Wr, S, Cf, passes, Rsk11, T, tau + s, R);
+    if (side && h > 2 * k) {
+        // the k x k finish (T-solve, tau, R products) depends only on Wr and S: run it on the side stream
+        // (idle during the panel) while the main stream does the tall Y2 TRSM; its scratch is carved here
+        // and it uses no split-K slices (those belong to the main stream)
+        double* scr = cx.alloc((size_t)2 * k * k);
+        cudaEvent_t ef, ej;
+        BQ_CUDA(cudaEventCreateWithFlags(&ef, cudaEventDisableTiming));
+        BQ_CUDA(cudaEventCreateWithFlags(&ej, cudaEventDisableTiming));
+        BQ_CUDA(cudaEventRecord(ef, cx.stream));
+        BQ_CUDA(cudaStreamWaitEvent(side->stream, ef, 0));
+        Ctx sc = *side;
+        sc.splitk = nullptr;
+        sc.splitk_elems = 0;
+        sc.timer = nullptr;
+        recon_finish(sc, k, Wr, S, Cf, passes, Rsk11, T, tau + s, R, scr);
+        BQ_CUDA(cudaEventRecord(ej, side->stream));
+        recon_rows(cx, h - k, k, Q + k, h, Wr, Cl);
+        copy_matrix(cx, k, k, Wr, k, Q, h);  // L \ U on top
+        BQ_CUDA(cudaStreamWaitEvent(cx.stream, ej, 0));
+        BQ_CUDA(cudaEventDestroy(ef));
+        BQ_CUDA(cudaEventDestroy(ej));
+    } else {
+        if (h > k) recon_rows(cx, h - k, k, Q + k, h, Wr, Cl);
+        copy_matrix(cx, k, k, Wr, k, Q, h);  // L \ U on top
+        recon_finish(cx, k, Wr, S, Cf, passes, Rsk11, T, tau + s, R, nullptr);
+    }
     write_panel(cx, h, k, Q, h, R, S, Ap, lda);
     cx.ws_used = mark;
     return 0;

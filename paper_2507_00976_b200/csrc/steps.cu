@@ -345,7 +345,7 @@ int bqrrp_step_recon_finish(int64_t k, const double* Wr, const double* S, const 
                                                                                                     Rsk11);
         BQ_LAUNCH_CHECK();
         const double* Cf[2] = {C1, C2};
-        recon_finish(cx, k, Wr, S, Cf, C2 ? 2 : 1, Rsk11, T, tau, R);
+        recon_finish(cx, k, Wr, S, Cf, C2 ? 2 : 1, Rsk11, T, tau, R, nullptr);
         return 0;
     });
 }
