@@ -226,6 +226,13 @@ static int64_t factor_impl(Ctx& cx, Ctx* cxb, cudaEvent_t ev_top, cudaEvent_t ev
     double* W = cx.alloc((size_t)bb * n);
     double* W2 = cx.alloc((size_t)bb * n);
     bool bulk_pending = false;
+    cudaEvent_t ev_x0 = nullptr, ev_x1 = nullptr;  // side-stream X of the sample update
+    BQ_CUDA(cudaEventCreateWithFlags(&ev_x0, cudaEventDisableTiming));
+    BQ_CUDA(cudaEventCreateWithFlags(&ev_x1, cudaEventDisableTiming));
+    struct EvGuard {
+        cudaEvent_t a, b;
+        ~EvGuard() { cudaEventDestroy(a); cudaEventDestroy(b); }
+    } ev_guard{ev_x0, ev_x1};
 
     cx.mark(PH_OTHER);
     init_j_kernel<<<(unsigned)imin(cdiv(n, 256), 1024), 256, 0, cx.stream>>>(n, J);
@@ -294,14 +301,31 @@ static int64_t factor_impl(Ctx& cx, Ctx* cxb, cudaEvent_t ev_top, cudaEvent_t ev
         cx.mark(PH_APPLY_QT);
         const bool terminal = (k < kmax || c == n || r == m);
         if (hio && !terminal) hio->flush(cx.stream, m, A, lda, c);  // block column [s, c) is final
+        // a6's X = R_sk11 R11^{-1} (b x b) needs only the panel: on the idle side stream during GEMM1
+        // (ahead of the bulk rows there, which wait for GEMM1 anyway); no split-K slices on that stream
+        const bool x_side = !terminal && cxb;
+        if (x_side) {
+            BQ_CUDA(cudaEventRecord(ev_x0, cx.stream));
+            BQ_CUDA(cudaStreamWaitEvent(cxb->stream, ev_x0, 0));
+            Ctx sc = *cxb;
+            sc.timer = nullptr;
+            copy_matrix(sc, b, b, Rsk11, k, X, b);
+            trsm_right_upper(sc, b, b, A + s + s * lda, lda, false, false, X, b);  // X = R_sk11 R11^{-1}
+            zero_triangle(sc, 'U', b, b, X, b);
+            BQ_CUDA(cudaEventRecord(ev_x1, cxb->stream));
+        }
         wy_update(cx, terminal ? nullptr : cxb, m, n, A, lda, s, k, Vp, Tp, W, W2, ev_top, ev_bulk);
         if (!terminal && cxb && h > k && n - s - k > 0) bulk_pending = true;
         if (terminal) { ell = s + k; break; }
         // ---- a6: sketch update (k == b here)
         cx.mark(PH_SAMPLE_UPDATE);
-        copy_matrix(cx, b, b, Rsk11, k, X, b);
-        trsm_right_upper(cx, b, b, A + s + s * lda, lda, false, false, X, b);  // X = R_sk11 R11^{-1}
-        zero_triangle(cx, 'U', b, b, X, b);
+        if (x_side) {
+            BQ_CUDA(cudaStreamWaitEvent(cx.stream, ev_x1, 0));
+        } else {
+            copy_matrix(cx, b, b, Rsk11, k, X, b);
+            trsm_right_upper(cx, b, b, A + s + s * lda, lda, false, false, X, b);  // X = R_sk11 R11^{-1}
+            zero_triangle(cx, 'U', b, b, X, b);
+        }
         gemm(cx, true, true, n - c, b, b, -1.0, A + s + c * lda, lda, X, b, 1.0, MskT + c, n);
     }
     // O4: tau(ell:) = 0, A(ell:m, ell:n) = 0 (reading Z16)
