@@ -134,6 +134,7 @@ static Layout layout(int64_t m, int64_t n, int64_t b, int64_t d)
     P += r((size_t)2 * d) * 3;             // vec tmp (int64), tq, tsrc
     P += r((size_t)d) + r(8) + r((size_t)n);  // ipiv, nt, perm
     P += r(bb * bb) * 3;                   // Rsk11, X, T
+    P += r((size_t)d * d) + r((size_t)n * d);  // deferred R_sk GEMM: Q_sk and its output rows
     P += r((size_t)m * bb) + r(bb * (size_t)n) * 2;  // V, W, W2
     P += r(8) * 2;                         // ref, flags
     // temporaries: sketch QR vs panel (never live together)
@@ -226,6 +227,12 @@ static int64_t factor_impl(Ctx& cx, Ctx* cxb, cudaEvent_t ev_top, cudaEvent_t ev
     double* W = cx.alloc((size_t)bb * n);
     double* W2 = cx.alloc((size_t)bb * n);
     bool bulk_pending = false;
+    RskDefer rsk;  // the R_sk(:, d:) GEMM of every pivot selection on the side stream (lookahead only)
+    if (cxb) {
+        rsk.side = cxb;
+        rsk.Q = cx.alloc((size_t)d * d);
+        rsk.Y = cx.alloc((size_t)n * d);
+    }
     cudaEvent_t ev_x0 = nullptr, ev_x1 = nullptr;  // side-stream X of the sample update
     BQ_CUDA(cudaEventCreateWithFlags(&ev_x0, cudaEventDisableTiming));
     BQ_CUDA(cudaEventCreateWithFlags(&ev_x1, cudaEventDisableTiming));
@@ -272,7 +279,7 @@ static int64_t factor_impl(Ctx& cx, Ctx* cxb, cudaEvent_t ev_top, cudaEvent_t ev
         const int64_t nlu = imin(w, d);
         touched_from_perm(cx, w, nlu, perm, T);
         permute_rows(cx, d, MskT + s, n, T, rowscr);
-        sketch_qr(cx, MskT + s, n, w, d);
+        sketch_qr(cx, MskT + s, n, w, d, RowBlocks(), cxb ? &rsk : nullptr);
         cx.mark(PH_TRI_RANK);
         tri_rank_kernel<<<1, 1024, 0, cx.stream>>>(MskT + s, n, kmax, i == 0, rank_tol, ref, cx.flags);
         BQ_LAUNCH_CHECK();

@@ -33,7 +33,16 @@ struct RowBlocks {
     const int64_t* len = nullptr;
     int64_t n = -1;  // < 0: all rows
 };
-void sketch_qr(Ctx& cx, double* MskT, int64_t ldm, int64_t w, int64_t d, const RowBlocks& rows = RowBlocks());
+// defer: run the R_sk(:, d:w) GEMM (the bulk of the sketch QR's flops, 2 (w - d) d^2) on a second stream,
+// ordered after the work already queued there; Q (d x d) and Y ((w - d) x d) are caller-owned buffers that
+// stay alive until that stream has run it.  The caller orders the next reader of those rows after it.
+struct RskDefer {
+    Ctx* side = nullptr;
+    double* Q = nullptr;
+    double* Y = nullptr;
+};
+void sketch_qr(Ctx& cx, double* MskT, int64_t ldm, int64_t w, int64_t d, const RowBlocks& rows = RowBlocks(),
+               const RskDefer* defer = nullptr);
 
 // a3: touched set and gathers
 void touched_from_perm(Ctx& cx, int64_t w, int64_t nlu, const int* perm, Touched& T);

@@ -693,7 +693,8 @@ __global__ void store_rsk_kernel(int64_t p, int64_t d, const double* Wq, double*
 }
 
 // R_sk of the d x w sketch window MskT(0:w, 0:d)^T (MskT points at row s, ld ldm); in place.
-void sketch_qr(Ctx& cx, double* MskT, int64_t ldm, int64_t w, int64_t d, const RowBlocks& rows)
+void sketch_qr(Ctx& cx, double* MskT, int64_t ldm, int64_t w, int64_t d, const RowBlocks& rows,
+               const RskDefer* defer)
 {
     int64_t p = imin(d, w);
     if (p <= 0) return;
@@ -717,14 +718,29 @@ void sketch_qr(Ctx& cx, double* MskT, int64_t ldm, int64_t w, int64_t d, const R
         // p == d here.  Q_sk = H_1...H_p = I - V T V^T formed explicitly (d x d), then
         // R_sk(:, p:w)^T = Wsk(:, p:w)^T Q_sk in one GEMM (2 rest d^2 flops instead of 6 rest d p).
         double* Xt = MskT + p;  // rest x d
-        double* Q = cx.alloc((size_t)d * d);
+        const bool deferred = defer && defer->side && rows.n < 0;
+        double* Q = deferred ? defer->Q : cx.alloc((size_t)d * d);
         double* Wt = cx.alloc((size_t)p * d);
-        double* Y = cx.alloc((size_t)rest * d);
+        double* Y = deferred ? defer->Y : cx.alloc((size_t)rest * d);
         gemm(cx, false, true, p, d, p, 1.0, Tf, p, V, d, 0.0, Wt, p);  // Wt = T V^T
         BQ_CUDA(cudaMemsetAsync(Q, 0, sizeof(double) * d * d, cx.stream));
         zero_triangle(cx, 'L', d, d, Q, d, /*unit_diag=*/true);
         gemm(cx, false, false, d, d, p, -1.0, V, d, Wt, p, 1.0, Q, d);  // Q = I - V Wt
-        if (rows.n < 0) {
+        if (deferred) {
+            // on the second stream: after what is queued there (the previous bulk update), overlapping the
+            // critical chain's permutation and latency-bound panel
+            cudaEvent_t e;
+            BQ_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            BQ_CUDA(cudaEventRecord(e, cx.stream));
+            BQ_CUDA(cudaStreamWaitEvent(defer->side->stream, e, 0));
+            BQ_CUDA(cudaEventDestroy(e));
+            Ctx sc = *defer->side;
+            sc.splitk = nullptr;
+            sc.splitk_elems = 0;
+            sc.timer = nullptr;
+            gemm(sc, false, false, rest, d, d, 1.0, Xt, ldm, Q, d, 0.0, Y, rest);
+            copy_matrix(sc, rest, d, Y, rest, Xt, ldm);
+        } else if (rows.n < 0) {
             gemm(cx, false, false, rest, d, d, 1.0, Xt, ldm, Q, d, 0.0, Y, rest);
             copy_matrix(cx, rest, d, Y, rest, Xt, ldm);
         } else {
