@@ -87,8 +87,11 @@ int bqrrp_factor_ex(int64_t m, int64_t n, double* A, int64_t lda, int64_t b, int
                     int64_t* J, int64_t* rank, void* workspace, size_t ws_bytes, void* stream,
                     const bqrrp_options* opts);
 
-/* End-to-end variant on HOST buffers (A_host m x n col-major, tau_host, J_host): copies A to the device,
- * factors, copies A, tau, J back; synchronous.  Device memory is allocated and freed inside. */
+/* End-to-end variant on HOST buffers (A_host m x n col-major, ideally pinned; tau_host, J_host): A is
+ * uploaded in column chunks on a copy stream while the sketch of the chunks already on the device is
+ * computed, and each block column is copied back as soon as its iteration has finalised it, so both PCIe
+ * directions overlap the factorization; tau and J at the end.  Synchronous; A_host is read and then
+ * overwritten in place.  Device memory comes from the library's pool (see bqrrp_trim_memory). */
 int bqrrp_factor_host(int64_t m, int64_t n, double* A_host, int64_t lda, int64_t b, int64_t d, uint64_t seed,
                       double* tau_host, int64_t* J_host, int64_t* rank, void* stream, const bqrrp_options* opts);
 
