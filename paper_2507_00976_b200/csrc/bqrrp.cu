@@ -106,11 +106,6 @@ __global__ void extract_rsk11_kernel(int64_t k, const double* MskT_s, int64_t ld
     }
 }
 
-__global__ void ipiv_to_int_kernel(int64_t n, const int64_t* in1, int* out0)
-{
-    int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (j < n) out0[j] = (int)(in1[j] - 1);
-}
 __global__ void ipiv_to_i64_kernel(int64_t n, const int* in0, int64_t* out1)
 {
     int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
