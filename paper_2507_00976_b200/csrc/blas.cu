@@ -71,7 +71,8 @@ static void launch_gemm(Ctx& cx, bool ta, bool tb, const GemmArgs& g, int nsplit
 // small and skinny GEMMs of the recursions).  Split-K (fixed slices, fixed-order sum) when even the
 // chosen tiling leaves the SMs idle and K is long.
 void gemm(Ctx& cx, bool ta, bool tb, int64_t M, int64_t N, int64_t K, double alpha, const double* A, int64_t lda,
-          const double* B, int64_t ldb, double beta, double* C, int64_t ldc, bool tri, int ctas_per_sm)
+          const double* B, int64_t ldb, double beta, double* C, int64_t ldc, bool tri, int ctas_per_sm,
+          bool no_split)
 {
     if (M <= 0 || N <= 0) return;
     auto ntiles = [&](int bm, int bn) {
@@ -87,7 +88,7 @@ void gemm(Ctx& cx, bool ta, bool tb, int64_t M, int64_t N, int64_t K, double alp
     int64_t tiles = ntiles(bm, bn);
     int nsplit = 1;
     int64_t kchunk = K > 0 ? K : 1;
-    if (K >= 256 && tiles < 2 * cx.num_sms && cx.splitk && ctas_per_sm == 0) {
+    if (K >= 256 && tiles < 2 * cx.num_sms && cx.splitk && ctas_per_sm == 0 && !no_split) {
         int64_t want = cdiv(2 * cx.num_sms, tiles);
         want = imin(want, 32);
         want = imin(want, K / 128);
@@ -97,7 +98,7 @@ void gemm(Ctx& cx, bool ta, bool tb, int64_t M, int64_t N, int64_t K, double alp
             kchunk = cdiv(cdiv(K, want), Cfg2Mid::BK) * Cfg2Mid::BK;
             nsplit = (int)cdiv(K, kchunk);
         }
-    } else if (K >= 4096 && tiles < 8 * 4 * cx.num_sms && cx.splitk && ctas_per_sm == 0 && cfg == 1) {
+    } else if (K >= 4096 && tiles < 8 * 4 * cx.num_sms && cx.splitk && ctas_per_sm == 0 && cfg == 1 && !no_split) {
         // a few waves of long-K tiles (the panel's Gram SYRKs, late-iteration GEMM1): pick the split whose
         // last wave is fullest (4 resident 64x64 CTAs per SM), if it beats no split by > 4 %
         const int64_t slots = 4 * (int64_t)cx.num_sms;

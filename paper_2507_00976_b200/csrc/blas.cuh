@@ -7,8 +7,11 @@ namespace bqrrp {
 // C = alpha op(A) op(B) + beta C (column-major).  tri: only the lower triangle of C is needed.
 // ctas_per_sm > 0: persistent launch of at most ctas_per_sm CTAs per SM looping over the tiles (no
 // split-K).  Not used by the driver (measured slower for the bulk update).
+// no_split: never split K (each element's K order then does not depend on how M / N are tiled or
+// chunked — the sketch uses it so the host entry's chunked sketch is bitwise the device entry's).
 void gemm(Ctx& cx, bool ta, bool tb, int64_t M, int64_t N, int64_t K, double alpha, const double* A, int64_t lda,
-          const double* B, int64_t ldb, double beta, double* C, int64_t ldc, bool tri = false, int ctas_per_sm = 0);
+          const double* B, int64_t ldb, double beta, double* C, int64_t ldc, bool tri = false, int ctas_per_sm = 0,
+          bool no_split = false);
 
 // X op(T) = B, right side, op(T) upper triangular (n x n), in place on B (rows x n).
 //   t_lower = false: T stored upper, op(T) = T;  t_lower = true: T stored lower, op(T) = T^T.

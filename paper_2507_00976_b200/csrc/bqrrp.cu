@@ -253,7 +253,8 @@ static int64_t factor_impl(Ctx& cx, Ctx* cxb, cudaEvent_t ev_top, cudaEvent_t ev
             cudaEvent_t e = hio->event();
             BQ_CUDA(cudaEventRecord(e, hio->h2d));
             BQ_CUDA(cudaStreamWaitEvent(cx.stream, e, 0));
-            gemm(cx, true, false, nc, d, m, 1.0, A + c0 * lda, lda, colscr, m, 0.0, MskT + c0, n);  // MskT rows
+            gemm(cx, true, false, nc, d, m, 1.0, A + c0 * lda, lda, colscr, m, 0.0, MskT + c0, n, false, 0,
+                 /*no_split=*/true);  // MskT rows (no split-K: bitwise the device entry's one-GEMM sketch)
         }
     } else {
         sketch_apply(cx, m, n, A, lda, d, seed, MskT, n, colscr);

@@ -31,7 +31,7 @@ void sketch_apply(Ctx& cx, int64_t m, int64_t n, const double* A, int64_t lda, i
 {
     sketch_operator_T(cx, m, d, seed, St, m);
     // MskT (n x d) = A^T (n x m) * St (m x d)
-    gemm(cx, true, false, n, d, m, 1.0, A, lda, St, m, 0.0, MskT, ldm);
+    gemm(cx, true, false, n, d, m, 1.0, A, lda, St, m, 0.0, MskT, ldm, false, 0, /*no_split=*/true);
 }
 
 }  // namespace bqrrp
