@@ -1,11 +1,13 @@
 // lu.cu — K-LU: partial-pivot LU of the tall w x d sketch transpose, for its pivots
 // (Alg. 2 "Practical wide QRCP": GETRF on the transposed sketch).
 //
-// Recursive right-looking LU.  Leaves are jb-column panels factored by one cooperative kernel: the
-// panel rows are split over G CTAs and held in shared memory; each column step is ONE grid-wide
-// barrier: every CTA publishes its local first-max candidate (|value|, row, full panel row) and the
-// current row j, then all CTAs pick the same winner (largest |value|, lowest row index on ties:
-// IDAMAX, reading Z19), swap and apply the rank-1 update to their own rows.  An exactly-zero pivot
+// Recursive right-looking LU.  Leaves are jb-column panels factored by one kernel launch whose CTAs split
+// the panel rows; per column every CTA offers its local first-max candidate (|value|, row, full panel row),
+// all CTAs pick the same winner (largest |value|, lowest row index on ties: IDAMAX, reading Z19), swap and
+// apply the rank-1 update to their own rows.  Three leaf kernels by active row count:
+// <= 4096 rows a register-resident cluster leaf, <= one 16-CTA cluster's shared memory a shared-memory
+// cluster leaf (both exchange by st.async + mbarrier pushes), larger a cooperative grid leaf (one grid
+// barrier per column, exchange through L2).  An exactly-zero pivot
 // column is skipped (no swap, no scaling; Z18).  Each interchange is applied at once to the whole row
 // of the LU matrix (all d columns, as LAPACK's laswp on both sides would) and to the permutation
 // vector perm (perm = J_qr - 1 of piv_transform), so no separate laswp pass exists and the

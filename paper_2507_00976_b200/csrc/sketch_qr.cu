@@ -3,14 +3,14 @@
 //
 // The sketch lives transposed (MskT, n x d); its trailing window Wsk = MskT(s:n, :)^T is d x w.
 // GPU form (same result in exact arithmetic as QR of the whole d x w matrix):
-//   1. Wq = Wsk(:, 0:p) (d x p, p = min(d, w)), Householder QR by recursive blocking: jb-column leaf
-//      panels factored by one cooperative kernel (rows over G CTAs, one grid barrier per column:
-//      partial norms and partial dot products are published together, reflector convention H of
-//      DESIGN.md Z9/Z20), the leaf also returns its T block (LAPACK larft recurrence); interior
-//      nodes apply Q_left^T to the right half with three DMMA GEMMs and merge T
-//      (T12 = -T11 (V1^T V2) T22).
-//   2. R_sk(:, p:w) = Q_sk^T Wsk(:, p:w), i.e. in the transposed storage
-//      MskT(s+p:n, :) <- MskT(s+p:n, :) - ((MskT(s+p:n, :) V) T) V^T  (three DMMA GEMMs).
+//   1. Wq = Wsk(:, 0:p) (d x p, p = min(d, w)), Householder QR by recursive blocking: 32-column leaf
+//      panels factored by one kernel launch (the register cluster leaf for <= 16 x 256 rows: one row per
+//      thread, partial norms and dot products pushed to every CTA with st.async + mbarrier; otherwise a
+//      shared-memory cluster or cooperative grid leaf; reflector convention H of DESIGN.md Z9/Z20), the
+//      leaf also returns its T block (larft); interior nodes apply Q_left^T to the right half with three
+//      DMMA GEMMs and merge T (T12 = -T11 (V1^T V2) T22).
+//   2. R_sk(:, p:w)^T = Wsk(:, p:w)^T Q_sk with Q_sk = I - V T V^T formed explicitly: ONE DMMA GEMM
+//      (optionally deferred to a second stream, or restricted to this rank's row blocks).
 //   3. R_sk(:, 0:p)^T (upper trapezoidal, explicit zeros) is written back to MskT(s:s+p, :).
 #include <cooperative_groups.h>
 #include <cstdlib>
