@@ -439,3 +439,37 @@ def test_lookahead_and_serial_schedules_agree(gpu):
     assert rh == r1
     assert np.array_equal(Ah_out.numpy(), _host(Ag1)) and np.array_equal(tauh.numpy(), _host(tau1))
     assert np.array_equal(Jh.numpy(), _host(J1))
+
+
+@pytest.mark.parametrize("shape,b,d,exact_j", [((1, 100), 1, 1, True), ((100, 1), 8, 8, True), ((40, 300), 16, 40, False),
+                                               ((333, 77), 100, 120, True), ((257, 257), 64, 64, True),
+                                               ((130, 129), 128, 130, True), ((64, 1000), 64, 64, True)])
+def test_factor_degenerate_shapes_match_oracle(gpu, shape, b, d, exact_j):
+    """Degenerate and ragged shapes (P:241-242 notation): a single row (d = m = 1), a single column (n < b),
+    d = m (the sketch is the whole row space), b > n (one ragged block), a last block of ONE column
+    (257 = 4 * 64 + 1, 129 = 128 + 1), and a wide matrix whose loop ends after one block (m = b).
+    40 x 300 with d = 40: the last iteration has h = 8 trailing rows, so the updated sketch has rank <= 8 and
+    its LU pivots 9..40 are decided on rounding noise; they only permute columns beyond l = m, so there J(:l)
+    and R(:l, :) column by column are what is unique (GEQP3 format leaves the order after l free)."""
+    m, n = shape
+    A = inputs.gaussian(m, n, seed=m + 7 * n)
+    out_o, g = _run_both(A, b, d, seed=0)
+    assert out_o.min_margin > 1e-10
+    _compare(out_o, g, exact_j=exact_j)
+    res = oracle.residual(A, oracle.OracleResult(g[0], g[1], g[2], g[3], None, 0, None))
+    assert res <= 1e-13
+
+
+def test_factor_duplicate_and_zero_columns(gpu):
+    """Exactly dependent columns (a duplicate, a multiple, a zero column): the rank is n - 3 on both sides,
+    J(:l) and R(:l, :) agree (the order of the three dependent columns after l is decided on rounding noise,
+    so only its being a permutation is checked)."""
+    A = inputs.gaussian(300, 200, seed=5)
+    A[:, 17] = A[:, 5]
+    A[:, 9] = 0.0
+    A[:, 150] = 2.0 * A[:, 40]
+    out_o, g = _run_both(A, 64, 80, seed=0)
+    assert out_o.rank == 197
+    _compare(out_o, g, exact_j=False)
+    res = oracle.residual(A, oracle.OracleResult(g[0], g[1], g[2], g[3], None, 0, None))
+    assert res <= 1e-13
