@@ -473,3 +473,47 @@ def test_factor_duplicate_and_zero_columns(gpu):
     _compare(out_o, g, exact_j=False)
     res = oracle.residual(A, oracle.OracleResult(g[0], g[1], g[2], g[3], None, 0, None))
     assert res <= 1e-13
+
+
+@pytest.mark.parametrize("pad", [1, 37])
+def test_factor_padded_lda_matches_unpadded(gpu, pad):
+    """The C ABI takes A with a leading dimension lda >= m (GEQP3 argument convention): a view
+    into a taller column-major buffer (lda = m + pad; odd lda also disables the 16-byte vector loads of the
+    GEMM engine) gives the bitwise-same factorization as the dense lda = m call, and the padding rows are
+    left untouched."""
+    import torch
+
+    bq = _bq()
+    m, n, b, d = 700, 650, 128, 160
+    A = inputs.gaussian(m, n, seed=21)
+    Ad, taud, Jd, rd = bq.factor(_dev(A), b, d, seed=3)
+    big = np.full((m + pad, n), 7.25)
+    big[:m] = A
+    Bt = _dev(big)
+    view = Bt[:m]
+    assert view.stride() == (1, m + pad)
+    Ap, taup, Jp, rp = bq.factor(view, b, d, seed=3)
+    assert rp == rd
+    assert torch.equal(Jp, Jd) and torch.equal(taup, taud)
+    assert np.array_equal(_host(Ap), _host(Ad))
+    assert np.all(_host(Bt)[m:] == 7.25)
+
+
+def test_factor_on_caller_stream(gpu):
+    """The C ABI runs on the caller's stream (its internal streams fork from and join back to it): a
+    factorization issued on a non-default torch stream, with the input produced on that same stream just
+    before the call, equals the default-stream result bitwise."""
+    import torch
+
+    bq = _bq()
+    A = inputs.gaussian(900, 900, seed=5)
+    Ad, taud, Jd, rd = bq.factor(_dev(A), 128, 128, seed=1)
+    src = _dev(A)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        X = src.t().contiguous().t()  # produced on s, consumed by the library on s
+        Xs, taus, Js, rs = bq.factor(X, 128, 128, seed=1)
+    s.synchronize()
+    assert rs == rd and torch.equal(Js, Jd) and torch.equal(taus, taud)
+    assert torch.equal(Xs, Ad)
