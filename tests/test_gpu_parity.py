@@ -109,8 +109,11 @@ def test_sketch_integer_inputs_exact(gpu):
 
 
 # ----------------------------------------------------------------------------- a2 LU pivots
-@pytest.mark.parametrize("w,d", [(300, 64), (1000, 160), (5000, 300), (200, 200), (150, 400), (20000, 96)])
+@pytest.mark.parametrize("w,d", [(300, 64), (1000, 160), (5000, 300), (200, 200), (150, 400), (20000, 96),
+                                 (40000, 64), (70001, 100)])
 def test_lu_pivots_match_oracle(gpu, w, d):
+    """Every leaf regime of K-LU: the register cluster leaf (<= 4096 rows), the shared-memory cluster leaf
+    (<= ~25k rows), and the cooperative grid leaf (40000, 70001 rows: the C3 regime, ragged row count)."""
     bq = _bq()
     L = inputs.gaussian(w, d, seed=w + d)
     _, ipiv_o, margin = oracle.getf2(L)
