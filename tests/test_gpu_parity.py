@@ -140,8 +140,11 @@ def test_lu_zero_and_tied_columns(gpu):
 
 
 # ----------------------------------------------------------------------------- a2 sketch QR
-@pytest.mark.parametrize("w,d", [(1000, 160), (64, 64), (300, 100), (50, 80), (4000, 512)])
+@pytest.mark.parametrize("w,d", [(1000, 160), (64, 64), (300, 100), (50, 80), (4000, 512), (3000, 1500),
+                                 (2100, 2048)])
 def test_sketch_qr_matches_oracle(gpu, w, d):
+    """K-SQR up to the C3 sketch depth (d = 2048: the full recursion over register cluster leaves) and a
+    ragged d = 1500."""
     bq = _bq()
     WT = inputs.gaussian(w, d, seed=w * d)
     F, _ = oracle.house_qr(WT.T)  # d x w, convention H
