@@ -172,7 +172,8 @@ def test_permute_bitexact(gpu, rows, w, nlu):
 
 
 # ----------------------------------------------------------------------------- a4/a5 panel
-@pytest.mark.parametrize("h,k,t", [(256, 32, 40), (1000, 100, 0), (3000, 128, 200), (129, 129, 3)])
+@pytest.mark.parametrize("h,k,t", [(256, 32, 40), (1000, 100, 0), (3000, 128, 200), (129, 129, 3), (8192, 1024, 64),
+                                   (65536, 256, 0)])
 @pytest.mark.parametrize("passes", [0, 1, 2])
 def test_panel_matches_householder_oracle(gpu, h, k, t, passes):
     """c.1: CholQR + reconstruction gives the unique (V, tau, R) with tau in [1,2] = convention-H QR."""
