@@ -5,6 +5,7 @@ b and d), where the oracle cannot run end to end:
   * properties that hold at any size: J a permutation, rank = min(m, n) on Gaussian inputs, tau in [1, 2],
     residual ||A(:,J) X - Q R X|| / ||A(:,J) X|| and orthogonality ||Q^T Q X - X|| / ||X|| for random X
     (estimators of the north-star bounds, readings Z24/Z25);
+  * column norms: ||R(0:j+1, j)|| = ||A(:, J(j))|| at sampled j (Q orthogonal), each side summed exactly;
   * bitwise determinism of two full factorizations.
 """
 import math
@@ -62,6 +63,15 @@ def _check_properties(A0, A, tau, J, rank, nvec=4, tol_res=1e-13, tol_orth=None)
     if tol_orth is None:
         tol_orth = 1e-13 * max(1.0, rank / 1024.0)  # Z24: literal up to 1024, size-scaled beyond
     assert orth <= tol_orth, orth
+    # column by column (sampled): Q is orthogonal, so ||R(0:j+1, j)|| = ||A(:, J(j))|| for every j of a
+    # full-rank factorization -- each side summed exactly (fsum) from its own column
+    if rank == m:
+        rng = np.random.default_rng(7)
+        for j in sorted(set(int(x) for x in rng.integers(0, n, 24)) | {0, n - 1}):
+            rj = A[:min(j + 1, m), j].cpu().numpy()
+            aj = A0[:, int(Jh[j]) - 1].cpu().numpy()
+            nr, na = math.sqrt(math.fsum(rj * rj)), math.sqrt(math.fsum(aj * aj))
+            assert abs(nr - na) <= 1e-12 * na, (j, nr, na)
     return res, orth
 
 
