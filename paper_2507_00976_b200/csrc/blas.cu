@@ -88,7 +88,29 @@ void gemm(Ctx& cx, bool ta, bool tb, int64_t M, int64_t N, int64_t K, double alp
     int64_t tiles = ntiles(bm, bn);
     int nsplit = 1;
     int64_t kchunk = K > 0 ? K : 1;
-    if (K >= 256 && tiles < 2 * cx.num_sms && cx.splitk && ctas_per_sm == 0 && !no_split) {
+    static int deep = -1;
+    if (deep < 0) {
+        const char* e = std::getenv("BQRRP_DEEP_SPLIT");  // 0: off (A/B experiments)
+        deep = (e && e[0] == '0') ? 0 : 1;
+    }
+    if (deep && K >= 32768 && ntiles(Cfg2Mid::BM, Cfg2Mid::BN) < cx.num_sms && cx.splitk && ctas_per_sm == 0 &&
+        !no_split) {
+        // few output tiles over a very long K (the panel Grams of tall, narrow panels: C4's 262144 x 512):
+        // 64x64 tiles split into K-chunks of >= 2048 rows, ~2 waves of 4 resident CTAs per SM.  The 64x32
+        // two-wave split below left these HBM-bound (every tile pair re-streams its K range: 25.8 GB for one
+        // 262144 x 512 Gram); consecutive CTAs here share a K-chunk, so the chunk is read from L2.
+        cfg = 1;
+        bm = Cfg2Mid::BM;
+        bn = Cfg2Mid::BN;
+        tiles = ntiles(bm, bn);
+        int64_t sp = cdiv(8 * (int64_t)cx.num_sms, tiles);
+        sp = imin(sp, imin(K / 2048, (int64_t)64));
+        sp = imin(sp, (int64_t)(cx.splitk_elems / (size_t)(M * N)));
+        if (sp >= 2) {
+            kchunk = cdiv(cdiv(K, sp), Cfg2Mid::BK) * Cfg2Mid::BK;
+            nsplit = (int)cdiv(K, kchunk);
+        }
+    } else if (K >= 256 && tiles < 2 * cx.num_sms && cx.splitk && ctas_per_sm == 0 && !no_split) {
         int64_t want = cdiv(2 * cx.num_sms, tiles);
         want = imin(want, 32);
         want = imin(want, K / 128);
