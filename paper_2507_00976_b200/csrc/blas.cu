@@ -93,12 +93,12 @@ void gemm(Ctx& cx, bool ta, bool tb, int64_t M, int64_t N, int64_t K, double alp
         const char* e = std::getenv("BQRRP_DEEP_SPLIT");  // 0: off (A/B experiments)
         deep = (e && e[0] == '0') ? 0 : 1;
     }
-    if (deep && K >= 32768 && ntiles(Cfg2Mid::BM, Cfg2Mid::BN) < cx.num_sms && cx.splitk && ctas_per_sm == 0 &&
+    if (deep && K >= 8192 && ntiles(Cfg2Mid::BM, Cfg2Mid::BN) < cx.num_sms && cx.splitk && ctas_per_sm == 0 &&
         !no_split) {
-        // few output tiles over a very long K (the panel Grams of tall, narrow panels: C4's 262144 x 512):
-        // 64x64 tiles split into K-chunks of >= 2048 rows, ~2 waves of 4 resident CTAs per SM.  The 64x32
-        // two-wave split below left these HBM-bound (every tile pair re-streams its K range: 25.8 GB for one
-        // 262144 x 512 Gram); consecutive CTAs here share a K-chunk, so the chunk is read from L2.
+        // few output tiles over a long K (the panel Grams of tall, narrow panels: C4's 262144 x 512, C2's
+        // 16384 x 1024): 64x64 tiles split into K-chunks of >= 2048 rows, ~2 waves of 4 resident CTAs per
+        // SM.  The 64x32 two-wave split below left these HBM-bound (every tile pair re-streams its K range:
+        // 25.8 GB for one 262144 x 512 Gram); consecutive CTAs here share a K-chunk, read from L2.
         cfg = 1;
         bm = Cfg2Mid::BM;
         bn = Cfg2Mid::BN;
