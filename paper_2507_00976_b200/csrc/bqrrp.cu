@@ -139,7 +139,10 @@ static Layout layout(int64_t m, int64_t n, int64_t b, int64_t d)
     size_t pn = r(bb * bb) * 8 + r(bb) + r((size_t)cdiv((int64_t)bb, 64) * 4096 + 4096);  // + TRSM Dinv
     size_t T = sq > pn ? sq : pn;
     T = T > lu ? T : lu;
-    size_t sk = r((size_t)16 * (p > bb ? p * p : bb * bb) + (size_t)4 * 1024 * 1024);
+    // split-K partials: 16 slices of the largest square product, plus 4 slices of a b x n GEMM1 output so
+    // the wave-efficiency split of few-wave W = V^T C calls is not capped by the buffer (C4: 25.9 TFLOP/s
+    // at split 1 for 512 x 3584 x 258048, where 5 slices fill the last wave)
+    size_t sk = r((size_t)16 * (p > bb ? p * p : bb * bb) + (size_t)4 * 1024 * 1024 + (size_t)4 * bb * (size_t)n);
     Layout L{P, T, sk, P + T + sk + (1u << 20)};
     return L;
 }
