@@ -92,3 +92,15 @@ def test_step_entry_argument_checks_without_gpu():
     # split trailing update
     assert L.bqrrp_step_wy_top(8, 4, 4, dummy, dummy, dummy, 8, None, 4, None) == -9  # no W2
     assert L.bqrrp_step_wy_bulk(8, 4, 4, dummy, dummy, 2, dummy, 8, None) == -6       # ldw < k
+
+
+def test_missing_library_fails_loudly(monkeypatch):
+    """No CPU fallback: without the CUDA library the binding raises instead of computing anything."""
+    import paper_2507_00976_b200 as bq
+
+    monkeypatch.setattr(bq, "_lib", None)
+    monkeypatch.setattr(bq, "_LIB_PATH", "/nonexistent/libbqrrp.so")
+    with pytest.raises(ImportError):
+        bq.lib()
+    with pytest.raises(ImportError):
+        bq.workspace_query(64, 64, 16, 16)
