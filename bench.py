@@ -56,8 +56,9 @@ def canonical_flops(m: int, n: int) -> float:
 
 
 def trailing_update_flops(m: int, n: int, b: int) -> float:
-    """Algorithmic flops of the a5 compact-WY update over a full-rank run: per iteration
-    GEMM1 2hkt + TRMM-as-GEMM 2k^2 t + GEMM2 2hkt (h = m-s, k = b, t = n-s-k)."""
+    """Algorithmic flops of the a5 compact-WY update over a full-rank run: per
+    iteration GEMM1 2hkt + the TRMM W2 = T^T W k^2 t (T triangular; the kernel skips the zero half) + GEMM2
+    2hkt (h = m-s, k = b, t = n-s-k)."""
     tot = 0.0
     s = 0
     mn = min(m, n)
@@ -65,7 +66,7 @@ def trailing_update_flops(m: int, n: int, b: int) -> float:
         k = min(b, mn - s)
         h, t = m - s, n - s - k
         if t > 0:
-            tot += 4.0 * h * k * t + 2.0 * k * k * t
+            tot += 4.0 * h * k * t + 1.0 * k * k * t
         s += b
     return tot
 
@@ -370,9 +371,12 @@ def run_distributed(args, cfg, world, rank, local, dev):
 
     import inputs
     import paper_2507_00976_b200 as bq
-    from paper_2507_00976_b200.dist import factor_dist, local_columns
+    from paper_2507_00976_b200.dist import comm_nccl, comm_torch, factor_dist, local_columns
 
     m, n, b, d = cfg["m"], cfg["n"], cfg["b"], cfg["d"]
+    # the library's own communicator: an NCCL clique (bqrrp_comm_init) on the GPU box, a torch.distributed
+    # transport for the gloo tests that share one GPU
+    comm = comm_nccl() if args.backend == "nccl" else comm_torch()
     stream = torch.cuda.current_stream()
     A_full = inputs.gaussian_cuda(m, n, seed=args.seed, device=dev)  # identical on every rank
     A_loc0, bc = local_columns(A_full, b, world, rank)
@@ -381,7 +385,7 @@ def run_distributed(args, cfg, world, rank, local, dev):
     A_loc = torch.empty_like(A_loc0.t()).t()
 
     def step():
-        return factor_dist(A_loc, m, n, b, d, seed=args.seed)
+        return factor_dist(A_loc, m, n, b, d, seed=args.seed, comm=comm)
 
     for _ in range(args.warmup):
         A_loc.copy_(A_loc0)
@@ -435,7 +439,8 @@ def run_distributed(args, cfg, world, rank, local, dev):
             "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"{args.config} {cfg['desc']}", "m": m, "n": n, "b": b, "d": d,
-                       "parallelism": f"block-cyclic columns over {world} GPUs (dist_nb = b)",
+                       "parallelism": f"block-cyclic columns over {world} GPUs (dist_nb = b), bqrrp_factor_dist "
+                                      f"({'NCCL' if args.backend == 'nccl' else args.backend})",
                        "l2": "inputs larger than L2", "rank_found": out[3],
                        "timing": "per-step CUDA events around factor_dist, max over ranks"},
             "pct_fp64_peak": 100.0 * per_gpu / peak,
@@ -446,6 +451,7 @@ def run_distributed(args, cfg, world, rank, local, dev):
             "cpu_baseline": None, "e2e": e2e, "gpu_launches": launches, "clocks": clk.summary(),
         }
         print(json.dumps(line))
+    comm.destroy()
     dist.destroy_process_group()
     return 0
 

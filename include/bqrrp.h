@@ -59,7 +59,19 @@ typedef struct bqrrp_options {
      * update and the next pivot selection.  1: everything on one stream, serialised (the
      * per-phase times then partition the whole step; used to measure each phase alone). */
     int no_lookahead;
+    /* bqrrp_factor_dist only: width of the 1-D block-cyclic column blocks;
+     * <= 0 selects b.  Must divide b or be a multiple of it (so each panel lives on one rank). */
+    int64_t dist_nb;
+    /* Test hooks, 0 in production.  BQRRP_DEBUG_FORCE_BREAKDOWN: every panel reports a POTRF breakdown, so the
+     * Householder fallback (or, with no_hqr_fallback, BQRRP_ENUMERIC) is exercised deterministically. */
+    int debug_flags;
+    /* bqrrp_factor_dist only.  BQRRP_DIST_SHARD_PANEL: the panel's rows are split over min(G, h/k) ranks (the
+     * k x k factors replicated from all-reduced Gram matrices; SURVEY §8(e) phase 2 item 3) instead of being
+     * factored by the panel's owner.  Off (default), the result is bitwise the one-GPU bqrrp_factor's. */
+    int dist_flags;
 } bqrrp_options;
+#define BQRRP_DEBUG_FORCE_BREAKDOWN 1
+#define BQRRP_DIST_SHARD_PANEL 1
 
 /* Bytes of device workspace bqrrp_factor needs for an m x n matrix with block b and sketch d. */
 int bqrrp_workspace_query(int64_t m, int64_t n, int64_t b, int64_t d, size_t* bytes);
@@ -131,86 +143,67 @@ int bqrrp_debug_permute(int64_t rows, int64_t w, double* X, int64_t ldx, int64_t
 int bqrrp_debug_panel(int64_t h, int64_t k, int64_t t, double* P, int64_t ld, const double* Rsk11, double* tau,
                       int cholqr_passes, void* stream);
 
-/* ---- multi-GPU step entry points (driven by paper_2507_00976_b200/dist.py) ----
- * A is distributed 1-D block-cyclically over column positions (block width dist_nb = b); the transposed
- * sketch MskT (n x d) and J are replicated; the caller moves data between ranks (torch.distributed:
- * NCCL all-reduce / broadcast on a multi-GPU node).  All pointers device, all calls stream-ordered. */
+/* ---- multi-GPU -----------------------------------------------------------
+ * One process per GPU.  A is distributed 1-D block-cyclically over column POSITIONS: position p (0-based) lives on
+ * rank (p / nb) mod G, nb = opts->dist_nb (default b; nb must be a multiple of b, so each panel lives on one rank),
+ * as local column (p / (nb G)) nb + p mod nb of that rank's A_local.  Pivoted columns move to the rank owning the
+ * position they are assigned.  The collectives (P:1099-1165 distributed analogue): an
+ * all-gather of the sketch rows (a1, and after every sample update), the column all-to-all-v of the touched set
+ * (a3), a broadcast of the panel's V, T, tau (a4) and of R11 (a6), plus one 3-double all-reduce of flags per
+ * iteration.  They run on NCCL (bqrrp_comm_init) or on a caller transport (bqrrp_comm_init_transport). */
 
-/* a2 on the replicated sketch window MskT(s:n, :): LU pivots, J_qr touched set (tq[t] <- tsrc[t],
- * positions relative to s, *nt entries in unspecified order, capacity 2 min(n-s, d)), sketch rows and J(s:n) permuted
- * (J may be NULL), R_sk in place, k = tri_rank (ref = |R_sk(0,0)| stored when first).
- * Synchronises the stream; *k_out host. */
-int bqrrp_step_pivots(int64_t n, int64_t d, int64_t s, int64_t kmax, double* MskT, int64_t ldm, int64_t* J,
-                      double rank_tol, double* ref, int first, int* tq, int* tsrc, int* nt, int64_t* k_out,
-                      void* stream);
-/* dst(:, t) = X(:, idx[t]) (rows x n_idx), slots with idx[t] < 0 untouched. */
-int bqrrp_step_gather_columns(int64_t rows, const double* X, int64_t ldx, const int* idx, int64_t nidx, double* dst,
-                              int64_t ldd, void* stream);
-/* X(:, idx[t]) = src(:, t), slots with idx[t] < 0 skipped. */
-int bqrrp_step_scatter_columns(int64_t rows, double* X, int64_t ldx, const int* idx, int64_t nidx, const double* src,
-                               int64_t lds, void* stream);
-/* *is_zero_host = 1 iff col(0:h) is all zeros (the P:1008 early exit).  Synchronises. */
-int bqrrp_step_zero_column_check(int64_t h, const double* col, int* is_zero_host, void* stream);
-/* a4 on the owner of the panel: P (h x k, ldp) in place in GEQP3 format, tau (k), explicit V (h x k, ld h)
- * and T (k x k); R_sk11 read from the sketch window MskT_s (= MskT + s).  BQRRP_ENUMERIC on breakdown. */
-int bqrrp_step_panel(int64_t h, int64_t k, double* P, int64_t ldp, const double* MskT_s, int64_t ldm, double* tau,
-                     double* V, double* T, int cholqr_passes, void* stream);
-/* a5 on one rank's trailing columns: C (h x t, ldc) <- C - V T^T (V^T C). */
-int bqrrp_step_wy_update(int64_t h, int64_t k, int64_t t, const double* V, const double* T, double* C, int64_t ldc,
-                         void* stream);
-/* Row-distributed sketch: as bqrrp_step_pivots, but the rows of R_sk(:, d:w) (the d x d
- * QR's GEMM part) are computed only for the row blocks listed (host arrays; offsets counted from
- * window row min(d, w), i.e. position s + d): this rank's positions.  The other rows of MskT are left stale and
- * must be refreshed (all-gather) before the next pivot selection reads them. */
-int bqrrp_step_pivots_rows(int64_t n, int64_t d, int64_t s, int64_t kmax, double* MskT, int64_t ldm, int64_t* J,
-                           double rank_tol, double* ref, int first, int* tq, int* tsrc, int* nt, int64_t* k_out,
-                           const int64_t* row_off, const int64_t* row_len, int64_t n_rows, void* stream);
-/* a6 on this rank's positions only: X = R_sk11 R11^{-1}; for block j: MskT_s(b + pos_off[j] .. + len[j], 0:b)
- * -= R12(:, col_off[j] ..)^T X^T with R12 this rank's k x t_loc top rows (host arrays). */
-int bqrrp_step_sample_update_rows(int64_t b, const double* R11, int64_t ldr, const double* R12, int64_t ld12,
-                                  double* MskT_s, int64_t ldm, const int64_t* pos_off, const int64_t* col_off,
-                                  const int64_t* len, int64_t nblk, void* stream);
-/* a4 row-sharded (SURVEY §8(e) phase 2 item 3): each rank holds a block of the panel's rows
- * (column-major, rows x k); the k x k pieces are computed redundantly from all-reduced Gram matrices.
- * Preconditioning + first Gram (Alg. 3 cholqr:precond): Q = P R_sk11^{-1} (R_sk11 = R_sk(0:k,0:k) read
- * from MskT_s), G = Q^T Q (lower, k x k, ld k; zero when rows == 0).  P may equal Q (ldp == ldq). */
-int bqrrp_step_cholqr_pre(int64_t rows, int64_t k, const double* P, int64_t ldp, const double* MskT_s, int64_t ldm,
-                          double* Q, int64_t ldq, double* G, void* stream);
-/* Lower Cholesky of the (all-reduced) Gram G in place, upper part zeroed.  Synchronises; BQRRP_ENUMERIC on a
- * non-positive pivot (the caller then factors the panel with the Householder variant). */
-int bqrrp_step_potrf(int64_t k, double* G, int64_t ldg, void* stream);
-/* Second CholQR pass on a row block: Q <- Q C^{-T}, G = Q^T Q (lower; zero when rows == 0). */
-int bqrrp_step_cholqr_pass(int64_t rows, int64_t k, double* Q, int64_t ldq, const double* C, double* G, void* stream);
-/* Householder reconstruction (Alg. 3 cholqr:orhr_col) on the block holding the panel's top k rows:
- * Wr = Q_top C^{-T} (k x k, ld k) factored in place as L \ U with S_jj = -sgn (S: k values). */
-int bqrrp_step_recon_top(int64_t k, const double* Qtop, int64_t ldq, const double* C, double* Wr, double* S,
-                         void* stream);
-/* Y2 rows: Q <- Q (U C^T)^{-1} for a block of rows below the top k (U from Wr). */
-int bqrrp_step_recon_rows(int64_t rows, int64_t k, double* Q, int64_t ldq, const double* Wr, const double* C,
-                          void* stream);
-/* k x k results: T = -U S L^{-T} (compact WY), tau = diag(T), R = C2^T C1^T R_sk11 (C2 may be NULL for one
- * pass; R11 = S R). */
-int bqrrp_step_recon_finish(int64_t k, const double* Wr, const double* S, const double* C1, const double* C2,
-                            const double* MskT_s, int64_t ldm, double* T, double* tau, double* R, void* stream);
-/* top != 0: the first k rows of the block become the explicit unit-lower V rows of L (from Wr). */
-int bqrrp_step_v_rows(int64_t rows, int64_t k, double* Q, int64_t ldq, const double* Wr, int top, void* stream);
-/* GEQP3 write of the panel A (h x k, lda): S R on and above the diagonal, V (explicit, h x k, ldv) below. */
-int bqrrp_step_write_panel(int64_t h, int64_t k, double* V, int64_t ldv, const double* R, const double* S, double* A,
-                           int64_t lda, void* stream);
-/* a5 split for the lookahead (DESIGN.md §7.5 / §8.1): bqrrp_step_wy_top computes W2 = T^T (V^T C) into the
- * caller's W2 (k x t, ldw >= k; it must stay alive until the bulk call has run) and applies C -= V W2 to rows
- * 0:k (R12) only; bqrrp_step_wy_bulk applies rows k:h, typically on a second stream ordered after the top call.
- * Together they equal bqrrp_step_wy_update. */
-int bqrrp_step_wy_top(int64_t h, int64_t k, int64_t t, const double* V, const double* T, double* C, int64_t ldc,
-                      double* W2, int64_t ldw, void* stream);
-int bqrrp_step_wy_bulk(int64_t h, int64_t k, int64_t t, const double* V, const double* W2, int64_t ldw, double* C,
-                       int64_t ldc, void* stream);
-/* a6 on the replicated sketch: X = R_sk11 R11^{-1} (R_sk11 from MskT_s), MskT_s(b:b+t, 0:b) -= R12^T X^T with
- * R11 (b x b, ldr) and R12 (b x t, ld12) gathered in position order. */
-int bqrrp_step_sample_update(int64_t b, int64_t t, const double* R11, int64_t ldr, const double* R12, int64_t ld12,
-                             double* MskT_s, int64_t ldm, void* stream);
-/* X(0:rows, 0:cols) = 0. */
-int bqrrp_step_zero(int64_t rows, int64_t cols, double* X, int64_t ldx, void* stream);
+/* Writes the 128-byte ncclUniqueId of a new NCCL clique into id_out (rank 0; the caller broadcasts it, e.g. with
+ * torch.distributed).  NCCL is the process's libnccl.so.2 (dlopen'ed; normally the one torch loaded).
+ * BQRRP_ENCCL if NCCL is unavailable. */
+int bqrrp_nccl_unique_id(void* id_out);
+/* Joins the clique as `rank` of `nranks` on the current CUDA device (collective: every rank calls it).  *comm_out
+ * is an opaque handle owned by the caller until bqrrp_comm_destroy.  BQRRP_ENCCL on NCCL failure. */
+int bqrrp_comm_init(const void* nccl_unique_id, int rank, int nranks, void** comm_out);
+/* Caller-supplied transport (e.g. torch.distributed over gloo in tests).  Every callback gets device buffers and
+ * the stream (already synchronised by the library) and must have moved the bytes when it returns 0:
+ *   allreduce_sum_f64: buf <- sum over ranks (count doubles);  allgather: recv = nranks blocks of `bytes`, rank
+ *   order;  broadcast: `bytes` from root;  alltoallv: per peer byte counts / displacements (nranks entries each,
+ *   the own entry is 0). */
+typedef struct bqrrp_transport {
+    void* ctx;
+    int rank, nranks;
+    int (*allreduce_sum_f64)(void* ctx, double* buf, size_t count, void* stream);
+    int (*allgather)(void* ctx, const void* send, void* recv, size_t bytes, void* stream);
+    int (*broadcast)(void* ctx, void* buf, size_t bytes, int root, void* stream);
+    int (*alltoallv)(void* ctx, const void* send, const size_t* send_bytes, const size_t* send_displs, void* recv,
+                     const size_t* recv_bytes, const size_t* recv_displs, void* stream);
+} bqrrp_transport;
+int bqrrp_comm_init_transport(const bqrrp_transport* transport, void** comm_out);
+/* Releases a handle of bqrrp_comm_init / _init_transport (NULL is a no-op). */
+int bqrrp_comm_destroy(void* comm);
+
+/* Number of columns rank `rank` holds of an n-column matrix in the layout above (host only). */
+int bqrrp_dist_local_columns(int64_t n, int64_t nb, int nranks, int rank, int64_t* n_local);
+/* Device workspace bytes of bqrrp_factor_dist for the largest rank share (host only). */
+int bqrrp_workspace_query_dist(int64_t m, int64_t n, int64_t b, int64_t d, int nranks, int64_t dist_nb, size_t* bytes);
+/* The a3 exchange plan of one rank (host only; exposed for tests): the nt touched positions move p[t] -> q[t]
+ * (0-based).  Slots are taken in ascending q.  send_idx: this rank's local source columns sent to other ranks,
+ * grouped by destination rank (send_counts[r] each); recv_idx: local destination columns received, grouped by
+ * source rank (recv_counts[r]); local_src -> local_dst: moves within this rank (*n_local_moves).  Output arrays
+ * have room for nt entries (counts: nranks). */
+int bqrrp_dist_exchange_plan(int64_t n, int64_t nb, int nranks, int rank, int64_t nt, const int64_t* q,
+                             const int64_t* p, int32_t* send_idx, int64_t* send_counts, int32_t* recv_idx,
+                             int64_t* recv_counts, int32_t* local_src, int32_t* local_dst, int64_t* n_local_moves);
+
+/*
+ * Distributed BQRRP (collective: every rank of `comm` calls it with the same m, n, b, d, seed, opts).
+ *   A_local   device, m x n_local (bqrrp_dist_local_columns), lda_local >= max(1, m): this rank's columns in the
+ *             layout above; overwritten with the same GEQP3 content as bqrrp_factor's A in those columns
+ *   tau, J    device, replicated on every rank (min(m, n) doubles; n int64, one-based gather)
+ *   rank      host out: l, identical on every rank
+ *   workspace device (>= bqrrp_workspace_query_dist bytes) or NULL (library pool)
+ * Returns as bqrrp_factor_ex (+ BQRRP_ENCCL; -11 comm NULL, -15 dist_nb not a multiple of b).  Synchronises the
+ * stream a few times per iteration (the block rank k, the touched set for the exchange plan, the flags).  With
+ * dist_flags = 0 the output is bitwise bqrrp_factor_ex's on the whole matrix (tests/test_dist.py).
+ */
+int bqrrp_factor_dist(int64_t m, int64_t n, double* A_local, int64_t lda_local, int64_t b, int64_t d, uint64_t seed,
+                      double* tau, int64_t* J, int64_t* rank, void* comm, void* workspace, size_t ws_bytes,
+                      void* stream, const bqrrp_options* opts);
 
 /* Number of CUDA kernels this library has launched in the calling process (all threads). */
 unsigned long long bqrrp_launch_count(void);

@@ -32,7 +32,8 @@ class BqrrpError(RuntimeError):
 
 class Options(ctypes.Structure):
     _fields_ = [("rank_tol", ctypes.c_double), ("cholqr_passes", ctypes.c_int), ("no_hqr_fallback", ctypes.c_int),
-                ("phase_ms", ctypes.POINTER(ctypes.c_float)), ("no_lookahead", ctypes.c_int)]
+                ("phase_ms", ctypes.POINTER(ctypes.c_float)), ("no_lookahead", ctypes.c_int),
+                ("dist_nb", ctypes.c_int64), ("debug_flags", ctypes.c_int), ("dist_flags", ctypes.c_int)]
 
 
 def lib() -> ctypes.CDLL:
@@ -112,8 +113,11 @@ def workspace_query(m: int, n: int, b: int, d: int) -> int:
     return int(out.value)
 
 
-def _options(rank_tol, cholqr_passes, phases, hqr_fallback=True, lookahead=True):
+def _options(rank_tol, cholqr_passes, phases, hqr_fallback=True, lookahead=True, debug_force_breakdown=False,
+             dist_nb=0):
     o = Options()
+    o.dist_nb = int(dist_nb)
+    o.debug_flags = 1 if debug_force_breakdown else 0
     o.no_lookahead = 0 if lookahead else 1
     o.rank_tol = float(rank_tol) if rank_tol else 0.0
     o.cholqr_passes = int(cholqr_passes)
@@ -123,7 +127,8 @@ def _options(rank_tol, cholqr_passes, phases, hqr_fallback=True, lookahead=True)
 
 
 def factor(A, b: int, d: int | None = None, seed: int = 0, rank_tol: float | None = None, cholqr_passes: int = 2,
-           workspace=None, tau=None, J=None, stream=None, phase_times: bool = False, hqr_fallback: bool = True, lookahead: bool = True):
+           workspace=None, tau=None, J=None, stream=None, phase_times: bool = False, hqr_fallback: bool = True,
+           lookahead: bool = True, debug_force_breakdown: bool = False):
     """BQRRP of A in place (Alg. 1); returns (A, tau, J, rank[, phase_ms dict]).
 
     A: float64 CUDA tensor in column-major layout (m x n); overwritten in GEQP3 format.
@@ -131,6 +136,7 @@ def factor(A, b: int, d: int | None = None, seed: int = 0, rank_tol: float | Non
     hqr_fallback: a panel whose Cholesky QR breaks down is re-factored by Householder QR (else
     BqrrpError status 1); panel_fallbacks() counts them.
     lookahead: False runs every step on one stream (phase times then measure each step alone).
+    debug_force_breakdown: test hook (bqrrp_options.debug_flags): every panel reports a CholQR breakdown.
     """
     import torch
 
@@ -147,7 +153,7 @@ def factor(A, b: int, d: int | None = None, seed: int = 0, rank_tol: float | Non
         ws_ptr, ws_bytes = ctypes.c_void_p(workspace.data_ptr()), workspace.numel() * workspace.element_size()
     rank = ctypes.c_int64(0)
     phases = (ctypes.c_float * len(PHASES))() if phase_times else None
-    opts = _options(rank_tol, cholqr_passes, phases, hqr_fallback, lookahead)
+    opts = _options(rank_tol, cholqr_passes, phases, hqr_fallback, lookahead, debug_force_breakdown)
     st = lib().bqrrp_factor_ex(m, n, ctypes.c_void_p(A.data_ptr()), lda, b, d, seed, ctypes.c_void_p(tau.data_ptr()),
                                ctypes.c_void_p(J.data_ptr()), ctypes.byref(rank), ws_ptr, ws_bytes,
                                _stream_ptr(stream), ctypes.byref(opts))

@@ -45,12 +45,9 @@ GemmTrace g_trace;
 template <class Cfg, bool TA, bool TB>
 static void launch_gemm_t(Ctx& cx, const GemmArgs& g, dim3 grid)
 {
-    static bool attr_set = false;
+    static AttrOnce attr;
     constexpr size_t sm = dgemm2_smem_bytes<Cfg, TA, TB>();
-    if (!attr_set) {
-        BQ_CUDA(cudaFuncSetAttribute(dgemm2_kernel<Cfg, TA, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-        attr_set = true;
-    }
+    ensure_attr(attr, dgemm2_kernel<Cfg, TA, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     dgemm2_kernel<Cfg, TA, TB><<<grid, Cfg::THREADS, sm, cx.stream>>>(g, dgemm2_vec_ok(g));
     BQ_LAUNCH_CHECK();
 }
@@ -72,28 +69,38 @@ static void launch_gemm(Ctx& cx, bool ta, bool tb, const GemmArgs& g, int nsplit
 // chosen tiling leaves the SMs idle and K is long.
 void gemm(Ctx& cx, bool ta, bool tb, int64_t M, int64_t N, int64_t K, double alpha, const double* A, int64_t lda,
           const double* B, int64_t ldb, double beta, double* C, int64_t ldc, bool tri, int ctas_per_sm,
-          bool no_split)
+          bool no_split, const GemmExtra* extra)
 {
     if (M <= 0 || N <= 0) return;
+    const bool fixed = extra && (extra->fixed_tiles || extra->hs_state);
+    if (fixed) {
+        static_assert(Cfg2Mid::BM == GEMM_FIXED_TILE && Cfg2Mid::BN == GEMM_FIXED_TILE, "fixed tile");
+        GemmArgs g{M, N, K, alpha, beta, A, lda, B, ldb, C, ldc, nullptr, K > 0 ? K : 1, tri ? 1 : 0,
+                   extra->a_lower ? 1 : 0, extra->hs_state, extra->hs_readers};
+        launch_gemm<Cfg2Mid>(cx, ta, tb, g, 1, 0);
+        return;
+    }
+    // The split-K decision (the only choice that changes result bits: the tiling never changes an element's K
+    // order) is taken on the decision shape Md x Nd: the real one, or the hint of a caller computing one
+    // block of a larger product (the multi-GPU driver's per-rank columns), so that every
+    // element gets the same K slices as in the whole product.
+    const int64_t Md = (extra && extra->split_m > 0) ? extra->split_m : M;
+    const int64_t Nd = (extra && extra->split_n > 0) ? extra->split_n : N;
     auto ntiles = [&](int bm, int bn) {
-        int64_t tm = cdiv(M, bm), tn = cdiv(N, bn);
+        int64_t tm = cdiv(Md, bm), tn = cdiv(Nd, bn);
         return tri ? (tm * tn + tm) / 2 : tm * tn;
     };
     // v2 64x64 / BK 16 / 3 stages / grouped rasterisation is the best tile on every large shape and operand
     // order (35.3-36.0 TFLOP/s, profiles/gemm_tune_r01d_v2.json); 64x32 gives more CTAs to small GEMMs.
     int cfg;  // 1 mid (64x64), 2 small (64x32)
     int bm, bn;
-    if (N > 32 && ntiles(Cfg2Mid::BM, Cfg2Mid::BN) >= cx.num_sms) { cfg = 1; bm = Cfg2Mid::BM; bn = Cfg2Mid::BN; }
+    if (Nd > 32 && ntiles(Cfg2Mid::BM, Cfg2Mid::BN) >= cx.num_sms) { cfg = 1; bm = Cfg2Mid::BM; bn = Cfg2Mid::BN; }
     else { cfg = 2; bm = Cfg2Small::BM; bn = Cfg2Small::BN; }
     int64_t tiles = ntiles(bm, bn);
+    const size_t MNd = (size_t)(Md * Nd);
     int nsplit = 1;
     int64_t kchunk = K > 0 ? K : 1;
-    static int deep = -1;
-    if (deep < 0) {
-        const char* e = std::getenv("BQRRP_DEEP_SPLIT");  // 0: off (A/B experiments)
-        deep = (e && e[0] == '0') ? 0 : 1;
-    }
-    if (deep && K >= 8192 && ntiles(Cfg2Mid::BM, Cfg2Mid::BN) < cx.num_sms && cx.splitk && ctas_per_sm == 0 &&
+    if (K >= 8192 && ntiles(Cfg2Mid::BM, Cfg2Mid::BN) < cx.num_sms && cx.splitk && ctas_per_sm == 0 &&
         !no_split) {
         // few output tiles over a long K (the panel Grams of tall, narrow panels: C4's 262144 x 512, C2's
         // 16384 x 1024): 64x64 tiles split into K-chunks of >= 2048 rows, ~2 waves of 4 resident CTAs per
@@ -105,7 +112,7 @@ void gemm(Ctx& cx, bool ta, bool tb, int64_t M, int64_t N, int64_t K, double alp
         tiles = ntiles(bm, bn);
         int64_t sp = cdiv(8 * (int64_t)cx.num_sms, tiles);
         sp = imin(sp, imin(K / 2048, (int64_t)64));
-        sp = imin(sp, (int64_t)(cx.splitk_elems / (size_t)(M * N)));
+        sp = imin(sp, (int64_t)(cx.splitk_elems / MNd));
         if (sp >= 2) {
             kchunk = cdiv(cdiv(K, sp), Cfg2Mid::BK) * Cfg2Mid::BK;
             nsplit = (int)cdiv(K, kchunk);
@@ -114,7 +121,7 @@ void gemm(Ctx& cx, bool ta, bool tb, int64_t M, int64_t N, int64_t K, double alp
         int64_t want = cdiv(2 * cx.num_sms, tiles);
         want = imin(want, 32);
         want = imin(want, K / 128);
-        int64_t cap = (int64_t)(cx.splitk_elems / (size_t)(M * N));
+        int64_t cap = (int64_t)(cx.splitk_elems / MNd);
         want = imin(want, cap);
         if (want >= 2) {
             kchunk = cdiv(cdiv(K, want), Cfg2Mid::BK) * Cfg2Mid::BK;
@@ -128,7 +135,7 @@ void gemm(Ctx& cx, bool ta, bool tb, int64_t M, int64_t N, int64_t K, double alp
             const int64_t w = tiles * sp;
             return (double)w / (double)(cdiv(w, slots) * slots);
         };
-        const int64_t cap = imin(16, imin(K / 1024, (int64_t)(cx.splitk_elems / (size_t)(M * N))));
+        const int64_t cap = imin(16, imin(K / 1024, (int64_t)(cx.splitk_elems / MNd)));
         int64_t best = 1;
         double beff = eff(1);
         for (int64_t sp = 2; sp <= cap; ++sp)
@@ -138,7 +145,8 @@ void gemm(Ctx& cx, bool ta, bool tb, int64_t M, int64_t N, int64_t K, double alp
             nsplit = (int)cdiv(K, kchunk);
         }
     }
-    GemmArgs g{M, N, K, alpha, beta, A, lda, B, ldb, C, ldc, nsplit > 1 ? cx.splitk : nullptr, kchunk, tri ? 1 : 0};
+    GemmArgs g{M, N, K, alpha, beta, A, lda, B, ldb, C, ldc, nsplit > 1 ? cx.splitk : nullptr, kchunk, tri ? 1 : 0,
+               (extra && extra->a_lower) ? 1 : 0, nullptr, nullptr};
     GemmTraceRec rec{};
     if (g_trace.path) {
         rec = GemmTraceRec{M, N, K, ta, tb, tri, nsplit, nullptr, nullptr};
@@ -245,11 +253,8 @@ constexpr size_t TB_SMEM = sizeof(double) * (TRSM_NB * (TRSM_NB + 1) + TRSM_NB +
 static void trsm_base(Ctx& cx, int n, int64_t nr, const double* T, int64_t ldt, int mode, int unit, double* B,
                       int64_t st, int64_t sr)
 {
-    static bool attr = false;
-    if (!attr) {
-        BQ_CUDA(cudaFuncSetAttribute(trsm_base_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TB_SMEM));
-        attr = true;
-    }
+    static AttrOnce attr;
+    ensure_attr(attr, trsm_base_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TB_SMEM);
     trsm_base_kernel<<<(unsigned)cdiv(nr, TB_R), TB_THREADS, TB_SMEM, cx.stream>>>(n, nr, T, ldt, mode, unit, B, st, sr);
     BQ_LAUNCH_CHECK();
 }
@@ -380,22 +385,14 @@ void trsm_right_upper(Ctx& cx, int64_t rows, int64_t n, const double* T, int64_t
                       double* B, int64_t ldb, bool well_conditioned)
 {
     if (rows <= 0 || n <= 0) return;
-    static int inv_mode = -1;
-    if (inv_mode < 0) {
-        const char* e = std::getenv("BQRRP_TRSM_INV");  // 0: substitution everywhere (A/B experiments)
-        inv_mode = (e && e[0] == '0') ? 0 : 1;
-    }
     // the inversion launch pays off only when the apply kernels are wide (tall B: the CholQR passes and Y2)
-    if (!well_conditioned || !inv_mode || rows < TRSM_INV_MIN_ROWS) {
+    if (!well_conditioned || rows < TRSM_INV_MIN_ROWS) {
         trsm_ru_rec(cx, rows, n, T, ldt, t_lower, unit, B, ldb, nullptr);
         return;
     }
-    static bool attr = false;
-    if (!attr) {
-        BQ_CUDA(cudaFuncSetAttribute(trsm_inv_apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TI_SMEM));
-        BQ_CUDA(cudaFuncSetAttribute(tri_inv_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TINV_SMEM));
-        attr = true;
-    }
+    static AttrOnce attr_apply, attr_inv;
+    ensure_attr(attr_apply, trsm_inv_apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TI_SMEM);
+    ensure_attr(attr_inv, tri_inv_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TINV_SMEM);
     const size_t mark = cx.ws_used;
     const int64_t nblk = cdiv(n, TRSM_NB);
     double* Dinv = cx.alloc((size_t)nblk * TRSM_NB * TRSM_NB);

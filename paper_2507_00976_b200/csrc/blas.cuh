@@ -9,9 +9,24 @@ namespace bqrrp {
 // split-K).  Not used by the driver (measured slower for the bulk update).
 // no_split: never split K (each element's K order then does not depend on how M / N are tiled or
 // chunked — the sketch uses it so the host entry's chunked sketch is bitwise the device entry's).
+// Extra GEMM modes (all off by default):
+//   a_lower: op(A) is lower triangular (the TRMM W2 = T^T W of the compact-WY update: T upper, k^2 t flops
+//            instead of 2 k^2 t); the zeros above the diagonal are skipped, the K order is unchanged.
+//   fixed_tiles: always 64 x 64 tiles and no split-K, so every element's result is independent of M, N and of
+//            the other tiles (two such GEMMs over the same operand rows / columns agree bitwise).
+//   hs_state / hs_readers: the tile handshake of GemmArgs (implies fixed_tiles).
+//   split_m / split_n: the split-K decision is taken as for an Md x Nd product (0 = the real M / N).
+struct GemmExtra {
+    int64_t split_m = 0, split_n = 0;
+    bool a_lower = false;
+    bool fixed_tiles = false;
+    int* hs_state = nullptr;
+    int* hs_readers = nullptr;
+};
+constexpr int GEMM_FIXED_TILE = 64;  // tile edge of fixed_tiles / handshake GEMMs
 void gemm(Ctx& cx, bool ta, bool tb, int64_t M, int64_t N, int64_t K, double alpha, const double* A, int64_t lda,
           const double* B, int64_t ldb, double beta, double* C, int64_t ldc, bool tri = false, int ctas_per_sm = 0,
-          bool no_split = false);
+          bool no_split = false, const GemmExtra* extra = nullptr);
 
 // X op(T) = B, right side, op(T) upper triangular (n x n), in place on B (rows x n).
 //   t_lower = false: T stored upper, op(T) = T;  t_lower = true: T stored lower, op(T) = T^T.

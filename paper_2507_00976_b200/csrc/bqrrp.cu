@@ -23,7 +23,7 @@
 
 namespace bqrrp {
 
-static thread_local std::string g_last_error;
+thread_local std::string g_last_error;
 
 cudaMemPool_t lib_pool()
 {
@@ -44,7 +44,7 @@ cudaMemPool_t lib_pool()
     return pools[dev];
 }
 thread_local long long g_panel_fallbacks = 0;
-unsigned long long g_launches = 0;
+std::atomic<unsigned long long> g_launches{0};
 
 // ----------------------------------------------------------------------------------- small kernels
 __global__ void init_j_kernel(int64_t n, int64_t* J)
@@ -112,12 +112,37 @@ __global__ void ipiv_to_i64_kernel(int64_t n, const int* in0, int64_t* out1)
     if (j < n) out1[j] = (int64_t)in0[j] + 1;
 }
 
-// ----------------------------------------------------------------------------------- workspace
-struct Layout {
-    size_t persistent, temp, splitk, total;
-};
+void init_j(Ctx& cx, int64_t n, int64_t* J)
+{
+    if (n <= 0) return;
+    init_j_kernel<<<(unsigned)imin(cdiv(n, 256), 1024), 256, 0, cx.stream>>>(n, J);
+    BQ_LAUNCH_CHECK();
+}
+void nonfinite_check(Ctx& cx, int64_t rows, int64_t cols, const double* X, int64_t ldx)
+{
+    if (rows <= 0 || cols <= 0) return;
+    nonfinite_kernel<<<(unsigned)imin(cdiv(rows * cols, 256), 4 * cx.num_sms), 256, 0, cx.stream>>>(rows, cols, X, ldx,
+                                                                                                      cx.flags);
+    BQ_LAUNCH_CHECK();
+}
+void tri_rank_flags(Ctx& cx, const double* MskT_s, int64_t ldm, int64_t kmax, bool first, double rank_tol, double* ref)
+{
+    tri_rank_kernel<<<1, 1024, 0, cx.stream>>>(MskT_s, ldm, kmax, first ? 1 : 0, rank_tol, ref, cx.flags);
+    BQ_LAUNCH_CHECK();
+}
+void zero_col_flag(Ctx& cx, int64_t h, const double* col)
+{
+    zero_col_kernel<<<(unsigned)imin(cdiv(h, 256), 64), 256, 0, cx.stream>>>(h, col, cx.flags);
+    BQ_LAUNCH_CHECK();
+}
+void extract_rsk11(Ctx& cx, int64_t k, const double* MskT_s, int64_t ldm, double* R)
+{
+    extract_rsk11_kernel<<<(unsigned)imin(cdiv(k * k, 256), 4 * cx.num_sms), 256, 0, cx.stream>>>(k, MskT_s, ldm, R);
+    BQ_LAUNCH_CHECK();
+}
 
-static Layout layout(int64_t m, int64_t n, int64_t b, int64_t d)
+// ----------------------------------------------------------------------------------- workspace
+Layout layout(int64_t m, int64_t n, int64_t b, int64_t d)
 {
     auto r = [](size_t doubles) { return ((doubles * 8 + 255) & ~size_t(255)); };
     size_t mn = (size_t)imin(m, n);
@@ -131,18 +156,28 @@ static Layout layout(int64_t m, int64_t n, int64_t b, int64_t d)
     P += r(bb * bb) * 3;                   // Rsk11, X, T
     P += r((size_t)d * d) + r((size_t)n * d);  // deferred R_sk GEMM: Q_sk and its output rows
     P += r((size_t)m * bb) + r(bb * (size_t)n) * 2;  // V, W, W2
+    // lookahead: second V, the gathered next panel, W2's gathered columns, the bulk GEMM's
+    // tile handshake (state + readers per 64 x 64 tile) and the gather's post flags
+    const size_t tiles = (size_t)cdiv(m, 64) * (size_t)cdiv(n, 64);
+    P += r((size_t)m * bb) * 2 + r(bb * bb) + r((tiles + 1) / 2) * 2 + r(((size_t)cdiv(m, 64) * bb + 1) / 2);
     P += r(8) * 2;                         // ref, flags
     // temporaries: sketch QR vs panel (never live together)
     size_t p = (size_t)d;
     size_t sq = r(p * p) * 7 + r(p) + r(2 * 160 * 33 + 160 * 32 * 32) + r(64) + r((size_t)n * p);
     size_t lu = r(2 * 160 * 34) + r(64);
-    size_t pn = r(bb * bb) * 8 + r(bb) + r((size_t)cdiv((int64_t)bb, 64) * 4096 + 4096);  // + TRSM Dinv
+    // panel: 8 k x k factors / products, S, the main stream's TRSM Dinv, and the side-stream arena of
+    // recon_finish (its two k x k products come out of the 8; its own TRSM Dinv)
+    const size_t dinv = (size_t)cdiv((int64_t)bb, 64) * 4096 + 4096;
+    size_t pn = r(bb * bb) * 8 + r(bb) + r(dinv) + r(dinv + 64);
     size_t T = sq > pn ? sq : pn;
     T = T > lu ? T : lu;
     // split-K partials: 16 slices of the largest square product, plus 4 slices of a b x n GEMM1 output so
     // the wave-efficiency split of few-wave W = V^T C calls is not capped by the buffer (C4: 25.9 TFLOP/s
-    // at split 1 for 512 x 3584 x 258048, where 5 slices fill the last wave)
-    size_t sk = r((size_t)16 * (p > bb ? p * p : bb * bb) + (size_t)4 * 1024 * 1024 + (size_t)4 * bb * (size_t)n);
+    // at split 1 for 512 x 3584 x 258048, where 5 slices fill the last wave).  That split is only taken
+    // below 32 x num_sms 64 x 64 tiles (blas.cu), so the GEMM1 slices are capped at that output size.
+    const size_t gemm1_cap = (size_t)32 * 160 * 64 * 64;
+    const size_t g1 = bb * (size_t)n < gemm1_cap ? bb * (size_t)n : gemm1_cap;
+    size_t sk = r((size_t)16 * (p > bb ? p * p : bb * bb) + (size_t)4 * 1024 * 1024 + (size_t)4 * g1);
     Layout L{P, T, sk, P + T + sk + (1u << 20)};
     return L;
 }
@@ -199,144 +234,318 @@ struct HostIO {
     }
 };
 
-static int64_t factor_impl(Ctx& cx, Ctx* cxb, cudaEvent_t ev_top, cudaEvent_t ev_bulk, int64_t m, int64_t n, double* A,
-                           int64_t lda, int64_t b, int64_t d, uint64_t seed, double* tau, int64_t* J, double rank_tol,
-                           int passes, bool hqr_fallback, int* host_flags, HostIO* hio = nullptr)
-{
-    const int64_t mn = imin(m, n);
-    double* MskT = cx.alloc((size_t)n * d);
-    double* Lb = cx.alloc((size_t)n * d);
-    double* colscr = cx.alloc(imax(2 * d * m, m * d));
-    double* rowscr = cx.alloc((size_t)2 * d * d);
-    int64_t* vtmp = cx.alloc_as<int64_t>((size_t)2 * d);
+// Streams of one factorization.  crit (high priority): the critical chain; bulk (low priority):
+// the bulk rows of every trailing update; aux (high priority): small fork-join pieces of the critical chain
+// (the panel's k x k finish, the sample update's X, the pivot selection's R_sk(:, d:) GEMM).  nullptr bulk =
+// one stream, serialised (no_lookahead).
+struct Sched {
+    Ctx* bulk = nullptr;
+    Ctx* aux = nullptr;
+    cudaEvent_t ev_top = nullptr, ev_bulk = nullptr;
+};
+
+// Buffers and steps of one factorization; the two schedules below compose the steps.
+struct Run {
+    Ctx& cx;
+    const Sched& sc;
+    int64_t m, n, b, d;
+    double* A;
+    int64_t lda;
+    uint64_t seed;
+    double* tau;
+    int64_t* J;
+    double rank_tol;
+    int passes;
+    bool hqr_fallback;
+    int* hf;
+    HostIO* hio;
+    int64_t mn, bb;
+    double *MskT, *Lb, *colscr, *rowscr, *Rsk11, *X, *ref, *Vp[2], *Tp, *W, *W2;
+    double *Pn = nullptr, *W2g = nullptr;  // lookahead: the next panel (gathered), W2's gathered columns
+    int *hs_state = nullptr, *hs_readers = nullptr, *post = nullptr;
+    int64_t* vtmp;
     Touched T;
-    T.tq = cx.alloc_as<int>((size_t)2 * d);
-    T.tsrc = cx.alloc_as<int>((size_t)2 * d);
-    T.nt = cx.alloc_as<int>(2);
-    int* ipiv = cx.alloc_as<int>((size_t)d);
-    int* perm = cx.alloc_as<int>((size_t)n);
-    int64_t bb = imin(b, mn);
-    double* Rsk11 = cx.alloc((size_t)bb * bb);
-    double* X = cx.alloc((size_t)bb * bb);
-    double* ref = cx.alloc(1);
-    // panel outputs and WY scratch stay alive across the overlap of the bulk GEMM with the next a2
-    double* Vp = cx.alloc((size_t)m * bb);
-    double* Tp = cx.alloc((size_t)bb * bb);
-    double* W = cx.alloc((size_t)bb * n);
-    double* W2 = cx.alloc((size_t)bb * n);
-    bool bulk_pending = false;
-    RskDefer rsk;  // the R_sk(:, d:) GEMM of every pivot selection on the side stream (lookahead only)
-    if (cxb) {
-        rsk.side = cxb;
-        rsk.Q = cx.alloc((size_t)d * d);
-        rsk.Y = cx.alloc((size_t)n * d);
-    }
-    cudaEvent_t ev_x0 = nullptr, ev_x1 = nullptr;  // side-stream X of the sample update
-    BQ_CUDA(cudaEventCreateWithFlags(&ev_x0, cudaEventDisableTiming));
-    BQ_CUDA(cudaEventCreateWithFlags(&ev_x1, cudaEventDisableTiming));
-    struct EvGuard {
-        cudaEvent_t a, b;
-        ~EvGuard() { cudaEventDestroy(a); cudaEventDestroy(b); }
-    } ev_guard{ev_x0, ev_x1};
+    int *ipiv, *perm;
+    RskDefer rsk;
+    std::vector<cudaEvent_t> evs;
 
-    cx.mark(PH_OTHER);
-    init_j_kernel<<<(unsigned)imin(cdiv(n, 256), 1024), 256, 0, cx.stream>>>(n, J);
-    BQ_LAUNCH_CHECK();
-    BQ_CUDA(cudaMemsetAsync(tau, 0, sizeof(double) * mn, cx.stream));
-    BQ_CUDA(cudaMemsetAsync(cx.flags, 0, sizeof(int) * F_NFLAGS, cx.stream));
-    // a1: sketch (S^T lives in the column scratch until the loop starts)
-    if (hio) {
-        sketch_operator_T(cx, m, d, seed, colscr, m);
-        const int64_t chunk = imax(b, cdiv(n, 16));
-        for (int64_t c0 = 0; c0 < n; c0 += chunk) {
-            const int64_t nc = imin(chunk, n - c0);
-            BQ_CUDA(cudaMemcpy2DAsync(A + c0 * lda, lda * sizeof(double), hio->A_in + c0 * hio->ld_host,
-                                      hio->ld_host * sizeof(double), m * sizeof(double), nc, cudaMemcpyHostToDevice,
-                                      hio->h2d));
-            cudaEvent_t e = hio->event();
-            BQ_CUDA(cudaEventRecord(e, hio->h2d));
-            BQ_CUDA(cudaStreamWaitEvent(cx.stream, e, 0));
-            gemm(cx, true, false, nc, d, m, 1.0, A + c0 * lda, lda, colscr, m, 0.0, MskT + c0, n, false, 0,
-                 /*no_split=*/true);  // MskT rows (no split-K: bitwise the device entry's one-GEMM sketch)
+    Run(Ctx& cx_, const Sched& sc_, int64_t m_, int64_t n_, double* A_, int64_t lda_, int64_t b_, int64_t d_,
+        uint64_t seed_, double* tau_, int64_t* J_, double rank_tol_, int passes_, bool hqr_, int* hf_, HostIO* hio_)
+        : cx(cx_), sc(sc_), m(m_), n(n_), b(b_), d(d_), A(A_), lda(lda_), seed(seed_), tau(tau_), J(J_),
+          rank_tol(rank_tol_), passes(passes_), hqr_fallback(hqr_), hf(hf_), hio(hio_)
+    {
+        mn = imin(m, n);
+        bb = imin(b, mn);
+        MskT = cx.alloc((size_t)n * d);
+        Lb = cx.alloc((size_t)n * d);
+        colscr = cx.alloc(imax(2 * d * m, m * d));
+        rowscr = cx.alloc((size_t)2 * d * d);
+        vtmp = cx.alloc_as<int64_t>((size_t)2 * d);
+        T.tq = cx.alloc_as<int>((size_t)2 * d);
+        T.tsrc = cx.alloc_as<int>((size_t)2 * d);
+        T.nt = cx.alloc_as<int>(2);
+        ipiv = cx.alloc_as<int>((size_t)d);
+        perm = cx.alloc_as<int>((size_t)n);
+        Rsk11 = cx.alloc((size_t)bb * bb);
+        X = cx.alloc((size_t)bb * bb);
+        ref = cx.alloc(1);
+        Vp[0] = cx.alloc((size_t)m * bb);
+        Vp[1] = sc.bulk ? cx.alloc((size_t)m * bb) : Vp[0];  // panel i+1 is built while bulk i reads V_i
+        Tp = cx.alloc((size_t)bb * bb);
+        W = cx.alloc((size_t)bb * n);
+        W2 = cx.alloc((size_t)bb * n);
+        if (sc.bulk) {
+            rsk.side = sc.aux;
+            rsk.Q = cx.alloc((size_t)d * d);
+            rsk.Y = cx.alloc((size_t)n * d);
+            Pn = cx.alloc((size_t)m * bb);
+            W2g = cx.alloc((size_t)bb * bb);
+            const size_t tiles = (size_t)cdiv(m, GEMM_FIXED_TILE) * (size_t)cdiv(n, GEMM_FIXED_TILE);
+            hs_state = cx.alloc_as<int>(tiles);
+            hs_readers = cx.alloc_as<int>(tiles);
+            post = cx.alloc_as<int>((size_t)cdiv(m, GEMM_FIXED_TILE) * bb);
+            BQ_CUDA(cudaMemsetAsync(hs_readers, 0, tiles * sizeof(int), cx.stream));
         }
-    } else {
-        sketch_apply(cx, m, n, A, lda, d, seed, MskT, n, colscr);
     }
-    nonfinite_kernel<<<(unsigned)imin(cdiv(n * d, 256), 4 * cx.num_sms), 256, 0, cx.stream>>>(n, d, MskT, n, cx.flags);
-    BQ_LAUNCH_CHECK();
+    ~Run()
+    {
+        for (auto e : evs) cudaEventDestroy(e);
+    }
+    cudaEvent_t event()
+    {
+        cudaEvent_t e;
+        BQ_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        evs.push_back(e);
+        return e;
+    }
+    // `to` waits for the work queued so far on `from`
+    void join(cudaStream_t to, cudaStream_t from)
+    {
+        cudaEvent_t e = event();
+        BQ_CUDA(cudaEventRecord(e, from));
+        BQ_CUDA(cudaStreamWaitEvent(to, e, 0));
+    }
 
-    int64_t ell = mn;
-    for (int64_t i = 0;; ++i) {
-        const int64_t s = i * b;
-        if (s >= mn) { ell = mn; break; }
-        const int64_t c = imin(n, s + b), r = imin(m, s + b), w = n - s, h = m - s;
-        const int64_t kmax = imin(imin(b, w), h);
-        // ---- a2: pivots from LU of the sketch transpose, then R_sk
+    // O2 + a1: J = 1..n, tau = 0, flags, the sketch (host entry: per uploaded column chunk)
+    void prologue()
+    {
+        cx.mark(PH_OTHER);
+        init_j_kernel<<<(unsigned)imin(cdiv(n, 256), 1024), 256, 0, cx.stream>>>(n, J);
+        BQ_LAUNCH_CHECK();
+        BQ_CUDA(cudaMemsetAsync(tau, 0, sizeof(double) * mn, cx.stream));
+        BQ_CUDA(cudaMemsetAsync(cx.flags, 0, sizeof(int) * F_NFLAGS, cx.stream));
+        if (hio) {  // S^T lives in the column scratch until the loop starts
+            sketch_operator_T(cx, m, d, seed, colscr, m);
+            const int64_t chunk = imax(b, cdiv(n, 16));
+            for (int64_t c0 = 0; c0 < n; c0 += chunk) {
+                const int64_t nc = imin(chunk, n - c0);
+                BQ_CUDA(cudaMemcpy2DAsync(A + c0 * lda, lda * sizeof(double), hio->A_in + c0 * hio->ld_host,
+                                          hio->ld_host * sizeof(double), m * sizeof(double), nc,
+                                          cudaMemcpyHostToDevice, hio->h2d));
+                cudaEvent_t e = hio->event();
+                BQ_CUDA(cudaEventRecord(e, hio->h2d));
+                BQ_CUDA(cudaStreamWaitEvent(cx.stream, e, 0));
+                gemm(cx, true, false, nc, d, m, 1.0, A + c0 * lda, lda, colscr, m, 0.0, MskT + c0, n, false, 0,
+                     /*no_split=*/true);  // MskT rows (no split-K: bitwise the device entry's one-GEMM sketch)
+            }
+        } else {
+            sketch_apply(cx, m, n, A, lda, d, seed, MskT, n, colscr);
+        }
+        nonfinite_kernel<<<(unsigned)imin(cdiv(n * d, 256), 4 * cx.num_sms), 256, 0, cx.stream>>>(n, d, MskT, n,
+                                                                                                    cx.flags);
+        BQ_LAUNCH_CHECK();
+    }
+
+    // a2 on the window at s (Alg. 2): LU pivots of the sketch transpose, the touched set of J_qr,
+    // sketch rows permuted, R_sk (its (w-d) x d GEMM part deferred to aux in the lookahead), tri_rank -> flags
+    void pivots(int64_t i, int64_t s)
+    {
+        const int64_t w = n - s, kmax = imin(imin(b, w), m - s);
         cx.mark(PH_QRCP_WIDE);
         copy_matrix(cx, w, d, MskT + s, n, Lb, n);
         getrf_pivots(cx, Lb, n, w, d, ipiv, perm);
-        const int64_t nlu = imin(w, d);
-        touched_from_perm(cx, w, nlu, perm, T);
+        touched_from_perm(cx, w, imin(w, d), perm, T);
         permute_rows(cx, d, MskT + s, n, T, rowscr);
-        sketch_qr(cx, MskT + s, n, w, d, RowBlocks(), cxb ? &rsk : nullptr);
+        sketch_qr(cx, MskT + s, n, w, d, RowBlocks(), sc.bulk ? &rsk : nullptr);
         cx.mark(PH_TRI_RANK);
         tri_rank_kernel<<<1, 1024, 0, cx.stream>>>(MskT + s, n, kmax, i == 0, rank_tol, ref, cx.flags);
         BQ_LAUNCH_CHECK();
-        // ---- a3: column permutation of A (all m rows) and J (after the previous bulk update landed)
+    }
+
+    // a3: columns of A(0:m, s:n) and J(s:n) gathered by J_qr (touched set only)
+    void permute(int64_t s)
+    {
         cx.mark(PH_COL_PERM);
-        if (bulk_pending) {
-            BQ_CUDA(cudaStreamWaitEvent(cx.stream, ev_bulk, 0));
-            bulk_pending = false;
-        }
         permute_columns(cx, m, A + s * lda, lda, T, colscr);
         permute_vector(cx, J + s, T, vtmp);
-        zero_col_kernel<<<(unsigned)imin(cdiv(h, 256), 64), 256, 0, cx.stream>>>(h, A + s + s * lda, cx.flags);
+    }
+
+    // the zero-column test (reading Z12) of a column of h rows, then the loop's one host read of
+    // {k, zero flag, non-finite flag, POTRF breakdown}.  Returns false on a numerical failure.
+    bool check(int64_t h, const double* col)
+    {
+        zero_col_kernel<<<(unsigned)imin(cdiv(h, 256), 64), 256, 0, cx.stream>>>(h, col, cx.flags);
         BQ_LAUNCH_CHECK();
-        BQ_CUDA(cudaMemcpyAsync(host_flags, cx.flags, sizeof(int) * F_NFLAGS, cudaMemcpyDeviceToHost, cx.stream));
+        BQ_CUDA(cudaMemcpyAsync(hf, cx.flags, sizeof(int) * F_NFLAGS, cudaMemcpyDeviceToHost, cx.stream));
         BQ_CUDA(cudaStreamSynchronize(cx.stream));
-        if (host_flags[F_NONFINITE] || host_flags[F_POTRF_INFO]) return -1;
-        const int64_t k = host_flags[F_K];
-        if (k == 0 || host_flags[F_ZERO_COL]) { ell = s; break; }
-        // ---- a4 + a5: panel and trailing update
+        return !(hf[F_NONFINITE] || hf[F_POTRF_INFO]);
+    }
+
+    // a4 (Alg. 3) on the panel Ap (h x k, ld), tau(s:s+k); V, T into Vp[slot], Tp
+    void panel(int64_t s, int64_t h, int64_t k, double* Ap, int64_t ld, int slot)
+    {
         cx.mark(PH_QR_TALL);
         extract_rsk11_kernel<<<(unsigned)imin(cdiv(k * k, 256), 4 * cx.num_sms), 256, 0, cx.stream>>>(k, MskT + s, n,
                                                                                                         Rsk11);
         BQ_LAUNCH_CHECK();
-        g_panel_fallbacks += panel_factor(cx, m, A, lda, s, k, Rsk11, tau, passes, Vp, Tp, hqr_fallback, cxb);
-        // ---- a5 (the bulk rows overlap the sketch update and the next a2) and a7
-        cx.mark(PH_APPLY_QT);
-        const bool terminal = (k < kmax || c == n || r == m);
-        if (hio && !terminal) hio->flush(cx.stream, m, A, lda, c);  // block column [s, c) is final
-        // a6's X = R_sk11 R11^{-1} (b x b) needs only the panel: on the idle side stream during GEMM1
-        // (ahead of the bulk rows there, which wait for GEMM1 anyway); no split-K slices on that stream
-        const bool x_side = !terminal && cxb;
-        if (x_side) {
-            BQ_CUDA(cudaEventRecord(ev_x0, cx.stream));
-            BQ_CUDA(cudaStreamWaitEvent(cxb->stream, ev_x0, 0));
-            Ctx sc = *cxb;
-            sc.timer = nullptr;
-            copy_matrix(sc, b, b, Rsk11, k, X, b);
-            trsm_right_upper(sc, b, b, A + s + s * lda, lda, false, false, X, b);  // X = R_sk11 R11^{-1}
-            zero_triangle(sc, 'U', b, b, X, b);
-            BQ_CUDA(cudaEventRecord(ev_x1, cxb->stream));
-        }
-        wy_update(cx, terminal ? nullptr : cxb, m, n, A, lda, s, k, Vp, Tp, W, W2, ev_top, ev_bulk);
-        if (!terminal && cxb && h > k && n - s - k > 0) bulk_pending = true;
-        if (terminal) { ell = s + k; break; }
-        // ---- a6: sketch update (k == b here)
-        cx.mark(PH_SAMPLE_UPDATE);
-        if (x_side) {
-            BQ_CUDA(cudaStreamWaitEvent(cx.stream, ev_x1, 0));
-        } else {
-            copy_matrix(cx, b, b, Rsk11, k, X, b);
-            trsm_right_upper(cx, b, b, A + s + s * lda, lda, false, false, X, b);  // X = R_sk11 R11^{-1}
+        g_panel_fallbacks += panel_factor(cx, h, Ap, ld, k, Rsk11, tau + s, passes, Vp[slot], Tp, hqr_fallback,
+                                          sc.aux);
+    }
+
+    // a6's X = R_sk11 R11^{-1} (b x b; R11 = A(s:s+b, s:s+b), upper), on aux when there is one
+    cudaEvent_t sample_x(int64_t s)
+    {
+        if (!sc.aux) {
+            copy_matrix(cx, b, b, Rsk11, b, X, b);
+            trsm_right_upper(cx, b, b, A + s + s * lda, lda, false, false, X, b);
             zero_triangle(cx, 'U', b, b, X, b);
+            return nullptr;
         }
+        join(sc.aux->stream, cx.stream);
+        Ctx ac = side_ctx(cx, *sc.aux, 0);  // allocates nothing (substitution TRSM)
+        copy_matrix(ac, b, b, Rsk11, b, X, b);
+        trsm_right_upper(ac, b, b, A + s + s * lda, lda, false, false, X, b);
+        zero_triangle(ac, 'U', b, b, X, b);
+        cudaEvent_t e = event();
+        BQ_CUDA(cudaEventRecord(e, sc.aux->stream));
+        return e;
+    }
+
+    // a6: MskT(c:n, 0:b) -= R12^T X^T
+    void sample_update(int64_t s, int64_t c, cudaEvent_t ex)
+    {
+        cx.mark(PH_SAMPLE_UPDATE);
+        if (ex) BQ_CUDA(cudaStreamWaitEvent(cx.stream, ex, 0));
         gemm(cx, true, true, n - c, b, b, -1.0, A + s + c * lda, lda, X, b, 1.0, MskT + c, n);
     }
+};
+
+// One stream, Alg. 1 in order (no_lookahead).
+static int64_t loop_serial(Run& R)
+{
+    Ctx& cx = R.cx;
+    const int64_t m = R.m, n = R.n, b = R.b;
+    for (int64_t i = 0;; ++i) {
+        const int64_t s = i * b;
+        if (s >= R.mn) return R.mn;
+        const int64_t c = imin(n, s + b), r = imin(m, s + b), w = n - s, h = m - s;
+        const int64_t kmax = imin(imin(b, w), h);
+        R.pivots(i, s);
+        R.permute(s);
+        if (!R.check(h, R.A + s + s * R.lda)) return -1;
+        const int64_t k = R.hf[F_K];
+        if (k == 0 || R.hf[F_ZERO_COL]) return s;
+        R.panel(s, h, k, R.A + s + s * R.lda, R.lda, 0);
+        cx.mark(PH_APPLY_QT);
+        const bool terminal = (k < kmax || c == n || r == m);
+        if (R.hio && !terminal) R.hio->flush(cx.stream, m, R.A, R.lda, c);
+        wy_update(cx, h, k, n - s - k, R.Vp[0], h, R.Tp, R.A + s + (s + k) * R.lda, R.lda, R.W, R.W2);
+        if (terminal) return s + k;
+        R.sample_x(s);
+        R.sample_update(s, c, nullptr);
+    }
+}
+
+// The pivot-aware lookahead.  Iteration i, with panel i factored:
+//   crit: GEMM1 W = V^T C, W2 = T^T W, R12 rows -> [bulk stream: C(k:h) -= V(k:h) W2, tile handshake]
+//   crit: a6 (X from aux), a2 of i+1 (R_sk GEMM on aux), then the next panel's columns gathered from the
+//         trailing block while the bulk runs (la_gather_pre / _post around the same update of just those
+//         columns, bitwise the bulk's), the host read of k, panel i+1 on the gathered copy
+//   crit: wait for the bulk, a3 of i+1 on A and J, the factored panel copied into place.
+// So panel i+1 (and the latency-bound pivot selection) overlaps the bulk GEMM of iteration i; only GEMM1, the
+// permutation and the copy are serial.
+static int64_t loop_lookahead(Run& R)
+{
+    Ctx& cx = R.cx;
+    const Sched& sc = R.sc;
+    const int64_t m = R.m, n = R.n, b = R.b;
+    double* A = R.A;
+    const int64_t lda = R.lda;
+    // iteration 0: pivots, permutation, panel in place
+    R.pivots(0, 0);
+    R.permute(0);
+    if (!R.check(m, A)) return -1;
+    int64_t k = R.hf[F_K];
+    if (k == 0 || R.hf[F_ZERO_COL]) return 0;
+    R.panel(0, m, k, A, lda, 0);
+    for (int64_t i = 0;; ++i) {
+        const int64_t s = i * b, slot = i & 1;
+        const int64_t c = imin(n, s + b), r = imin(m, s + b), w = n - s, h = m - s;
+        const int64_t kmax = imin(imin(b, w), h);
+        const bool terminal = (k < kmax || c == n || r == m);
+        if (R.hio && !terminal) R.hio->flush(cx.stream, m, A, lda, c);  // block column [s, c) is final
+        double* V = R.Vp[slot];
+        double* C = A + s + (s + k) * lda;
+        const int64_t t = n - s - k;
+        cx.mark(PH_APPLY_QT);
+        if (terminal) {
+            wy_update(cx, h, k, t, V, h, R.Tp, C, lda, R.W, R.W2);
+            return s + k;
+        }
+        // ---- a5: critical part, then the bulk rows on the bulk stream (k == b here)
+        cudaEvent_t ex = R.sample_x(s);
+        const int64_t tiles_m = cdiv(h - k, GEMM_FIXED_TILE), tiles_n = cdiv(t, GEMM_FIXED_TILE);
+        BQ_CUDA(cudaMemsetAsync(R.hs_state, 0, sizeof(int) * tiles_m * tiles_n, cx.stream));
+        wy_top(cx, h, k, t, V, h, R.Tp, C, lda, R.W, R.W2, /*rows=*/k);
+        BQ_CUDA(cudaEventRecord(sc.ev_top, cx.stream));
+        BQ_CUDA(cudaStreamWaitEvent(sc.bulk->stream, sc.ev_top, 0));
+        if (sc.bulk->timer) sc.bulk->timer->begin_interval(sc.bulk->stream, PH_APPLY_QT_BULK);
+        wy_bulk(*sc.bulk, h, k, t, V, h, R.W2, C, lda, R.hs_state, R.hs_readers);
+        if (sc.bulk->timer) sc.bulk->timer->end_interval(sc.bulk->stream);
+        BQ_CUDA(cudaEventRecord(sc.ev_bulk, sc.bulk->stream));
+        // ---- a6, then a2 of the next iteration (overlapping the bulk)
+        R.sample_update(s, c, ex);
+        const int64_t s1 = c, h1 = m - s1, w1 = n - s1;
+        const int64_t kmax1 = imin(imin(b, w1), h1);
+        R.pivots(i + 1, s1);
+        // ---- the next panel's columns: P(:, q) = C(k:h, perm[q]) - V(k:h) W2(:, perm[q]), q < kmax1
+        cx.mark(PH_QR_TALL);
+        double* Cb = A + s1 + s1 * lda;  // = C + k rows: the bulk's rows, columns from the next window's start
+        la_gather_pre(cx, h1, Cb, lda, R.perm, kmax1, tiles_n, R.hs_state, R.hs_readers, R.Pn, h1, R.post);
+        gather_cols_idx(cx, k, R.W2, k, R.perm, kmax1, R.W2g, k);
+        GemmExtra fixed;
+        fixed.fixed_tiles = true;  // the bulk's tiling: bitwise the bulk's values for these columns
+        gemm(cx, false, false, h1, kmax1, k, -1.0, V + k, h, R.W2g, k, 1.0, R.Pn, h1, false, 0, true, &fixed);
+        la_gather_post(cx, h1, Cb, lda, R.perm, kmax1, tiles_n, R.hs_state, R.Pn, h1, R.post);
+        if (!R.check(h1, R.Pn)) return -1;
+        const int64_t k1 = R.hf[F_K];
+        if (k1 == 0 || R.hf[F_ZERO_COL]) {  // early exit after the permutation (oracle O3 f, g)
+            BQ_CUDA(cudaStreamWaitEvent(cx.stream, sc.ev_bulk, 0));
+            R.permute(s1);
+            return s1;
+        }
+        R.panel(s1, h1, k1, R.Pn, h1, (int)(slot ^ 1));
+        // ---- a3 of i+1 once the bulk has landed, and the factored panel into place
+        BQ_CUDA(cudaStreamWaitEvent(cx.stream, sc.ev_bulk, 0));
+        R.permute(s1);
+        copy_matrix(cx, h1, k1, R.Pn, h1, Cb, lda);
+        k = k1;
+    }
+}
+
+static int64_t factor_impl(Ctx& cx, const Sched& sc, int64_t m, int64_t n, double* A, int64_t lda, int64_t b,
+                           int64_t d, uint64_t seed, double* tau, int64_t* J, double rank_tol, int passes,
+                           bool hqr_fallback, int* host_flags, HostIO* hio = nullptr)
+{
+    Run R(cx, sc, m, n, A, lda, b, d, seed, tau, J, rank_tol, passes, hqr_fallback, host_flags, hio);
+    R.prologue();
+    int64_t ell = sc.bulk ? loop_lookahead(R) : loop_serial(R);
+    if (ell < 0) return -1;
     // O4: tau(ell:) = 0, A(ell:m, ell:n) = 0 (reading Z16)
     cx.mark(PH_OTHER);
-    if (bulk_pending) BQ_CUDA(cudaStreamWaitEvent(cx.stream, ev_bulk, 0));
+    if (sc.bulk) BQ_CUDA(cudaStreamWaitEvent(cx.stream, sc.ev_bulk, 0));
+    if (sc.aux) R.join(cx.stream, sc.aux->stream);
+    const int64_t mn = R.mn;
     if (ell < mn) BQ_CUDA(cudaMemsetAsync(tau + ell, 0, sizeof(double) * (mn - ell), cx.stream));
     set_zero(cx, m - ell, n - ell, A + ell + ell * lda, lda);
     if (hio) hio->flush(cx.stream, m, A, lda, n);
@@ -347,14 +556,14 @@ static int64_t factor_impl(Ctx& cx, Ctx* cxb, cudaEvent_t ev_top, cudaEvent_t ev
     return ell;
 }
 
-static int* pinned_flags()
+int* pinned_flags()
 {
     static thread_local int* p = nullptr;
     if (!p) BQ_CUDA(cudaMallocHost(&p, sizeof(int) * F_NFLAGS));
     return p;
 }
 
-static void setup_ctx(Ctx& cx, void* stream)
+void setup_ctx(Ctx& cx, void* stream)
 {
     cx.stream = (cudaStream_t)stream;
     int dev = 0;
@@ -363,7 +572,7 @@ static void setup_ctx(Ctx& cx, void* stream)
 }
 
 // Carve splitk + flags from the tail of the workspace.
-static void carve(Ctx& cx, void* ws, size_t bytes, const Layout& L)
+void carve(Ctx& cx, void* ws, size_t bytes, const Layout& L)
 {
     cx.ws = (char*)ws;
     cx.ws_bytes = bytes;
@@ -376,23 +585,6 @@ static void carve(Ctx& cx, void* ws, size_t bytes, const Layout& L)
 }  // namespace bqrrp
 
 using namespace bqrrp;
-
-template <typename F>
-static int guarded(F&& f)
-{
-    try {
-        return f();
-    } catch (const CudaError& e) {
-        g_last_error = e.what();
-        return BQRRP_ECUDA;
-    } catch (const std::bad_alloc& e) {
-        g_last_error = e.what();
-        return BQRRP_ENOMEM;
-    } catch (const std::exception& e) {
-        g_last_error = e.what();
-        return std::strstr(e.what(), "workspace") ? BQRRP_ENOMEM : BQRRP_ECUDA;
-    }
-}
 
 extern "C" {
 
@@ -429,6 +621,7 @@ static int factor_ex_impl(int64_t m, int64_t n, double* A, int64_t lda, int64_t 
     return guarded([&]() -> int {
         Ctx cx;
         setup_ctx(cx, stream);
+        cx.force_breakdown = opts && (opts->debug_flags & BQRRP_DEBUG_FORCE_BREAKDOWN);
         if (m == 0 || n == 0) {
             *rank = 0;
             if (n > 0) {
@@ -436,6 +629,18 @@ static int factor_ex_impl(int64_t m, int64_t n, double* A, int64_t lda, int64_t 
                 BQ_LAUNCH_CHECK();
             }
             return 0;
+        }
+        // shape limits of the leaf kernels, before any launch
+        if (n > lu_max_rows(cx.num_sms)) {
+            g_last_error = "n = " + std::to_string(n) + " exceeds the K-LU grid leaf's capacity (" +
+                           std::to_string(lu_max_rows(cx.num_sms)) + " sketch rows)";
+            return -2;
+        }
+        if (m > qr_max_rows(cx.num_sms) && (passes == 0 || !(opts && opts->no_hqr_fallback))) {
+            g_last_error = "m = " + std::to_string(m) + " exceeds the Householder panel's capacity (" +
+                           std::to_string(qr_max_rows(cx.num_sms)) + " rows; needed by cholqr_passes = 0 and by the "
+                           "CholQR-breakdown fallback: set no_hqr_fallback)";
+            return -1;
         }
         Layout L = layout(m, n, b, d);
         void* ws = workspace;
@@ -449,26 +654,30 @@ static int factor_ex_impl(int64_t m, int64_t n, double* A, int64_t lda, int64_t 
             return -11;
         }
         carve(cx, ws, ws_bytes, L);
-        // critical chain on a high-priority stream, the bulk trailing GEMM on a low-priority one;
-        // both joined to the caller's stream at entry and exit
+        // critical chain and its helper (aux) on high-priority streams, the bulk trailing GEMM on a
+        // low-priority one (Sched); all joined to the caller's stream at entry and exit
         int prio_lo = 0, prio_hi = 0;
         BQ_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
-        cudaStream_t user = cx.stream, s_hi = nullptr, s_lo = nullptr;
-        cudaEvent_t ev_in = nullptr, ev_top = nullptr, ev_bulk = nullptr, ev_hi_done = nullptr;
+        cudaStream_t user = cx.stream, s_hi = nullptr, s_lo = nullptr, s_aux = nullptr;
+        cudaEvent_t ev_in = nullptr, ev_top = nullptr, ev_bulk = nullptr, ev_done = nullptr;
         BQ_CUDA(cudaStreamCreateWithPriority(&s_hi, cudaStreamNonBlocking, prio_hi));
         BQ_CUDA(cudaStreamCreateWithPriority(&s_lo, cudaStreamNonBlocking, prio_lo));
+        BQ_CUDA(cudaStreamCreateWithPriority(&s_aux, cudaStreamNonBlocking, prio_hi));
         BQ_CUDA(cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming));
         BQ_CUDA(cudaEventCreateWithFlags(&ev_top, cudaEventDisableTiming));
         BQ_CUDA(cudaEventCreateWithFlags(&ev_bulk, cudaEventDisableTiming));
-        BQ_CUDA(cudaEventCreateWithFlags(&ev_hi_done, cudaEventDisableTiming));
+        BQ_CUDA(cudaEventCreateWithFlags(&ev_done, cudaEventDisableTiming));
         BQ_CUDA(cudaEventRecord(ev_in, user));
-        BQ_CUDA(cudaStreamWaitEvent(s_hi, ev_in, 0));
-        BQ_CUDA(cudaStreamWaitEvent(s_lo, ev_in, 0));
+        for (cudaStream_t st : {s_hi, s_lo, s_aux}) BQ_CUDA(cudaStreamWaitEvent(st, ev_in, 0));
         cx.stream = s_hi;
-        Ctx cxb = cx;
+        Ctx cxb = cx, cxa = cx;
         cxb.stream = s_lo;
-        cxb.splitk = nullptr;  // the split-K scratch belongs to the critical stream
-        cxb.splitk_elems = 0;
+        cxa.stream = s_aux;
+        for (Ctx* c : {&cxb, &cxa}) {  // the split-K scratch belongs to the critical stream
+            c->splitk = nullptr;
+            c->splitk_elems = 0;
+        }
+        cxa.timer = nullptr;
         Timer tm;
         if (opts && opts->phase_ms) {
             tm.on = true;
@@ -476,24 +685,27 @@ static int factor_ex_impl(int64_t m, int64_t n, double* A, int64_t lda, int64_t 
             cx.timer = &tm;
             cxb.timer = &tm;
         }
+        Sched sc;
+        if (!(opts && opts->no_lookahead)) {
+            sc.bulk = &cxb;
+            sc.aux = &cxa;
+            sc.ev_top = ev_top;
+            sc.ev_bulk = ev_bulk;
+        }
         int64_t ell = -1;
         int status = 0;
         auto cleanup = [&]() {
-            cudaEventRecord(ev_hi_done, s_hi);
-            cudaStreamWaitEvent(user, ev_hi_done, 0);
-            cudaEventRecord(ev_bulk, s_lo);
-            cudaStreamWaitEvent(user, ev_bulk, 0);
-            cudaStreamDestroy(s_hi);
-            cudaStreamDestroy(s_lo);
-            cudaEventDestroy(ev_in);
-            cudaEventDestroy(ev_top);
-            cudaEventDestroy(ev_bulk);
-            cudaEventDestroy(ev_hi_done);
+            for (cudaStream_t st : {s_hi, s_lo, s_aux}) {
+                cudaEventRecord(ev_done, st);
+                cudaStreamWaitEvent(user, ev_done, 0);
+            }
+            for (cudaStream_t st : {s_hi, s_lo, s_aux}) cudaStreamDestroy(st);
+            for (cudaEvent_t e : {ev_in, ev_top, ev_bulk, ev_done}) cudaEventDestroy(e);
             cx.stream = user;
         };
         try {
-            ell = factor_impl(cx, (opts && opts->no_lookahead) ? nullptr : &cxb, ev_top, ev_bulk, m, n, A, lda, b, d,
-                              seed, tau, J, rank_tol, passes, !(opts && opts->no_hqr_fallback), pinned_flags(), hio);
+            ell = factor_impl(cx, sc, m, n, A, lda, b, d, seed, tau, J, rank_tol, passes,
+                              !(opts && opts->no_hqr_fallback), pinned_flags(), hio);
         } catch (...) {
             cleanup();
             if (own) cudaFreeAsync(ws, user);
@@ -766,8 +978,8 @@ int bqrrp_debug_panel(int64_t h, int64_t k, int64_t t, double* P, int64_t ld, co
         double* Tb = cx.alloc((size_t)k * k);
         double* W = cx.alloc((size_t)k * (t + 1));
         double* W2 = cx.alloc((size_t)k * (t + 1));
-        panel_factor(cx, h, P, ld, 0, k, Rsk11, tau, cholqr_passes, V, Tb);
-        wy_update(cx, nullptr, h, k + t, P, ld, 0, k, V, Tb, W, W2, nullptr, nullptr);
+        panel_factor(cx, h, P, ld, k, Rsk11, tau, cholqr_passes, V, Tb);
+        wy_update(cx, h, k, t, V, h, Tb, P + k * ld, ld, W, W2);
         int* hf = pinned_flags();
         BQ_CUDA(cudaMemcpyAsync(hf, cx.flags, sizeof(int) * F_NFLAGS, cudaMemcpyDeviceToHost, cx.stream));
         cudaFreeAsync(ws, cx.stream);
@@ -790,7 +1002,7 @@ const char* bqrrp_strerror(int status)
 
 const char* bqrrp_last_error(void) { return g_last_error.c_str(); }
 
-unsigned long long bqrrp_launch_count(void) { return g_launches; }
+unsigned long long bqrrp_launch_count(void) { return g_launches.load(); }
 
 long long bqrrp_panel_fallbacks(void) { return g_panel_fallbacks; }
 

@@ -1,8 +1,57 @@
 // bqrrp_internal.cuh — internal interfaces between the BQRRP kernels and the driver.
 #pragma once
+#include <string>
+
+#include "../../include/bqrrp.h"
 #include "common.cuh"
 
 namespace bqrrp {
+
+// ---- driver plumbing shared by the one-GPU (bqrrp.cu) and the multi-GPU (dist.cu) entries
+struct Layout {
+    size_t persistent, temp, splitk, total;
+};
+// workspace of bqrrp_factor: persistent buffers, temporaries, split-K slices (the slice capacity is part of
+// the split-K decision, so the multi-GPU driver carves the same splitk size as the one-GPU run)
+Layout layout(int64_t m, int64_t n, int64_t b, int64_t d);
+void setup_ctx(Ctx& cx, void* stream);
+void carve(Ctx& cx, void* ws, size_t bytes, const Layout& L);
+int* pinned_flags();
+extern thread_local std::string g_last_error;
+
+struct NcclError : std::runtime_error {
+    explicit NcclError(const std::string& s) : std::runtime_error(s) {}
+};
+
+// Exceptions -> C-ABI status codes (+ the thread-local message).
+template <typename F>
+int guarded(F&& f)
+{
+    try {
+        return f();
+    } catch (const CudaError& e) {
+        g_last_error = e.what();
+        return BQRRP_ECUDA;
+    } catch (const NcclError& e) {
+        g_last_error = e.what();
+        return BQRRP_ENCCL;
+    } catch (const std::bad_alloc& e) {
+        g_last_error = e.what();
+        return BQRRP_ENOMEM;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return std::string(e.what()).find("workspace") != std::string::npos ? BQRRP_ENOMEM : BQRRP_ECUDA;
+    }
+}
+
+// small step kernels of the driver (bqrrp.cu): J = 1..n; flags[F_NONFINITE] if X has a non-finite entry;
+// flags[F_K] = tri_rank (readings Z10 / Z11) and the zero-column flag armed; the zero-column test
+// clears it; R_sk11 (k x k upper, ld k) out of the transposed sketch window
+void init_j(Ctx& cx, int64_t n, int64_t* J);
+void nonfinite_check(Ctx& cx, int64_t rows, int64_t cols, const double* X, int64_t ldx);
+void tri_rank_flags(Ctx& cx, const double* MskT_s, int64_t ldm, int64_t kmax, bool first, double rank_tol, double* ref);
+void zero_col_flag(Ctx& cx, int64_t h, const double* col);
+void extract_rsk11(Ctx& cx, int64_t k, const double* MskT_s, int64_t ldm, double* R);
 
 // Touched set of the local permutation J_qr (positions relative to s).
 struct Touched {
@@ -21,6 +70,10 @@ void sketch_apply(Ctx& cx, int64_t m, int64_t n, const double* A, int64_t lda, i
 // a2: partial-pivot LU of the w x d matrix L (in place), ipiv[j] = 0-based pivot row, j < min(w,d);
 // perm (w) = the row permutation of piv_transform (J_qr - 1).
 void getrf_pivots(Ctx& cx, double* L, int64_t ld, int64_t w, int64_t d, int* ipiv, int* perm);
+// Largest sketch-transpose height (w = n - s rows) K-LU's grid leaf holds; largest panel height the
+// Householder panel (HQR variant and CholQR-breakdown fallback) holds.  Checked before any launch.
+int64_t lu_max_rows(int num_sms);
+int64_t qr_max_rows(int num_sms);
 // Householder QR (GEQRF semantics, convention H) of A (rows x cols, lda) in place: R on/above the
 // diagonal, reflectors below; V (rows x cols, ld rows) explicit, T (cols x cols) the compact-WY factor.
 void householder_panel(Ctx& cx, double* A, int64_t lda, int64_t rows, int64_t cols, double* tau, double* V, double* T);
@@ -59,7 +112,8 @@ void permute_vector(Ctx& cx, int64_t* J, const Touched& T, int64_t* tmp);
 extern thread_local long long g_panel_fallbacks;
 // hqr_fallback: after the Cholesky passes, read the POTRF breakdown flag (one host sync) and on a breakdown
 // factor this panel with Householder QR instead (returns 1; 0 otherwise; the flag is cleared).
-int panel_factor(Ctx& cx, int64_t m, double* A, int64_t lda, int64_t s, int64_t k, const double* Rsk11, double* tau,
+// The panel Ap (h x k, lda: A(s:m, s:s+k) in place, or the lookahead's gathered copy), tau = tau + s.
+int panel_factor(Ctx& cx, int64_t h, double* Ap, int64_t lda, int64_t k, const double* Rsk11, double* tau,
                  int passes, double* V, double* T, bool hqr_fallback = false, Ctx* side = nullptr);
 // Phases of the CholQR panel (panel.cu), on a block of panel rows unless k x k:
 //   M_pre = P R_sk11^{-1} -> Q (ld ldq), G = M_pre^T M_pre (lower; zero if rows == 0)
@@ -78,9 +132,30 @@ void recon_finish(Ctx& cx, int64_t k, const double* Wr, const double* S, const d
 void write_panel(Ctx& cx, int64_t h, int64_t k, double* Q, int64_t ldq, const double* R, const double* S, double* Ap,
                  int64_t lda);
 void force_breakdown_hook(Ctx& cx);
-// a5: C = A(s:m, s+k:n) <- C - V T^T (V^T C).  With cx_bulk, rows k:h of the last GEMM run on
-// cx_bulk->stream after ev_top (recorded on cx.stream), and ev_bulk marks their completion.
-void wy_update(Ctx& cx, Ctx* cx_bulk, int64_t m, int64_t n, double* A, int64_t lda, int64_t s, int64_t k,
-               const double* V, const double* T, double* W, double* W2, cudaEvent_t ev_top, cudaEvent_t ev_bulk);
+// a5: C (h x t, ldc) <- C - V T^T (V^T C) (panel.cu): one stream (wy_update), or split for the lookahead into the
+// critical part (wy_top with rows = k: W, W2 = T^T W, R12) and the bulk rows k:h (wy_bulk, on the bulk stream,
+// fixed tiles, optional tile handshake).  V explicit h x k (ld ldv), T k x k upper, W / W2 k x t (ld k).
+void wy_update(Ctx& cx, int64_t h, int64_t k, int64_t t, const double* V, int64_t ldv, const double* T, double* C,
+               int64_t ldc, double* W, double* W2);
+// split_n: the split-K decisions of the per-column GEMMs taken for a t = split_n wide update (multi-GPU: the
+// whole trailing width, so each rank's columns get the one-GPU bits; 0 = t)
+void wy_top(Ctx& cx, int64_t h, int64_t k, int64_t t, const double* V, int64_t ldv, const double* T, double* C,
+            int64_t ldc, double* W, double* W2, int64_t rows, int64_t split_n = 0);
+void wy_bulk(Ctx& cb, int64_t h, int64_t k, int64_t t, const double* V, int64_t ldv, const double* W2, double* C,
+             int64_t ldc, int* hs_state, int* hs_readers);
+
+// a3 for the pivot-aware lookahead (perm.cu).  The next panel's columns (positions q < nq of the
+// next window, source perm[q]) of the trailing block C (rows x w, ldc) while the bulk GEMM (fixed 64 x 64 tiles,
+// tiles_n tile columns) may be updating C:
+//   la_gather_pre: P(:, q) = C(:, perm[q]) for every 64-row tile the bulk has not started (copied under the
+//                  tile's reader count); post[R + q * tiles_m] = 1 for the others;
+//   la_gather_post: P(R rows, q) = C(R rows, perm[q]) for the marked tiles once the bulk has written them.
+// gather_cols_idx: dst(:, q) = X(:, idx[q]) for q < nq.
+void la_gather_pre(Ctx& cx, int64_t rows, const double* C, int64_t ldc, const int* perm, int64_t nq, int64_t tiles_n,
+                   int* hs_state, int* hs_readers, double* P, int64_t ldp, int* post);
+void la_gather_post(Ctx& cx, int64_t rows, const double* C, int64_t ldc, const int* perm, int64_t nq, int64_t tiles_n,
+                    const int* hs_state, double* P, int64_t ldp, const int* post);
+void gather_cols_idx(Ctx& cx, int64_t rows, const double* X, int64_t ldx, const int* idx, int64_t nq, double* dst,
+                     int64_t ldd);
 
 }  // namespace bqrrp

@@ -1,6 +1,7 @@
 // common.cuh — shared plumbing of the BQRRP CUDA library (no method arithmetic here).
 #pragma once
 #include <cuda_runtime.h>
+#include <atomic>
 #include <cstdint>
 #include <cstdio>
 #include <stdexcept>
@@ -24,13 +25,30 @@ struct CudaError : std::runtime_error {
     } while (0)
 
 // Every kernel launch of the library is followed by BQ_LAUNCH_CHECK (or counted explicitly for
-// cooperative launches): g_launches is the count bqrrp_launch_count() reports.
-extern unsigned long long g_launches;
+// cooperative launches): g_launches is the count bqrrp_launch_count() reports (atomic: calls on
+// several host threads / streams are allowed).
+extern std::atomic<unsigned long long> g_launches;
 #define BQ_LAUNCH_CHECK()                \
     do {                                 \
         ++::bqrrp::g_launches;           \
         BQ_CUDA(cudaGetLastError());     \
     } while (0)
+
+// Kernel attributes (dynamic shared memory above 48 KB, non-portable cluster sizes) are per DEVICE: each
+// call site keeps one bit per device that has been configured (a race only repeats the idempotent call).
+struct AttrOnce {
+    std::atomic<unsigned long long> done{0};
+};
+template <typename K>
+inline void ensure_attr(AttrOnce& o, K* kernel, cudaFuncAttribute attr, int value)
+{
+    int dev = 0;
+    BQ_CUDA(cudaGetDevice(&dev));
+    const unsigned long long bit = 1ull << (dev & 63);
+    if (o.done.load(std::memory_order_acquire) & bit) return;
+    BQ_CUDA(cudaFuncSetAttribute((const void*)kernel, attr, value));
+    o.done.fetch_or(bit, std::memory_order_release);
+}
 
 inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 inline int64_t imin(int64_t a, int64_t b) { return a < b ? a : b; }
@@ -133,6 +151,7 @@ struct Ctx {
     size_t splitk_elems = 0;
     int* flags = nullptr;  // device int[8]: see Flags
     Timer* timer = nullptr;
+    bool force_breakdown = false;  // test hook (bqrrp_options.debug_flags): report a POTRF breakdown per panel
     void mark(int phase) { if (timer) timer->mark(phase); }
 
     double* alloc(size_t n_doubles)
@@ -149,6 +168,22 @@ struct Ctx {
         return reinterpret_cast<T*>(alloc((n * sizeof(T) + 7) / 8));
     }
 };
+
+// A context for work queued on a second stream.  Its bump allocator is an arena reserved on the main
+// context (later main-stream allocations cannot overlap it); it has no split-K slices (those belong to the
+// main stream) and no timer.  The main context releases the arena (resets ws_used below it) only after its
+// stream has waited for the side stream's work.
+inline Ctx side_ctx(Ctx& main, const Ctx& side, size_t arena_doubles)
+{
+    Ctx sc = side;
+    sc.splitk = nullptr;
+    sc.splitk_elems = 0;
+    sc.timer = nullptr;
+    sc.ws = arena_doubles ? reinterpret_cast<char*>(main.alloc(arena_doubles)) : nullptr;
+    sc.ws_bytes = arena_doubles * sizeof(double);
+    sc.ws_used = 0;
+    return sc;
+}
 
 // Device flag slots (int) written by kernels and read back once per iteration.
 enum Flags { F_K = 0, F_ZERO_COL = 1, F_POTRF_INFO = 2, F_NONFINITE = 3, F_NT = 4, F_NFLAGS = 8 };

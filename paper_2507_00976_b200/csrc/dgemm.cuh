@@ -120,7 +120,26 @@ struct GemmArgs {
     double* ws;      // split-K slices (M x N each, ld M) or nullptr
     int64_t kchunk;  // K range per split (multiple of BK)
     int tri;         // 1: only tiles touching the lower triangle (m >= n) are computed
+    int a_lower;     // 1: op(A) is lower triangular (TRMM): the K range of row tile m0 ends at m0 + BM (v2)
+    // Tile handshake with a concurrent reader of C (v2, the pivot-aware lookahead).  Per
+    // output tile (tile_m * tiles_n + tile_n): hs_state 0 = not started, 1 = started, 2 = written;
+    // hs_readers = readers currently copying the tile's PRE-update values.  A CTA publishes 1 (SC fence)
+    // before anything else, waits for hs_readers == 0 before its epilogue stores, and publishes 2 after.
+    int* hs_state;
+    int* hs_readers;
 };
+
+__device__ __forceinline__ int ld_acquire_gpu(const int* p)
+{
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_gpu(int* p, int v)
+{
+    asm volatile("st.release.gpu.global.b32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void fence_sc_gpu() { asm volatile("fence.sc.gpu;\n" ::: "memory"); }
 
 template <int BM_, int BN_, int WARPS_M_, int WARPS_N_, int STAGES_>
 struct GemmCfg {
@@ -444,8 +463,14 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS) dgemm2_kernel(G
     const int64_t m0 = tile_m * BM, n0 = tile_n * BN;
     if (g.tri && m0 + BM <= n0) continue;
     const int64_t kbeg = (int64_t)blockIdx.z * g.kchunk;
-    const int64_t kend = (kbeg + g.kchunk < g.K) ? kbeg + g.kchunk : g.K;
+    int64_t kend = (kbeg + g.kchunk < g.K) ? kbeg + g.kchunk : g.K;
+    if (g.a_lower && kend > m0 + BM) kend = (m0 + BM > kbeg) ? m0 + BM : kbeg;  // op(A)(r, k) = 0 for k > r
     const int nk = (int)((kend - kbeg + BK - 1) / BK);
+    int* const hs_st = g.hs_state ? g.hs_state + (tile_m * tiles_n + tile_n) : nullptr;
+    if (hs_st && tid == 0) {
+        atomicExch(hs_st, 1);
+        fence_sc_gpu();  // Dekker with the reader: its (readers++, fence.sc, read state) vs (state = 1, fence.sc)
+    }
 
     const int gid = lane >> 2, tig = lane & 3;
     // fragment -> matrix index maps (interleaved for MN-major operands, see above)
@@ -561,6 +586,11 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS) dgemm2_kernel(G
                     if (r < g.M && c < g.N) W[r + c * g.M] = acc[i][j][h];
                 }
     } else {
+    if (hs_st) {  // no store while a reader is copying this tile's pre-update values
+        if (tid == 0)
+            while (ld_acquire_gpu(g.hs_readers + (hs_st - g.hs_state)) != 0) __nanosleep(64);
+        __syncthreads();
+    }
 #pragma unroll
     for (int i = 0; i < MI; ++i)
 #pragma unroll
@@ -577,6 +607,10 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS) dgemm2_kernel(G
             }
     }
     __syncthreads();  // the next tile's prologue overwrites stages other warps may still be reading
+    if (hs_st && tid == 0) {
+        __threadfence();
+        st_release_gpu(hs_st, 2);
+    }
   }
 }
 

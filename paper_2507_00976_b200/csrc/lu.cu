@@ -564,14 +564,9 @@ __global__ void __launch_bounds__(LU_THREADS, 1) lu_leaf_reg_kernel(LuPanelArgs 
 
 static bool lu_reg_fits(int64_t rows)
 {
-    static int use = -1;
-    if (use < 0) {  // BQRRP_LU_LEAF=0: the shared-memory slab kernels only (A/B)
-        const char* e = std::getenv("BQRRP_LU_LEAF");
-        use = (e && e[0] == '0') ? 0 : 1;
-    }
     // one row per thread: with two rows per thread it measured slower than the shared-memory cluster kernel
     // (8192 rows: 8.5 vs 6.5 us per column), at <= 4096 rows slightly faster (5.7-5.9 vs 5.9-6.1)
-    return use && rows <= (int64_t)LR_CLMAX * LU_THREADS;
+    return rows <= (int64_t)LR_CLMAX * LU_THREADS;
 }
 
 static bool lu_panel_reg(Ctx& cx, double* L, int64_t ld, int64_t w, int64_t d, int64_t c0, int jb, int* ipiv, int* perm)
@@ -581,12 +576,9 @@ static bool lu_panel_reg(Ctx& cx, double* L, int64_t ld, int64_t w, int64_t d, i
     const int rpt = rows <= (int64_t)LR_CLMAX * LU_THREADS ? 1 : 2;
     const int G = (int)cdiv(rows, (int64_t)LU_THREADS * rpt);
     LuPanelArgs a{L, ld, w, d, c0, jb, LU_THREADS * rpt, ipiv, perm, nullptr, nullptr};
-    static bool attr = false;
-    if (!attr) {
-        BQ_CUDA(cudaFuncSetAttribute(lu_leaf_reg_kernel<1>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-        BQ_CUDA(cudaFuncSetAttribute(lu_leaf_reg_kernel<2>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-        attr = true;
-    }
+    static AttrOnce attr1, attr2;
+    ensure_attr(attr1, lu_leaf_reg_kernel<1>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    ensure_attr(attr2, lu_leaf_reg_kernel<2>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(G);
     cfg.blockDim = dim3(LU_THREADS);
@@ -624,13 +616,9 @@ static bool lu_panel_cluster(Ctx& cx, double* L, int64_t ld, int64_t w, int64_t 
 {
     int CL, R;
     if (!lu_cluster_fits(w - c0, jb, &CL, &R)) return false;
-    static bool attr = false;
-    if (!attr) {
-        BQ_CUDA(cudaFuncSetAttribute(lu_panel_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)LUC_SMEM_MAX));
-        BQ_CUDA(cudaFuncSetAttribute(lu_panel_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-        attr = true;
-    }
+    static AttrOnce attr_smem, attr_cl;
+    ensure_attr(attr_smem, lu_panel_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LUC_SMEM_MAX);
+    ensure_attr(attr_cl, lu_panel_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     LuPanelArgs a{L, ld, w, d, c0, jb, R, ipiv, perm, nullptr, nullptr};
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(CL);
@@ -671,12 +659,10 @@ static void lu_panel(Ctx& cx, double* L, int64_t ld, int64_t w, int64_t d, int64
         R = (int)cdiv(rows, G);
     }
     size_t smem = (size_t)R * jb * sizeof(double);
-    if (smem > 200 * 1024) throw std::runtime_error("lu_panel: panel too tall for shared memory");
-    static bool attr = false;
-    if (!attr) {
-        BQ_CUDA(cudaFuncSetAttribute(lu_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        attr = true;
-    }
+    if (smem > 200 * 1024)
+        throw std::runtime_error("lu_panel: sketch transpose taller than lu_max_rows (" + std::to_string(rows) + " rows)");
+    static AttrOnce attr;
+    ensure_attr(attr, lu_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     LuPanelArgs a{L, ld, w, d, c0, jb, R, ipiv, perm, xbuf, rowj};
     void* args[] = {&a};
     BQ_CUDA(cudaLaunchCooperativeKernel((void*)lu_panel_kernel, dim3(G), dim3(LU_THREADS), args, smem, cx.stream));
@@ -690,11 +676,16 @@ static int lu_leaf_width(int64_t rows, int num_sms)
     int CL, R;
     if (lu_cluster_fits(rows, 32, &CL, &R)) return 32;
     if (lu_cluster_fits(rows, 16, &CL, &R)) return 16;
-    int64_t Rg = cdiv(rows, num_sms);
-    if (Rg * 32 * 8 <= 200 * 1024) return 32;
-    if (Rg * 16 * 8 <= 200 * 1024) return 16;
-    return 8;
+    // the cooperative grid leaf keeps a slab of cdiv(rows, num_sms) rows x leaf columns per CTA in shared
+    // memory: narrower leaves for taller sketches (down to one column: 148 x 25600 rows; taller inputs are
+    // rejected up front, lu_max_rows)
+    const int64_t Rg = cdiv(rows, num_sms);
+    for (int leaf = 32; leaf > 1; leaf /= 2)
+        if (Rg * leaf * 8 <= 200 * 1024) return leaf;
+    return 1;
 }
+
+int64_t lu_max_rows(int num_sms) { return (int64_t)num_sms * (200 * 1024 / 8); }
 
 static void getrf_rec(Ctx& cx, double* L, int64_t ld, int64_t w, int64_t d, int64_t c0, int64_t c1, int* ipiv,
                       int* perm, LuExchange& ex, int leaf)

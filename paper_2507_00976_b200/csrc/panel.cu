@@ -129,18 +129,16 @@ void write_panel(Ctx& cx, int64_t h, int64_t k, double* Q, int64_t ldq, const do
 
 void force_breakdown_hook(Ctx& cx)
 {
-    // test hook: BQRRP_DEBUG_FORCE_BREAKDOWN=1 reports a POTRF breakdown on every panel, so the fallback /
-    // error path is exercised deterministically (a real breakdown depends on rounding)
-    const char* f = std::getenv("BQRRP_DEBUG_FORCE_BREAKDOWN");
-    if (f && f[0] == '1') BQ_CUDA(cudaMemsetAsync(cx.flags + F_POTRF_INFO, 1, 1, cx.stream));
+    // test hook (bqrrp_options.debug_flags & BQRRP_DEBUG_FORCE_BREAKDOWN): report a POTRF breakdown on every
+    // panel, so the fallback / error path is exercised deterministically (a real breakdown depends on rounding)
+    if (cx.force_breakdown) BQ_CUDA(cudaMemsetAsync(cx.flags + F_POTRF_INFO, 1, 1, cx.stream));
 }
 
-int panel_factor(Ctx& cx, int64_t m, double* A, int64_t lda, int64_t s, int64_t k, const double* Rsk11, double* tau,
+int panel_factor(Ctx& cx, int64_t h, double* Ap, int64_t lda, int64_t k, const double* Rsk11, double* tau,
                  int passes, double* V, double* T, bool hqr_fallback, Ctx* side)
 {
-    const int64_t h = m - s;
     if (passes == 0) {  // BQRRP_HQR: Householder QR of the panel itself
-        householder_panel(cx, A + s + s * lda, lda, h, k, tau + s, V, T);
+        householder_panel(cx, Ap, lda, h, k, tau, V, T);
         return 0;
     }
     size_t mark = cx.ws_used;
@@ -150,7 +148,6 @@ int panel_factor(Ctx& cx, int64_t m, double* A, int64_t lda, int64_t s, int64_t 
     double* S = cx.alloc((size_t)k);
     double* Wr = cx.alloc((size_t)k * k);
     double* R = cx.alloc((size_t)k * k);
-    double* Ap = A + s + s * lda;
 
     // Cholesky QR passes; the last pass's TRSM is applied only to the top k rows (recon_top_lu) and folded into
     // the reconstruction's TRSM (Y2 = Q_prev,2 C^{-T} U^{-1} = Q_prev,2 (U C^T)^{-1}, recon_rows)
@@ -168,7 +165,7 @@ int panel_factor(Ctx& cx, int64_t m, double* A, int64_t lda, int64_t s, int64_t 
         if (info) {
             BQ_CUDA(cudaMemsetAsync(cx.flags + F_POTRF_INFO, 0, sizeof(int), cx.stream));
             cx.ws_used = mark;
-            householder_panel(cx, Ap, lda, h, k, tau + s, V, T);
+            householder_panel(cx, Ap, lda, h, k, tau, V, T);
             return 1;
         }
     }
@@ -176,19 +173,16 @@ int panel_factor(Ctx& cx, int64_t m, double* A, int64_t lda, int64_t s, int64_t 
     recon_top_lu(cx, k, Q, h, Cl, Wr, S);
     if (side && h > 2 * k) {
         // the k x k finish (T-solve, tau, R products) depends only on Wr and S: run it on the side stream
-        // (idle during the panel) while the main stream does the tall Y2 TRSM; its scratch is carved here
-        // and it uses no split-K slices (those belong to the main stream)
-        double* scr = cx.alloc((size_t)2 * k * k);
+        // (idle during the panel) while the main stream does the tall Y2 TRSM; its scratch (the two k x k
+        // products and the inverse-diagonal blocks of its k x k TRSM) is an arena carved here
+        Ctx sc = side_ctx(cx, *side, (size_t)2 * k * k + (size_t)(cdiv(k, 64) + 1) * 64 * 64 + 64);
+        double* scr = sc.alloc((size_t)2 * k * k);
         cudaEvent_t ef, ej;
         BQ_CUDA(cudaEventCreateWithFlags(&ef, cudaEventDisableTiming));
         BQ_CUDA(cudaEventCreateWithFlags(&ej, cudaEventDisableTiming));
         BQ_CUDA(cudaEventRecord(ef, cx.stream));
         BQ_CUDA(cudaStreamWaitEvent(side->stream, ef, 0));
-        Ctx sc = *side;
-        sc.splitk = nullptr;
-        sc.splitk_elems = 0;
-        sc.timer = nullptr;
-        recon_finish(sc, k, Wr, S, Cf, passes, Rsk11, T, tau + s, R, scr);
+        recon_finish(sc, k, Wr, S, Cf, passes, Rsk11, T, tau, R, scr);
         BQ_CUDA(cudaEventRecord(ej, side->stream));
         recon_rows(cx, h - k, k, Q + k, h, Wr, Cl);
         copy_matrix(cx, k, k, Wr, k, Q, h);  // L \ U on top
@@ -198,37 +192,48 @@ int panel_factor(Ctx& cx, int64_t m, double* A, int64_t lda, int64_t s, int64_t 
     } else {
         if (h > k) recon_rows(cx, h - k, k, Q + k, h, Wr, Cl);
         copy_matrix(cx, k, k, Wr, k, Q, h);  // L \ U on top
-        recon_finish(cx, k, Wr, S, Cf, passes, Rsk11, T, tau + s, R, nullptr);
+        recon_finish(cx, k, Wr, S, Cf, passes, Rsk11, T, tau, R, nullptr);
     }
     write_panel(cx, h, k, Q, h, R, S, Ap, lda);
     cx.ws_used = mark;
     return 0;
 }
 
-void wy_update(Ctx& cx, Ctx* cx_bulk, int64_t m, int64_t n, double* A, int64_t lda, int64_t s, int64_t k,
-               const double* V, const double* T, double* W, double* W2, cudaEvent_t ev_top, cudaEvent_t ev_bulk)
+// a5, one stream: C (h x t) <- C - V T^T (V^T C): W = V^T C, W2 = T^T W (TRMM: T upper), C -= V W2.
+void wy_update(Ctx& cx, int64_t h, int64_t k, int64_t t, const double* V, int64_t ldv, const double* T, double* C,
+               int64_t ldc, double* W, double* W2)
 {
-    const int64_t h = m - s, t = n - s - k;
     if (t <= 0) return;
-    double* C = A + s + (s + k) * lda;
-    gemm(cx, true, false, k, t, h, 1.0, V, h, C, lda, 0.0, W, k);   // W  = V^T C
-    gemm(cx, true, false, k, t, k, 1.0, T, k, W, k, 0.0, W2, k);    // W2 = T^T W
-    if (!cx_bulk || h <= k) {
-        gemm(cx, false, false, h, t, k, -1.0, V, h, W2, k, 1.0, C, lda);  // C -= V W2
-        return;
-    }
-    // rows 0:k (R12, needed next by the sketch update) on the critical stream; rows k:h (the bulk,
-    // needed only by the next column permutation) on the bulk stream
-    gemm(cx, false, false, k, t, k, -1.0, V, h, W2, k, 1.0, C, lda);
-    BQ_CUDA(cudaEventRecord(ev_top, cx.stream));
-    BQ_CUDA(cudaStreamWaitEvent(cx_bulk->stream, ev_top, 0));
-    if (cx_bulk->timer) cx_bulk->timer->begin_interval(cx_bulk->stream, PH_APPLY_QT_BULK);
-    // one CTA per tile: the high-priority GEMMs of the sketch update and the next pivot selection take SMs
-    // as the bulk's CTAs retire (a persistent bulk with 2-4 CTAs/SM starved them: C3 +0.5-0.8 s,
-    // profiles/bulk_persistent_r01.json)
-    gemm(*cx_bulk, false, false, h - k, t, k, -1.0, V + k, h, W2, k, 1.0, C + k, lda);
-    if (cx_bulk->timer) cx_bulk->timer->end_interval(cx_bulk->stream);
-    BQ_CUDA(cudaEventRecord(ev_bulk, cx_bulk->stream));
+    wy_top(cx, h, k, t, V, ldv, T, C, ldc, W, W2, /*rows=*/h);
+}
+
+// a5 critical part: W = V^T C (K = h), W2 = T^T W, and C(0:rows) -= V(0:rows) W2 (rows = k: R12 only, the
+// bulk rows k:h follow on the bulk stream, wy_bulk; rows = h: the whole update).
+void wy_top(Ctx& cx, int64_t h, int64_t k, int64_t t, const double* V, int64_t ldv, const double* T, double* C,
+            int64_t ldc, double* W, double* W2, int64_t rows, int64_t split_n)
+{
+    if (t <= 0) return;
+    GemmExtra hint, trmm;
+    hint.split_n = trmm.split_n = split_n;
+    trmm.a_lower = true;
+    gemm(cx, true, false, k, t, h, 1.0, V, ldv, C, ldc, 0.0, W, k, false, 0, false, &hint);        // W  = V^T C
+    gemm(cx, true, false, k, t, k, 1.0, T, k, W, k, 0.0, W2, k, false, 0, false, &trmm);           // W2 = T^T W
+    gemm(cx, false, false, rows, t, k, -1.0, V, ldv, W2, k, 1.0, C, ldc, false, 0, false, &hint);  // C -= V W2
+}
+
+// a5 bulk rows k:h on the bulk context: C(k:h) -= V(k:h) W2, in fixed 64 x 64 tiles (bitwise the values the
+// lookahead's panel gather computes for its columns) with the tile handshake when hs_state is given.
+// One CTA per tile: the high-priority GEMMs of the critical chain take SMs as the bulk's CTAs retire (a
+// persistent bulk with 2-4 CTAs/SM starved them: C3 +0.5-0.8 s, profiles/bulk_persistent_r01.json).
+void wy_bulk(Ctx& cb, int64_t h, int64_t k, int64_t t, const double* V, int64_t ldv, const double* W2, double* C,
+             int64_t ldc, int* hs_state, int* hs_readers)
+{
+    if (t <= 0 || h <= k) return;
+    GemmExtra x;
+    x.fixed_tiles = true;
+    x.hs_state = hs_state;
+    x.hs_readers = hs_readers;
+    gemm(cb, false, false, h - k, t, k, -1.0, V + k, ldv, W2, k, 1.0, C + k, ldc, false, 0, true, &x);
 }
 
 }  // namespace bqrrp

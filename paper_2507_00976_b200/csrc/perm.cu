@@ -39,16 +39,30 @@ __global__ void perm_from_ipiv_kernel(int64_t w, int64_t nlu, const int64_t* __r
     }
 }
 
-// scratch(:, t) = X(:, src[t]) for all `rows` rows; column-contiguous copies, 2-D grid (t, row chunk).
+// One column segment d[0:rows] = s[0:rows], by the CTA slice (chunk, nchunks): 16-byte copies when both
+// columns are 16-byte aligned (even leading dimensions, the usual case), 8-byte otherwise.  Coalesced: the
+// thread-fastest index is the row.
+__device__ __forceinline__ void copy_col(double* __restrict__ d, const double* __restrict__ s, int64_t rows, int64_t chunk,
+                                         int64_t nchunks)
+{
+    if (((((uintptr_t)d) | ((uintptr_t)s)) & 15) == 0) {
+        const int64_t pairs = rows >> 1;
+        const double2* s2 = reinterpret_cast<const double2*>(s);
+        double2* d2 = reinterpret_cast<double2*>(d);
+        for (int64_t p = chunk * blockDim.x + threadIdx.x; p < pairs; p += nchunks * blockDim.x) d2[p] = __ldg(s2 + p);
+        if ((rows & 1) && chunk == 0 && threadIdx.x == 0) d[rows - 1] = s[rows - 1];
+    } else {
+        for (int64_t r = chunk * blockDim.x + threadIdx.x; r < rows; r += nchunks * blockDim.x) d[r] = s[r];
+    }
+}
+
+// scratch(:, t) = X(:, src[t]) for all `rows` rows; 2-D grid (row chunk, t).
 __global__ void gather_cols_kernel(int64_t rows, const double* __restrict__ X, int64_t ldx, const int* __restrict__ src,
                                    const int* __restrict__ nt, double* __restrict__ scratch, int64_t lds)
 {
     int t = blockIdx.y;
     if (t >= *nt) return;
-    const double* s = X + (int64_t)src[t] * ldx;
-    double* d = scratch + (int64_t)t * lds;
-    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x)
-        d[r] = s[r];
+    copy_col(scratch + (int64_t)t * lds, X + (int64_t)src[t] * ldx, rows, blockIdx.x, gridDim.x);
 }
 
 __global__ void scatter_cols_kernel(int64_t rows, double* __restrict__ X, int64_t ldx, const int* __restrict__ dst,
@@ -56,10 +70,80 @@ __global__ void scatter_cols_kernel(int64_t rows, double* __restrict__ X, int64_
 {
     int t = blockIdx.y;
     if (t >= *nt) return;
-    double* d = X + (int64_t)dst[t] * ldx;
-    const double* s = scratch + (int64_t)t * lds;
-    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x)
-        d[r] = s[r];
+    copy_col(X + (int64_t)dst[t] * ldx, scratch + (int64_t)t * lds, rows, blockIdx.x, gridDim.x);
+}
+
+// dst(:, q) = X(:, idx[q]), q < nq (grid (row chunk, q)).
+__global__ void gather_idx_kernel(int64_t rows, const double* __restrict__ X, int64_t ldx, const int* __restrict__ idx,
+                                  double* __restrict__ dst, int64_t ldd)
+{
+    const int q = blockIdx.y;
+    copy_col(dst + (int64_t)q * ldd, X + (int64_t)idx[q] * ldx, rows, blockIdx.x, gridDim.x);
+}
+
+// ---- pivot-aware lookahead gathers.  Warp per (64-row tile R, panel column q); the bulk
+// GEMM's tile holding those rows of column perm[q] is T = R * tiles_n + perm[q] / 64.
+constexpr int LA_TILE = 64;
+
+__device__ __forceinline__ int la_ld_acquire(const int* p)
+{
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// C is read through L2 (ld.global.cg: never a stale L1 line) and is not __restrict__: the bulk GEMM writes it
+// concurrently (other tiles).
+__global__ void la_gather_pre_kernel(int64_t rows, const double* C, int64_t ldc, const int* __restrict__ perm,
+                                     int64_t nq, int64_t tiles_n, int* hs_state, int* hs_readers, double* __restrict__ P,
+                                     int64_t ldp, int* post)
+{
+    const int lane = threadIdx.x & 31;
+    const int64_t q = (int64_t)blockIdx.y * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int64_t R = blockIdx.x;
+    if (q >= nq) return;
+    const int src = perm[q];
+    const int64_t T = R * tiles_n + src / LA_TILE;
+    int pre = 0;
+    if (lane == 0) {
+        // Dekker with the bulk CTA of T: (readers++, fence.sc, read state) vs its (state = 1, fence.sc, read
+        // readers): either we see "started" or it sees our reader and holds its stores until we are done
+        atomicAdd(hs_readers + T, 1);
+        asm volatile("fence.sc.gpu;\n" ::: "memory");
+        pre = (la_ld_acquire(hs_state + T) == 0);
+        if (!pre) atomicSub(hs_readers + T, 1);
+    }
+    pre = __shfl_sync(0xffffffffu, pre, 0);
+    if (lane == 0) post[R + q * gridDim.x] = pre ? 0 : 1;
+    if (!pre) return;
+    const int64_t r0 = R * LA_TILE;
+    const double* s = C + (int64_t)src * ldc;
+    double* d = P + q * ldp;
+    for (int64_t r = r0 + lane; r < r0 + LA_TILE && r < rows; r += 32) d[r] = __ldcg(s + r);
+    __syncwarp();
+    if (lane == 0) {
+        __threadfence();  // the warp's loads are complete (their values are stored) before the release
+        atomicSub(hs_readers + T, 1);
+    }
+}
+
+__global__ void la_gather_post_kernel(int64_t rows, const double* C, int64_t ldc, const int* __restrict__ perm,
+                                      int64_t nq, int64_t tiles_n, const int* hs_state, double* __restrict__ P, int64_t ldp,
+                                      const int* post)
+{
+    const int lane = threadIdx.x & 31;
+    const int64_t q = (int64_t)blockIdx.y * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int64_t R = blockIdx.x;
+    if (q >= nq || !post[R + q * gridDim.x]) return;
+    const int src = perm[q];
+    const int64_t T = R * tiles_n + src / LA_TILE;
+    if (lane == 0)
+        while (la_ld_acquire(hs_state + T) != 2) __nanosleep(128);
+    __syncwarp();
+    const int64_t r0 = R * LA_TILE;
+    const double* s = C + (int64_t)src * ldc;
+    double* d = P + q * ldp;
+    for (int64_t r = r0 + lane; r < r0 + LA_TILE && r < rows; r += 32) d[r] = __ldcg(s + r);
 }
 
 // Rows of a column-major matrix (cols columns): scratch[t + c*maxnt] = X[src[t] + c*ldx].
@@ -136,6 +220,34 @@ void permute_vector(Ctx& cx, int64_t* J, const Touched& T, int64_t* tmp)
 {
     if (T.maxnt <= 0) return;
     permute_vec_kernel<<<1, 1024, 0, cx.stream>>>(J, T.tq, T.tsrc, T.nt, tmp);
+    BQ_LAUNCH_CHECK();
+}
+
+void gather_cols_idx(Ctx& cx, int64_t rows, const double* X, int64_t ldx, const int* idx, int64_t nq, double* dst,
+                     int64_t ldd)
+{
+    if (rows <= 0 || nq <= 0) return;
+    dim3 grid((unsigned)imin(cdiv(rows, 256 * 8), 64), (unsigned)nq);
+    gather_idx_kernel<<<grid, 256, 0, cx.stream>>>(rows, X, ldx, idx, dst, ldd);
+    BQ_LAUNCH_CHECK();
+}
+
+void la_gather_pre(Ctx& cx, int64_t rows, const double* C, int64_t ldc, const int* perm, int64_t nq, int64_t tiles_n,
+                   int* hs_state, int* hs_readers, double* P, int64_t ldp, int* post)
+{
+    if (rows <= 0 || nq <= 0) return;
+    dim3 grid((unsigned)cdiv(rows, LA_TILE), (unsigned)cdiv(nq, 8));
+    la_gather_pre_kernel<<<grid, 256, 0, cx.stream>>>(rows, C, ldc, perm, nq, tiles_n, hs_state, hs_readers, P, ldp,
+                                                      post);
+    BQ_LAUNCH_CHECK();
+}
+
+void la_gather_post(Ctx& cx, int64_t rows, const double* C, int64_t ldc, const int* perm, int64_t nq, int64_t tiles_n,
+                    const int* hs_state, double* P, int64_t ldp, const int* post)
+{
+    if (rows <= 0 || nq <= 0) return;
+    dim3 grid((unsigned)cdiv(rows, LA_TILE), (unsigned)cdiv(nq, 8));
+    la_gather_post_kernel<<<grid, 256, 0, cx.stream>>>(rows, C, ldc, perm, nq, tiles_n, hs_state, P, ldp, post);
     BQ_LAUNCH_CHECK();
 }
 

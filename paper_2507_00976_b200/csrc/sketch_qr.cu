@@ -24,6 +24,7 @@ namespace cg = cooperative_groups;
 namespace bqrrp {
 
 constexpr int QR_JBMAX = 32;
+constexpr size_t QR_GRID_SMEM = 200 * 1024;  // slab of the cooperative grid leaf (rows per CTA x leaf width)
 constexpr int QR_XSTRIDE = 1 + QR_JBMAX;  // s2, p[1..jb)
 constexpr int QR_THREADS = 256;
 
@@ -553,21 +554,15 @@ __global__ void __launch_bounds__(QL_THREADS, 1) qr_leaf_reg_kernel(QrLeafArgs a
 static bool qr_leaf_reg(Ctx& cx, double* A, int64_t ld, int64_t m, int64_t c0, int jb, double* tau, double* V,
                         double* T, int64_t ldt)
 {
-    static int use = -1;
-    if (use < 0) {  // BQRRP_QR_LEAF=0: the shared-memory cluster kernel (A/B)
-        const char* e = std::getenv("BQRRP_QR_LEAF");
-        use = (e && e[0] == '0') ? 0 : 1;
-    }
     const int64_t rows = m - c0;
-    const int CL = (int)cdiv(rows, QL_THREADS);
-    if (!use || CL > QL_CLMAX || jb > 32) return false;
+    // at least 2 CTAs: the DSMEM pushes (mapa + st.async) need a real cluster (compute-sanitizer memcheck flags
+    // them in a 1-CTA cluster); a CTA without rows pushes exact zeros, which leave the fixed-order sums unchanged
+    const int CL = (int)imax(2, cdiv(rows, QL_THREADS));
+    if (CL > QL_CLMAX || jb > 32) return false;
     const size_t smem = ((size_t)2 * CL * QL_WARPS * 32 + 64) * sizeof(double);
-    static bool attr = false;
-    if (!attr) {
-        BQ_CUDA(cudaFuncSetAttribute(qr_leaf_reg_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
-        BQ_CUDA(cudaFuncSetAttribute(qr_leaf_reg_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-        attr = true;
-    }
+    static AttrOnce attr_smem, attr_cl;
+    ensure_attr(attr_smem, qr_leaf_reg_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+    ensure_attr(attr_cl, qr_leaf_reg_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     QrLeafArgs args{A, ld, m, c0, jb, tau, V, T, ldt};
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(CL);
@@ -594,11 +589,8 @@ static bool qr_panel_cluster(Ctx& cx, double* A, int64_t ld, int64_t m, int64_t 
     int R = (int)cdiv(rows, CL);
     size_t smem = ((size_t)R * jb + 64 + 64 + 32 * 32) * sizeof(double);
     if (smem > 200 * 1024) return false;
-    static bool attr = false;
-    if (!attr) {
-        BQ_CUDA(cudaFuncSetAttribute(qr_panel_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        attr = true;
-    }
+    static AttrOnce attr;
+    ensure_attr(attr, qr_panel_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     QrClusterArgs args{A, ld, m, c0, jb, R, tau, V, T, ldt};
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(CL);
@@ -626,12 +618,10 @@ static void qr_panel(Ctx& cx, double* A, int64_t ld, int64_t m, int64_t c0, int 
     int G = (int)imin(cx.num_sms, imax(1, cdiv(rows, 64)));
     int R = (int)cdiv(rows, G);
     size_t smem = (size_t)R * jb * sizeof(double);
-    if (smem > 160 * 1024) throw std::runtime_error("qr_panel: panel too tall");
-    static bool attr = false;
-    if (!attr) {
-        BQ_CUDA(cudaFuncSetAttribute(qr_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
-        attr = true;
-    }
+    if (smem > QR_GRID_SMEM)
+        throw std::runtime_error("qr_panel: panel taller than qr_max_rows (" + std::to_string(rows) + " rows)");
+    static AttrOnce attr;
+    ensure_attr(attr, qr_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)QR_GRID_SMEM);
     QrPanelArgs a{A, ld, m, c0, jb, R, tau, V, T, ldt, xbuf, rowj};
     void* args[] = {&a};
     BQ_CUDA(cudaLaunchCooperativeKernel((void*)qr_panel_kernel, dim3(G), dim3(QR_THREADS), args, smem, cx.stream));
@@ -641,16 +631,29 @@ static void qr_panel(Ctx& cx, double* A, int64_t ld, int64_t m, int64_t c0, int 
 // Recursive QR of columns [c0, c1) of Wq (rows [c0, m)); V (m x p explicit), Tf (p x p).
 // Recursive Householder QR of columns [c0, c1) of A (rows [c0, m), leading dimension lda); V (m x p
 // explicit, ld m, pre-zeroed), Tf (p x p, ld p).
+// Leaf width: 32 columns unless the panel is so tall that the cooperative grid leaf's slab (cdiv(rows,
+// num_sms) x leaf doubles per CTA) would not fit shared memory; then narrower, down to one column
+// (num_sms x 25600 rows; taller inputs are rejected up front, qr_max_rows).
+static int qr_leaf_width(int64_t rows, int num_sms)
+{
+    const int64_t Rg = cdiv(rows, num_sms);
+    for (int leaf = QR_JBMAX; leaf > 1; leaf /= 2)
+        if ((size_t)Rg * leaf * 8 <= QR_GRID_SMEM) return leaf;
+    return 1;
+}
+
+int64_t qr_max_rows(int num_sms) { return (int64_t)num_sms * (int64_t)(QR_GRID_SMEM / 8); }
+
 static void geqrf_rec(Ctx& cx, double* A, int64_t lda, int64_t m, int64_t c0, int64_t c1, double* tau, double* V,
-                      double* Tf, int64_t p, double* W1, double* W2, double* xbuf, double* rowj)
+                      double* Tf, int64_t p, double* W1, double* W2, double* xbuf, double* rowj, int leaf)
 {
     int64_t nc = c1 - c0;
-    if (nc <= QR_JBMAX) {
+    if (nc <= leaf) {
         qr_panel(cx, A, lda, m, c0, (int)nc, tau, V, Tf, p, xbuf, rowj);
         return;
     }
-    int64_t mid = c0 + cdiv(nc / 2, QR_JBMAX) * QR_JBMAX;
-    geqrf_rec(cx, A, lda, m, c0, mid, tau, V, Tf, p, W1, W2, xbuf, rowj);
+    int64_t mid = c0 + cdiv(nc / 2, leaf) * leaf;
+    geqrf_rec(cx, A, lda, m, c0, mid, tau, V, Tf, p, W1, W2, xbuf, rowj, leaf);
     int64_t k1 = mid - c0, ncr = c1 - mid, h = m - c0;
     const double* V1 = V + c0 + c0 * m;    // h x k1
     const double* T11 = Tf + c0 + c0 * p;  // k1 x k1
@@ -659,7 +662,7 @@ static void geqrf_rec(Ctx& cx, double* A, int64_t lda, int64_t m, int64_t c0, in
     gemm(cx, true, false, k1, ncr, h, 1.0, V1, m, A2, lda, 0.0, W1, k1);
     gemm(cx, true, false, k1, ncr, k1, 1.0, T11, p, W1, k1, 0.0, W2, k1);
     gemm(cx, false, false, h, ncr, k1, -1.0, V1, m, W2, k1, 1.0, A2, lda);
-    geqrf_rec(cx, A, lda, m, mid, c1, tau, V, Tf, p, W1, W2, xbuf, rowj);
+    geqrf_rec(cx, A, lda, m, mid, c1, tau, V, Tf, p, W1, W2, xbuf, rowj, leaf);
     // T12 = -T11 (V1^T V2) T22, V2 = V(c0:m, mid:c1) (zeros above row mid)
     const double* V2 = V + c0 + mid * m;
     gemm(cx, true, false, k1, ncr, h, 1.0, V1, m, V2, m, 0.0, W1, k1);
@@ -678,7 +681,7 @@ void householder_panel(Ctx& cx, double* A, int64_t lda, int64_t rows, int64_t co
     double* rowj = cx.alloc(2 * QR_JBMAX);
     BQ_CUDA(cudaMemsetAsync(V, 0, sizeof(double) * rows * cols, cx.stream));
     BQ_CUDA(cudaMemsetAsync(T, 0, sizeof(double) * cols * cols, cx.stream));
-    geqrf_rec(cx, A, lda, rows, 0, cols, tau, V, T, cols, W1, W2, xbuf, rowj);
+    geqrf_rec(cx, A, lda, rows, 0, cols, tau, V, T, cols, W1, W2, xbuf, rowj, qr_leaf_width(rows, cx.num_sms));
     cx.ws_used = mark;
 }
 
@@ -712,7 +715,7 @@ void sketch_qr(Ctx& cx, double* MskT, int64_t ldm, int64_t w, int64_t d, const R
     transpose_copy(cx, p, d, MskT, ldm, Wq, d);
     BQ_CUDA(cudaMemsetAsync(V, 0, sizeof(double) * d * p, cx.stream));
     BQ_CUDA(cudaMemsetAsync(Tf, 0, sizeof(double) * p * p, cx.stream));
-    geqrf_rec(cx, Wq, d, d, 0, p, tau, V, Tf, p, W1, W2, xbuf, rowj);
+    geqrf_rec(cx, Wq, d, d, 0, p, tau, V, Tf, p, W1, W2, xbuf, rowj, qr_leaf_width(d, cx.num_sms));
     int64_t rest = w - p;
     if (rest > 0) {
         // p == d here.  Q_sk = H_1...H_p = I - V T V^T formed explicitly (d x d), then
@@ -734,20 +737,17 @@ void sketch_qr(Ctx& cx, double* MskT, int64_t ldm, int64_t w, int64_t d, const R
             BQ_CUDA(cudaEventRecord(e, cx.stream));
             BQ_CUDA(cudaStreamWaitEvent(defer->side->stream, e, 0));
             BQ_CUDA(cudaEventDestroy(e));
-            Ctx sc = *defer->side;
-            sc.splitk = nullptr;
-            sc.splitk_elems = 0;
-            sc.timer = nullptr;
+            Ctx sc = side_ctx(cx, *defer->side, 0);  // allocates nothing
             gemm(sc, false, false, rest, d, d, 1.0, Xt, ldm, Q, d, 0.0, Y, rest);
             copy_matrix(sc, rest, d, Y, rest, Xt, ldm);
         } else if (rows.n < 0) {
-            gemm(cx, false, false, rest, d, d, 1.0, Xt, ldm, Q, d, 0.0, Y, rest);
+            gemm(cx, false, false, rest, d, d, 1.0, Xt, ldm, Q, d, 0.0, Y, rest, false, 0, /*no_split=*/true);
             copy_matrix(cx, rest, d, Y, rest, Xt, ldm);
         } else {
             for (int64_t j = 0; j < rows.n; ++j) {
                 const int64_t o = rows.off[j], l = imin(rows.len[j], rest - o);
                 if (o < 0 || l <= 0) continue;
-                gemm(cx, false, false, l, d, d, 1.0, Xt + o, ldm, Q, d, 0.0, Y, l);
+                gemm(cx, false, false, l, d, d, 1.0, Xt + o, ldm, Q, d, 0.0, Y, l, false, 0, /*no_split=*/true);
                 copy_matrix(cx, l, d, Y, l, Xt + o, ldm);
             }
         }

@@ -63,35 +63,26 @@ def test_product_package_does_not_import_oracle():
                 assert "import oracle" not in txt and "from oracle" not in txt and "bqrrp_oracle" not in txt, f
 
 
-def test_step_entry_argument_checks_without_gpu():
-    """The multi-GPU step entries reject illegal arguments before any CUDA call (LAPACK-style -i codes)."""
+def test_dist_entry_argument_checks_without_gpu():
+    """The multi-GPU entries reject illegal arguments before any CUDA or NCCL call (LAPACK-style -i codes)."""
     from paper_2507_00976_b200.dist import _declare
 
     L = _declare()
     P = ctypes.c_void_p
     dummy = P(16)
-    k = ctypes.c_int64(0)
-    # row-distributed pivots: negative block count
-    assert L.bqrrp_step_pivots_rows(8, 4, 0, 4, dummy, 8, dummy, 1e-15, dummy, 1, dummy, dummy, dummy,
-                                    ctypes.byref(k), None, None, -1, None) == -17
-    # row-distributed sample update: negative / missing block arrays
-    assert L.bqrrp_step_sample_update_rows(4, dummy, 4, dummy, 4, dummy, 8, None, None, None, -1, None) == -12
-    assert L.bqrrp_step_sample_update_rows(4, dummy, 4, dummy, 4, dummy, 8, None, None, None, 2, None) == -12
-    # row-sharded panel phases
-    assert L.bqrrp_step_cholqr_pre(-1, 4, dummy, 4, dummy, 4, dummy, 4, dummy, None) == -1
-    assert L.bqrrp_step_cholqr_pre(8, 0, dummy, 8, dummy, 8, dummy, 8, dummy, None) == -2
-    assert L.bqrrp_step_cholqr_pre(8, 4, dummy, 4, dummy, 8, dummy, 8, dummy, None) == -4  # ld < rows
-    assert L.bqrrp_step_potrf(0, dummy, 4, None) == -1
-    assert L.bqrrp_step_potrf(4, dummy, 2, None) == -3  # ld < k
-    assert L.bqrrp_step_cholqr_pass(-1, 4, dummy, 4, dummy, dummy, None) == -1
-    assert L.bqrrp_step_recon_top(0, dummy, 4, dummy, dummy, dummy, None) == -1
-    assert L.bqrrp_step_recon_rows(-1, 4, dummy, 4, dummy, dummy, None) == -1
-    assert L.bqrrp_step_recon_finish(0, dummy, dummy, dummy, None, dummy, 4, dummy, dummy, dummy, None) == -1
-    assert L.bqrrp_step_write_panel(0, 4, dummy, 4, dummy, dummy, dummy, 4, None) == -1
-    assert L.bqrrp_step_write_panel(4, 8, dummy, 4, dummy, dummy, dummy, 4, None) == -2  # k > h
-    # split trailing update
-    assert L.bqrrp_step_wy_top(8, 4, 4, dummy, dummy, dummy, 8, None, 4, None) == -9  # no W2
-    assert L.bqrrp_step_wy_bulk(8, 4, 4, dummy, dummy, 2, dummy, 8, None) == -6       # ldw < k
+    rank = ctypes.c_int64(0)
+    h = P()
+    assert L.bqrrp_comm_init(None, 0, 2, ctypes.byref(h)) == -1
+    assert L.bqrrp_comm_init(dummy, 2, 2, ctypes.byref(h)) == -2
+    assert L.bqrrp_comm_init_transport(None, ctypes.byref(h)) == -1
+    assert L.bqrrp_comm_destroy(None) == 0
+    args = (8, 8, dummy, 8, 2, 2, 0, dummy, dummy, ctypes.byref(rank))
+    assert L.bqrrp_factor_dist(*args, None, None, 0, None, None) == -11  # no communicator
+    out = ctypes.c_size_t(0)
+    assert L.bqrrp_workspace_query_dist(64, 64, 8, 8, 2, 0, ctypes.byref(out)) == 0 and out.value > 0
+    assert L.bqrrp_workspace_query_dist(64, 64, 8, 4, 2, 0, ctypes.byref(out)) == -4  # d < b
+    n_loc = ctypes.c_int64(0)
+    assert L.bqrrp_dist_local_columns(10, 0, 2, 0, ctypes.byref(n_loc)) == -2
 
 
 def test_missing_library_fails_loudly(monkeypatch):

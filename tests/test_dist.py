@@ -1,9 +1,12 @@
-"""Multi-GPU BQRRP driver (paper_2507_00976_b200/dist.py).
+"""Multi-GPU BQRRP (bqrrp_factor_dist, csrc/dist.cu).
 
-CPU part: the block-cyclic position map.  GPU part: two ranks sharing the one B200 of the test box (gloo
-process group, whose all-reduce / broadcast accept CUDA tensors) run the distributed factorization and
-must reproduce the single-GPU factorization: same J and rank, R / V / tau to rounding (1e-12), zeros past
-the rank — the column exchange, the panel broadcast and the replicated sketch update all exercised.
+CPU part (no GPU): the block-cyclic layout and the a3 exchange plan of the C library, checked against a
+direct simulation — and, at world size 2 and 3 over gloo on CPU, by actually moving column ids between processes
+with the plans each rank computes.  GPU part: two or three ranks sharing the test box's one B200 (a gloo
+transport, bqrrp_comm_init_transport) run the distributed factorization through the C ABI; with the owner panel
+and the lookahead (the defaults) the result must be BITWISE the single-GPU factorization (SURVEY §8(e)'s
+strongest pin), with the row-sharded panel or without the lookahead J / rank identical and R, V, tau per column
+to 1e-12.
 """
 import os
 import socket
@@ -14,28 +17,6 @@ import torch
 import torch.multiprocessing as mp
 
 
-def test_block_cyclic_map():
-    from paper_2507_00976_b200.dist import BlockCyclic
-
-    n, nb, G = 23, 4, 3
-    maps = [BlockCyclic(n, nb, G, r) for r in range(G)]
-    allpos = np.sort(np.concatenate([mp_.pos for mp_ in maps]))
-    assert np.array_equal(allpos, np.arange(n))  # a partition of the positions
-    for r, bc in enumerate(maps):
-        assert np.all((bc.pos // nb) % G == r)
-        assert np.array_equal(bc.loc_of[bc.pos], np.arange(bc.n_loc))
-        for p in range(n + 1):  # local suffix of positions >= p is contiguous
-            j = bc.first_local_at_or_after(p)
-            assert np.all(bc.pos[j:] >= p) and np.all(bc.pos[:j] < p)
-        for p in range(0, n, nb):  # the row blocks the row-distributed sketch computes and all-gathers
-            blocks = bc.own_blocks_from(p)
-            covered = np.concatenate([np.arange(q0, min(q0 + nb, n)) for q0 in blocks]) if blocks else np.arange(0)
-            assert np.array_equal(covered, bc.pos[bc.first_local_at_or_after(p):])
-    for p in range(0, n, nb):  # every position >= p is in exactly one rank's blocks
-        union = np.sort(np.concatenate([np.arange(q0, min(q0 + nb, n)) for bc in maps for q0 in bc.own_blocks_from(p)]))
-        assert np.array_equal(union, np.arange(p, n))
-
-
 def _free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
@@ -44,84 +25,201 @@ def _free_port():
     return p
 
 
-def _require_contiguous_collectives(dist):
-    """NCCL rejects non-contiguous tensors ("Tensors must be contiguous"); gloo does not.  The tests run on gloo,
-    so make every collective the driver issues check it, as NCCL would."""
-    def wrap(fn):
-        def checked(*args, **kw):
-            for a in list(args) + list(kw.values()):
-                if hasattr(a, "is_contiguous") and hasattr(a, "is_cuda"):
-                    assert a.is_contiguous(), f"{fn.__name__}: non-contiguous tensor {tuple(a.shape)} {a.stride()}"
-            return fn(*args, **kw)
-        return checked
+def _lib_local_columns(n, nb, G, r):
+    import ctypes
 
-    for name in ("broadcast", "all_reduce", "all_gather_into_tensor", "all_to_all_single"):
-        setattr(dist, name, wrap(getattr(dist, name)))
+    from paper_2507_00976_b200.dist import _declare
+
+    out = ctypes.c_int64(0)
+    assert _declare().bqrrp_dist_local_columns(n, nb, G, r, ctypes.byref(out)) == 0
+    return out.value
 
 
-def _worker(rank, world, port, m, n, b, d, seed, gen, out, exchange="allreduce", lookahead=True, shard=True):
+def test_block_cyclic_layout_matches_library():
+    from paper_2507_00976_b200.dist import BlockCyclic
+
+    for n, nb, G in [(23, 4, 3), (64, 8, 2), (5, 8, 4), (100, 3, 7), (0, 2, 2)]:
+        maps = [BlockCyclic(n, nb, G, r) for r in range(G)]
+        allpos = np.sort(np.concatenate([m.pos for m in maps])) if n else np.zeros(0)
+        assert np.array_equal(allpos, np.arange(n))  # a partition of the positions
+        for r, bc in enumerate(maps):
+            assert np.all((bc.pos // nb) % G == r)
+            assert bc.n_loc == _lib_local_columns(n, nb, G, r)
+
+
+def _simulate_exchange(n, nb, G, q, p):
+    """Apply every rank's plan to local arrays of column ids; returns the resulting global position -> id map."""
+    from paper_2507_00976_b200.dist import BlockCyclic, exchange_plan
+
+    maps = [BlockCyclic(n, nb, G, r) for r in range(G)]
+    local = [m.pos.copy() for m in maps]  # column id = original position
+    plans = [exchange_plan(n, nb, G, r, q, p) for r in range(G)]
+    sends = {}
+    for r, P in enumerate(plans):
+        off = 0
+        for dst in range(G):
+            c = int(P["send_counts"][dst])
+            sends[(r, dst)] = local[r][P["send_idx"][off:off + c]].copy()
+            off += c
+        moved = local[r][P["local_src"]].copy()
+        local[r] = local[r].copy()
+        local[r][P["local_dst"]] = moved
+    for r, P in enumerate(plans):
+        off = 0
+        for src in range(G):
+            c = int(P["recv_counts"][src])
+            assert c == len(sends[(src, r)])
+            local[r][P["recv_idx"][off:off + c]] = sends[(src, r)]
+            off += c
+    glob = np.zeros(n, dtype=np.int64)
+    for r, m in enumerate(maps):
+        glob[m.pos] = local[r]
+    return glob
+
+
+@pytest.mark.parametrize("n,nb,G,nlu", [(40, 4, 2, 10), (97, 8, 3, 30), (64, 16, 4, 16), (33, 5, 2, 33)])
+def test_exchange_plan_realises_the_gather(n, nb, G, nlu):
+    """The touched-set exchange (gather semantics new(q) = old(J_qr(q) - 1)) realised by the per-rank
+    plans equals the global gather, for random LU swap lists."""
+    import oracle
+
+    rng = np.random.default_rng(n * G + nlu)
+    for _ in range(5):
+        s = nb * int(rng.integers(0, max(1, (n // nb) - 1)))
+        w = n - s
+        k = min(nlu, w)
+        ipiv = np.array([rng.integers(j, w) + 1 for j in range(k)], dtype=np.int64)
+        Jqr = oracle.piv_transform(w, ipiv)
+        qs = np.nonzero(Jqr - 1 != np.arange(w))[0]
+        q, p = s + qs, s + (Jqr[qs] - 1)
+        glob = _simulate_exchange(n, nb, G, q, p)
+        expect = np.arange(n)
+        expect[s:] = s + (Jqr - 1)
+        assert np.array_equal(glob, expect)
+
+
+def _cpu_exchange_worker(rank, world, port, n, nb, q, p, out):
+    import torch.distributed as dist
+
+    from paper_2507_00976_b200.dist import BlockCyclic, exchange_plan
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        bc = BlockCyclic(n, nb, world, rank)
+        P = exchange_plan(n, nb, world, rank, q, p)
+        local = torch.as_tensor(bc.pos.copy(), dtype=torch.int64)
+        send = local[torch.as_tensor(P["send_idx"], dtype=torch.int64)].clone()
+        moved = local[torch.as_tensor(P["local_src"], dtype=torch.int64)].clone()
+        recv = torch.zeros(int(P["recv_counts"].sum()), dtype=torch.int64)
+        dist.all_to_all_single(recv, send, P["recv_counts"].tolist(), P["send_counts"].tolist())
+        local[torch.as_tensor(P["local_dst"], dtype=torch.int64)] = moved
+        local[torch.as_tensor(P["recv_idx"], dtype=torch.int64)] = recv
+        glob = torch.zeros(n, dtype=torch.int64)
+        glob[torch.as_tensor(bc.pos)] = local
+        dist.all_reduce(glob)
+        if rank == 0:
+            out["glob"] = glob.numpy().copy()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_exchange_plan_over_gloo_cpu(world):
+    """The N > 1 column exchange on CPU: world-size 2 / 3 gloo processes move column ids with all_to_all_single
+    following the library's plans; the result is the global gather."""
+    import oracle
+
+    n, nb = 60, 4
+    rng = np.random.default_rng(world)
+    s = 8
+    w = n - s
+    ipiv = np.array([rng.integers(j, w) + 1 for j in range(16)], dtype=np.int64)
+    Jqr = oracle.piv_transform(w, ipiv)
+    qs = np.nonzero(Jqr - 1 != np.arange(w))[0]
+    q, p = s + qs, s + (Jqr[qs] - 1)
+    out = mp.Manager().dict()
+    mp.spawn(_cpu_exchange_worker, args=(world, _free_port(), n, nb, q, p, out), nprocs=world, join=True)
+    expect = np.arange(n)
+    expect[s:] = s + (Jqr - 1)
+    assert np.array_equal(out["glob"], expect)
+
+
+# ------------------------------------------------------------------------------------------------ GPU
+def _worker(rank, world, port, m, n, b, d, seed, gen, out, lookahead, shard, nb):
     import torch.distributed as dist
 
     import inputs
     import paper_2507_00976_b200 as bq
-    from paper_2507_00976_b200.dist import factor_dist, local_columns
+    from paper_2507_00976_b200.dist import comm_torch, factor_dist, local_columns
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     torch.cuda.set_device(0)
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    _require_contiguous_collectives(dist)
+    comm = comm_torch()
     try:
         A = inputs.low_rank(m, n, gen, seed=seed) if gen else inputs.gaussian(m, n, seed=seed)
         Ad = torch.tensor(np.ascontiguousarray(A.T), device="cuda").t()
-        A_loc, bc = local_columns(Ad, b, world, rank)
-        A_loc, tau, J, ell = factor_dist(A_loc, m, n, b, d, seed=seed + 1, exchange=exchange, lookahead=lookahead,
-                                         shard_panel=shard, shard_sketch=shard)
+        A_loc, bc = local_columns(Ad, nb or b, world, rank)
+        A_loc, tau, J, ell = factor_dist(A_loc, m, n, b, d, seed=seed + 1, comm=comm, lookahead=lookahead,
+                                         shard_panel=shard, dist_nb=nb)
         full = torch.zeros((n, m), dtype=torch.float64, device="cuda").t()
         full[:, torch.as_tensor(bc.pos, device="cuda")] = A_loc
         dist.all_reduce(full.t())  # the contiguous storage behind the column-major view
         if rank == 0:
             Ar, taur, Jr, ellr = bq.factor(Ad.clone().t().contiguous().t(), b, d, seed=seed + 1)
-            same_j = bool(torch.equal(J, Jr))
-            l = ellr
-            prefix_j = bool(torch.equal(J[:l], Jr[:l]))
-            Rg, Rr = torch.triu(full)[:l], torch.triu(Ar)[:l]
-            if not same_j:  # rank-deficient: J(l:) is decided on rounding noise; compare by column index
-                Rg, Rr = Rg[:, torch.argsort(J)], Rr[:, torch.argsort(Jr)]
-            Vg, Vr = torch.tril(full[:, :l], -1), torch.tril(Ar[:, :l], -1)
-            out["res"] = dict(
-                ell=ell, ellr=ellr, same_j=same_j, prefix_j=prefix_j, gen=gen,
-                dR=float(torch.linalg.norm(Rg - Rr) / torch.linalg.norm(Rr)),
-                dV=float(torch.linalg.norm(Vg - Vr) / max(float(torch.linalg.norm(Vr)), 1.0)),
-                dtau=float((tau - taur).abs().max()) if len(tau) else 0.0,
-                tail_zero=bool((full[l:, l:] == 0).all()),
-                bitwise=bool(torch.equal(full, Ar)))
+            out["res"] = dict(ell=ell, ellr=ellr, F=full.cpu().numpy(), tau=tau.cpu().numpy(), J=J.cpu().numpy(),
+                              Fr=Ar.cpu().numpy(), taur=taur.cpu().numpy(), Jr=Jr.cpu().numpy())
     finally:
+        comm.destroy()
         dist.barrier()
         dist.destroy_process_group()
 
 
+def _run(world, m, n, b, d, gen, lookahead=True, shard=False, nb=0):
+    out = mp.Manager().dict()
+    mp.spawn(_worker, args=(world, _free_port(), m, n, b, d, 5, gen, out, lookahead, shard, nb), nprocs=world,
+             join=True)
+    return out["res"]
+
+
 @pytest.mark.gpu
 @pytest.mark.parametrize("m,n,b,d,gen", [(1024, 1024, 128, 160, 0), (700, 450, 64, 80, 0), (512, 768, 64, 64, 0),
-                                         (512, 512, 64, 80, 150)])
+                                         (512, 512, 64, 80, 150), (2048, 1024, 256, 256, 0)])
 @pytest.mark.parametrize("world", [2, 3])
-@pytest.mark.parametrize("exchange,lookahead,shard", [("allreduce", True, False), ("a2a", True, True),
-                                                     ("a2a", False, True), ("allreduce", False, False)])
-def test_dist_matches_single_gpu(gpu, m, n, b, d, gen, world, exchange, lookahead, shard):
-    """The distributed factorization equals the single-GPU one, for both column-exchange forms (X3 as an
-    exact-sum all-reduce, or point-to-point all_to_all moves as used on NCCL), with / without the lookahead,
-    and with the panel on its owner or row-sharded over the ranks (shard also restricts the R_sk GEMM and the
-    sample update to each rank's positions, with the sketch rows all-gathered)."""
-    port = _free_port()
-    mgr = mp.Manager()
-    out = mgr.dict()
-    mp.spawn(_worker, args=(world, port, m, n, b, d, 5, gen, out, exchange, lookahead, shard), nprocs=world,
-             join=True)
-    r = out["res"]
+def test_dist_bitwise_equals_single_gpu(gpu, m, n, b, d, gen, world):
+    """Owner panel + lookahead (the defaults): A, tau, J and the rank are bitwise the one-GPU bqrrp_factor's."""
+    r = _run(world, m, n, b, d, gen)
     assert r["ell"] == r["ellr"]
-    assert r["same_j"] if not gen else r["prefix_j"]
-    assert r["dR"] <= 1e-12 and r["dV"] <= 1e-12 and r["dtau"] <= 1e-12, r
-    assert r["tail_zero"]
+    assert np.array_equal(r["J"], r["Jr"])
+    assert np.array_equal(r["tau"], r["taur"])
+    assert np.array_equal(r["F"], r["Fr"]), float(np.abs(r["F"] - r["Fr"]).max())
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("m,n,b,d,gen", [(1024, 1024, 128, 160, 0), (700, 450, 64, 80, 0), (512, 512, 64, 80, 150)])
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("lookahead,shard,nb", [(True, True, 0), (False, False, 0), (False, True, 0), (True, False, 2)])
+def test_dist_matches_single_gpu(gpu, m, n, b, d, gen, world, lookahead, shard, nb):
+    """Row-sharded panel (all-reduced Grams: a different summation order), no lookahead, or a block width
+    dist_nb = 2b: J and rank identical (J(:l) for rank-deficient inputs), R / V / tau per column to 1e-12."""
+    import _parity
+
+    r = _run(world, m, n, b, d, gen, lookahead, shard, nb * b)
+    l = r["ellr"]
+    assert r["ell"] == l
+    if gen:
+        assert np.array_equal(r["J"][:l], r["Jr"][:l])
+        Rg = _parity.r_cols(r["F"], l)[:, np.argsort(r["J"])]
+        Rr = _parity.r_cols(r["Fr"], l)[:, np.argsort(r["Jr"])]
+        _parity.assert_colwise(Rg, Rr, what="R (by original column)")
+        _parity.assert_colwise(_parity.v_cols(r["F"], l), _parity.v_cols(r["Fr"], l), what="V")
+    else:
+        assert np.array_equal(r["J"], r["Jr"])
+        _parity.compare_factors(r["F"], r["tau"], r["Fr"], r["taur"], l)
+    assert np.all(r["F"][l:, l:] == 0) and np.all(r["tau"][l:] == 0)
 
 
 @pytest.mark.gpu

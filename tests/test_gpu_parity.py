@@ -7,6 +7,7 @@ normwise and max|dtau| <= 1e-12 (reading Z25); residual <= 1e-13, orthogonality 
 import numpy as np
 import pytest
 
+import _parity
 import inputs
 import oracle
 
@@ -173,7 +174,7 @@ def test_permute_bitexact(gpu, rows, w, nlu):
 
 # ----------------------------------------------------------------------------- a4/a5 panel
 @pytest.mark.parametrize("h,k,t", [(256, 32, 40), (1000, 100, 0), (3000, 128, 200), (129, 129, 3), (8192, 1024, 64),
-                                   (65536, 256, 0)])
+                                   (65536, 256, 0), (4096, 2048, 64)])
 @pytest.mark.parametrize("passes", [0, 1, 2])
 def test_panel_matches_householder_oracle(gpu, h, k, t, passes):
     """c.1: CholQR + reconstruction gives the unique (V, tau, R) with tau in [1,2] = convention-H QR."""
@@ -187,13 +188,10 @@ def test_panel_matches_householder_oracle(gpu, h, k, t, passes):
     Pg, taug = bq.debug_panel(_dev(P), k, _dev(Rsk), cholqr_passes=passes)
     F_g = _host(Pg)
     tol = 1e-9 if passes == 1 else 1e-12  # 0 = Householder panel (BQRRP_HQR), 2 = CholQR2
-    assert np.max(np.abs(_host(taug) - tau_o)) <= tol
-    R_o, R_g = np.triu(F_o[:k, :k]), np.triu(F_g[:k, :k])
-    assert np.linalg.norm(R_g - R_o) <= tol * np.linalg.norm(R_o)
-    V_o, V_g = np.tril(F_o[:, :k], -1), np.tril(F_g[:, :k], -1)
-    assert np.linalg.norm(V_g - V_o) <= tol * max(np.linalg.norm(V_o), 1.0)
+    # per column: R11, the reflectors, tau; the trailing block (R12 on top of the updated rows) per column
+    _parity.compare_factors(F_g[:, :k], _host(taug), F_o[:, :k], tau_o, k, tol)
     if t > 0:
-        assert np.linalg.norm(F_g[:, k:] - F_o[:, k:]) <= tol * np.linalg.norm(F_o[:, k:])
+        _parity.assert_colwise(F_g[:, k:], F_o[:, k:], tol, "trailing block")
 
 
 # ----------------------------------------------------------------------------- end to end
@@ -205,7 +203,8 @@ def _run_both(A, b, d, seed=0, rank_tol=None, passes=2):
 
 
 def _compare(out_o, g, exact_j=True):
-    """exact_j: J identical.  Otherwise (rank-deficient inputs: the pivots after l are decided on
+    """Per column (tests/_parity.py): R(:, j) and v_j relative 1e-12, tau per entry 1e-12.
+    exact_j: J identical.  Otherwise (rank-deficient inputs: the pivots after l are decided on
     rounding noise, so only J(:l) is unique) J(:l) identical, J a permutation, and R(:l, :) compared
     column by column through the original column index it holds."""
     Ag, taug, Jg, rk = g
@@ -213,16 +212,15 @@ def _compare(out_o, g, exact_j=True):
     assert rk == l
     if exact_j:
         assert np.array_equal(Jg, out_o.J)
-        Ro, Rg = np.triu(out_o.A)[:l], np.triu(Ag)[:l]
+        _parity.compare_factors(Ag, taug, out_o.A, out_o.tau, l)
     else:
         assert np.array_equal(Jg[:l], out_o.J[:l])
         assert sorted(Jg) == list(range(1, len(Jg) + 1))
-        Ro = np.triu(out_o.A)[:l][:, np.argsort(out_o.J)]
-        Rg = np.triu(Ag)[:l][:, np.argsort(Jg)]
-    assert np.linalg.norm(Rg - Ro) <= 1e-12 * np.linalg.norm(Ro)
-    Vo, Vg = np.tril(out_o.A[:, :l], -1), np.tril(Ag[:, :l], -1)
-    assert np.linalg.norm(Vg - Vo) <= 1e-12 * max(np.linalg.norm(Vo), 1.0)
-    assert np.max(np.abs(taug - out_o.tau)) <= 1e-12
+        Ro = _parity.r_cols(out_o.A, l)[:, np.argsort(out_o.J)]
+        Rg = _parity.r_cols(Ag, l)[:, np.argsort(Jg)]
+        _parity.assert_colwise(Rg, Ro, what="R (by original column)")
+        _parity.assert_colwise(_parity.v_cols(Ag, l), _parity.v_cols(out_o.A, l), what="V")
+        assert np.max(np.abs(taug[:l] - out_o.tau[:l]), initial=0.0) <= _parity.TOL
     assert np.all(Ag[l:, l:] == 0) and np.all(taug[l:] == 0)
 
 
@@ -328,7 +326,7 @@ def _compare_ill_conditioned(A, out_o, g):
         assert np.array_equal(Jg[:l], out_o.J[:l])
         Ro = np.triu(out_o.A)[:l][:, np.argsort(out_o.J)]
         Rg = np.triu(Ag)[:l][:, np.argsort(Jg)]
-        assert np.linalg.norm(Rg - Ro) <= 1e-12 * np.linalg.norm(Ro)
+        _parity.assert_colwise(Rg, Ro, what="R (by original column)")
     res = oracle.OracleResult(Ag, taug, Jg, rk, None, 0, None)
     assert oracle.residual(A, res) <= 1e-13
     assert oracle.orthogonality(res) <= 1e-13
@@ -352,7 +350,7 @@ def test_factor_kahan_matches_oracle(gpu):
     _compare_ill_conditioned(A, out_o, g)
 
 
-def test_cholqr_breakdown_falls_back_to_householder(gpu, monkeypatch):
+def test_cholqr_breakdown_falls_back_to_householder(gpu):
     """CholQR breakdown handling: a panel whose POTRF reports a non-positive pivot is
     re-factored by Householder QR and the factorization stays backward stable — with the same pivots and
     R as the oracle, since the HQR panel and CholQR2 + reconstruction give the same (V, tau, R) (SURVEY
@@ -360,16 +358,39 @@ def test_cholqr_breakdown_falls_back_to_householder(gpu, monkeypatch):
     breaks POTRF down depends on rounding, so the breakdown is forced through the library's test hook."""
     bq = _bq()
     A = np.asfortranarray(inputs.gaussian(1000, 1000, seed=4))
-    monkeypatch.setenv("BQRRP_DEBUG_FORCE_BREAKDOWN", "1")
-    out_o, g = _run_both(A, 128, 160, seed=0)
+    out_o = oracle.bqrrp(A, 128, 160, seed=0)
+    Ag, taug, Jg, rk = bq.factor(_dev(A), 128, 160, seed=0, debug_force_breakdown=True)
     assert bq.panel_fallbacks() == 8  # every panel of the 8 iterations
-    _compare(out_o, g)
+    _compare(out_o, (_host(Ag), _host(taug), _host(Jg), rk))
     with pytest.raises(bq.BqrrpError) as e:
-        bq.factor(_dev(A), 128, 160, seed=0, hqr_fallback=False)
+        bq.factor(_dev(A), 128, 160, seed=0, hqr_fallback=False, debug_force_breakdown=True)
     assert e.value.status == 1
-    monkeypatch.delenv("BQRRP_DEBUG_FORCE_BREAKDOWN")
     bq.factor(_dev(A), 128, 160, seed=0)
     assert bq.panel_fallbacks() == 0
+
+
+@pytest.mark.parametrize("h,k,t", [(131072, 64, 16), (300000, 40, 8)])
+def test_tall_householder_panel(gpu, h, k, t):
+    """the Householder panel (BQRRP_HQR, and the CholQR-breakdown fallback) on panels taller than
+    the 32-column grid leaf holds (94 720 rows): narrower leaves (16 / 8 columns), same (V, tau, R)."""
+    bq = _bq()
+    rng = np.random.default_rng(h + k)
+    P = rng.standard_normal((h, k + t))
+    F_o, tau_o = oracle.house_qr(P, kref=k)
+    Pg, taug = bq.debug_panel(_dev(P), k, _dev(np.eye(k)), cholqr_passes=0)
+    F_g = _host(Pg)
+    _parity.compare_factors(F_g[:, :k], _host(taug), F_o[:, :k], tau_o, k)
+    _parity.assert_colwise(F_g[:, k:], F_o[:, k:], what="trailing block")
+
+
+def test_tall_breakdown_fallback_matches_oracle(gpu):
+    """The CholQR-breakdown fallback on a C4-like tall matrix (h > 94 720 rows) end to end."""
+    bq = _bq()
+    A = inputs.gaussian(131072, 192, seed=11)
+    out_o = oracle.bqrrp(A, 64, 64, seed=2)
+    Ag, taug, Jg, rk = bq.factor(_dev(A), 64, 64, seed=2, debug_force_breakdown=True)
+    assert bq.panel_fallbacks() == 3
+    _compare(out_o, (_host(Ag), _host(taug), _host(Jg), rk))
 
 
 def test_numerically_singular_panels_stay_backward_stable(gpu):

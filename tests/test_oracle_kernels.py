@@ -201,17 +201,27 @@ def test_sample_update_scalar_example():
 
 
 def test_sample_update_dense_bracket_expression():
-    """Alg. 1 step 24: top block = R_sk12 - R_sk11 R11^{-1} R12, to <= 8u relative."""
+    """Alg. 1 step 24: top block = R_sk12 - R_sk11 R11^{-1} R12 to <= 8u, against the exact
+    value of the bracket expression (50-digit mpmath, no shared rounding with any fp64 routine): normwise
+    and componentwise relative to the expression's natural scale |R_sk12| + |R_sk11| |R11^{-1} R12|."""
+    import mpmath
+
+    mpmath.mp.dps = 50
     rng = np.random.default_rng(4)
+    M = lambda a: mpmath.matrix(np.asarray(a).tolist())  # noqa: E731
     for _ in range(20):
         b, t = 4, 16
         Rsk11 = np.triu(rng.standard_normal((b, b))) + 3 * np.eye(b)
         R11 = np.triu(rng.standard_normal((b, b))) + 3 * np.eye(b)
         R12 = rng.standard_normal((b, t))
         Rsk12 = rng.standard_normal((b, t))
-        out = oracle.sample_update(Rsk11, R11, R12, Rsk12.T.copy())
-        ref = Rsk12 - Rsk11 @ scipy.linalg.solve_triangular(R11, R12, lower=False)
-        assert np.linalg.norm(out.T - ref) <= 64 * oracle.U * np.linalg.norm(ref) * 10
+        out = oracle.sample_update(Rsk11, R11, R12, Rsk12.T.copy()).T
+        exact = M(Rsk12) - M(Rsk11) * (mpmath.inverse(M(R11)) * M(R12))
+        err = np.array((M(out) - exact).tolist(), dtype=float)
+        ref = np.array(exact.tolist(), dtype=float)
+        assert np.linalg.norm(err) <= 8 * oracle.U * np.linalg.norm(ref)
+        scale = np.abs(Rsk12) + np.abs(Rsk11) @ np.abs(scipy.linalg.solve_triangular(R11, R12, lower=False))
+        assert np.all(np.abs(err) <= 8 * oracle.U * scale)
 
 
 def test_flop_counts():

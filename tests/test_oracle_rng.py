@@ -112,3 +112,40 @@ def test_sketch_integer_inputs_exact():
         for i in range(5):
             exact = math.fsum(A[l, j] * S[i, l] for l in range(40))
             assert abs(MskT[j, i] - exact) <= 40 * np.spacing(max(abs(exact), 1.0))
+
+
+def test_gauss_against_spec_in_high_precision():
+    """The whole Box-Muller composition recomputed from the spec (SURVEY c.2) in 60-digit
+    arithmetic, from the Philox words alone (the Philox round function is pinned by the KATs): key =
+    (lo32 seed, hi32 seed), counter = (i, lo32 j, hi32 j, stream); u1 = ((x0:x1 >> 12) + 1/2) 2^-52 with x0
+    the HIGH word, u2 = (x2:x3 >> 11) 2^-53, z = sqrt(-2 ln u1) cos(2 pi u2).  A wrong word order, shift or
+    constant in the oracle's C code (or the swapped roles of u1 / u2) would still give N(0,1) samples and
+    pass the moment tests, but not this one: the oracle must agree with the exact value to a few ulps
+    (its log / cos are correctly rounded to ~1 ulp; sqrt and the product add <= 1 ulp each)."""
+    import mpmath
+
+    mpmath.mp.dps = 60
+    cases = [(0, 0, 0, 0), (7, 0, 1, 2), (0xDEADBEEFCAFEF00D, 0, 123456, 1 << 33), (2**64 - 1, 3, 2**32 - 1, 17),
+             (5, 1, 0, 99)]
+    rng = np.random.default_rng(0)
+    for _ in range(300):
+        cases.append((int(rng.integers(0, 2**63)), int(rng.integers(0, 5)), int(rng.integers(0, 2**32)),
+                      int(rng.integers(0, 2**40))))
+    worst = 0.0
+    for seed, stream, i, j in cases:
+        ctr = [i & 0xFFFFFFFF, j & 0xFFFFFFFF, (j >> 32) & 0xFFFFFFFF, stream]
+        key = [seed & 0xFFFFFFFF, (seed >> 32) & 0xFFFFFFFF]
+        x = [int(v) for v in oracle.philox4x32_10(ctr, key)]
+        a = (x[0] << 32) | x[1]
+        c = (x[2] << 32) | x[3]
+        u1 = (mpmath.mpf(a >> 12) + mpmath.mpf(1) / 2) * mpmath.mpf(2) ** -52
+        u2 = mpmath.mpf(c >> 11) * mpmath.mpf(2) ** -53
+        z = mpmath.sqrt(-2 * mpmath.log(u1)) * mpmath.cos(2 * mpmath.pi * u2)
+        got = oracle.gauss(seed, stream, i, j)
+        ulps = abs(mpmath.mpf(got) - z) / mpmath.mpf(np.spacing(abs(float(z))))
+        worst = max(worst, float(ulps))
+        # u2 near 1/4 or 3/4 (cos ~ 0) loses relative accuracy to the absolute error of cos: allow
+        # that absolute error there
+        assert abs(mpmath.mpf(got) - z) <= 4 * np.spacing(abs(float(z))) + 4e-16 * float(
+            mpmath.sqrt(-2 * mpmath.log(u1))), (seed, stream, i, j, got, float(z))
+    assert worst < 8
