@@ -132,6 +132,64 @@ class ClockSampler:
         return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
 
 
+# ------------------------------------------------------------------------------------- HBM paths
+def hbm_peak() -> tuple[float, str]:
+    try:
+        return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs"
+    except Exception:
+        return 6550.0, "B200_PROFILING.md fallback"
+
+
+def hbm_paths(bq, A0, A, m: int, n: int, d: int, stream, reps: int = 3) -> dict:
+    """GB/s of the HBM-bound kernels on the bench workload's own buffers, outside the timed region (SURVEY §8(d.2),
+    north_star "HBM GB/s for the permutation and norm paths"): each kernel timed alone with CUDA events on the
+    stream it runs on (best of `reps` after one warm launch); algorithmic bytes = what the operation must move.
+      K-NORM columns: ||A0(:, j)||, every column of the pristine input (reads m n 8 B);
+      K-NORM trailing: ||R(i:, i:)||_F of the factorization just computed (reads the upper trapezoid once);
+      K-PERM: the a3 touched-set move (gather to scratch + scatter back) of 2d columns of A, the C3 iteration-0
+              touched-set size, random positions (reads + writes 2 x 2d x m x 8 B)."""
+    import torch
+
+    peak, src = hbm_peak()
+    mn = min(m, n)
+    out = {"peak_gbs": peak, "peak_source": src}
+
+    def timed(fn):
+        fn()
+        best = None
+        for _ in range(reps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            fn()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            t = e0.elapsed_time(e1)
+            best = t if best is None else min(best, t)
+        return best
+
+    norms = torch.empty(n, dtype=torch.float64, device=A0.device)
+    t = timed(lambda: bq.column_norms(A0, out=norms, stream=stream))
+    byts = m * n * 8
+    out["k_norm_columns"] = {"ms": t, "bytes": byts, "gbs": byts / t / 1e6, "frac": byts / t / 1e6 / peak,
+                             "kernel": "col_norms_kernel"}
+    tn = torch.empty(mn, dtype=torch.float64, device=A0.device)
+    ws = torch.empty(bq.trailing_norms_workspace(m, n), dtype=torch.uint8, device=A0.device)
+    t = timed(lambda: bq.trailing_norms(A, out=tn, workspace=ws, stream=stream))
+    byts = (n * mn - mn * (mn - 1) // 2) * 8
+    out["k_norm_trailing"] = {"ms": t, "bytes": byts, "gbs": byts / t / 1e6, "frac": byts / t / 1e6 / peak,
+                              "kernel": "trailing_rows_kernel + rowsum + scan (3 launches)"}
+    nt = min(2 * d, n)
+    g = torch.Generator().manual_seed(5)
+    tq = torch.randperm(n, generator=g)[:nt].to(torch.int32)
+    tsrc = tq[torch.randperm(nt, generator=g)]
+    tq, tsrc = tq.to(A.device), tsrc.to(A.device)
+    t = timed(lambda: bq.debug_permute_touched(A, tq, tsrc, stream=stream))
+    byts = 4 * nt * m * 8
+    out["k_perm"] = {"ms": t, "bytes": byts, "gbs": byts / t / 1e6, "frac": byts / t / 1e6 / peak, "columns": nt,
+                     "kernel": "gather_cols_kernel + scatter_cols_kernel (16-byte copies)"}
+    return out
+
+
 # ------------------------------------------------------------------------------------- multi-rank
 def max_over_ranks(value: float, device=None) -> float:
     """The contract's multi-GPU timing rule: every rank times itself on its device; the job time is the
@@ -308,6 +366,8 @@ def main():
                 "algorithmic_flops_per_step": tr_flops, "kernel_ms_per_step": apply_ms,
                 "peak_source": peak_src, "share_of_step": apply_ms / (t_ms / args.steps)}
 
+    hbm = hbm_paths(bq, A0, A, m, n, d, stream) if rank == 0 else None
+
     # ---- end to end through the C ABI with host buffers (H2D + factor + D2H inside the timed region)
     e2e = None
     if not args.no_e2e:
@@ -353,7 +413,7 @@ def main():
                        "timing": "per-step CUDA events around bqrrp_factor; A restored from a pristine copy outside the events",
                        "rank_found": ranks_found},
             "pct_fp64_peak": 100.0 * (value / world) / peak,
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "roofline": roofline, "hbm_paths": hbm, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk.summary(), "phase_ms_per_step": {k_: v_ / args.steps for k_, v_ in phases_acc.items()},
         }
         print(json.dumps(line))

@@ -69,6 +69,11 @@ typedef struct bqrrp_options {
      * k x k factors replicated from all-reduced Gram matrices; SURVEY §8(e) phase 2 item 3) instead of being
      * factored by the panel's owner.  Off (default), the result is bitwise the one-GPU bqrrp_factor's. */
     int dist_flags;
+    /* One-GPU lookahead schedule of panel i+1: 0 (default) per iteration by a cost model —
+     * factored from a gathered copy of its columns WHILE the bulk trailing GEMM of iteration i runs when that
+     * bulk is long enough to hide it, else after the bulk, in place; 1 = always overlapped; -1 = never.  The
+     * result is bitwise the same for every value. */
+    int panel_lookahead;
 } bqrrp_options;
 #define BQRRP_DEBUG_FORCE_BREAKDOWN 1
 #define BQRRP_DIST_SHARD_PANEL 1
@@ -137,11 +142,35 @@ int bqrrp_debug_sketch_qr(int64_t w, int64_t d, double* WT, int64_t ld, void* st
 int bqrrp_debug_permute(int64_t rows, int64_t w, double* X, int64_t ldx, int64_t nlu, const int64_t* ipiv,
                         int64_t* Jqr_out, void* stream);
 
+/* The a3 column move on an explicit touched set (the kernels bqrrp_factor runs, exposed to time them alone):
+ * X(:, tq[t]) <- X_old(:, tsrc[t]) for t < nt (device int32 0-based positions; {tq} = {tsrc} as sets, every
+ * source read before any destination is written, through scratch from the library pool).  Asynchronous; the
+ * host value nt is copied to the device on `stream` (pinned source not required: nt is staged). */
+int bqrrp_debug_permute_touched(int64_t rows, double* X, int64_t ldx, int64_t nt, const int* tq, const int* tsrc,
+                                void* stream);
+
 /* Panel: CholQR(passes) + Householder reconstruction (passes 1..4) or Householder QR (passes 0) of P (h x k, ld) preconditioned by Rsk11 (k x k
  * upper, ld k), written in GEQP3 format in place (R11 on/above, V below) with tau (k), plus the
  * compact-WY update of the trailing C (h x t, ld) that follows P in memory (t may be 0). */
 int bqrrp_debug_panel(int64_t h, int64_t k, int64_t t, double* P, int64_t ld, const double* Rsk11, double* tau,
                       int cholqr_passes, void* stream);
+
+/* ---- K-NORM: HBM-bound norm kernels of the pivot-quality / verification path ----
+ * Reductions run in a fixed order (bitwise reproducible, independent of the launch grid); sums of squares
+ * are formed in fp64, and a column whose sum over- or underflows is recomputed scaled by its largest
+ * magnitude.  Asynchronous on `stream`. */
+
+/* norms[j] = ||A(:, j)||_2 for j < n (A device m x n, lda >= max(1, m); norms device, n doubles).  Used for
+ * the invariant ||R(0:j+1, j)||_2 = ||A(:, J(j))||_2 of a GEQP3 output (Q orthogonal). */
+int bqrrp_column_norms(int64_t m, int64_t n, const double* A, int64_t lda, double* norms, void* stream);
+
+/* out[i] = ||R(i:mn, i:n)||_F for i < mn = min(m, n), R the upper trapezoid of the device m x n matrix (entries
+ * below the diagonal are ignored, so a GEQP3 output with its reflectors can be passed as is) — the paper's first
+ * pivot-quality metric (the residual norm of the rank-i approximation Q(:, :i) R(:i, :)).
+ * workspace: device scratch of >= bqrrp_trailing_norms_workspace bytes, or NULL (library pool; -7 if too small). */
+int bqrrp_trailing_norms(int64_t m, int64_t n, const double* R, int64_t ldr, double* out, void* workspace,
+                         size_t ws_bytes, void* stream);
+int bqrrp_trailing_norms_workspace(int64_t m, int64_t n, size_t* bytes);
 
 /* ---- multi-GPU -----------------------------------------------------------
  * One process per GPU.  A is distributed 1-D block-cyclically over column POSITIONS: position p (0-based) lives on
@@ -163,7 +192,7 @@ int bqrrp_comm_init(const void* nccl_unique_id, int rank, int nranks, void** com
  * the stream (already synchronised by the library) and must have moved the bytes when it returns 0:
  *   allreduce_sum_f64: buf <- sum over ranks (count doubles);  allgather: recv = nranks blocks of `bytes`, rank
  *   order;  broadcast: `bytes` from root;  alltoallv: per peer byte counts / displacements (nranks entries each,
- *   the own entry is 0). */
+ *   the own entry is 0).  Every callback is collective: all ranks call it in the same order, also with zero counts. */
 typedef struct bqrrp_transport {
     void* ctx;
     int rank, nranks;

@@ -275,3 +275,38 @@ def geqrf_flops(m: int, n: int) -> float:
 def geqrf_flops_leading(m: int, n: int) -> float:
     """BASELINE.json's canonical count 2mn^2 - 2n^3/3."""
     return 2.0 * m * n * n - 2.0 * n ** 3 / 3.0
+
+
+def _fro(x: np.ndarray) -> float:
+    """sqrt(sum x^2), written as s sqrt(sum (x/s)^2) with s = max|x| so that no square over- or underflows."""
+    x = np.abs(np.ravel(np.asarray(x, dtype=np.float64)))
+    s = float(x.max()) if x.size else 0.0
+    if s == 0.0:
+        return 0.0
+    y = x / s
+    return s * float(np.sqrt(np.dot(y, y)))
+
+
+def column_norms(A: np.ndarray) -> np.ndarray:
+    """||A(:, j)||_2 for every column (the definition, one scaled sum of squares per column)."""
+    A = np.asarray(A, dtype=np.float64)
+    return np.array([_fro(A[:, j]) for j in range(A.shape[1])], dtype=np.float64)
+
+
+def trailing_norms(R: np.ndarray) -> np.ndarray:
+    """||R(i:, i:)||_F for i < min(m, n) of the upper trapezoid of R — the first pivot-quality metric of P:1269-1272
+    ("the Frobenius norms of the trailing submatrix of the output R-factor, R(i:, i:)"), each entry taken by its
+    definition: the Frobenius norm of the trailing block of triu(R) (O(min(m,n) m n): small cases; `indices` of
+    trailing_norms_at for samples)."""
+    return trailing_norms_at(R, range(min(R.shape)))
+
+
+def trailing_norms_at(R: np.ndarray, indices) -> np.ndarray:
+    """||triu(R)(i:, i:)||_F for the given i (one Frobenius norm per requested i)."""
+    R = np.asarray(R, dtype=np.float64)
+    mn = min(R.shape)
+    out = []
+    for i in indices:
+        blk = np.triu(R[i:mn, i:])  # rows i..mn-1 of the upper trapezoid (triu of the block keeps j >= row)
+        out.append(_fro(blk))
+    return np.array(out, dtype=np.float64)

@@ -11,7 +11,8 @@ import ctypes
 import math
 import os
 
-__all__ = ["lib", "factor", "factor_host", "workspace_query", "trim_memory", "BqrrpError", "default_rank_tol", "PHASES"]
+__all__ = ["lib", "factor", "factor_host", "workspace_query", "trim_memory", "BqrrpError", "default_rank_tol", "PHASES",
+           "column_norms", "trailing_norms"]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(_HERE, "libbqrrp.so")
@@ -33,7 +34,8 @@ class BqrrpError(RuntimeError):
 class Options(ctypes.Structure):
     _fields_ = [("rank_tol", ctypes.c_double), ("cholqr_passes", ctypes.c_int), ("no_hqr_fallback", ctypes.c_int),
                 ("phase_ms", ctypes.POINTER(ctypes.c_float)), ("no_lookahead", ctypes.c_int),
-                ("dist_nb", ctypes.c_int64), ("debug_flags", ctypes.c_int), ("dist_flags", ctypes.c_int)]
+                ("dist_nb", ctypes.c_int64), ("debug_flags", ctypes.c_int), ("dist_flags", ctypes.c_int),
+                ("panel_lookahead", ctypes.c_int)]
 
 
 def lib() -> ctypes.CDLL:
@@ -55,6 +57,10 @@ def lib() -> ctypes.CDLL:
         L.bqrrp_debug_sketch_qr.argtypes = [i64, i64, P, i64, P]
         L.bqrrp_debug_permute.argtypes = [i64, i64, P, i64, i64, P, P, P]
         L.bqrrp_debug_panel.argtypes = [i64, i64, i64, P, i64, P, P, i32, P]
+        L.bqrrp_debug_permute_touched.argtypes = [i64, P, i64, i64, P, P, P]
+        L.bqrrp_column_norms.argtypes = [i64, i64, P, i64, P, P]
+        L.bqrrp_trailing_norms.argtypes = [i64, i64, P, i64, P, P, ctypes.c_size_t, P]
+        L.bqrrp_trailing_norms_workspace.argtypes = [i64, i64, ctypes.POINTER(ctypes.c_size_t)]
         L.bqrrp_strerror.restype = ctypes.c_char_p
         L.bqrrp_strerror.argtypes = [i32]
         L.bqrrp_last_error.restype = ctypes.c_char_p
@@ -114,8 +120,9 @@ def workspace_query(m: int, n: int, b: int, d: int) -> int:
 
 
 def _options(rank_tol, cholqr_passes, phases, hqr_fallback=True, lookahead=True, debug_force_breakdown=False,
-             dist_nb=0):
+             dist_nb=0, panel_lookahead=0):
     o = Options()
+    o.panel_lookahead = int(panel_lookahead)
     o.dist_nb = int(dist_nb)
     o.debug_flags = 1 if debug_force_breakdown else 0
     o.no_lookahead = 0 if lookahead else 1
@@ -128,7 +135,7 @@ def _options(rank_tol, cholqr_passes, phases, hqr_fallback=True, lookahead=True,
 
 def factor(A, b: int, d: int | None = None, seed: int = 0, rank_tol: float | None = None, cholqr_passes: int = 2,
            workspace=None, tau=None, J=None, stream=None, phase_times: bool = False, hqr_fallback: bool = True,
-           lookahead: bool = True, debug_force_breakdown: bool = False):
+           lookahead: bool = True, debug_force_breakdown: bool = False, panel_lookahead: int = 0):
     """BQRRP of A in place (Alg. 1); returns (A, tau, J, rank[, phase_ms dict]).
 
     A: float64 CUDA tensor in column-major layout (m x n); overwritten in GEQP3 format.
@@ -137,6 +144,8 @@ def factor(A, b: int, d: int | None = None, seed: int = 0, rank_tol: float | Non
     BqrrpError status 1); panel_fallbacks() counts them.
     lookahead: False runs every step on one stream (phase times then measure each step alone).
     debug_force_breakdown: test hook (bqrrp_options.debug_flags): every panel reports a CholQR breakdown.
+    panel_lookahead: 0 = per-iteration cost model, 1 = panel i+1 always overlapped with the bulk GEMM of
+    iteration i, -1 = never (bitwise the same result).
     """
     import torch
 
@@ -153,7 +162,8 @@ def factor(A, b: int, d: int | None = None, seed: int = 0, rank_tol: float | Non
         ws_ptr, ws_bytes = ctypes.c_void_p(workspace.data_ptr()), workspace.numel() * workspace.element_size()
     rank = ctypes.c_int64(0)
     phases = (ctypes.c_float * len(PHASES))() if phase_times else None
-    opts = _options(rank_tol, cholqr_passes, phases, hqr_fallback, lookahead, debug_force_breakdown)
+    opts = _options(rank_tol, cholqr_passes, phases, hqr_fallback, lookahead, debug_force_breakdown,
+                    panel_lookahead=panel_lookahead)
     st = lib().bqrrp_factor_ex(m, n, ctypes.c_void_p(A.data_ptr()), lda, b, d, seed, ctypes.c_void_p(tau.data_ptr()),
                                ctypes.c_void_p(J.data_ptr()), ctypes.byref(rank), ws_ptr, ws_bytes,
                                _stream_ptr(stream), ctypes.byref(opts))
@@ -189,6 +199,43 @@ def factor_host(A_host, b: int, d: int | None = None, seed: int = 0, rank_tol: f
                                  ctypes.byref(rank), _stream_ptr(stream), ctypes.byref(opts))
     _check(st, "bqrrp_factor_host")
     return A_host, tau_host[:mn], J_host[:n], int(rank.value)
+
+
+# ------------------------------------------------------------------ K-NORM (bqrrp_column_norms / _trailing_norms)
+def column_norms(A, out=None, stream=None):
+    """||A(:, j)||_2 for every column of the column-major float64 CUDA tensor A (bqrrp_column_norms)."""
+    import torch
+
+    lda = _require_fortran_f64_cuda(A)
+    m, n = A.shape
+    if out is None:
+        out = torch.empty(max(n, 1), dtype=torch.float64, device=A.device)
+    _check(lib().bqrrp_column_norms(m, n, ctypes.c_void_p(A.data_ptr()), lda, ctypes.c_void_p(out.data_ptr()),
+                                    _stream_ptr(stream)), "bqrrp_column_norms")
+    return out[:n]
+
+
+def trailing_norms_workspace(m: int, n: int) -> int:
+    out = ctypes.c_size_t(0)
+    _check(lib().bqrrp_trailing_norms_workspace(m, n, ctypes.byref(out)), "bqrrp_trailing_norms_workspace")
+    return int(out.value)
+
+
+def trailing_norms(R, out=None, workspace=None, stream=None):
+    """||R(i:, i:)||_F for i < min(m, n) of the upper trapezoid of R (bqrrp_trailing_norms)."""
+    import torch
+
+    ldr = _require_fortran_f64_cuda(R)
+    m, n = R.shape
+    mn = min(m, n)
+    if out is None:
+        out = torch.empty(max(mn, 1), dtype=torch.float64, device=R.device)
+    ws_ptr, ws_bytes = None, 0
+    if workspace is not None:
+        ws_ptr, ws_bytes = ctypes.c_void_p(workspace.data_ptr()), workspace.numel() * workspace.element_size()
+    _check(lib().bqrrp_trailing_norms(m, n, ctypes.c_void_p(R.data_ptr()), ldr, ctypes.c_void_p(out.data_ptr()),
+                                      ws_ptr, ws_bytes, _stream_ptr(stream)), "bqrrp_trailing_norms")
+    return out[:mn]
 
 
 # ------------------------------------------------------------------ debug entry points (tests)
@@ -256,6 +303,16 @@ def debug_permute(X, ipiv):
                                      ctypes.c_void_p(ipiv.data_ptr()), ctypes.c_void_p(Jqr.data_ptr()),
                                      _stream_ptr()), "bqrrp_debug_permute")
     return X, Jqr[:w]
+
+
+def debug_permute_touched(X, tq, tsrc, stream=None):
+    """X(:, tq[t]) = X_old(:, tsrc[t]) (int32 CUDA tensors; bqrrp_debug_permute_touched)."""
+    ld = _require_fortran_f64_cuda(X)
+    rows = X.shape[0]
+    _check(lib().bqrrp_debug_permute_touched(rows, ctypes.c_void_p(X.data_ptr()), ld, tq.numel(),
+                                             ctypes.c_void_p(tq.data_ptr()), ctypes.c_void_p(tsrc.data_ptr()),
+                                             _stream_ptr(stream)), "bqrrp_debug_permute_touched")
+    return X
 
 
 def debug_panel(P, k: int, Rsk11, cholqr_passes: int = 2):

@@ -242,7 +242,20 @@ struct Sched {
     Ctx* bulk = nullptr;
     Ctx* aux = nullptr;
     cudaEvent_t ev_top = nullptr, ev_bulk = nullptr;
+    int panel_la = 0;  // bqrrp_options.panel_lookahead: 0 cost model, 1 always, -1 never
 };
+
+// Does overlapping panel i+1 with the bulk GEMM of iteration i pay?  The overlapped form costs an extra GEMM
+// (the next panel's columns are updated twice: 2 h b^2 flops) and slows both by contention; it pays when the
+// bulk is long enough to hide the next pivot selection AND the panel.  Bulk: 2 (h - k) k t flops at ~30 TFLOP/s
+// under contention; bracket: the latency-bound d pivot columns (LU + sketch QR, ~30 us per column measured at
+// C3 under contention) and the panel's k-long chain (~25 us per column); overlap when bulk > 2 x bracket.
+static bool panel_overlap_pays(int64_t h, int64_t k, int64_t t, int64_t d, int64_t k1)
+{
+    const double bulk_s = 2.0 * (double)(h - k) * (double)k * (double)t / 30e12;
+    const double bracket_s = 30e-6 * (double)d + 25e-6 * (double)k1;
+    return bulk_s > 2.0 * bracket_s;
+}
 
 // Buffers and steps of one factorization; the two schedules below compose the steps.
 struct Run {
@@ -508,9 +521,20 @@ static int64_t loop_lookahead(Run& R)
         const int64_t s1 = c, h1 = m - s1, w1 = n - s1;
         const int64_t kmax1 = imin(imin(b, w1), h1);
         R.pivots(i + 1, s1);
+        double* Cb = A + s1 + s1 * lda;  // = C + k rows: the bulk's rows, columns from the next window's start
+        if (!(sc.panel_la > 0 || (sc.panel_la == 0 && panel_overlap_pays(h, k, t, R.d, kmax1)))) {
+            // ---- panel i+1 after the bulk, in place (Alg. 1 order): a3, the zero test, a4
+            BQ_CUDA(cudaStreamWaitEvent(cx.stream, sc.ev_bulk, 0));
+            R.permute(s1);
+            if (!R.check(h1, Cb)) return -1;
+            const int64_t k1 = R.hf[F_K];
+            if (k1 == 0 || R.hf[F_ZERO_COL]) return s1;
+            R.panel(s1, h1, k1, Cb, lda, (int)(slot ^ 1));
+            k = k1;
+            continue;
+        }
         // ---- the next panel's columns: P(:, q) = C(k:h, perm[q]) - V(k:h) W2(:, perm[q]), q < kmax1
         cx.mark(PH_QR_TALL);
-        double* Cb = A + s1 + s1 * lda;  // = C + k rows: the bulk's rows, columns from the next window's start
         la_gather_pre(cx, h1, Cb, lda, R.perm, kmax1, tiles_n, R.hs_state, R.hs_readers, R.Pn, h1, R.post);
         gather_cols_idx(cx, k, R.W2, k, R.perm, kmax1, R.W2g, k);
         GemmExtra fixed;
@@ -691,6 +715,7 @@ static int factor_ex_impl(int64_t m, int64_t n, double* A, int64_t lda, int64_t 
             sc.aux = &cxa;
             sc.ev_top = ev_top;
             sc.ev_bulk = ev_bulk;
+            sc.panel_la = opts ? opts->panel_lookahead : 0;
         }
         int64_t ell = -1;
         int status = 0;
@@ -953,6 +978,37 @@ int bqrrp_debug_permute(int64_t rows, int64_t w, double* X, int64_t ldx, int64_t
         }
         cudaFreeAsync(ws, cx.stream);
         BQ_CUDA(cudaStreamSynchronize(cx.stream));
+        return 0;
+    });
+}
+
+int bqrrp_debug_permute_touched(int64_t rows, double* X, int64_t ldx, int64_t nt, const int* tq, const int* tsrc,
+                                void* stream)
+{
+    if (rows < 0) return -1;
+    if (!X && rows > 0 && nt > 0) return -2;
+    if (ldx < (rows > 1 ? rows : 1)) return -3;
+    if (nt < 0) return -4;
+    if ((!tq || !tsrc) && nt > 0) return -5;
+    return guarded([&]() -> int {
+        Ctx cx;
+        setup_ctx(cx, stream);
+        if (nt == 0 || rows == 0) return 0;
+        size_t wsb = (size_t)4096 + (size_t)nt * (size_t)rows * 8 + 256;
+        void* ws = nullptr;
+        BQ_CUDA(lib_malloc_async(&ws, wsb, cx.stream));
+        Layout Ly{0, 0, 0, 0};
+        carve(cx, ws, wsb, Ly);
+        Touched T;
+        T.tq = const_cast<int*>(tq);
+        T.tsrc = const_cast<int*>(tsrc);
+        T.nt = cx.flags + F_NT;
+        T.maxnt = nt;
+        const int ntv = (int)nt;
+        BQ_CUDA(cudaMemcpyAsync(T.nt, &ntv, sizeof(int), cudaMemcpyHostToDevice, cx.stream));
+        double* scr = cx.alloc((size_t)nt * rows);
+        permute_columns(cx, rows, X, ldx, T, scr);
+        BQ_CUDA(cudaFreeAsync(ws, cx.stream));
         return 0;
     });
 }

@@ -448,7 +448,9 @@ struct DistRun {
             so += sc[r];
             ro += rc[r];
         }
-        if (G > 1 && (so || ro))
+        // collective: every rank takes part even when it has nothing to send or receive (a caller transport's
+        // all-to-all blocks until all ranks enter it)
+        if (G > 1)
             comm.alltoallv((const char*)B.xbuf, sc.data(), sd.data(), (char*)B.rbuf, rc.data(), rd.data(), cx.stream);
         const unsigned chunks = (unsigned)imin(cdiv(m, 256 * 8), 64);
         if (nr) {

@@ -52,6 +52,13 @@ def test_workspace_query_and_argument_checks_without_gpu():
     st = lib.bqrrp_factor_ex(4, 4, dummy, 4, 0, 2, 0, dummy, dummy, ctypes.byref(rank), None, 0, None, None)
     assert st == -5  # b < 1
     assert lib.bqrrp_strerror(-5) == b"illegal argument"
+    # K-NORM entries: argument checks first
+    assert lib.bqrrp_column_norms(-1, 4, dummy, 4, dummy, None) == -1
+    assert lib.bqrrp_column_norms(8, 4, dummy, 4, dummy, None) == -4  # lda < m
+    assert lib.bqrrp_trailing_norms(8, 4, dummy, 8, None, None, 0, None) == -5
+    assert lib.bqrrp_trailing_norms(8, 4, dummy, 8, dummy, dummy, 8, None) == -7  # workspace too small
+    assert lib.bqrrp_trailing_norms_workspace(3000, 5000, ctypes.byref(out)) == 0
+    assert out.value == 5 * 3000 * 8  # ceil(5000 / 1024) column chunks x min(m, n) rows of partial sums
 
 
 def test_product_package_does_not_import_oracle():

@@ -8,6 +8,7 @@ and the lookahead (the defaults) the result must be BITWISE the single-GPU facto
 strongest pin), with the row-sharded panel or without the lookahead J / rank identical and R, V, tau per column
 to 1e-12.
 """
+import datetime
 import os
 import socket
 
@@ -157,7 +158,8 @@ def _worker(rank, world, port, m, n, b, d, seed, gen, out, lookahead, shard, nb)
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     torch.cuda.set_device(0)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    # a short collective timeout: a protocol mismatch between ranks fails the test instead of hanging the suite
+    dist.init_process_group("gloo", rank=rank, world_size=world, timeout=datetime.timedelta(seconds=240))
     comm = comm_torch()
     try:
         A = inputs.low_rank(m, n, gen, seed=seed) if gen else inputs.gaussian(m, n, seed=seed)
@@ -186,6 +188,7 @@ def _run(world, m, n, b, d, gen, lookahead=True, shard=False, nb=0):
 
 
 @pytest.mark.gpu
+@pytest.mark.timeout(900)
 @pytest.mark.parametrize("m,n,b,d,gen", [(1024, 1024, 128, 160, 0), (700, 450, 64, 80, 0), (512, 768, 64, 64, 0),
                                          (512, 512, 64, 80, 150), (2048, 1024, 256, 256, 0)])
 @pytest.mark.parametrize("world", [2, 3])
@@ -199,6 +202,7 @@ def test_dist_bitwise_equals_single_gpu(gpu, m, n, b, d, gen, world):
 
 
 @pytest.mark.gpu
+@pytest.mark.timeout(900)
 @pytest.mark.parametrize("m,n,b,d,gen", [(1024, 1024, 128, 160, 0), (700, 450, 64, 80, 0), (512, 512, 64, 80, 150)])
 @pytest.mark.parametrize("world", [2, 3])
 @pytest.mark.parametrize("lookahead,shard,nb", [(True, True, 0), (False, False, 0), (False, True, 0), (True, False, 2)])
