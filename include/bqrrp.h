@@ -69,10 +69,10 @@ typedef struct bqrrp_options {
      * k x k factors replicated from all-reduced Gram matrices; SURVEY §8(e) phase 2 item 3) instead of being
      * factored by the panel's owner.  Off (default), the result is bitwise the one-GPU bqrrp_factor's. */
     int dist_flags;
-    /* One-GPU lookahead schedule of panel i+1: 0 (default) per iteration by a cost model —
-     * factored from a gathered copy of its columns WHILE the bulk trailing GEMM of iteration i runs when that
-     * bulk is long enough to hide it, else after the bulk, in place; 1 = always overlapped; -1 = never.  The
-     * result is bitwise the same for every value. */
+    /* One-GPU lookahead schedule of panel i+1: 0 (default) = after the bulk trailing GEMM of
+     * iteration i, in place (Alg. 1 order; the next pivot selection overlaps the bulk); 1 = factored from a
+     * gathered copy of its columns WHILE the bulk runs (measured slower on B200: the panel and the bulk contend
+     * for SMs and the next panel's columns are updated twice).  The result is bitwise the same. */
     int panel_lookahead;
 } bqrrp_options;
 #define BQRRP_DEBUG_FORCE_BREAKDOWN 1

@@ -4,8 +4,9 @@ This module holds NO arithmetic of the method: it only draws test matrices of th
 value distributions of the paper's workloads (iid N(0,1) entries, "each matrix entry is
 independently sampled from the standard normal distribution"; rank-deficient and graded-spectrum
 variants for the rank / pivot-quality checks).  Host generation uses numpy's PCG64; the
-device generator (large bench sizes) uses torch's CUDA generator — both plumbing, neither is the
-sketch RNG of the method (that one is implemented separately on each side).
+device generator (large bench sizes) is a counter-based splitmix64 hash + Box-Muller in torch ops
+(`counter_gaussian`: a pure function of (seed, i, j), independent of torch's RNG) — both plumbing,
+neither is the sketch RNG of the method (Philox, implemented separately on each side).
 """
 from __future__ import annotations
 
@@ -71,12 +72,45 @@ def kahan(n: int, theta: float = 1.2, p: float = 1000.0) -> np.ndarray:
     return np.asfortranarray(K)
 
 
-def gaussian_cuda(m: int, n: int, seed: int = 0, device: str = "cuda"):
-    """Device-side N(0,1) matrix (torch CUDA generator), Fortran-strided view (m x n)."""
+# ---- counter-based N(0,1) for the large (device) inputs: entry (i, j) is a pure function of (seed, i, j), so the
+# bench matrices do not depend on the torch version's RNG.  A splitmix64 finaliser of the linear index (a generic
+# 64-bit hash, not the method's Philox sketch generator) gives two 53-bit uniforms, Box-Muller the normal.
+_GOLDEN = -7046029254386353131  # 0x9E3779B97F4A7C15 as int64
+_M1 = -4658895280553007687  # 0xBF58476D1CE4E5B9
+_M2 = -7723592293110705685  # 0x94D049BB133111EB
+
+
+def _splitmix64_torch(x):
+    """splitmix64 finaliser on int64 tensors (wrapping multiplies; logical shifts by masking)."""
+    x = x ^ ((x >> 30) & ((1 << 34) - 1))
+    x = x * _M1
+    x = x ^ ((x >> 27) & ((1 << 37) - 1))
+    x = x * _M2
+    return x ^ ((x >> 31) & ((1 << 33) - 1))
+
+
+def counter_gaussian(m: int, n: int, seed: int = 0, device: str = "cuda", chunk: int = 1 << 26):
+    """m x n column-major (Fortran-strided view) iid N(0,1): entry (i, j) from the 64-bit hash of the linear index
+    i + j m and the seed.  Identical on any device and torch version up to the last ulp of log/cos."""
     import torch
 
-    g = torch.Generator(device=device)
-    g.manual_seed(seed)
-    # column-major storage: allocate n x m row-major and view its transpose
-    t = torch.randn((n, m), generator=g, device=device, dtype=torch.float64)
-    return t.t()
+    out = torch.empty((n, m), dtype=torch.float64, device=device)
+    flat = out.view(-1)  # column-major: flat[i + j m]
+    key = (int(seed) * 0x632BE59BD9B4E019) & ((1 << 63) - 1)
+    two53 = 2.0 ** -53
+    for lo in range(0, m * n, chunk):
+        hi = min(m * n, lo + chunk)
+        idx = torch.arange(lo, hi, dtype=torch.int64, device=device)
+        base = idx * 2 * _GOLDEN + key
+        h1 = _splitmix64_torch(base)
+        h2 = _splitmix64_torch(base + _GOLDEN)
+        u1 = (((h1 >> 11) & ((1 << 53) - 1)).to(torch.float64) + 0.5) * two53  # (0, 1)
+        u2 = ((h2 >> 11) & ((1 << 53) - 1)).to(torch.float64) * two53  # [0, 1)
+        flat[lo:hi] = torch.sqrt(-2.0 * torch.log(u1)) * torch.cos((2.0 * torch.pi) * u2)
+        del idx, base, h1, h2, u1, u2
+    return out.t()
+
+
+def gaussian_cuda(m: int, n: int, seed: int = 0, device: str = "cuda"):
+    """Device-side N(0,1) matrix (m x n, Fortran-strided view): the counter-based generator above."""
+    return counter_gaussian(m, n, seed=seed, device=device)

@@ -144,8 +144,8 @@ def factor(A, b: int, d: int | None = None, seed: int = 0, rank_tol: float | Non
     BqrrpError status 1); panel_fallbacks() counts them.
     lookahead: False runs every step on one stream (phase times then measure each step alone).
     debug_force_breakdown: test hook (bqrrp_options.debug_flags): every panel reports a CholQR breakdown.
-    panel_lookahead: 0 = per-iteration cost model, 1 = panel i+1 always overlapped with the bulk GEMM of
-    iteration i, -1 = never (bitwise the same result).
+    panel_lookahead: 0 = panel i+1 after the bulk GEMM of iteration i (default), 1 = overlapped with it from a
+    gathered copy (bitwise the same result).
     """
     import torch
 

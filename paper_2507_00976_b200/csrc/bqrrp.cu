@@ -242,20 +242,9 @@ struct Sched {
     Ctx* bulk = nullptr;
     Ctx* aux = nullptr;
     cudaEvent_t ev_top = nullptr, ev_bulk = nullptr;
-    int panel_la = 0;  // bqrrp_options.panel_lookahead: 0 cost model, 1 always, -1 never
+    int panel_la = 0;  // bqrrp_options.panel_lookahead: 1 = panel i+1 overlapped with bulk i, else after it
 };
 
-// Does overlapping panel i+1 with the bulk GEMM of iteration i pay?  The overlapped form costs an extra GEMM
-// (the next panel's columns are updated twice: 2 h b^2 flops) and slows both by contention; it pays when the
-// bulk is long enough to hide the next pivot selection AND the panel.  Bulk: 2 (h - k) k t flops at ~30 TFLOP/s
-// under contention; bracket: the latency-bound d pivot columns (LU + sketch QR, ~30 us per column measured at
-// C3 under contention) and the panel's k-long chain (~25 us per column); overlap when bulk > 2 x bracket.
-static bool panel_overlap_pays(int64_t h, int64_t k, int64_t t, int64_t d, int64_t k1)
-{
-    const double bulk_s = 2.0 * (double)(h - k) * (double)k * (double)t / 30e12;
-    const double bracket_s = 30e-6 * (double)d + 25e-6 * (double)k1;
-    return bulk_s > 2.0 * bracket_s;
-}
 
 // Buffers and steps of one factorization; the two schedules below compose the steps.
 struct Run {
@@ -522,7 +511,8 @@ static int64_t loop_lookahead(Run& R)
         const int64_t kmax1 = imin(imin(b, w1), h1);
         R.pivots(i + 1, s1);
         double* Cb = A + s1 + s1 * lda;  // = C + k rows: the bulk's rows, columns from the next window's start
-        if (!(sc.panel_la > 0 || (sc.panel_la == 0 && panel_overlap_pays(h, k, t, R.d, kmax1)))) {
+        if (sc.panel_la != 1) {
+            // (default: measured faster than the overlapped form at C2 and C3, profiles/schedule_ab_r02.json)
             // ---- panel i+1 after the bulk, in place (Alg. 1 order): a3, the zero test, a4
             BQ_CUDA(cudaStreamWaitEvent(cx.stream, sc.ev_bulk, 0));
             R.permute(s1);

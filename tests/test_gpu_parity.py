@@ -467,9 +467,9 @@ def test_lookahead_and_serial_schedules_agree(gpu):
     assert rh == r1
     assert np.array_equal(Ah_out.numpy(), _host(Ag1)) and np.array_equal(tauh.numpy(), _host(tau1))
     assert np.array_equal(Jh.numpy(), _host(J1))
-    # the panel-lookahead forms (panel i+1 overlapped with the bulk GEMM of iteration i from a gathered copy, or
-    # after the bulk in place) are bitwise the same factorization
-    for pl in (1, -1):
+    # the overlapped panel lookahead (panel i+1 factored from a gathered copy while the bulk GEMM of iteration i
+    # runs) is bitwise the default schedule's factorization
+    for pl in (1,):
         Ag2, tau2, J2, r2 = bq.factor(_dev(A), 256, 256, seed=2, panel_lookahead=pl)
         assert r2 == r1 and torch.equal(J2, J1) and torch.equal(tau2, tau1) and torch.equal(Ag2, Ag1), pl
 

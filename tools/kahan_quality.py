@@ -35,9 +35,13 @@ def run(n, b, rank_tol):
     sigma = np.linalg.svd(M, compute_uv=False)
     Rg, _ = scipy.linalg.qr(M, pivoting=True, mode="r")
     dA = torch.tensor(np.ascontiguousarray(M.T), device="cuda").t()
-    Ab, tau, J, rank = bq.factor(dA, b, b, seed=0, rank_tol=rank_tol)
+    Ab, tau, J, rank, ph = bq.factor(dA, b, b, seed=0, rank_tol=rank_tol, phase_times=True)
     Rb = np.triu(Ab.cpu().numpy())[:n]
-    tg, tb = trailing_norms(Rg), trailing_norms(Rb)
+    # the BQRRP side's metric on the GPU (K-NORM, bqrrp_trailing_norms: R's trailing Frobenius norms straight off
+    # the GEQP3-format output); the GEQP3 side in numpy — and the two forms cross-checked on the BQRRP R
+    tb = bq.trailing_norms(Ab).cpu().numpy()
+    tg, tb_np = trailing_norms(Rg), trailing_norms(Rb)
+    knorm_vs_numpy = float(np.max(np.abs(tb - tb_np) / np.maximum(tb_np, 1e-300)))
     lim = min(rank, int(0.9 * n))
     ratio = tg[:lim] / tb[:lim]
     dg = np.abs(np.diag(Rg)) / sigma
@@ -48,14 +52,15 @@ def run(n, b, rank_tol):
             "ratio_max": float(ratio.max()),
             "diag_over_sigma_bqrrp_min": float(db[:lim].min()), "diag_over_sigma_bqrrp_max": float(db[:lim].max()),
             "diag_over_sigma_geqp3_min": float(dg[:lim].min()), "diag_over_sigma_geqp3_max": float(dg[:lim].max()),
-            "geqp3_lower_bound": lower,
+            "geqp3_lower_bound": lower, "panel_fallbacks": bq.panel_fallbacks(), "factor_ms": ph["total"],
+            "knorm_vs_numpy_max_rel": knorm_vs_numpy,
             "ratio_samples": {str(i): float(ratio[i]) for i in np.linspace(0, lim - 1, 12).astype(int)}}
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--sizes", default="1024,4096")
-    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "kahan_quality_r01.json"))
+    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "kahan_quality_r02.json"))
     args = ap.parse_args()
     rows = []
     for n in [int(x) for x in args.sizes.split(",")]:

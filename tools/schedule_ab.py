@@ -1,5 +1,5 @@
-"""A/B of the one-GPU schedules on one config: panel_lookahead in {-1 (after the bulk), 0 (cost model), 1 (always
-overlapped)} and the serial schedule; each warm, then `reps` factorizations timed with CUDA events (best and
+"""A/B of the one-GPU schedules on one config: panel_lookahead 0 (panel i+1 after the bulk, default) or 1
+(overlapped with the bulk from a gathered copy), and the serial schedule; each warm, then `reps` factorizations timed with CUDA events (best and
 mean), phases of the last.  Usage: python tools/schedule_ab.py C3 [reps]"""
 import json
 import os
@@ -21,8 +21,8 @@ m, n, b, d = cfg["m"], cfg["n"], cfg["b"], cfg["d"]
 A0 = inputs.gaussian_cuda(m, n, seed=0)
 A = torch.empty_like(A0.t()).t()
 ws = torch.empty(bq.workspace_query(m, n, b, d), dtype=torch.uint8, device="cuda")
-modes = [("panel_after_bulk", dict(panel_lookahead=-1)), ("cost_model", dict(panel_lookahead=0)),
-         ("panel_overlapped", dict(panel_lookahead=1)), ("serial", dict(lookahead=False))]
+modes = [("panel_after_bulk", dict(panel_lookahead=0)), ("panel_overlapped", dict(panel_lookahead=1)),
+         ("serial", dict(lookahead=False))]
 res = {}
 for label, kw in modes:
     times = []

@@ -26,7 +26,10 @@ def main():
     ap.add_argument("--blocks", default="32,64,128,256,512,1024,2048")
     ap.add_argument("--reps", type=int, default=2)
     ap.add_argument("--max-iters", type=int, default=256, help="skip (m, b) with more block iterations")
-    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "sweep_r01.json"))
+    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "sweep_r02.json"))
+    ap.add_argument("--variants", default="cqr", help="comma list of cqr (CholQR2 panel), hqr (cholqr_passes = 0, the "
+                    "paper's BQRRP_HQR), and the suffix -serial (one stream: the phases then partition the whole step, "
+                    "the fig gpu_runtime_breakdown analogue, P:1226-1258)")
     args = ap.parse_args()
     sizes = [int(x) for x in args.sizes.split(",")]
     blocks = [int(x) for x in args.blocks.split(",")]
@@ -38,23 +41,27 @@ def main():
             if b > m or m // b > args.max_iters:
                 continue
             ws = torch.empty(bq.workspace_query(m, m, b, b), dtype=torch.uint8, device="cuda")
-            best = None
-            for r in range(args.reps + 1):
-                A.copy_(A0)
-                torch.cuda.synchronize()
-                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                e0.record()
-                out = bq.factor(A, b, b, seed=0, workspace=ws, phase_times=True)
-                e1.record()
-                torch.cuda.synchronize()
-                ms = e0.elapsed_time(e1)
-                if r > 0 and (best is None or ms < best[0]):
-                    best = (ms, out[4], out[3])
-            ms, ph, rank = best
-            tf = bench.canonical_flops(m, m) / (ms * 1e-3) / 1e12
-            rows.append({"m": m, "b": b, "d": b, "ms": ms, "tflops": tf, "rank": rank,
-                         "pct_p64": 100 * tf / bench.peak_fp64()[0], "phases_ms": ph})
-            print(json.dumps(rows[-1]), flush=True)
+            for var in args.variants.split(","):
+                passes = 0 if var.startswith("hqr") else 2
+                lookahead = not var.endswith("-serial")
+                best = None
+                for r in range(args.reps + 1):
+                    A.copy_(A0)
+                    torch.cuda.synchronize()
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record()
+                    out = bq.factor(A, b, b, seed=0, workspace=ws, phase_times=True, cholqr_passes=passes,
+                                    lookahead=lookahead)
+                    e1.record()
+                    torch.cuda.synchronize()
+                    ms = e0.elapsed_time(e1)
+                    if r > 0 and (best is None or ms < best[0]):
+                        best = (ms, out[4], out[3])
+                ms, ph, rank = best
+                tf = bench.canonical_flops(m, m) / (ms * 1e-3) / 1e12
+                rows.append({"m": m, "b": b, "d": b, "variant": var, "ms": ms, "tflops": tf, "rank": rank,
+                             "pct_p64": 100 * tf / bench.peak_fp64()[0], "phases_ms": ph})
+                print(json.dumps(rows[-1]), flush=True)
             del ws
         del A0, A
         torch.cuda.empty_cache()
