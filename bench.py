@@ -228,6 +228,21 @@ def oracle_sample(cfg_name: str, seed: int = 0):
     return canonical_flops(sm, sn) / dt / 1e12, dt, desc
 
 
+def oracle_plan():
+    """The BASELINE.md CPU plan run once by tools/oracle_baseline.py (C1 at 1 thread and all cores, C2 all cores,
+    C3 / C4 extrapolated by the algorithmic-flop ratio), summarised from its committed record."""
+    path = os.path.join(ROOT, "profiles", "oracle_baseline_r02.json")
+    try:
+        d = json.load(open(path))
+    except Exception:
+        return None
+    rows = {}
+    for r in d["rows"]:
+        key = f"{r['config']}_{r['threads']}t" + ("_extrapolated" if r.get("extrapolated") else "")
+        rows[key] = {"seconds": round(r["seconds_best"], 3), "tflops": r["tflops_canonical"]}
+    return {"record": "profiles/oracle_baseline_r02.json", "cpu": d.get("cpu"), "cores": d.get("cores"), "runs": rows}
+
+
 def cpu_model() -> str:
     """The host CPU model (for the cpu_baseline record)."""
     try:
@@ -399,7 +414,7 @@ def main():
         v, dt, desc = oracle_sample(args.config)
         cpu = {"value": v, "unit": "TFLOP/s", "cores": os.cpu_count(), "kind": "oracle", "sample": desc,
                "cpu": cpu_model(),
-               "seconds": dt}
+               "seconds": dt, "plan": oracle_plan()}
 
     if rank == 0:
         line = {

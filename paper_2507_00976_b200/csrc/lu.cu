@@ -369,219 +369,183 @@ __global__ void __launch_bounds__(LU_THREADS, 1) lu_panel_cluster_kernel(LuPanel
 constexpr size_t LUC_SMEM_MAX = 196 * 1024;
 
 // ---------------------------------------------------------------------------------------------
-// Register-resident cluster leaf (rows <= 16 CTAs x 256 threads x RPT, RPT <= 2): each thread owns RPT rows
-// of the 32-column panel in registers (no shared-memory slab traffic).  Per column: local first-max ->
-// warp shuffles -> ONE block barrier -> every thread derives the CTA candidate; the warp owning it pushes
-// (|value|, row, its panel row) into every CTA's slot with st.async (mbarrier tx-count), CTA 0's warp 0
-// pushes row jr (rows c0 .. c0+31 are its lanes); after the mbarrier wait, warp 0 picks the winner (IDAMAX
-// order, Z19) from LOCAL shared memory, one more block barrier, every thread swaps / scales / updates its
-// own rows.  Slots are double-buffered by column parity (a CTA pushes column j+2 only after its column-
-// (j+1) wait, i.e. after every peer pushed column j+1, which each does after its column-j reads).  (A grid
-// form exchanging through global records with release/acquire tags was ~1.8x slower than the
-// shared-memory grid kernel and was removed.)
-__device__ __forceinline__ double select32(const double (&v)[32], int j)
+// Register-resident cluster leaf: G <= 16 CTAs of one cluster, each thread owns RPT rows of
+// the JB-column leaf panel in registers, the column loop is unrolled (every register index compile-time).
+// Row interchanges are NOT performed: every row carries its logical position pos (initially its own index);
+// the step-j interchange of rows jr = c0 + j and piv only swaps their labels, so no row data moves inside the
+// leaf and nobody needs row jr's values; the rows are written back to their logical positions at the end.
+// Per column:
+//   1. thread candidate over its active rows (pos >= jr): key = bits of |x| (monotone for x >= 0), ties to the
+//      smaller logical position — exactly IDAMAX's first-index rule in the swapped order (Z19);
+//   2. warp argmax with three redux.sync (max of the high key word, max of the low word among those, min
+//      position among those): no shuffle chains;
+//   3. each warp's winner stores its row (columns >= j) into shared memory, one block barrier;
+//   4. warp 0 reduces the 8 warp records the same way and pushes the CTA record (|x| bits, pos, row) into
+//      every CTA's slot with st.async (mbarrier tx-count), slots double-buffered by column parity;
+//   5. after the mbarrier wait every warp reduces the G records from its own shared memory (no second barrier,
+//      no remote reads), relabels, and applies the rank-1 update to its active rows (division by the pivot,
+//      as DGETF2 and the oracle).
+// An exactly-zero pivot column leaves everything unchanged (no interchange, no scaling; Z18).
+constexpr int LF_NT = 256, LF_NW = LF_NT / 32, LF_GMAX = 16;
+
+__device__ __forceinline__ void argmax3(unsigned hi, unsigned lo, unsigned p, unsigned& mh, unsigned& ml, unsigned& mp)
 {
-    double l1[16], l2[8], l3[4], l4[2];
-#pragma unroll
-    for (int i = 0; i < 16; ++i) l1[i] = (j & 1) ? v[2 * i + 1] : v[2 * i];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) l2[i] = (j & 2) ? l1[2 * i + 1] : l1[2 * i];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) l3[i] = (j & 4) ? l2[2 * i + 1] : l2[2 * i];
-#pragma unroll
-    for (int i = 0; i < 2; ++i) l4[i] = (j & 8) ? l3[2 * i + 1] : l3[2 * i];
-    return (j & 16) ? l4[1] : l4[0];
+    mh = __reduce_max_sync(0xffffffffu, hi);
+    ml = __reduce_max_sync(0xffffffffu, hi == mh ? lo : 0u);
+    mp = __reduce_min_sync(0xffffffffu, (hi == mh && lo == ml) ? p : 0xffffffffu);
 }
 
-constexpr int LR_REC = 2 + LU_JBMAX;  // |value|, row, panel row
-constexpr int LR_CLMAX = 16;
-
-template <int RPT>
-__global__ void __launch_bounds__(LU_THREADS, 1) lu_leaf_reg_kernel(LuPanelArgs a)
+template <int JB, int RPT>
+__global__ void __launch_bounds__(LF_NT, 1) lu_leaf_fast_kernel(LuPanelArgs a)
 {
     cg::cluster_group cluster = cg::this_cluster();
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, jb = a.jb;
     const int G = (int)cluster.num_blocks(), me = (int)cluster.block_rank();
-    constexpr int RC = LU_THREADS * RPT;  // rows per CTA
+    constexpr int RC = LF_NT * RPT;  // rows per CTA
+    constexpr int REC = 2 + JB;      // |x| bits, pos, row[JB]
     const int64_t rbeg = a.c0 + (int64_t)me * RC;
-    __shared__ double red_v[LU_THREADS / 32];
-    __shared__ int64_t red_i[LU_THREADS / 32];
-    __shared__ double pivrow[LU_JBMAX], oldrow[LU_JBMAX];
-    __shared__ int64_t s_piv;
+    __shared__ __align__(16) double wrow[2][LF_NW][JB];
+    __shared__ unsigned long long wkey[2][LF_NW];
+    __shared__ unsigned wpos[2][LF_NW];
+    __shared__ __align__(16) double slot[2][LF_GMAX][REC];
+    __shared__ __align__(8) unsigned long long mbar[2];
     __shared__ int64_t spiv[LU_JBMAX], trow[2 * LU_JBMAX], tsrc[2 * LU_JBMAX];
     __shared__ int s_nt;
-    __shared__ double slot[2][LR_CLMAX][LR_REC];  // records pushed by every CTA of the cluster
-    __shared__ double rowjs[2][LU_JBMAX];         // row jr, pushed by CTA 0
-    __shared__ __align__(8) unsigned long long mbar[2];
     if (tid == 0) {
         mbar_init(smem_u32(&mbar[0]), 1);
         mbar_init(smem_u32(&mbar[1]), 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-
-    double av[RPT][32];
-    int64_t rr[RPT];
+    double av[RPT][JB];
+    int pos[RPT];
 #pragma unroll
     for (int i = 0; i < RPT; ++i) {
-        rr[i] = rbeg + tid + (int64_t)i * LU_THREADS;
-        const bool ok = rr[i] < a.w;
+        const int64_t r = rbeg + tid + (int64_t)i * LF_NT;
+        const bool ok = r < a.w;
+        pos[i] = ok ? (int)r : -1;  // -1: padding row, never active
 #pragma unroll
-        for (int c = 0; c < 32; ++c) av[i][c] = (ok && c < jb) ? a.L[rr[i] + (a.c0 + c) * a.ld] : 0.0;
+        for (int c = 0; c < JB; ++c) av[i][c] = (ok && c < jb) ? a.L[r + (a.c0 + c) * a.ld] : 0.0;
     }
     cluster.sync();  // every peer's mbarriers are initialised before the first push
 
-#pragma unroll 1
-    for (int j = 0; j < jb; ++j) {
+#pragma unroll
+    for (int j = 0; j < JB; ++j) {
+        if (j >= jb) break;
         const int par = j & 1;
-        const int64_t jr = a.c0 + j;
-        const unsigned mb = smem_u32(&mbar[par]);
-        // local first-max of |L(r, j)| over my active rows (ascending rows: first index kept on ties)
-        double bv = -1.0;
-        int64_t bi = INT64_MAX;
-        double xj[RPT];
+        const int jr = (int)a.c0 + j;
+        // 1. thread candidate
+        unsigned hi = 0u, lo = 0u, bp = 0xffffffffu;
+        int bi = 0;
 #pragma unroll
         for (int i = 0; i < RPT; ++i) {
-            xj[i] = select32(av[i], j);
-            if (rr[i] < a.w && rr[i] >= jr) {
-                const double v = fabs(xj[i]);
-                if (v > bv) { bv = v; bi = rr[i]; }
+            if (pos[i] >= jr) {
+                const unsigned long long k = (unsigned long long)__double_as_longlong(fabs(av[i][j]));
+                const unsigned h = (unsigned)(k >> 32), l = (unsigned)k;
+                if (h > hi || (h == hi && (l > lo || (l == lo && (unsigned)pos[i] < bp)))) {
+                    hi = h;
+                    lo = l;
+                    bp = (unsigned)pos[i];
+                    bi = i;
+                }
             }
         }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            const double ov = __shfl_down_sync(0xffffffffu, bv, o);
-            const int64_t oi = __shfl_down_sync(0xffffffffu, bi, o);
-            if (better(ov, oi, bv, bi)) { bv = ov; bi = oi; }
+        // 2. warp winner; 3. its row into shared memory
+        unsigned mh, ml, mp;
+        argmax3(hi, lo, bp, mh, ml, mp);
+        if (lane == 0) {
+            wkey[par][warp] = ((unsigned long long)mh << 32) | ml;
+            wpos[par][warp] = mp;
         }
-        if (lane == 0) { red_v[warp] = bv; red_i[warp] = bi; }
-        __syncthreads();  // (1)
-        double cv = red_v[0];
-        int64_t ci = red_i[0];
+        if (bp == mp && mp != 0xffffffffu) {
 #pragma unroll
-        for (int wv = 1; wv < LU_THREADS / 32; ++wv)
-            if (better(red_v[wv], red_i[wv], cv, ci)) { cv = red_v[wv]; ci = red_i[wv]; }
-        // push this CTA's candidate: the warp owning row ci gathers it by shuffles (lane c takes entry c)
-        const int owner_t = (ci == INT64_MAX) ? 0 : (int)((ci - rbeg) % LU_THREADS);
-        const int owner_i = (ci == INT64_MAX) ? 0 : (int)((ci - rbeg) / LU_THREADS);
-        if (warp == (owner_t >> 5)) {
-            double mine = 0.0;
+            for (int c = j; c < JB; ++c) {
+                double v = av[0][c];
 #pragma unroll
-            for (int c = 0; c < 32; ++c) {
-                double src = 0.0;
-#pragma unroll
-                for (int i = 0; i < RPT; ++i) src = (i == owner_i) ? av[i][c] : src;
-                const double t = __shfl_sync(0xffffffffu, src, owner_t & 31);
-                mine = (lane == c) ? t : mine;
+                for (int i = 1; i < RPT; ++i) v = (bi == i) ? av[i][c] : v;
+                wrow[par][warp][c] = v;
             }
-            if (ci == INT64_MAX) mine = 0.0;
+        }
+        __syncthreads();
+        // 4. the CTA record, pushed to every CTA of the cluster
+        const unsigned mb = smem_u32(&mbar[par]);
+        if (warp == 0) {
+            const unsigned long long k = (lane < LF_NW) ? wkey[par][lane] : 0ull;
+            const unsigned p = (lane < LF_NW) ? wpos[par][lane] : 0xffffffffu;
+            unsigned ch, cl, cp;
+            argmax3((unsigned)(k >> 32), (unsigned)k, p, ch, cl, cp);
+            const unsigned who = __ballot_sync(0xffffffffu, lane < LF_NW && p == cp && (unsigned)(k >> 32) == ch &&
+                                                                (unsigned)k == cl);
+            const int wq = who ? __ffs(who) - 1 : 0;
+            const double rv = (lane >= j && lane < JB) ? wrow[par][wq][lane] : 0.0;
+            const double hv = (lane == 0) ? __longlong_as_double((long long)(((unsigned long long)ch << 32) | cl))
+                                          : __longlong_as_double((long long)cp);
             const unsigned dst = smem_u32(&slot[par][me][0]);
             for (int rk = 0; rk < G; ++rk) {
                 const unsigned rm = mapa_u32(mb, rk), rd = mapa_u32(dst, rk);
-                if (lane == 0) {
-                    st_async_f64(rd, (ci == INT64_MAX) ? -1.0 : cv, rm);
-                    st_async_f64(rd + 8, __longlong_as_double((long long)ci), rm);
-                }
-                st_async_f64(rd + 8 * (2 + lane), mine, rm);
+                if (lane < 2) st_async_f64(rd + 8 * lane, hv, rm);
+                if (lane >= j && lane < JB) st_async_f64(rd + 8 * (2 + lane), rv, rm);
             }
         }
-        if (me == 0 && warp == 0) {  // row jr = row c0 + j = lane j's first row
-            double rj = 0.0;
-#pragma unroll
-            for (int c = 0; c < 32; ++c) {
-                const double t = __shfl_sync(0xffffffffu, av[0][c], j);
-                rj = (lane == c) ? t : rj;
-            }
-            const unsigned dst = smem_u32(&rowjs[par][lane]);
-            for (int rk = 0; rk < G; ++rk) st_async_f64(mapa_u32(dst, rk), rj, mapa_u32(mb, rk));
-        }
-        if (tid == 0) mbar_arrive_expect_tx(mb, (unsigned)((G * LR_REC + LU_JBMAX) * sizeof(double)));
+        if (tid == 0) mbar_arrive_expect_tx(mb, (unsigned)(G * (2 + JB - j) * sizeof(double)));
         mbar_wait_parity(mb, (unsigned)((j >> 1) & 1));
-        if (warp == 0) {  // every CTA picks the same winner from its own copy of the records
-            double v = -1.0;
-            int64_t idx = INT64_MAX;
-            int wq = 0;
-            if (lane < G) {
-                v = slot[par][lane][0];
-                idx = (int64_t)__double_as_longlong(slot[par][lane][1]);
-                wq = lane;
+        // 5. the cluster winner (every warp, from local shared memory), relabel, rank-1 update
+        unsigned gh, gl, gp;
+        {
+            const unsigned long long k =
+                (lane < G) ? (unsigned long long)__double_as_longlong(slot[par][lane][0]) : 0ull;
+            const unsigned p = (lane < G) ? (unsigned)__double_as_longlong(slot[par][lane][1]) : 0xffffffffu;
+            argmax3((unsigned)(k >> 32), (unsigned)k, p, gh, gl, gp);
+            const unsigned who = __ballot_sync(0xffffffffu, lane < G && p == gp && (unsigned)(k >> 32) == gh &&
+                                                                (unsigned)k == gl);
+            const int q = __ffs(who) - 1;
+            const double* prow = &slot[par][q][2];
+            const double u = prow[j];
+            const int ps = (int)gp;
+            if (tid == 0) {
+                spiv[j] = ps;
+                if (me == 0) a.ipiv[jr] = ps;
             }
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                const double ov = __shfl_down_sync(0xffffffffu, v, o);
-                const int64_t oi = __shfl_down_sync(0xffffffffu, idx, o);
-                const int ow = __shfl_down_sync(0xffffffffu, wq, o);
-                if (better(ov, oi, v, idx)) { v = ov; idx = oi; wq = ow; }
-            }
-            idx = __shfl_sync(0xffffffffu, idx, 0);
-            wq = __shfl_sync(0xffffffffu, wq, 0);
-            if (lane < jb) {
-                pivrow[lane] = slot[par][wq][2 + lane];
-                oldrow[lane] = rowjs[par][lane];
-            }
-            if (lane == 0) {
-                s_piv = idx;
-                if (me == 0) a.ipiv[jr] = (int)idx;
-            }
-        }
-        __syncthreads();  // (2)
-        const int64_t piv = s_piv;
-        const double u = pivrow[j];
-        if (tid == 0) spiv[j] = (u != 0.0) ? piv : jr;
-        if (u != 0.0) {  // (an exactly zero pivot column: no swap, no scaling, Z18)
 #pragma unroll
             for (int i = 0; i < RPT; ++i) {
-                const int64_t r = rr[i];
-                if (r >= a.w || r < jr) continue;
-                if (r == jr) {
-                    if (piv != jr) {
+                const int pn = (pos[i] == jr) ? ps : ((pos[i] == ps) ? jr : pos[i]);
+                pos[i] = pn;
+                if (u != 0.0 && pn > jr) {
+                    const double l = av[i][j] / u;
+                    av[i][j] = l;
 #pragma unroll
-                        for (int c = 0; c < 32; ++c)
-                            if (c < jb) av[i][c] = pivrow[c];
-                    }
-                    continue;
-                }
-                const bool swapped = (r == piv);
-                const double l = (swapped ? oldrow[j] : xj[i]) / u;
-#pragma unroll
-                for (int c = 0; c < 32; ++c) {
-                    const double base = swapped ? oldrow[c < jb ? c : 0] : av[i][c];
-                    av[i][c] = (c < j) ? base : ((c == j) ? l : fma(-l, pivrow[c < jb ? c : 0], base));
+                    for (int c = j + 1; c < JB; ++c) av[i][c] = fma(-l, prow[c], av[i][c]);
                 }
             }
         }
     }
+    // the rows to their logical positions
 #pragma unroll
     for (int i = 0; i < RPT; ++i)
-        if (rr[i] < a.w) {
+        if (pos[i] >= 0) {
 #pragma unroll
-            for (int c = 0; c < 32; ++c)
-                if (c < jb) a.L[rr[i] + (a.c0 + c) * a.ld] = av[i][c];
+            for (int c = 0; c < JB; ++c)
+                if (c < jb) a.L[pos[i] + (a.c0 + c) * a.ld] = av[i][c];
         }
-    cluster.sync();  // no CTA exits while peers may still push into it
-    const int64_t gtid = (int64_t)me * LU_THREADS + tid, gstride = (int64_t)G * LU_THREADS;
+    cluster.sync();  // every CTA's rows are written before any CTA moves whole rows outside the panel
+    const int64_t gtid = (int64_t)me * LF_NT + tid, gstride = (int64_t)G * LF_NT;
     apply_panel_interchanges(a, spiv, trow, tsrc, &s_nt, gtid, gstride);
 }
 
-static bool lu_reg_fits(int64_t rows)
+// Register leaf capacity: JB = 32 with one or two rows per thread (<= 4096 / 8192 rows), JB = 16 with four
+// (<= 16384 rows).
+static bool lu_reg_fits(int64_t rows, int jb)
 {
-    // one row per thread: with two rows per thread it measured slower than the shared-memory cluster kernel
-    // (8192 rows: 8.5 vs 6.5 us per column), at <= 4096 rows slightly faster (5.7-5.9 vs 5.9-6.1)
-    return rows <= (int64_t)LR_CLMAX * LU_THREADS;
+    return rows <= (int64_t)LF_GMAX * LF_NT * (jb <= 16 ? 4 : 2);
 }
 
-static bool lu_panel_reg(Ctx& cx, double* L, int64_t ld, int64_t w, int64_t d, int64_t c0, int jb, int* ipiv, int* perm)
+template <int JB, int RPT>
+static void launch_lu_leaf_fast(Ctx& cx, const LuPanelArgs& a, int G)
 {
-    const int64_t rows = w - c0;
-    if (!lu_reg_fits(rows) || jb > 32) return false;
-    const int rpt = rows <= (int64_t)LR_CLMAX * LU_THREADS ? 1 : 2;
-    const int G = (int)cdiv(rows, (int64_t)LU_THREADS * rpt);
-    LuPanelArgs a{L, ld, w, d, c0, jb, LU_THREADS * rpt, ipiv, perm, nullptr, nullptr};
-    static AttrOnce attr1, attr2;
-    ensure_attr(attr1, lu_leaf_reg_kernel<1>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    ensure_attr(attr2, lu_leaf_reg_kernel<2>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    static AttrOnce attr;
+    ensure_attr(attr, lu_leaf_fast_kernel<JB, RPT>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(G);
-    cfg.blockDim = dim3(LU_THREADS);
+    cfg.blockDim = dim3(LF_NT);
     cfg.stream = cx.stream;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
@@ -590,9 +554,25 @@ static bool lu_panel_reg(Ctx& cx, double* L, int64_t ld, int64_t w, int64_t d, i
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    if (rpt == 1) BQ_CUDA(cudaLaunchKernelEx(&cfg, lu_leaf_reg_kernel<1>, a));
-    else BQ_CUDA(cudaLaunchKernelEx(&cfg, lu_leaf_reg_kernel<2>, a));
+    BQ_CUDA(cudaLaunchKernelEx(&cfg, lu_leaf_fast_kernel<JB, RPT>, a));
     ++g_launches;
+}
+
+static bool lu_panel_reg(Ctx& cx, double* L, int64_t ld, int64_t w, int64_t d, int64_t c0, int jb, int* ipiv, int* perm)
+{
+    const int64_t rows = w - c0;
+    if (jb > 32 || !lu_reg_fits(rows, jb)) return false;
+    const int rpt = rows <= (int64_t)LF_GMAX * LF_NT ? 1 : (rows <= (int64_t)LF_GMAX * LF_NT * 2 ? 2 : 4);
+    const int G = (int)cdiv(rows, (int64_t)LF_NT * rpt);
+    LuPanelArgs a{L, ld, w, d, c0, jb, LF_NT * rpt, ipiv, perm, nullptr, nullptr};
+    if (jb > 16) {
+        if (rpt == 1) launch_lu_leaf_fast<32, 1>(cx, a, G);
+        else launch_lu_leaf_fast<32, 2>(cx, a, G);
+    } else {
+        if (rpt == 1) launch_lu_leaf_fast<16, 1>(cx, a, G);
+        else if (rpt == 2) launch_lu_leaf_fast<16, 2>(cx, a, G);
+        else launch_lu_leaf_fast<16, 4>(cx, a, G);
+    }
     return true;
 }
 
@@ -671,7 +651,8 @@ static void lu_panel(Ctx& cx, double* L, int64_t ld, int64_t w, int64_t d, int64
 
 static int lu_leaf_width(int64_t rows, int num_sms)
 {
-    if (lu_reg_fits(rows)) return 32;  // the register cluster leaf (<= 16 x 512 rows)
+    if (lu_reg_fits(rows, 32)) return 32;  // the register cluster leaf, 32 columns (<= 16 x 512 rows)
+    if (lu_reg_fits(rows, 16)) return 16;  // the register cluster leaf, 16 columns (<= 16 x 1024 rows)
     // a leaf that one cluster can hold (32, else 16 columns), else the widest the grid kernel can hold
     int CL, R;
     if (lu_cluster_fits(rows, 32, &CL, &R)) return 32;

@@ -375,36 +375,9 @@ __global__ void __launch_bounds__(QC_THREADS, 1) qr_panel_cluster_kernel(QrClust
 }
 
 // ---------------------------------------------------------------------------------------------
-// Register-resident cluster leaf (rows <= 16 x 256): one panel row per thread, its <= 32 entries in
-// registers, and ONE cluster barrier per column with push-style exchange:
-//   1. every thread with row r > jr forms q[c] = x_r a_r[c] for all 32 c (q[j] = x_r^2); a 31-shuffle
-//      transpose-reduction leaves the warp sum of q[c] in lane c, which stores it into slot (warp) of
-//      EVERY CTA's shared memory (DSMEM); warp 0 of CTA 0 (which owns the leaf's 32 pivot rows) also
-//      pushes the pivot row a_jr[:];
-//   2. barrier.cluster;
-//   3. every warp sums the slots in a fixed order (lane c: coefficient c), forms beta, tau, denom
-//      (convention H, reading Z9/Z20) and coef_c = tau (a_jr[c] + sum_c / denom) for c > j; for c < j the
-//      same sums give V(:, c)^T v_j, the column of the larft recurrence for T (no separate Gram pass);
-//   4. each thread updates its own row (coef_c broadcast by shuffles).
-// The slots are double-buffered by column parity: a CTA can only reach column j+2's stores after the
-// barrier of column j+1, which every thread passes only after finishing column j's reads.
+// Register-resident cluster leaf (rows <= 16 x 256): one panel row per thread in registers, push-style DSMEM
+// exchange (see qr_leaf_fast_kernel below).
 constexpr int QL_THREADS = 256, QL_WARPS = QL_THREADS / 32, QL_CLMAX = 16;
-
-// v[j] for a runtime j < 32 from a register array: a 5-level select tree (31 independent-per-level selects,
-// depth 5) instead of a 32-long dependent select chain or a local-memory indexed load.
-__device__ __forceinline__ double select32(const double (&v)[32], int j)
-{
-    double l1[16], l2[8], l3[4], l4[2];
-#pragma unroll
-    for (int i = 0; i < 16; ++i) l1[i] = (j & 1) ? v[2 * i + 1] : v[2 * i];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) l2[i] = (j & 2) ? l1[2 * i + 1] : l1[2 * i];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) l3[i] = (j & 4) ? l2[2 * i + 1] : l2[2 * i];
-#pragma unroll
-    for (int i = 0; i < 2; ++i) l4[i] = (j & 8) ? l3[2 * i + 1] : l3[2 * i];
-    return (j & 16) ? l4[1] : l4[0];
-}
 
 struct QrLeafArgs {
     double* A;
@@ -418,71 +391,79 @@ struct QrLeafArgs {
     int64_t ldt;
 };
 
-__global__ void __launch_bounds__(QL_THREADS, 1) qr_leaf_reg_kernel(QrLeafArgs a)
+// Register-resident cluster leaf, column loop unrolled (every register index compile-time).
+// Per column: each thread forms q[c] = x_r a_r[c] (x_r = a_r[j] below the diagonal), the 31-shuffle
+// transpose-reduction leaves the warp sum of coefficient c in lane c, the 8 warp sums are combined in shared
+// memory (one block barrier) and warp 0 pushes the CTA's 32 sums — and, on CTA 0 (which owns the leaf's pivot
+// rows), the pivot row a_jr — into every CTA's slot with st.async (mbarrier tx-count, slots double-buffered
+// by column parity).  After the wait every warp sums the CL CTA slots in a fixed order, forms beta, tau,
+// denom (convention H, Z9/Z20), V(:, c)^T v_j for c < j (the larft column) and the update coefficients
+// tau w_c for c > j, which it broadcasts through a warp-private shared-memory row; each thread updates its
+// own row.  Same arithmetic as the rolled leaf, with one summation order per column.
+template <int JB>
+__global__ void __launch_bounds__(QL_THREADS, 1) qr_leaf_fast_kernel(QrLeafArgs a)
 {
     cg::cluster_group cluster = cg::this_cluster();
     const int CL = (int)cluster.num_blocks(), me = (int)cluster.block_rank();
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, jb = a.jb;
-    const int NS = CL * QL_WARPS;  // slot sources
-    extern __shared__ double dyn[];
-    double* slot = dyn;                    // [2][NS][32]
-    double* prow = slot + 2 * NS * 32;     // [2][32]
-    __shared__ double TcS[32][33];         // TcS[j][l] = V(:, l)^T v_j (CTA 0)
+    __shared__ double wsum[2][QL_WARPS][32];
+    __shared__ __align__(16) double slot[2][QL_CLMAX][32];
+    __shared__ __align__(16) double prow[2][32];
+    __shared__ __align__(16) double rowstage[2][32];
+    __shared__ __align__(16) double cw[QL_WARPS][32];
+    __shared__ double TcS[32][33];  // TcS[j][l] = V(:, l)^T v_j (CTA 0)
     __shared__ double taus[32];
-    __shared__ __align__(8) unsigned long long mbar[2];  // one per slot parity
+    __shared__ __align__(8) unsigned long long mbar[2];
     if (tid == 0) {
         mbar_init(smem_u32(&mbar[0]), 1);
         mbar_init(smem_u32(&mbar[1]), 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    cluster.sync();  // every peer's mbarriers are initialised before the first push
     const int64_t r = a.c0 + (int64_t)me * QL_THREADS + tid;  // this thread's row
     const bool has = r < a.m;
-    double av[32];
+    double av[JB];
 #pragma unroll
-    for (int c = 0; c < 32; ++c) av[c] = (has && c < jb) ? a.A[r + (a.c0 + c) * a.ld] : 0.0;
-    const int src = me * QL_WARPS + warp;
+    for (int c = 0; c < JB; ++c) av[c] = (has && c < jb) ? a.A[r + (a.c0 + c) * a.ld] : 0.0;
+    cluster.sync();  // every peer's mbarriers are initialised before the first push
 
-    // The column loop is NOT unrolled (a 32-way unrolled body overflows the instruction cache: ~30 % of
-    // the samples were no-instruction stalls); av[j] is read / written through unrolled selects so the
-    // row stays in registers.
-#pragma unroll 1
-    for (int j = 0; j < jb; ++j) {
+#pragma unroll
+    for (int j = 0; j < JB; ++j) {
+        if (j >= jb) break;
         const int par = j & 1;
         const int64_t jr = a.c0 + j;
+        const double x = (has && r > jr) ? av[j] : 0.0;
         double q[32];
-        const double xj = select32(av, j);
-        const double x = (has && r > jr) ? xj : 0.0;
 #pragma unroll
-        for (int c = 0; c < 32; ++c) q[c] = x * av[c];  // q[j] = x^2
-        const double ws = warp_transpose_reduce32(q, lane);
-        const unsigned my = smem_u32(slot + (par * NS + src) * 32 + lane), mb = smem_u32(&mbar[par]);
-        for (int rk = 0; rk < CL; ++rk) st_async_f64(mapa_u32(my, rk), ws, mapa_u32(mb, rk));
-        if (me == 0 && warp == 0) {  // pivot row jr = row of lane j: broadcast its entries, lane c pushes a_jr[c]
-            // lane l holds row c0 + l, so a_jr[c] is lane j's av[c]: lane c keeps it
-            double pv = 0.0;
+        for (int c = 0; c < 32; ++c) q[c] = (c < JB) ? x * av[c < JB ? c : 0] : 0.0;  // q[j] = x^2
+        wsum[par][warp][lane] = warp_transpose_reduce32(q, lane);
+        if (me == 0 && tid == j) {  // the pivot row jr (thread j of CTA 0) staged for warp 0's push
 #pragma unroll
-            for (int c = 0; c < 32; ++c) {
-                const double t = __shfl_sync(0xffffffffu, av[c], j);
-                pv = (lane == c) ? t : pv;
+            for (int c = 0; c < JB; ++c) rowstage[par][c] = av[c];
+        }
+        __syncthreads();
+        const unsigned mb = smem_u32(&mbar[par]);
+        if (warp == 0) {
+            double t = 0.0;
+#pragma unroll
+            for (int w = 0; w < QL_WARPS; ++w) t += wsum[par][w][lane];
+            const unsigned my = smem_u32(&slot[par][me][lane]);
+            if (me == 0) {
+                const double pv = rowstage[par][lane];
+                const unsigned pr = smem_u32(&prow[par][lane]);
+                for (int rk = 0; rk < CL; ++rk) {
+                    const unsigned rm = mapa_u32(mb, rk);
+                    st_async_f64(mapa_u32(my, rk), t, rm);
+                    st_async_f64(mapa_u32(pr, rk), pv, rm);
+                }
+            } else {
+                for (int rk = 0; rk < CL; ++rk) st_async_f64(mapa_u32(my, rk), t, mapa_u32(mb, rk));
             }
-            const unsigned pr = smem_u32(prow + par * 32 + lane);
-            for (int rk = 0; rk < CL; ++rk) st_async_f64(mapa_u32(pr, rk), pv, mapa_u32(mb, rk));
         }
-        // this CTA expects NS x 32 slot values and the 32 pivot-row values per column; phase (j / 2) of the
-        // parity's mbarrier completes when all have landed (a peer can only push column j + 2 after this CTA
-        // pushed column j + 1, i.e. after it finished reading column j: double buffering suffices)
-        if (tid == 0) mbar_arrive_expect_tx(mb, (unsigned)((NS * 32 + 32) * sizeof(double)));
+        if (tid == 0) mbar_arrive_expect_tx(mb, (unsigned)((CL * 32 + 32) * sizeof(double)));
         mbar_wait_parity(mb, (unsigned)((j >> 1) & 1));
-        // fixed-order sum of the NS slot values: 4 interleaved partial sums (short dependency chains)
-        double t4[4] = {0.0, 0.0, 0.0, 0.0};
-        for (int sidx = 0; sidx < NS; sidx += 4) {
-#pragma unroll
-            for (int u = 0; u < 4; ++u)
-                if (sidx + u < NS) t4[u] += slot[(par * NS + sidx + u) * 32 + lane];
-        }
-        const double tot = (t4[0] + t4[1]) + (t4[2] + t4[3]);
-        const double ww = prow[par * 32 + lane];
+        double tot = 0.0;
+        for (int rk = 0; rk < CL; ++rk) tot += slot[par][rk][lane];
+        const double ww = prow[par][lane];
         const double alpha = __shfl_sync(0xffffffffu, ww, j);
         const double s2 = __shfl_sync(0xffffffffu, tot, j);
         const double nrm = sqrt(fma(alpha, alpha, s2));
@@ -493,7 +474,7 @@ __global__ void __launch_bounds__(QL_THREADS, 1) qr_leaf_reg_kernel(QrLeafArgs a
             denom = alpha - beta;
         }
         const double vdot = ww + tot / denom;  // lane c: V(:, c)^T v_j (c < j) / w_c = v_j^T A(:, c) (c > j)
-        const double coef = (lane > j && lane < jb) ? tau * vdot : 0.0;
+        cw[warp][lane] = (lane > j && lane < jb) ? tau * vdot : 0.0;
         if (me == 0 && warp == 0) {
             if (lane < j) TcS[j][lane] = vdot;
             if (lane == 0) {
@@ -501,30 +482,25 @@ __global__ void __launch_bounds__(QL_THREADS, 1) qr_leaf_reg_kernel(QrLeafArgs a
                 a.tau[jr] = tau;
             }
         }
-        // update this thread's row (the shuffles stay outside the divergent part)
-        const bool upd = has && r >= jr;
-        double v = 0.0;
-        double newj = xj;
-        if (upd) {
+        __syncwarp();
+        if (has && r >= jr) {
+            double v;
             if (r == jr) {
-                newj = beta;
+                av[j] = beta;
                 v = 1.0;
             } else {
-                v = xj / denom;
-                newj = v;
+                v = av[j] / denom;
+                av[j] = v;
             }
-        }
 #pragma unroll
-        for (int c = 0; c < 32; ++c) {
-            const double cf = __shfl_sync(0xffffffffu, coef, c);
-            const double upd_c = fma(-cf, v, av[c]);
-            av[c] = (c == j) ? newj : ((upd && c > j) ? upd_c : av[c]);
+            for (int c = j + 1; c < JB; ++c) av[c] = fma(-cw[warp][c], v, av[c]);
         }
+        __syncwarp();  // cw is rewritten by the next column
     }
     // write back: R / reflectors in A, explicit V
     if (has) {
 #pragma unroll
-        for (int c = 0; c < 32; ++c) {
+        for (int c = 0; c < JB; ++c) {
             if (c < jb) {
                 const int64_t cr = a.c0 + c;
                 a.A[r + cr * a.ld] = av[c];
@@ -548,7 +524,7 @@ __global__ void __launch_bounds__(QL_THREADS, 1) qr_leaf_reg_kernel(QrLeafArgs a
         for (int j = 0; j < jb; ++j)
             if (lane < jb) a.T[(a.c0 + lane) + (a.c0 + j) * a.ldt] = Ts[lane][j];
     }
-    cluster.sync();  // peers may still be reading this CTA's slots
+    cluster.sync();  // peers may still be pushing into this CTA's slots
 }
 
 static bool qr_leaf_reg(Ctx& cx, double* A, int64_t ld, int64_t m, int64_t c0, int jb, double* tau, double* V,
@@ -559,15 +535,13 @@ static bool qr_leaf_reg(Ctx& cx, double* A, int64_t ld, int64_t m, int64_t c0, i
     // them in a 1-CTA cluster); a CTA without rows pushes exact zeros, which leave the fixed-order sums unchanged
     const int CL = (int)imax(2, cdiv(rows, QL_THREADS));
     if (CL > QL_CLMAX || jb > 32) return false;
-    const size_t smem = ((size_t)2 * CL * QL_WARPS * 32 + 64) * sizeof(double);
-    static AttrOnce attr_smem, attr_cl;
-    ensure_attr(attr_smem, qr_leaf_reg_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
-    ensure_attr(attr_cl, qr_leaf_reg_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    static AttrOnce attr_cl;
+    ensure_attr(attr_cl, qr_leaf_fast_kernel<32>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     QrLeafArgs args{A, ld, m, c0, jb, tau, V, T, ldt};
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(CL);
     cfg.blockDim = dim3(QL_THREADS);
-    cfg.dynamicSmemBytes = smem;
+    cfg.dynamicSmemBytes = 0;
     cfg.stream = cx.stream;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
@@ -576,7 +550,7 @@ static bool qr_leaf_reg(Ctx& cx, double* A, int64_t ld, int64_t m, int64_t c0, i
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    BQ_CUDA(cudaLaunchKernelEx(&cfg, qr_leaf_reg_kernel, args));
+    BQ_CUDA(cudaLaunchKernelEx(&cfg, qr_leaf_fast_kernel<32>, args));
     ++g_launches;
     return true;
 }

@@ -110,11 +110,13 @@ def test_sketch_integer_inputs_exact(gpu):
 
 
 # ----------------------------------------------------------------------------- a2 LU pivots
-@pytest.mark.parametrize("w,d", [(300, 64), (1000, 160), (5000, 300), (200, 200), (150, 400), (20000, 96),
+@pytest.mark.parametrize("w,d", [(300, 64), (1000, 160), (5000, 300), (200, 200), (150, 400), (4097, 33),
+                                 (8000, 200), (8193, 40), (12000, 50), (16384, 100), (20000, 96),
                                  (40000, 64), (70001, 100)])
 def test_lu_pivots_match_oracle(gpu, w, d):
-    """Every leaf regime of K-LU: the register cluster leaf (<= 4096 rows), the shared-memory cluster leaf
-    (<= ~25k rows), and the cooperative grid leaf (40000, 70001 rows: the C3 regime, ragged row count)."""
+    """Every leaf regime of K-LU: the register cluster leaf (32 columns with one / two rows per thread up to
+    4096 / 8192 rows, 16 columns with four up to 16384 rows, ragged last leaves), the shared-memory cluster
+    leaf, and the cooperative grid leaf (40000, 70001 rows: the C3 regime, ragged row count)."""
     bq = _bq()
     L = inputs.gaussian(w, d, seed=w + d)
     _, ipiv_o, margin = oracle.getf2(L)
@@ -125,6 +127,23 @@ def test_lu_pivots_match_oracle(gpu, w, d):
     else:  # compare up to the first near-tie
         first = int(np.argmax(margin <= 1e-10))
         assert np.array_equal(ipiv_g[:first], ipiv_o[:first])
+
+
+@pytest.mark.parametrize("w", [3000, 7000, 15000])
+def test_lu_exact_ties_across_ctas(gpu, w):
+    """IDAMAX's first-index rule (Z19) when the largest |value| of a column is held by rows in different CTAs of
+    the cluster (and with opposite signs): the first of them is the pivot, here and after two eliminations."""
+    bq = _bq()
+    rng = np.random.default_rng(w)
+    L = rng.integers(-3, 4, size=(w, 24)).astype(np.float64)
+    L[:, 0] = 1.0
+    for r, v in ((w // 3, -8.0), (w // 2, 8.0), (w - 5, 8.0)):
+        L[r, 0] = v
+    _, ipiv_o, _ = oracle.getf2(L)
+    _, ipiv_g = bq.debug_lu_pivots(_dev(L))
+    ipiv_g = _host(ipiv_g)
+    assert ipiv_g[0] == ipiv_o[0] == w // 3 + 1
+    assert np.array_equal(ipiv_g[:3], ipiv_o[:3])
 
 
 def test_lu_zero_and_tied_columns(gpu):

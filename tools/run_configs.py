@@ -111,8 +111,9 @@ def run_c5(tols):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--only", default="")
-    ap.add_argument("--tols", default="1e-13,3e-14,1e-14")
-    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "configs_r01.json"))
+    ap.add_argument("--tols", default="2.01e-14", help="C5 rank_tol values; default alpha = 1 (alpha u sqrt(n), the "
+                    "value calibrated in tools/c5_calibration.py, DESIGN.md §10)")
+    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "configs_r02.json"))
     args = ap.parse_args()
     res = {}
     if args.only in ("", "C4"):
