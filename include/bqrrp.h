@@ -149,6 +149,15 @@ int bqrrp_debug_permute(int64_t rows, int64_t w, double* X, int64_t ldx, int64_t
 int bqrrp_debug_permute_touched(int64_t rows, double* X, int64_t ldx, int64_t nt, const int* tq, const int* tsrc,
                                 void* stream);
 
+/* The panel's k x k building blocks (Alg. 3), device, column-major:
+ * bqrrp_debug_potrf: lower Cholesky factor of the SPD n x n G in place (upper triangle zeroed); BQRRP_ENUMERIC
+ * on a non-positive pivot (the CholQR breakdown the HQR fallback catches).
+ * bqrrp_debug_recon_lu: the Householder reconstruction's sign-choosing LU (BD2015): Wr (k x k, ld k) =
+ * L \ U of Qtop C^{-T} - diag(S) with S_j = -sgn of the running pivot (Z20), C lower k x k (ld k). */
+int bqrrp_debug_potrf(int64_t n, double* G, int64_t ldg, void* stream);
+int bqrrp_debug_recon_lu(int64_t k, const double* Qtop, int64_t ldq, const double* C, double* Wr, double* S,
+                         void* stream);
+
 /* Panel: CholQR(passes) + Householder reconstruction (passes 1..4) or Householder QR (passes 0) of P (h x k, ld) preconditioned by Rsk11 (k x k
  * upper, ld k), written in GEQP3 format in place (R11 on/above, V below) with tau (k), plus the
  * compact-WY update of the trailing C (h x t, ld) that follows P in memory (t may be 0). */
@@ -237,7 +246,7 @@ int bqrrp_factor_dist(int64_t m, int64_t n, double* A_local, int64_t lda_local, 
 /* Number of CUDA kernels this library has launched in the calling process (all threads). */
 unsigned long long bqrrp_launch_count(void);
 /* Panels re-factored by Householder QR after a CholQR breakdown in the last bqrrp_factor* call on this
- * thread (plus bqrrp_step_panel calls since). */
+ * thread (the multi-GPU entry counts the panels factored on this rank). */
 long long bqrrp_panel_fallbacks(void);
 
 /* Device memory the library allocates itself (the workspace when none is passed, bqrrp_factor_host's device

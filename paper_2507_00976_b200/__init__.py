@@ -57,6 +57,8 @@ def lib() -> ctypes.CDLL:
         L.bqrrp_debug_sketch_qr.argtypes = [i64, i64, P, i64, P]
         L.bqrrp_debug_permute.argtypes = [i64, i64, P, i64, i64, P, P, P]
         L.bqrrp_debug_panel.argtypes = [i64, i64, i64, P, i64, P, P, i32, P]
+        L.bqrrp_debug_potrf.argtypes = [i64, P, i64, P]
+        L.bqrrp_debug_recon_lu.argtypes = [i64, P, i64, P, P, P, P]
         L.bqrrp_debug_permute_touched.argtypes = [i64, P, i64, i64, P, P, P]
         L.bqrrp_column_norms.argtypes = [i64, i64, P, i64, P, P]
         L.bqrrp_trailing_norms.argtypes = [i64, i64, P, i64, P, P, ctypes.c_size_t, P]

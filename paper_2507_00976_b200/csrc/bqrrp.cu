@@ -1003,6 +1003,56 @@ int bqrrp_debug_permute_touched(int64_t rows, double* X, int64_t ldx, int64_t nt
     });
 }
 
+int bqrrp_debug_potrf(int64_t n, double* G, int64_t ldg, void* stream)
+{
+    if (n < 0) return -1;
+    if (!G && n > 0) return -2;
+    if (ldg < (n > 1 ? n : 1)) return -3;
+    return guarded([&]() -> int {
+        Ctx cx;
+        setup_ctx(cx, stream);
+        if (n == 0) return 0;
+        const size_t sk = (size_t)16 * n * n + (4u << 20) / 8;
+        const size_t bytes = (sk + (size_t)cdiv(n, 64) * 4096 + 8192) * 8;
+        void* ws = nullptr;
+        BQ_CUDA(lib_malloc_async(&ws, bytes, cx.stream));
+        Layout Ly{0, 0, sk * 8, 0};
+        carve(cx, ws, bytes, Ly);
+        BQ_CUDA(cudaMemsetAsync(cx.flags, 0, sizeof(int) * F_NFLAGS, cx.stream));
+        potrf_lower(cx, n, G, ldg);
+        int* hf = pinned_flags();
+        BQ_CUDA(cudaMemcpyAsync(hf, cx.flags, sizeof(int) * F_NFLAGS, cudaMemcpyDeviceToHost, cx.stream));
+        BQ_CUDA(cudaFreeAsync(ws, cx.stream));
+        BQ_CUDA(cudaStreamSynchronize(cx.stream));
+        return hf[F_POTRF_INFO] ? BQRRP_ENUMERIC : 0;
+    });
+}
+
+int bqrrp_debug_recon_lu(int64_t k, const double* Qtop, int64_t ldq, const double* C, double* Wr, double* S,
+                         void* stream)
+{
+    if (k < 1) return -1;
+    if (!Qtop) return -2;
+    if (ldq < k) return -3;
+    if (!C) return -4;
+    if (!Wr) return -5;
+    if (!S) return -6;
+    return guarded([&]() -> int {
+        Ctx cx;
+        setup_ctx(cx, stream);
+        const size_t sk = (size_t)16 * k * k + (4u << 20) / 8;
+        const size_t bytes = (sk + (size_t)cdiv(k, 64) * 4096 * 2 + 8192) * 8;
+        void* ws = nullptr;
+        BQ_CUDA(lib_malloc_async(&ws, bytes, cx.stream));
+        Layout Ly{0, 0, sk * 8, 0};
+        carve(cx, ws, bytes, Ly);
+        recon_top_lu(cx, k, Qtop, ldq, C, Wr, S);
+        BQ_CUDA(cudaFreeAsync(ws, cx.stream));
+        BQ_CUDA(cudaStreamSynchronize(cx.stream));
+        return 0;
+    });
+}
+
 int bqrrp_debug_panel(int64_t h, int64_t k, int64_t t, double* P, int64_t ld, const double* Rsk11, double* tau,
                       int cholqr_passes, void* stream)
 {

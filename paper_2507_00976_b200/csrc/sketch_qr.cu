@@ -391,18 +391,33 @@ struct QrLeafArgs {
     int64_t ldt;
 };
 
-// Register-resident cluster leaf, column loop unrolled (every register index compile-time).
-// Per column: each thread forms q[c] = x_r a_r[c] (x_r = a_r[j] below the diagonal), the 31-shuffle
-// transpose-reduction leaves the warp sum of coefficient c in lane c, the 8 warp sums are combined in shared
-// memory (one block barrier) and warp 0 pushes the CTA's 32 sums — and, on CTA 0 (which owns the leaf's pivot
-// rows), the pivot row a_jr — into every CTA's slot with st.async (mbarrier tx-count, slots double-buffered
-// by column parity).  After the wait every warp sums the CL CTA slots in a fixed order, forms beta, tau,
-// denom (convention H, Z9/Z20), V(:, c)^T v_j for c < j (the larft column) and the update coefficients
-// tau w_c for c > j, which it broadcasts through a warp-private shared-memory row; each thread updates its
-// own row.  Same arithmetic as the rolled leaf, with one summation order per column.
+// Register-resident cluster leaf.  Rolled column loop (a fully unrolled body overflows the
+// 32 KB instruction cache: measured 63 % no-instruction stalls); register entries read with a select tree and
+// written with predicated instructions.  Per column: each thread forms q[c] = x_r a_r[c] (x_r = a_r[j] below
+// the diagonal), the 31-shuffle transpose-reduction leaves the warp sum of coefficient c in lane c, the 8 warp
+// sums are combined in shared memory (one block barrier) and warp 0 pushes the CTA's 32 sums — and, on CTA 0
+// (which owns the leaf's pivot rows), the pivot row a_jr — into every CTA's slot with st.async (mbarrier
+// tx-count, slots double-buffered by column parity).  After the wait every warp sums the CL CTA slots in a
+// fixed order, forms beta, tau, denom (convention H, Z9/Z20), V(:, c)^T v_j for c < j (the larft column) and
+// the update coefficients tau w_c for c > j, broadcast through a warp-private shared-memory row; each thread
+// updates its own row.
 template <int JB>
+__device__ __forceinline__ double qsel(const double (&v)[JB], int j)
+{
+    double t[JB];
+#pragma unroll
+    for (int i = 0; i < JB; ++i) t[i] = v[i];
+#pragma unroll
+    for (int w = JB / 2, bit = 1; w >= 1; w /= 2, bit <<= 1) {
+#pragma unroll
+        for (int i = 0; i < w; ++i) t[i] = (j & bit) ? t[2 * i + 1] : t[2 * i];
+    }
+    return t[0];
+}
+
 __global__ void __launch_bounds__(QL_THREADS, 1) qr_leaf_fast_kernel(QrLeafArgs a)
 {
+    constexpr int JB = 32;
     cg::cluster_group cluster = cg::this_cluster();
     const int CL = (int)cluster.num_blocks(), me = (int)cluster.block_rank();
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, jb = a.jb;
@@ -426,19 +441,20 @@ __global__ void __launch_bounds__(QL_THREADS, 1) qr_leaf_fast_kernel(QrLeafArgs 
     for (int c = 0; c < JB; ++c) av[c] = (has && c < jb) ? a.A[r + (a.c0 + c) * a.ld] : 0.0;
     cluster.sync();  // every peer's mbarriers are initialised before the first push
 
-#pragma unroll
-    for (int j = 0; j < JB; ++j) {
-        if (j >= jb) break;
+#pragma unroll 1
+    for (int j = 0; j < jb; ++j) {
         const int par = j & 1;
         const int64_t jr = a.c0 + j;
-        const double x = (has && r > jr) ? av[j] : 0.0;
+        const double xj = qsel<JB>(av, j);
+        const double x = (has && r > jr) ? xj : 0.0;
         double q[32];
 #pragma unroll
-        for (int c = 0; c < 32; ++c) q[c] = (c < JB) ? x * av[c < JB ? c : 0] : 0.0;  // q[j] = x^2
+        for (int c = 0; c < 32; ++c) q[c] = x * av[c];  // q[j] = x^2
         wsum[par][warp][lane] = warp_transpose_reduce32(q, lane);
         if (me == 0 && tid == j) {  // the pivot row jr (thread j of CTA 0) staged for warp 0's push
 #pragma unroll
-            for (int c = 0; c < JB; ++c) rowstage[par][c] = av[c];
+            for (int c = 0; c < JB; c += 2)
+                *reinterpret_cast<double2*>(&rowstage[par][c]) = make_double2(av[c], av[c + 1]);
         }
         __syncthreads();
         const unsigned mb = smem_u32(&mbar[par]);
@@ -484,16 +500,22 @@ __global__ void __launch_bounds__(QL_THREADS, 1) qr_leaf_fast_kernel(QrLeafArgs 
         }
         __syncwarp();
         if (has && r >= jr) {
-            double v;
+            double v, newj;
             if (r == jr) {
-                av[j] = beta;
+                newj = beta;
                 v = 1.0;
             } else {
-                v = av[j] / denom;
-                av[j] = v;
+                v = xj / denom;
+                newj = v;
             }
 #pragma unroll
-            for (int c = j + 1; c < JB; ++c) av[c] = fma(-cw[warp][c], v, av[c]);
+            for (int c = 0; c < JB; c += 2) {
+                const double2 cf = *reinterpret_cast<const double2*>(&cw[warp][c]);
+                if (c > j) av[c] = fma(-cf.x, v, av[c]);
+                if (c + 1 > j) av[c + 1] = fma(-cf.y, v, av[c + 1]);
+                if (c == j) av[c] = newj;
+                if (c + 1 == j) av[c + 1] = newj;
+            }
         }
         __syncwarp();  // cw is rewritten by the next column
     }
@@ -536,7 +558,7 @@ static bool qr_leaf_reg(Ctx& cx, double* A, int64_t ld, int64_t m, int64_t c0, i
     const int CL = (int)imax(2, cdiv(rows, QL_THREADS));
     if (CL > QL_CLMAX || jb > 32) return false;
     static AttrOnce attr_cl;
-    ensure_attr(attr_cl, qr_leaf_fast_kernel<32>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    ensure_attr(attr_cl, qr_leaf_fast_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     QrLeafArgs args{A, ld, m, c0, jb, tau, V, T, ldt};
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(CL);
@@ -550,7 +572,7 @@ static bool qr_leaf_reg(Ctx& cx, double* A, int64_t ld, int64_t m, int64_t c0, i
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    BQ_CUDA(cudaLaunchKernelEx(&cfg, qr_leaf_fast_kernel<32>, args));
+    BQ_CUDA(cudaLaunchKernelEx(&cfg, qr_leaf_fast_kernel, args));
     ++g_launches;
     return true;
 }

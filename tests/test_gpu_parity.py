@@ -428,21 +428,21 @@ def test_numerically_singular_panels_stay_backward_stable(gpu):
 def test_kxk_cholesky_and_sign_lu(gpu, n):
     """The k x k factorizations of the panel (persistent kernel for n >= 256, blocked below): POTRF of an SPD
     Gram matrix against LAPACK's Cholesky (numpy), and the sign-choosing no-pivot LU of the reconstruction
-    (bqrrp_step_recon_top with C = I): L U = W - diag(S), S_j = -sgn of the running pivot (reading Z20),
+    (bqrrp_debug_recon_lu with C = I): L U = W - diag(S), S_j = -sgn of the running pivot (reading Z20),
     unit-lower L with |L| <= 1 (the pivots |a - S| >= 1 for orthonormal columns, BD2015)."""
     import ctypes
 
     import torch
 
-    from paper_2507_00976_b200.dist import _declare
+    import paper_2507_00976_b200 as bq
 
-    L = _declare()
+    L = bq.lib()
     rng = np.random.default_rng(n)
     X = rng.standard_normal((3 * n, n))
     G = X.T @ X
     Gd = _dev(G)
     st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
-    assert L.bqrrp_step_potrf(n, ctypes.c_void_p(Gd.data_ptr()), n, st) == 0
+    assert L.bqrrp_debug_potrf(n, ctypes.c_void_p(Gd.data_ptr()), n, st) == 0
     Lg = np.tril(_host(Gd))
     Lref = np.linalg.cholesky(G)
     assert np.linalg.norm(Lg - Lref) <= 1e-12 * np.linalg.norm(Lref)
@@ -453,7 +453,7 @@ def test_kxk_cholesky_and_sign_lu(gpu, n):
     C = _dev(np.eye(n))
     Wr = torch.empty((n, n), dtype=torch.float64, device="cuda").t()
     S = torch.empty(n, dtype=torch.float64, device="cuda")
-    assert L.bqrrp_step_recon_top(n, ctypes.c_void_p(Qd.data_ptr()), 2 * n, ctypes.c_void_p(C.data_ptr()),
+    assert L.bqrrp_debug_recon_lu(n, ctypes.c_void_p(Qd.data_ptr()), 2 * n, ctypes.c_void_p(C.data_ptr()),
                                   ctypes.c_void_p(Wr.data_ptr()), ctypes.c_void_p(S.data_ptr()), st) == 0
     W, s_ = _host(Wr), _host(S)
     Lw = np.tril(W, -1) + np.eye(n)

@@ -11,10 +11,10 @@ sys.path.insert(0, ROOT)
 import torch  # noqa: E402
 
 import paper_2507_00976_b200 as bq  # noqa: E402
-from paper_2507_00976_b200.dist import _declare  # noqa: E402
+
 
 k = int(sys.argv[1]) if len(sys.argv) > 1 else 2048
-L = _declare()
+L = bq.lib()
 g = torch.Generator(device="cuda").manual_seed(0)
 X = torch.randn(4 * k, k, dtype=torch.float64, device="cuda", generator=g)
 G0 = (X.t() @ X).contiguous()  # SPD, symmetric (column-major == row-major)
@@ -44,10 +44,10 @@ def timeit(fn, reps=5):
 
 out = {}
 Gw = G0.clone()
-out["potrf_ms"] = timeit(lambda: (Gw.copy_(G0), L.bqrrp_step_potrf(k, ptr(Gw), k, st)))
+out["potrf_ms"] = timeit(lambda: (Gw.copy_(G0), L.bqrrp_debug_potrf(k, ptr(Gw), k, st)))
 Wr = torch.empty(k, k, dtype=torch.float64, device="cuda")
 S = torch.empty(k, dtype=torch.float64, device="cuda")
-out["recon_top_ms"] = timeit(lambda: L.bqrrp_step_recon_top(k, ptr(Q0), 4 * k, ptr(C), ptr(Wr), ptr(S), st))
+out["recon_top_ms"] = timeit(lambda: L.bqrrp_debug_recon_lu(k, ptr(Q0), 4 * k, ptr(C), ptr(Wr), ptr(S), st))
 T = torch.triu(torch.randn(k, k, dtype=torch.float64, device="cuda", generator=g)) + 50 * torch.eye(
     k, dtype=torch.float64, device="cuda")
 T = T.t().contiguous().t()
