@@ -186,6 +186,9 @@ constexpr int TRSM_NB = 64;
 // branches.
 constexpr int TB_R = 128, TB_THREADS = TB_R;
 
+// NB = the triangular size rounded up to 16 / 32 / 64: a thread's solve costs NB (NB - 1) / 2 FMAs in a chain of
+// NB steps, so a 16-wide solve (the LU recursion's bottom nodes at 16-column leaves) does 120 instead of 2016.
+template <int NB>
 __global__ void __launch_bounds__(TB_THREADS) trsm_base_kernel(int n, int64_t nr, const double* __restrict__ T,
                                                                 int64_t ldt, int mode, int unit, double* __restrict__ B,
                                                                 int64_t st, int64_t sr)
@@ -193,12 +196,12 @@ __global__ void __launch_bounds__(TB_THREADS) trsm_base_kernel(int n, int64_t nr
     // mode 0: right, T stored upper (op(T) = T); mode 1: right, T stored lower (op(T) = T^T);
     // mode 2: left, T stored lower (unit)
     extern __shared__ double dsm[];
-    double(*C)[TRSM_NB + 1] = reinterpret_cast<double(*)[TRSM_NB + 1]>(dsm);  // C[l][t] = coef(l, t)
-    double* rdiag = dsm + TRSM_NB * (TRSM_NB + 1);                               // 1 / diag(t)
-    double(*Bs)[TB_R + 1] = reinterpret_cast<double(*)[TB_R + 1]>(rdiag + TRSM_NB);  // Bs[t][r] (sr != 1)
+    double(*C)[NB + 1] = reinterpret_cast<double(*)[NB + 1]>(dsm);                // C[l][t] = coef(l, t)
+    double* rdiag = dsm + NB * (NB + 1);                                            // 1 / diag(t)
+    double(*Bs)[TB_R + 1] = reinterpret_cast<double(*)[TB_R + 1]>(rdiag + NB);    // Bs[t][r] (sr != 1)
     const int tid = threadIdx.x;
-    for (int idx = tid; idx < TRSM_NB * TRSM_NB; idx += TB_THREADS) {
-        const int l = idx % TRSM_NB, t = idx / TRSM_NB;
+    for (int idx = tid; idx < NB * NB; idx += TB_THREADS) {
+        const int l = idx % NB, t = idx / NB;
         double v = 0.0;
         if (l < t && t < n) {
             if (mode == 0) v = T[l + (int64_t)t * ldt];
@@ -206,13 +209,13 @@ __global__ void __launch_bounds__(TB_THREADS) trsm_base_kernel(int n, int64_t nr
         }
         C[l][t] = v;
     }
-    if (tid < TRSM_NB) rdiag[tid] = (unit || tid >= n) ? 1.0 : 1.0 / T[tid + (int64_t)tid * ldt];
+    if (tid < NB) rdiag[tid] = (unit || tid >= n) ? 1.0 : 1.0 / T[tid + (int64_t)tid * ldt];
     const int64_t r0 = (int64_t)blockIdx.x * TB_R;
     const int nloc = (int)((nr - r0 < TB_R) ? nr - r0 : TB_R);
-    double x[TRSM_NB];
+    double x[NB];
     if (sr != 1) {  // left side: stage the n x TB_R tile through shared memory (coalesced along t)
-        for (int idx = tid; idx < TRSM_NB * TB_R; idx += TB_THREADS) {
-            const int t = idx % TRSM_NB, r = idx / TRSM_NB;
+        for (int idx = tid; idx < NB * TB_R; idx += TB_THREADS) {
+            const int t = idx % NB, r = idx / NB;
             Bs[t][r] = (t < n && r < nloc) ? B[t + (r0 + r) * sr] : 0.0;
         }
     }
@@ -220,43 +223,52 @@ __global__ void __launch_bounds__(TB_THREADS) trsm_base_kernel(int n, int64_t nr
     const bool mine = tid < nloc;
     if (sr == 1) {
 #pragma unroll
-        for (int t = 0; t < TRSM_NB; ++t) x[t] = (mine && t < n) ? B[t * st + (r0 + tid)] : 0.0;
+        for (int t = 0; t < NB; ++t) x[t] = (mine && t < n) ? B[t * st + (r0 + tid)] : 0.0;
     } else {
 #pragma unroll
-        for (int t = 0; t < TRSM_NB; ++t) x[t] = Bs[t][tid];
+        for (int t = 0; t < NB; ++t) x[t] = Bs[t][tid];
     }
 #pragma unroll
-    for (int t = 0; t < TRSM_NB; ++t) {
+    for (int t = 0; t < NB; ++t) {
         x[t] *= rdiag[t];
 #pragma unroll
-        for (int tt = t + 1; tt < TRSM_NB; ++tt) x[tt] = fma(-x[t], C[t][tt], x[tt]);
+        for (int tt = t + 1; tt < NB; ++tt) x[tt] = fma(-x[t], C[t][tt], x[tt]);
     }
     if (sr == 1) {
         if (mine) {
 #pragma unroll
-            for (int t = 0; t < TRSM_NB; ++t)
+            for (int t = 0; t < NB; ++t)
                 if (t < n) B[t * st + (r0 + tid)] = x[t];
         }
     } else {
 #pragma unroll
-        for (int t = 0; t < TRSM_NB; ++t) Bs[t][tid] = x[t];
+        for (int t = 0; t < NB; ++t) Bs[t][tid] = x[t];
         __syncthreads();
-        for (int idx = tid; idx < TRSM_NB * TB_R; idx += TB_THREADS) {
-            const int t = idx % TRSM_NB, r = idx / TRSM_NB;
+        for (int idx = tid; idx < NB * TB_R; idx += TB_THREADS) {
+            const int t = idx % NB, r = idx / NB;
             if (t < n && r < nloc) B[t + (r0 + r) * sr] = Bs[t][r];
         }
     }
 }
 
-constexpr size_t TB_SMEM = sizeof(double) * (TRSM_NB * (TRSM_NB + 1) + TRSM_NB + TRSM_NB * (TB_R + 1));
+template <int NB>
+static void trsm_base_launch(Ctx& cx, int n, int64_t nr, const double* T, int64_t ldt, int mode, int unit, double* B,
+                             int64_t st, int64_t sr)
+{
+    const size_t smem = sizeof(double) * (NB * (NB + 1) + NB + (sr != 1 ? NB * (TB_R + 1) : 0));
+    static AttrOnce attr;
+    ensure_attr(attr, trsm_base_kernel<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                (int)(sizeof(double) * (NB * (NB + 1) + NB + NB * (TB_R + 1))));
+    trsm_base_kernel<NB><<<(unsigned)cdiv(nr, TB_R), TB_THREADS, smem, cx.stream>>>(n, nr, T, ldt, mode, unit, B, st, sr);
+    BQ_LAUNCH_CHECK();
+}
 
 static void trsm_base(Ctx& cx, int n, int64_t nr, const double* T, int64_t ldt, int mode, int unit, double* B,
                       int64_t st, int64_t sr)
 {
-    static AttrOnce attr;
-    ensure_attr(attr, trsm_base_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TB_SMEM);
-    trsm_base_kernel<<<(unsigned)cdiv(nr, TB_R), TB_THREADS, TB_SMEM, cx.stream>>>(n, nr, T, ldt, mode, unit, B, st, sr);
-    BQ_LAUNCH_CHECK();
+    if (n <= 16) trsm_base_launch<16>(cx, n, nr, T, ldt, mode, unit, B, st, sr);
+    else if (n <= 32) trsm_base_launch<32>(cx, n, nr, T, ldt, mode, unit, B, st, sr);
+    else trsm_base_launch<64>(cx, n, nr, T, ldt, mode, unit, B, st, sr);
 }
 
 // ---- inverse-based base case (well-conditioned triangles only: CholQR / reconstruction factors)
