@@ -39,4 +39,9 @@ __device__ __forceinline__ void mbar_wait_parity(unsigned mbar, unsigned parity)
         "}\n" ::"r"(mbar), "r"(parity) : "memory");
 }
 
+// Split cluster barrier: arrive (release) now, wait (acquire) later — a CTA that has nothing left to share can
+// signal "done with my peers' memory" early and keep working (or exit) without waiting for the slowest CTA.
+__device__ __forceinline__ void cluster_arrive() { asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory"); }
+__device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
+
 }  // namespace bqrrp

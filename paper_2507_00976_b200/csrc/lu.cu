@@ -370,27 +370,27 @@ constexpr size_t LUC_SMEM_MAX = 196 * 1024;
 
 // ---------------------------------------------------------------------------------------------
 // Register-resident cluster leaf: G <= 16 CTAs of one cluster, each thread owns RPT rows of
-// the JB-column leaf panel in registers.  The column loop is rolled (a fully unrolled body overflows the
-// 32 KB instruction cache: measured 31-63 % no-instruction stalls); register entries are read with a select
-// tree and written with predicated instructions.
-// Row interchanges are NOT performed: every row carries its logical position pos (initially its own index);
-// the step-j interchange of rows jr = c0 + j and piv only swaps their labels, so no row data moves inside the
-// leaf and nobody needs row jr's values; the rows are written back to their logical positions at the end.
+// the JB-column leaf panel in registers.
+//  * Rows are never interchanged: every row carries its logical position pos (initially its own index); the
+//    step-j interchange of rows jr = c0 + j and piv only swaps their labels (nobody needs row jr's values).
+//  * The register window ROTATES: at step j a row's registers hold its columns j .. JB-1 in av[0 ..], so every
+//    register index is compile-time in a rolled loop (no select trees; a fully unrolled loop overflows the
+//    32 KB instruction cache).  The columns that leave the window are final and go straight to global memory
+//    at the row's PHYSICAL index: an active row's multiplier L(r, j) at step j, the pivot row's U part when it
+//    wins; at the end the moved rows (pos != own index, <= 2 JB of them) are moved to their logical positions
+//    in all d columns at once.
 // Per column:
 //   1. thread candidate over its active rows (pos >= jr): key = bits of |x| (monotone for x >= 0), ties to the
 //      smaller logical position — exactly IDAMAX's first-index rule in the swapped order (Z19);
 //   2. warp argmax with three redux.sync (max of the high key word, max of the low word among those, min
-//      position among those): no shuffle chains;
+//      position among those);
 //   3. each warp's winner stores its row into shared memory, one block barrier;
 //   4. warp 0 reduces the 8 warp records the same way and pushes the CTA record (|x| bits, pos, row) into
 //      every CTA's slot with st.async (mbarrier tx-count), slots double-buffered by column parity;
-//   5. after the mbarrier wait every warp reduces the G records from its own shared memory (no second barrier,
-//      no remote reads), relabels, and applies the rank-1 update to its active rows (division by the pivot,
-//      as DGETF2 and the oracle).
-// An exactly-zero pivot column leaves everything unchanged (no interchange, no scaling; Z18).  At the end the
-// rows that moved (pos != own index, <= 2 JB of them) are listed in every CTA's shared memory (DSMEM stores
-// after one cluster-wide counter), and the cluster applies those moves to the columns outside the panel and to
-// perm (every source read before any destination is written).
+//   5. after the mbarrier wait every warp picks the cluster winner from its own shared memory, relabels, and
+//      — lookahead — forms column j+1 of its rows and starts its exchange (the winner stores its row with the
+//      step-j update applied) BEFORE the full rank-1 update / rotation of step j, which then overlaps it.
+// Division by the pivot as DGETF2 and the oracle; an exactly zero pivot column changes nothing (Z18).
 constexpr int LF_NT = 256, LF_NW = LF_NT / 32, LF_GMAX = 16;
 
 __device__ __forceinline__ void argmax3(unsigned hi, unsigned lo, unsigned p, unsigned& mh, unsigned& ml, unsigned& mp)
@@ -400,38 +400,25 @@ __device__ __forceinline__ void argmax3(unsigned hi, unsigned lo, unsigned p, un
     mp = __reduce_min_sync(0xffffffffu, (hi == mh && lo == ml) ? p : 0xffffffffu);
 }
 
-// v[j] for a runtime j < JB (JB a power of two): a log2(JB)-level select tree.
-template <int JB>
-__device__ __forceinline__ double select_col(const double (&v)[JB], int j)
-{
-    double t[JB];
-#pragma unroll
-    for (int i = 0; i < JB; ++i) t[i] = v[i];
-#pragma unroll
-    for (int w = JB / 2, bit = 1; w >= 1; w /= 2, bit <<= 1) {
-#pragma unroll
-        for (int i = 0; i < w; ++i) t[i] = (j & bit) ? t[2 * i + 1] : t[2 * i];
-    }
-    return t[0];
-}
-
-// Columns outside the panel (and perm) of the moved rows: row dst <- old row src for every listed move.  Every
-// thread of the cluster owns a set of outside columns and reads all of its sources before any write.
-__device__ void apply_moves_outside(const LuPanelArgs& a, int nmv, const int* mv_src, const int* mv_dst, int64_t gtid,
-                                    int64_t gstride)
+// Rows src -> dst of the listed moves in all d columns and in perm (every source read before any write).  Every
+// thread of the cluster owns a set of columns.
+__device__ void apply_moves_all(const LuPanelArgs& a, int nmv, const int* mv_src, const int* mv_dst, int64_t gtid,
+                                int64_t gstride)
 {
     if (nmv == 0) return;
-    const int64_t n_out = a.d - a.jb;
-    for (int64_t e = gtid; e < n_out; e += gstride) {
-        const int64_t c = (e < a.c0) ? e : e + a.jb;
+    for (int64_t c = gtid; c < a.d; c += gstride) {
         double* pc = a.L + c * a.ld;
-        double v[2 * LU_JBMAX];
+        double v[2 * LU_JBMAX];  // (local memory: 8 loads in flight per chunk, registers stay with the leaf)
+        for (int t0 = 0; t0 < nmv; t0 += 8) {
 #pragma unroll
-        for (int t = 0; t < 2 * LU_JBMAX; ++t)
-            if (t < nmv) v[t] = pc[mv_src[t]];
+            for (int t = 0; t < 8; ++t)
+                if (t0 + t < nmv) v[t0 + t] = pc[mv_src[t0 + t]];
+        }
+        for (int t0 = 0; t0 < nmv; t0 += 8) {
 #pragma unroll
-        for (int t = 0; t < 2 * LU_JBMAX; ++t)
-            if (t < nmv) pc[mv_dst[t]] = v[t];
+            for (int t = 0; t < 8; ++t)
+                if (t0 + t < nmv) pc[mv_dst[t0 + t]] = v[t0 + t];
+        }
     }
     if (gtid == 0) {
         int pv[2 * LU_JBMAX];
@@ -447,7 +434,7 @@ __global__ void __launch_bounds__(LF_NT, 1) lu_leaf_fast_kernel(LuPanelArgs a)
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, jb = a.jb;
     const int G = (int)cluster.num_blocks(), me = (int)cluster.block_rank();
     constexpr int RC = LF_NT * RPT;  // rows per CTA
-    constexpr int REC = 2 + JB;      // |x| bits, pos, row[JB]
+    constexpr int REC = 2 + JB;      // |x| bits, pos, row (relative: column j + c at c)
     const int64_t rbeg = a.c0 + (int64_t)me * RC;
     __shared__ __align__(16) double wrow[2][LF_NW][JB];
     __shared__ unsigned long long wkey[2][LF_NW];
@@ -464,29 +451,29 @@ __global__ void __launch_bounds__(LF_NT, 1) lu_leaf_fast_kernel(LuPanelArgs a)
     }
     double av[RPT][JB];
     int pos[RPT];
+    int64_t rr[RPT];
 #pragma unroll
     for (int i = 0; i < RPT; ++i) {
-        const int64_t r = rbeg + tid + (int64_t)i * LF_NT;
-        const bool ok = r < a.w;
-        pos[i] = ok ? (int)r : -1;  // -1: padding row, never active
+        rr[i] = rbeg + tid + (int64_t)i * LF_NT;
+        const bool ok = rr[i] < a.w;
+        pos[i] = ok ? (int)rr[i] : -1;  // -1: padding row, never active
 #pragma unroll
-        for (int c = 0; c < JB; ++c) av[i][c] = (ok && c < jb) ? a.L[r + (a.c0 + c) * a.ld] : 0.0;
+        for (int c = 0; c < JB; ++c) av[i][c] = (ok && c < jb) ? a.L[rr[i] + (a.c0 + c) * a.ld] : 0.0;
     }
     cluster.sync();  // every peer's mbarriers are initialised before the first push
 
-#pragma unroll 1
-    for (int j = 0; j < jb; ++j) {
+    // Column j's candidate / record exchange (steps 1-4).  xc[i] = column j of my row i; the warp winner stores
+    // its row with the pending step-(j-1) update (multiplier lw[i], pivot row pr, relative to column j-1) applied
+    // and rotated: w[c] = av[c+1] - l pr[c] (columns j + c).
+    auto push_column = [&](int j, const double (&xc)[RPT], const double (&lw)[RPT], const double (&pr)[JB]) {
         const int par = j & 1;
         const int jr = (int)a.c0 + j;
-        // 1. thread candidate
         unsigned hi = 0u, lo = 0u, bp = 0xffffffffu;
         int bi = 0;
-        double xj[RPT];
 #pragma unroll
         for (int i = 0; i < RPT; ++i) {
-            xj[i] = select_col<JB>(av[i], j);
             if (pos[i] >= jr) {
-                const unsigned long long k = (unsigned long long)__double_as_longlong(fabs(xj[i]));
+                const unsigned long long k = (unsigned long long)__double_as_longlong(fabs(xc[i]));
                 const unsigned h = (unsigned)(k >> 32), l = (unsigned)k;
                 if (h > hi || (h == hi && (l > lo || (l == lo && (unsigned)pos[i] < bp)))) {
                     hi = h;
@@ -496,7 +483,6 @@ __global__ void __launch_bounds__(LF_NT, 1) lu_leaf_fast_kernel(LuPanelArgs a)
                 }
             }
         }
-        // 2. warp winner; 3. its row into shared memory
         unsigned mh, ml, mp;
         argmax3(hi, lo, bp, mh, ml, mp);
         if (lane == 0) {
@@ -507,13 +493,20 @@ __global__ void __launch_bounds__(LF_NT, 1) lu_leaf_fast_kernel(LuPanelArgs a)
 #pragma unroll
             for (int i = 0; i < RPT; ++i)
                 if (bi == i) {
+                    const double li = lw[i];
+                    if (j == 0) {
 #pragma unroll
-                    for (int c = 0; c < JB; c += 2)
-                        *reinterpret_cast<double2*>(&wrow[par][warp][c]) = make_double2(av[i][c], av[i][c + 1]);
+                        for (int c = 0; c < JB; c += 2)
+                            *reinterpret_cast<double2*>(&wrow[par][warp][c]) = make_double2(av[i][c], av[i][c + 1]);
+                    } else {
+#pragma unroll
+                        for (int c = 0; c < JB; c += 2)
+                            *reinterpret_cast<double2*>(&wrow[par][warp][c]) = make_double2(
+                                fma(-li, pr[c], av[i][c + 1]), c + 2 < JB ? fma(-li, pr[c + 1], av[i][c + 2]) : 0.0);
+                    }
                 }
         }
         __syncthreads();
-        // 4. the CTA record, pushed to every CTA of the cluster
         const unsigned mb = smem_u32(&mbar[par]);
         if (warp == 0) {
             const unsigned long long k = (lane < LF_NW) ? wkey[par][lane] : 0ull;
@@ -523,19 +516,36 @@ __global__ void __launch_bounds__(LF_NT, 1) lu_leaf_fast_kernel(LuPanelArgs a)
             const unsigned who = __ballot_sync(0xffffffffu, lane < LF_NW && p == cp && (unsigned)(k >> 32) == ch &&
                                                                 (unsigned)k == cl);
             const int wq = who ? __ffs(who) - 1 : 0;
-            const double rv = (lane >= j && lane < JB) ? wrow[par][wq][lane < JB ? lane : 0] : 0.0;
+            const int nv = JB - j;  // valid relative columns
+            const double rv = (lane < nv) ? wrow[par][wq][lane < JB ? lane : 0] : 0.0;
             const double hv = (lane == 0) ? __longlong_as_double((long long)(((unsigned long long)ch << 32) | cl))
                                           : __longlong_as_double((long long)cp);
             const unsigned dst = smem_u32(&slot[par][me][0]);
             for (int rk = 0; rk < G; ++rk) {
                 const unsigned rm = mapa_u32(mb, rk), rd = mapa_u32(dst, rk);
                 if (lane < 2) st_async_f64(rd + 8 * lane, hv, rm);
-                if (lane >= j && lane < JB) st_async_f64(rd + 8 * (2 + lane), rv, rm);
+                if (lane < nv) st_async_f64(rd + 8 * (2 + lane), rv, rm);
             }
         }
         if (tid == 0) mbar_arrive_expect_tx(mb, (unsigned)(G * (2 + JB - j) * sizeof(double)));
-        mbar_wait_parity(mb, (unsigned)((j >> 1) & 1));
-        // 5. the cluster winner (every warp, from local shared memory), relabel, rank-1 update
+    };
+
+    double xc[RPT], lm[RPT], pr[JB];
+#pragma unroll
+    for (int i = 0; i < RPT; ++i) {
+        xc[i] = av[i][0];
+        lm[i] = 0.0;
+    }
+#pragma unroll
+    for (int c = 0; c < JB; ++c) pr[c] = 0.0;
+    push_column(0, xc, lm, pr);
+
+#pragma unroll 1
+    for (int j = 0; j < jb; ++j) {
+        const int par = j & 1;
+        const int jr = (int)a.c0 + j;
+        mbar_wait_parity(smem_u32(&mbar[par]), (unsigned)((j >> 1) & 1));
+        // 5. the cluster winner (every warp, from local shared memory), relabel, multipliers
         const unsigned long long k = (lane < G) ? (unsigned long long)__double_as_longlong(slot[par][lane][0]) : 0ull;
         const unsigned p = (lane < G) ? (unsigned)__double_as_longlong(slot[par][lane][1]) : 0xffffffffu;
         unsigned gh, gl, gp;
@@ -543,54 +553,62 @@ __global__ void __launch_bounds__(LF_NT, 1) lu_leaf_fast_kernel(LuPanelArgs a)
         const unsigned who = __ballot_sync(0xffffffffu, lane < G && p == gp && (unsigned)(k >> 32) == gh &&
                                                             (unsigned)k == gl);
         const int q = __ffs(who) - 1;
-        const double* prow = &slot[par][q][2];
-        const double u = prow[j];
+        const double* prow = &slot[par][q][2];  // pivot row, columns j + c at c
+        const double u = prow[0];
         const int ps = (int)gp;
         if (tid == 0 && me == 0) a.ipiv[jr] = ps;
-        double pr[JB];
+        // pr[c] = pivot row column j + 1 + c (c < JB - 1), pr[JB-1] = 0
 #pragma unroll
-        for (int c = 0; c < JB; c += 2) {  // columns < j hold stale values; they are never used
-            const double2 t = *reinterpret_cast<const double2*>(prow + c);
-            pr[c] = t.x;
-            pr[c + 1] = t.y;
-        }
+        for (int c = 0; c + 1 < JB; ++c) pr[c] = prow[c + 1];
+        pr[JB - 1] = 0.0;
 #pragma unroll
         for (int i = 0; i < RPT; ++i) {
             const int pn = (pos[i] == jr) ? ps : ((pos[i] == ps) ? jr : pos[i]);
-            pos[i] = pn;
-            if (u != 0.0 && pn > jr) {
-                const double l = xj[i] / u;
+            const bool act = (pn > jr);  // still active after step j
+            if (pn == jr) {  // the pivot row: its U part (columns j ..) is final
 #pragma unroll
-                for (int c = 0; c < JB; ++c) {
-                    if (c == j) av[i][c] = l;
-                    if (c > j) av[i][c] = fma(-l, pr[c], av[i][c]);
-                }
+                for (int c = 0; c < JB; ++c)
+                    if (c < jb - j) a.L[rr[i] + (a.c0 + j + c) * a.ld] = av[i][c];
+            } else if (act) {  // L(r, j): the multiplier (the unscaled value on an exactly zero pivot column)
+                const double l = (u != 0.0) ? xc[i] / u : xc[i];
+                a.L[rr[i] + (int64_t)jr * a.ld] = l;
             }
+            pos[i] = pn;
+            lm[i] = (act && u != 0.0) ? xc[i] / u : 0.0;  // the update's multiplier (0: rotate only)
+        }
+        // lookahead: column j + 1 of my rows, its exchange started now
+        if (j + 1 < jb) {
+#pragma unroll
+            for (int i = 0; i < RPT; ++i) xc[i] = fma(-lm[i], pr[0], av[i][1]);
+            push_column(j + 1, xc, lm, pr);
+        }
+        // the step-j update with the rotation (overlaps the exchange of column j + 1)
+#pragma unroll
+        for (int i = 0; i < RPT; ++i) {
+#pragma unroll
+            for (int c = 0; c + 1 < JB; ++c) av[i][c] = fma(-lm[i], pr[c], av[i][c + 1]);
+            av[i][JB - 1] = 0.0;
         }
     }
-    // the rows to their logical positions; the moved ones listed in every CTA (counter in CTA 0)
+    // the moved rows listed in every CTA (counter in CTA 0), then moved in all d columns
     int* cnt0 = cluster.map_shared_rank(&mv_cnt, 0);
 #pragma unroll
     for (int i = 0; i < RPT; ++i) {
-        const int64_t r = rbeg + tid + (int64_t)i * LF_NT;
-        if (pos[i] >= 0) {
-#pragma unroll
-            for (int c = 0; c < JB; ++c)
-                if (c < jb) a.L[pos[i] + (a.c0 + c) * a.ld] = av[i][c];
-            if (pos[i] != (int)r) {
-                const int t = atomicAdd(cnt0, 1);
-                for (int rk = 0; rk < G; ++rk) {
-                    *cluster.map_shared_rank(&mv_src[t], rk) = (int)r;
-                    *cluster.map_shared_rank(&mv_dst[t], rk) = pos[i];
-                }
+        if (pos[i] >= 0 && pos[i] != (int)rr[i]) {
+            const int t = atomicAdd(cnt0, 1);
+            for (int rk = 0; rk < G; ++rk) {
+                *cluster.map_shared_rank(&mv_src[t], rk) = (int)rr[i];
+                *cluster.map_shared_rank(&mv_dst[t], rk) = pos[i];
             }
         }
     }
-    cluster.sync();  // rows written and the move list complete in every CTA
+    __threadfence();  // the panel's global writes before the other CTAs move rows
+    cluster.sync();   // move list complete in every CTA
     const int nmv = *cnt0;
+    cluster_arrive();  // CTA 0's counter is read: it may exit once every CTA has arrived here
     const int64_t gtid = (int64_t)me * LF_NT + tid, gstride = (int64_t)G * LF_NT;
-    apply_moves_outside(a, nmv, mv_src, mv_dst, gtid, gstride);
-    cluster.sync();  // CTA 0's counter stays alive until every CTA has read it
+    apply_moves_all(a, nmv, mv_src, mv_dst, gtid, gstride);
+    cluster_wait();
 }
 
 // Register leaf capacity: JB = 32 with one or two rows per thread (<= 4096 / 8192 rows), JB = 16 with four

@@ -391,30 +391,20 @@ struct QrLeafArgs {
     int64_t ldt;
 };
 
-// Register-resident cluster leaf.  Rolled column loop (a fully unrolled body overflows the
-// 32 KB instruction cache: measured 63 % no-instruction stalls); register entries read with a select tree and
-// written with predicated instructions.  Per column: each thread forms q[c] = x_r a_r[c] (x_r = a_r[j] below
-// the diagonal), the 31-shuffle transpose-reduction leaves the warp sum of coefficient c in lane c, the 8 warp
-// sums are combined in shared memory (one block barrier) and warp 0 pushes the CTA's 32 sums — and, on CTA 0
-// (which owns the leaf's pivot rows), the pivot row a_jr — into every CTA's slot with st.async (mbarrier
-// tx-count, slots double-buffered by column parity).  After the wait every warp sums the CL CTA slots in a
-// fixed order, forms beta, tau, denom (convention H, Z9/Z20), V(:, c)^T v_j for c < j (the larft column) and
-// the update coefficients tau w_c for c > j, broadcast through a warp-private shared-memory row; each thread
-// updates its own row.
-template <int JB>
-__device__ __forceinline__ double qsel(const double (&v)[JB], int j)
-{
-    double t[JB];
-#pragma unroll
-    for (int i = 0; i < JB; ++i) t[i] = v[i];
-#pragma unroll
-    for (int w = JB / 2, bit = 1; w >= 1; w /= 2, bit <<= 1) {
-#pragma unroll
-        for (int i = 0; i < w; ++i) t[i] = (j & bit) ? t[2 * i + 1] : t[2 * i];
-    }
-    return t[0];
-}
-
+// Register-resident cluster leaf, one panel row per thread.  The register window ROTATES:
+// at the start of step j av[m] holds column (j + m) mod 32 of the thread's row — columns < j already final
+// (reflector entries below the diagonal, R entries on and above it) — so every register index is
+// compile-time in a rolled loop: column j is av[0], the step's new value of column j re-enters at av[31],
+// and after 32 steps av[m] = column m again.  (Select trees over a fixed window, or a fully unrolled loop,
+// measured slower: the latter overflows the 32 KB instruction cache.)  A ragged leaf (jb < 32) runs the
+// padding columns as zero columns (tau = 0, no effect) and writes back only jb.
+// Per column: each thread forms q[m] = x_r av[m] (x_r = column j below the diagonal), the 31-shuffle
+// transpose-reduction leaves the warp sum for window slot m in lane m, the 8 warp sums are combined in shared
+// memory (one block barrier) and warp 0 pushes the CTA's 32 sums — and, on CTA 0 (which owns the leaf's pivot
+// rows), the pivot row's window — into every CTA's slot with st.async (mbarrier tx-count, double-buffered by
+// parity).  After the wait every warp sums the CL CTA slots (fixed order); lane 0 gives alpha and ||x||^2 ->
+// beta, tau, denom (convention H, Z9/Z20); lane m < 32 - j is column j + m (the update coefficient tau w_c for
+// m >= 1), lane m >= 32 - j is the earlier column c = m + j - 32 (V(:, c)^T v_j, the larft column).
 __global__ void __launch_bounds__(QL_THREADS, 1) qr_leaf_fast_kernel(QrLeafArgs a)
 {
     constexpr int JB = 32;
@@ -442,19 +432,18 @@ __global__ void __launch_bounds__(QL_THREADS, 1) qr_leaf_fast_kernel(QrLeafArgs 
     cluster.sync();  // every peer's mbarriers are initialised before the first push
 
 #pragma unroll 1
-    for (int j = 0; j < jb; ++j) {
+    for (int j = 0; j < JB; ++j) {
         const int par = j & 1;
         const int64_t jr = a.c0 + j;
-        const double xj = qsel<JB>(av, j);
-        const double x = (has && r > jr) ? xj : 0.0;
+        const double x = (has && r > jr) ? av[0] : 0.0;
         double q[32];
 #pragma unroll
-        for (int c = 0; c < 32; ++c) q[c] = x * av[c];  // q[j] = x^2
+        for (int m = 0; m < 32; ++m) q[m] = x * av[m];  // q[0] = x^2
         wsum[par][warp][lane] = warp_transpose_reduce32(q, lane);
-        if (me == 0 && tid == j) {  // the pivot row jr (thread j of CTA 0) staged for warp 0's push
+        if (me == 0 && tid == j) {  // the pivot row jr (thread j of CTA 0): its window, for warp 0's push
 #pragma unroll
-            for (int c = 0; c < JB; c += 2)
-                *reinterpret_cast<double2*>(&rowstage[par][c]) = make_double2(av[c], av[c + 1]);
+            for (int m = 0; m < JB; m += 2)
+                *reinterpret_cast<double2*>(&rowstage[par][m]) = make_double2(av[m], av[m + 1]);
         }
         __syncthreads();
         const unsigned mb = smem_u32(&mbar[par]);
@@ -480,8 +469,8 @@ __global__ void __launch_bounds__(QL_THREADS, 1) qr_leaf_fast_kernel(QrLeafArgs 
         double tot = 0.0;
         for (int rk = 0; rk < CL; ++rk) tot += slot[par][rk][lane];
         const double ww = prow[par][lane];
-        const double alpha = __shfl_sync(0xffffffffu, ww, j);
-        const double s2 = __shfl_sync(0xffffffffu, tot, j);
+        const double alpha = __shfl_sync(0xffffffffu, ww, 0);
+        const double s2 = __shfl_sync(0xffffffffu, tot, 0);
         const double nrm = sqrt(fma(alpha, alpha, s2));
         double beta = 0.0, tau = 0.0, denom = 1.0;
         if (nrm != 0.0) {
@@ -489,37 +478,37 @@ __global__ void __launch_bounds__(QL_THREADS, 1) qr_leaf_fast_kernel(QrLeafArgs 
             tau = (beta - alpha) / beta;
             denom = alpha - beta;
         }
-        const double vdot = ww + tot / denom;  // lane c: V(:, c)^T v_j (c < j) / w_c = v_j^T A(:, c) (c > j)
-        cw[warp][lane] = (lane > j && lane < jb) ? tau * vdot : 0.0;
+        const double vdot = ww + tot / denom;  // slot m: column j + m (m < 32 - j) or c = m + j - 32 (m >= 32 - j)
+        cw[warp][lane] = (lane >= 1 && lane < JB - j) ? tau * vdot : 0.0;
         if (me == 0 && warp == 0) {
-            if (lane < j) TcS[j][lane] = vdot;
+            if (lane >= JB - j) TcS[j][lane + j - JB] = vdot;
             if (lane == 0) {
                 taus[j] = tau;
-                a.tau[jr] = tau;
+                if (j < jb) a.tau[jr] = tau;
             }
         }
         __syncwarp();
+        // column j's new value, the update of the later columns, and the rotation, in one pass
+        double v = 0.0, newj = av[0];
         if (has && r >= jr) {
-            double v, newj;
             if (r == jr) {
                 newj = beta;
                 v = 1.0;
             } else {
-                v = xj / denom;
+                v = av[0] / denom;
                 newj = v;
             }
-#pragma unroll
-            for (int c = 0; c < JB; c += 2) {
-                const double2 cf = *reinterpret_cast<const double2*>(&cw[warp][c]);
-                if (c > j) av[c] = fma(-cf.x, v, av[c]);
-                if (c + 1 > j) av[c + 1] = fma(-cf.y, v, av[c + 1]);
-                if (c == j) av[c] = newj;
-                if (c + 1 == j) av[c + 1] = newj;
-            }
         }
+#pragma unroll
+        for (int m = 0; m + 1 < JB; m += 2) {
+            const double2 cf = *reinterpret_cast<const double2*>(&cw[warp][m]);
+            if (m > 0) av[m - 1] = fma(-cf.x, v, av[m]);
+            av[m] = fma(-cf.y, v, av[m + 1]);
+        }
+        av[JB - 1] = newj;
         __syncwarp();  // cw is rewritten by the next column
     }
-    // write back: R / reflectors in A, explicit V
+    // write back: R / reflectors in A, explicit V (av[m] = column m again)
     if (has) {
 #pragma unroll
         for (int c = 0; c < JB; ++c) {
@@ -530,6 +519,8 @@ __global__ void __launch_bounds__(QL_THREADS, 1) qr_leaf_fast_kernel(QrLeafArgs 
             }
         }
     }
+    // every push into this CTA has landed (the last wait); arrive now so that no CTA waits for CTA 0's larft
+    cluster_arrive();
     // T (larft): T_jj = tau_j, T(0:j, j) = -tau_j T(0:j, 0:j) (V(:, 0:j)^T v_j)
     if (me == 0 && warp == 0) {
         __shared__ double Ts[32][33];
@@ -546,7 +537,7 @@ __global__ void __launch_bounds__(QL_THREADS, 1) qr_leaf_fast_kernel(QrLeafArgs 
         for (int j = 0; j < jb; ++j)
             if (lane < jb) a.T[(a.c0 + lane) + (a.c0 + j) * a.ldt] = Ts[lane][j];
     }
-    cluster.sync();  // peers may still be pushing into this CTA's slots
+    cluster_wait();  // no CTA exits while its own pushes to peers may be in flight
 }
 
 static bool qr_leaf_reg(Ctx& cx, double* A, int64_t ld, int64_t m, int64_t c0, int jb, double* tau, double* V,
