@@ -23,6 +23,21 @@ namespace cg = cooperative_groups;
 
 namespace bqrrp {
 
+// Per-phase clock64 stamps of the register leaf (experiments only: compiled in with -DBQRRP_LEAF_TIMING into a
+// separate library, never in the product build; tools/leaf_timing.py reads them).
+#ifdef BQRRP_LEAF_TIMING
+__device__ long long g_leaf_ts[2][64][8];
+#define LEAF_TS(j, k)                                                                            \
+    do {                                                                                         \
+        if (threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1) && (j) < 64)     \
+            g_leaf_ts[blockIdx.x == 0 ? 0 : 1][(j)][(k)] = clock64();                            \
+    } while (0)
+#else
+#define LEAF_TS(j, k) \
+    do {              \
+    } while (0)
+#endif
+
 struct LuPanelArgs {
     double* L;
     int64_t ld;
@@ -441,13 +456,13 @@ __global__ void __launch_bounds__(LF_NT, 1) lu_leaf_fast_kernel(LuPanelArgs a)
     __shared__ unsigned wpos[2][LF_NW];
     __shared__ __align__(16) double slot[2][LF_GMAX][REC];
     __shared__ __align__(8) unsigned long long mbar[2];
-    __shared__ int mv_src[2 * LU_JBMAX], mv_dst[2 * LU_JBMAX];
-    __shared__ int mv_cnt;
+    __shared__ int mv_src[2 * LU_JBMAX], mv_dst[2 * LU_JBMAX], lmv_src[2 * LU_JBMAX], lmv_dst[2 * LU_JBMAX];
+    __shared__ int mv_cnt, lmv_cnt;
     if (tid == 0) {
         mbar_init(smem_u32(&mbar[0]), 1);
         mbar_init(smem_u32(&mbar[1]), 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        mv_cnt = 0;
+        lmv_cnt = 0;
     }
     double av[RPT][JB];
     int pos[RPT];
@@ -507,6 +522,7 @@ __global__ void __launch_bounds__(LF_NT, 1) lu_leaf_fast_kernel(LuPanelArgs a)
                 }
         }
         __syncthreads();
+        LEAF_TS(j - 1, 4);
         const unsigned mb = smem_u32(&mbar[par]);
         if (warp == 0) {
             const unsigned long long k = (lane < LF_NW) ? wkey[par][lane] : 0ull;
@@ -527,6 +543,7 @@ __global__ void __launch_bounds__(LF_NT, 1) lu_leaf_fast_kernel(LuPanelArgs a)
                 if (lane < nv) st_async_f64(rd + 8 * (2 + lane), rv, rm);
             }
         }
+        LEAF_TS(j - 1, 5);
         if (tid == 0) mbar_arrive_expect_tx(mb, (unsigned)(G * (2 + JB - j) * sizeof(double)));
     };
 
@@ -544,7 +561,9 @@ __global__ void __launch_bounds__(LF_NT, 1) lu_leaf_fast_kernel(LuPanelArgs a)
     for (int j = 0; j < jb; ++j) {
         const int par = j & 1;
         const int jr = (int)a.c0 + j;
+        LEAF_TS(j, 0);
         mbar_wait_parity(smem_u32(&mbar[par]), (unsigned)((j >> 1) & 1));
+        LEAF_TS(j, 1);
         // 5. the cluster winner (every warp, from local shared memory), relabel, multipliers
         const unsigned long long k = (lane < G) ? (unsigned long long)__double_as_longlong(slot[par][lane][0]) : 0ull;
         const unsigned p = (lane < G) ? (unsigned)__double_as_longlong(slot[par][lane][1]) : 0xffffffffu;
@@ -557,6 +576,7 @@ __global__ void __launch_bounds__(LF_NT, 1) lu_leaf_fast_kernel(LuPanelArgs a)
         const double u = prow[0];
         const int ps = (int)gp;
         if (tid == 0 && me == 0) a.ipiv[jr] = ps;
+        LEAF_TS(j, 2);
         // pr[c] = pivot row column j + 1 + c (c < JB - 1), pr[JB-1] = 0
 #pragma unroll
         for (int c = 0; c + 1 < JB; ++c) pr[c] = prow[c + 1];
@@ -576,12 +596,14 @@ __global__ void __launch_bounds__(LF_NT, 1) lu_leaf_fast_kernel(LuPanelArgs a)
             pos[i] = pn;
             lm[i] = (act && u != 0.0) ? xc[i] / u : 0.0;  // the update's multiplier (0: rotate only)
         }
+        LEAF_TS(j, 3);
         // lookahead: column j + 1 of my rows, its exchange started now
         if (j + 1 < jb) {
 #pragma unroll
             for (int i = 0; i < RPT; ++i) xc[i] = fma(-lm[i], pr[0], av[i][1]);
             push_column(j + 1, xc, lm, pr);
         }
+        LEAF_TS(j, 6);
         // the step-j update with the rotation (overlaps the exchange of column j + 1)
 #pragma unroll
         for (int i = 0; i < RPT; ++i) {
@@ -589,25 +611,38 @@ __global__ void __launch_bounds__(LF_NT, 1) lu_leaf_fast_kernel(LuPanelArgs a)
             for (int c = 0; c + 1 < JB; ++c) av[i][c] = fma(-lm[i], pr[c], av[i][c + 1]);
             av[i][JB - 1] = 0.0;
         }
+        LEAF_TS(j, 7);
     }
-    // the moved rows listed in every CTA (counter in CTA 0), then moved in all d columns
-    int* cnt0 = cluster.map_shared_rank(&mv_cnt, 0);
+    // the moved rows: each CTA lists its own (shared memory), every CTA gathers all lists in rank order after one
+    // cluster barrier (remote reads), then the cluster moves them in all d columns
 #pragma unroll
     for (int i = 0; i < RPT; ++i) {
         if (pos[i] >= 0 && pos[i] != (int)rr[i]) {
-            const int t = atomicAdd(cnt0, 1);
-            for (int rk = 0; rk < G; ++rk) {
-                *cluster.map_shared_rank(&mv_src[t], rk) = (int)rr[i];
-                *cluster.map_shared_rank(&mv_dst[t], rk) = pos[i];
-            }
+            const int t = atomicAdd(&lmv_cnt, 1);
+            lmv_src[t] = (int)rr[i];
+            lmv_dst[t] = pos[i];
         }
     }
     __threadfence();  // the panel's global writes before the other CTAs move rows
-    cluster.sync();   // move list complete in every CTA
-    const int nmv = *cnt0;
-    cluster_arrive();  // CTA 0's counter is read: it may exit once every CTA has arrived here
+    cluster.sync();   // every CTA's list complete
+    if (warp == 0) {
+        int nmv = 0;
+        for (int rk = 0; rk < G; ++rk) {
+            const int n = *cluster.map_shared_rank(&lmv_cnt, rk);
+            const int* rs = cluster.map_shared_rank(lmv_src, rk);
+            const int* rd = cluster.map_shared_rank(lmv_dst, rk);
+            for (int t = lane; t < n; t += 32) {
+                mv_src[nmv + t] = rs[t];
+                mv_dst[nmv + t] = rd[t];
+            }
+            nmv += n;
+        }
+        if (lane == 0) mv_cnt = nmv;
+    }
+    __syncthreads();
+    cluster_arrive();  // done reading the peers' lists: they may exit once every CTA has arrived here
     const int64_t gtid = (int64_t)me * LF_NT + tid, gstride = (int64_t)G * LF_NT;
-    apply_moves_all(a, nmv, mv_src, mv_dst, gtid, gstride);
+    apply_moves_all(a, mv_cnt, mv_src, mv_dst, gtid, gstride);
     cluster_wait();
 }
 
@@ -643,7 +678,9 @@ static bool lu_panel_reg(Ctx& cx, double* L, int64_t ld, int64_t w, int64_t d, i
     const int64_t rows = w - c0;
     if (jb > 32 || !lu_reg_fits(rows, jb)) return false;
     const int rpt = rows <= (int64_t)LF_GMAX * LF_NT ? 1 : (rows <= (int64_t)LF_GMAX * LF_NT * 2 ? 2 : 4);
-    const int G = (int)cdiv(rows, (int64_t)LF_NT * rpt);
+    // at least 2 CTAs: the DSMEM pushes need a real cluster (compute-sanitizer memcheck rejects st.async in a 1-CTA
+    // cluster); a CTA without rows offers no candidate
+    const int G = (int)imax(2, cdiv(rows, (int64_t)LF_NT * rpt));
     LuPanelArgs a{L, ld, w, d, c0, jb, LF_NT * rpt, ipiv, perm, nullptr, nullptr};
     if (jb > 16) {
         if (rpt == 1) launch_lu_leaf_fast<32, 1>(cx, a, G);
@@ -790,3 +827,10 @@ void getrf_pivots(Ctx& cx, double* L, int64_t ld, int64_t w, int64_t d, int* ipi
 }
 
 }  // namespace bqrrp
+
+#ifdef BQRRP_LEAF_TIMING
+extern "C" int bqrrp_debug_leaf_timing(long long* out)
+{
+    return cudaMemcpyFromSymbol(out, bqrrp::g_leaf_ts, sizeof(long long) * 2 * 64 * 8) == cudaSuccess ? 0 : -1;
+}
+#endif
