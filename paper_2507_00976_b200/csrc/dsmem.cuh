@@ -28,13 +28,15 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(unsigned mbar, unsigned by
 {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar), "r"(bytes) : "memory");
 }
+// acquire at CLUSTER scope: the peers' writes (st.async payloads) and everything they did before their pushes
+// (e.g. their DSMEM reads of this CTA's staging buffers) happen-before what this CTA does after the wait
 __device__ __forceinline__ void mbar_wait_parity(unsigned mbar, unsigned parity)
 {
     asm volatile(
         "{\n"
         ".reg .pred p;\n"
         "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
         "@!p bra WAIT_%=;\n"
         "}\n" ::"r"(mbar), "r"(parity) : "memory");
 }

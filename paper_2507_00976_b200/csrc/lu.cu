@@ -449,12 +449,12 @@ __global__ void __launch_bounds__(LF_NT, 1) lu_leaf_fast_kernel(LuPanelArgs a)
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, jb = a.jb;
     const int G = (int)cluster.num_blocks(), me = (int)cluster.block_rank();
     constexpr int RC = LF_NT * RPT;  // rows per CTA
-    constexpr int REC = 2 + JB;      // |x| bits, pos, row (relative: column j + c at c)
     const int64_t rbeg = a.c0 + (int64_t)me * RC;
     __shared__ __align__(16) double wrow[2][LF_NW][JB];
     __shared__ unsigned long long wkey[2][LF_NW];
     __shared__ unsigned wpos[2][LF_NW];
-    __shared__ __align__(16) double slot[2][LF_GMAX][REC];
+    __shared__ __align__(16) unsigned long long hdr[2][LF_GMAX][2];  // pushed CTA records: |x| bits, pos | warp << 32
+    __shared__ __align__(16) double prw[LF_NW][JB];                    // per-warp copy of the pulled pivot row
     __shared__ __align__(8) unsigned long long mbar[2];
     __shared__ int mv_src[2 * LU_JBMAX], mv_dst[2 * LU_JBMAX], lmv_src[2 * LU_JBMAX], lmv_dst[2 * LU_JBMAX];
     __shared__ int mv_cnt, lmv_cnt;
@@ -532,22 +532,22 @@ __global__ void __launch_bounds__(LF_NT, 1) lu_leaf_fast_kernel(LuPanelArgs a)
             const unsigned who = __ballot_sync(0xffffffffu, lane < LF_NW && p == cp && (unsigned)(k >> 32) == ch &&
                                                                 (unsigned)k == cl);
             const int wq = who ? __ffs(who) - 1 : 0;
-            const int nv = JB - j;  // valid relative columns
-            const double rv = (lane < nv) ? wrow[par][wq][lane < JB ? lane : 0] : 0.0;
-            const double hv = (lane == 0) ? __longlong_as_double((long long)(((unsigned long long)ch << 32) | cl))
-                                          : __longlong_as_double((long long)cp);
-            const unsigned dst = smem_u32(&slot[par][me][0]);
-            for (int rk = 0; rk < G; ++rk) {
-                const unsigned rm = mapa_u32(mb, rk), rd = mapa_u32(dst, rk);
-                if (lane < 2) st_async_f64(rd + 8 * lane, hv, rm);
-                if (lane < nv) st_async_f64(rd + 8 * (2 + lane), rv, rm);
+            // the CTA record (16 bytes) into every CTA's slot: lane rk pushes to rank rk (one st.async per lane);
+            // the row itself stays here (wrow[par][wq]) and is pulled by the CTAs after the winner is known
+            if (lane < G) {
+                const unsigned long long h0 = ((unsigned long long)ch << 32) | cl;
+                const unsigned long long h1 = (unsigned long long)cp | ((unsigned long long)wq << 32);
+                asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.b64 [%0], {%1, %2}, [%3];" ::"r"(
+                                 mapa_u32(smem_u32(&hdr[par][me][0]), lane)),
+                             "l"(h0), "l"(h1), "r"(mapa_u32(mb, lane))
+                             : "memory");
             }
         }
         LEAF_TS(j - 1, 5);
-        if (tid == 0) mbar_arrive_expect_tx(mb, (unsigned)(G * (2 + JB - j) * sizeof(double)));
+        if (tid == 0) mbar_arrive_expect_tx(mb, (unsigned)(G * 2 * sizeof(unsigned long long)));
     };
 
-    double xc[RPT], lm[RPT], pr[JB];
+    double xc[RPT], lm[RPT], pr[JB], u_pull = 0.0;
 #pragma unroll
     for (int i = 0; i < RPT; ++i) {
         xc[i] = av[i][0];
@@ -564,37 +564,49 @@ __global__ void __launch_bounds__(LF_NT, 1) lu_leaf_fast_kernel(LuPanelArgs a)
         LEAF_TS(j, 0);
         mbar_wait_parity(smem_u32(&mbar[par]), (unsigned)((j >> 1) & 1));
         LEAF_TS(j, 1);
-        // 5. the cluster winner (every warp, from local shared memory), relabel, multipliers
-        const unsigned long long k = (lane < G) ? (unsigned long long)__double_as_longlong(slot[par][lane][0]) : 0ull;
-        const unsigned p = (lane < G) ? (unsigned)__double_as_longlong(slot[par][lane][1]) : 0xffffffffu;
+        // 5. the cluster winner (every warp, from the pushed records), its row pulled from the winner CTA
+        const unsigned long long k = (lane < G) ? hdr[par][lane][0] : 0ull;
+        const unsigned long long pw = (lane < G) ? hdr[par][lane][1] : 0xffffffffull;
+        const unsigned p = (unsigned)pw;
         unsigned gh, gl, gp;
         argmax3((unsigned)(k >> 32), (unsigned)k, p, gh, gl, gp);
         const unsigned who = __ballot_sync(0xffffffffu, lane < G && p == gp && (unsigned)(k >> 32) == gh &&
                                                             (unsigned)k == gl);
         const int q = __ffs(who) - 1;
-        const double* prow = &slot[par][q][2];  // pivot row, columns j + c at c
-        const double u = prow[0];
+        const int wq = __shfl_sync(0xffffffffu, (int)(pw >> 32), q);
         const int ps = (int)gp;
         if (tid == 0 && me == 0) a.ipiv[jr] = ps;
         LEAF_TS(j, 2);
-        // pr[c] = pivot row column j + 1 + c (c < JB - 1), pr[JB-1] = 0
+        {
+            // lane c < JB - j: column j + c of the pivot row (DSMEM load from CTA q); staged as prw[warp][c - 1] so
+            // that pr[c] = column j + 1 + c is an aligned shared load, u from lane 0
+            double pv = 0.0;
+            if (lane < JB - j) {
+                const unsigned ra = mapa_u32(smem_u32(&wrow[par][wq][lane < JB ? lane : 0]), q);
+                asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(pv) : "r"(ra) : "memory");
+            }
+            if (lane >= 1 && lane < JB) prw[warp][lane - 1] = pv;  // (lane >= JB - j: zeros)
+            if (lane == 0) prw[warp][JB - 1] = 0.0;
+            u_pull = __shfl_sync(0xffffffffu, pv, 0);
+            __syncwarp();
 #pragma unroll
-        for (int c = 0; c + 1 < JB; ++c) pr[c] = prow[c + 1];
-        pr[JB - 1] = 0.0;
+            for (int c = 0; c < JB; c += 2) {
+                const double2 t = *reinterpret_cast<const double2*>(&prw[warp][c]);
+                pr[c] = t.x;
+                pr[c + 1] = t.y;
+            }
+            __syncwarp();  // prw is rewritten by the next column
+        }
+        const double u = u_pull;
+        int was[RPT];  // 0: inactive, 1: pivot row of step j, 2: active (updated)
+        double lq[RPT];
 #pragma unroll
         for (int i = 0; i < RPT; ++i) {
             const int pn = (pos[i] == jr) ? ps : ((pos[i] == ps) ? jr : pos[i]);
-            const bool act = (pn > jr);  // still active after step j
-            if (pn == jr) {  // the pivot row: its U part (columns j ..) is final
-#pragma unroll
-                for (int c = 0; c < JB; ++c)
-                    if (c < jb - j) a.L[rr[i] + (a.c0 + j + c) * a.ld] = av[i][c];
-            } else if (act) {  // L(r, j): the multiplier (the unscaled value on an exactly zero pivot column)
-                const double l = (u != 0.0) ? xc[i] / u : xc[i];
-                a.L[rr[i] + (int64_t)jr * a.ld] = l;
-            }
+            was[i] = (pn == jr) ? 1 : ((pn > jr) ? 2 : 0);
             pos[i] = pn;
-            lm[i] = (act && u != 0.0) ? xc[i] / u : 0.0;  // the update's multiplier (0: rotate only)
+            lq[i] = (was[i] == 2 && u != 0.0) ? xc[i] / u : xc[i];  // L(r, j) (unscaled on an exactly zero column)
+            lm[i] = (was[i] == 2 && u != 0.0) ? lq[i] : 0.0;         // the update's multiplier (0: rotate only)
         }
         LEAF_TS(j, 3);
         // lookahead: column j + 1 of my rows, its exchange started now
@@ -604,6 +616,17 @@ __global__ void __launch_bounds__(LF_NT, 1) lu_leaf_fast_kernel(LuPanelArgs a)
             push_column(j + 1, xc, lm, pr);
         }
         LEAF_TS(j, 6);
+        // the columns that leave the window (overlapping the exchange): L(r, j) of active rows, the pivot row's U
+#pragma unroll
+        for (int i = 0; i < RPT; ++i) {
+            if (was[i] == 2) {
+                a.L[rr[i] + (int64_t)jr * a.ld] = lq[i];
+            } else if (was[i] == 1) {
+#pragma unroll
+                for (int c = 0; c < JB; ++c)
+                    if (c < jb - j) a.L[rr[i] + (a.c0 + j + c) * a.ld] = av[i][c];
+            }
+        }
         // the step-j update with the rotation (overlaps the exchange of column j + 1)
 #pragma unroll
         for (int i = 0; i < RPT; ++i) {

@@ -451,17 +451,25 @@ __global__ void __launch_bounds__(QL_THREADS, 1) qr_leaf_fast_kernel(QrLeafArgs 
             double t = 0.0;
 #pragma unroll
             for (int w = 0; w < QL_WARPS; ++w) t += wsum[par][w][lane];
-            const unsigned my = smem_u32(&slot[par][me][lane]);
+            // 16-byte pushes, two ranks per instruction: lane l sends the pair (2p, 2p + 1), p = l & 15, to rank
+            // 2 it + (l >> 4) — half the st.async instructions of one 8-byte value per lane and rank
+            const int pi = lane & 15, half = lane >> 4;
+            const double t0 = __shfl_sync(0xffffffffu, t, 2 * pi), t1 = __shfl_sync(0xffffffffu, t, 2 * pi + 1);
+            const unsigned my = smem_u32(&slot[par][me][2 * pi]);
+            for (int rk = half; rk < CL; rk += 2)
+                asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];" ::"r"(
+                                 mapa_u32(my, rk)),
+                             "d"(t0), "d"(t1), "r"(mapa_u32(mb, rk))
+                             : "memory");
             if (me == 0) {
                 const double pv = rowstage[par][lane];
-                const unsigned pr = smem_u32(&prow[par][lane]);
-                for (int rk = 0; rk < CL; ++rk) {
-                    const unsigned rm = mapa_u32(mb, rk);
-                    st_async_f64(mapa_u32(my, rk), t, rm);
-                    st_async_f64(mapa_u32(pr, rk), pv, rm);
-                }
-            } else {
-                for (int rk = 0; rk < CL; ++rk) st_async_f64(mapa_u32(my, rk), t, mapa_u32(mb, rk));
+                const double p0 = __shfl_sync(0xffffffffu, pv, 2 * pi), p1 = __shfl_sync(0xffffffffu, pv, 2 * pi + 1);
+                const unsigned pr = smem_u32(&prow[par][2 * pi]);
+                for (int rk = half; rk < CL; rk += 2)
+                    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];" ::"r"(
+                                     mapa_u32(pr, rk)),
+                                 "d"(p0), "d"(p1), "r"(mapa_u32(mb, rk))
+                                 : "memory");
             }
         }
         if (tid == 0) mbar_arrive_expect_tx(mb, (unsigned)((CL * 32 + 32) * sizeof(double)));
