@@ -453,8 +453,7 @@ __global__ void __launch_bounds__(LF_NT, 1) lu_leaf_fast_kernel(LuPanelArgs a)
     __shared__ __align__(16) double wrow[2][LF_NW][JB];
     __shared__ unsigned long long wkey[2][LF_NW];
     __shared__ unsigned wpos[2][LF_NW];
-    __shared__ __align__(16) unsigned long long hdr[2][LF_GMAX][2];  // pushed CTA records: |x| bits, pos | warp << 32
-    __shared__ __align__(16) double prw[LF_NW][JB];                    // per-warp copy of the pulled pivot row
+    __shared__ __align__(16) double rec[2][LF_GMAX][2 + JB];  // pushed CTA records: |x| bits, pos, row
     __shared__ __align__(8) unsigned long long mbar[2];
     __shared__ int mv_src[2 * LU_JBMAX], mv_dst[2 * LU_JBMAX], lmv_src[2 * LU_JBMAX], lmv_dst[2 * LU_JBMAX];
     __shared__ int mv_cnt, lmv_cnt;
@@ -464,6 +463,7 @@ __global__ void __launch_bounds__(LF_NT, 1) lu_leaf_fast_kernel(LuPanelArgs a)
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         lmv_cnt = 0;
     }
+    for (int idx = tid; idx < 2 * LF_GMAX * (2 + JB); idx += LF_NT) (&rec[0][0][0])[idx] = 0.0;  // stale slots finite
     double av[RPT][JB];
     int pos[RPT];
     int64_t rr[RPT];
@@ -532,19 +532,29 @@ __global__ void __launch_bounds__(LF_NT, 1) lu_leaf_fast_kernel(LuPanelArgs a)
             const unsigned who = __ballot_sync(0xffffffffu, lane < LF_NW && p == cp && (unsigned)(k >> 32) == ch &&
                                                                 (unsigned)k == cl);
             const int wq = who ? __ffs(who) - 1 : 0;
-            // the CTA record (16 bytes) into every CTA's slot: lane rk pushes to rank rk (one st.async per lane);
-            // the row itself stays here (wrow[par][wq]) and is pulled by the CTAs after the winner is known
-            if (lane < G) {
-                const unsigned long long h0 = ((unsigned long long)ch << 32) | cl;
-                const unsigned long long h1 = (unsigned long long)cp | ((unsigned long long)wq << 32);
-                asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.b64 [%0], {%1, %2}, [%3];" ::"r"(
-                                 mapa_u32(smem_u32(&hdr[par][me][0]), lane)),
-                             "l"(h0), "l"(h1), "r"(mapa_u32(mb, lane))
+            // the CTA record (|x| bits, pos, row: columns j + c at c) into every CTA's slot, 16-byte st.async, the
+            // G x NCH chunks spread over the warp's lanes (one instruction moves 512 bytes)
+            const int NCH = 1 + (JB - j + 1) / 2;  // header + the live columns j .. JB-1 (stale beyond: never used)
+            const unsigned dst = smem_u32(&rec[par][me][0]);
+            for (int idx = lane; idx < G * NCH; idx += 32) {
+                const int rk = idx / NCH, e = idx - rk * NCH;
+                double v0, v1;
+                if (e == 0) {
+                    v0 = __longlong_as_double((long long)(((unsigned long long)ch << 32) | cl));
+                    v1 = __longlong_as_double((long long)cp);
+                } else {
+                    const double2 t = *reinterpret_cast<const double2*>(&wrow[par][wq][2 * e - 2]);
+                    v0 = t.x;
+                    v1 = t.y;
+                }
+                asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];" ::"r"(
+                                 mapa_u32(dst + 16 * e, rk)),
+                             "d"(v0), "d"(v1), "r"(mapa_u32(mb, rk))
                              : "memory");
             }
         }
         LEAF_TS(j - 1, 5);
-        if (tid == 0) mbar_arrive_expect_tx(mb, (unsigned)(G * 2 * sizeof(unsigned long long)));
+        if (tid == 0) mbar_arrive_expect_tx(mb, (unsigned)(G * (1 + (JB - j + 1) / 2) * 2 * sizeof(double)));
     };
 
     double xc[RPT], lm[RPT], pr[JB], u_pull = 0.0;
@@ -564,39 +574,22 @@ __global__ void __launch_bounds__(LF_NT, 1) lu_leaf_fast_kernel(LuPanelArgs a)
         LEAF_TS(j, 0);
         mbar_wait_parity(smem_u32(&mbar[par]), (unsigned)((j >> 1) & 1));
         LEAF_TS(j, 1);
-        // 5. the cluster winner (every warp, from the pushed records), its row pulled from the winner CTA
-        const unsigned long long k = (lane < G) ? hdr[par][lane][0] : 0ull;
-        const unsigned long long pw = (lane < G) ? hdr[par][lane][1] : 0xffffffffull;
-        const unsigned p = (unsigned)pw;
+        // 5. the cluster winner (every warp, from the pushed records in its own shared memory)
+        const unsigned long long k = (lane < G) ? (unsigned long long)__double_as_longlong(rec[par][lane][0]) : 0ull;
+        const unsigned p = (lane < G) ? (unsigned)__double_as_longlong(rec[par][lane][1]) : 0xffffffffu;
         unsigned gh, gl, gp;
         argmax3((unsigned)(k >> 32), (unsigned)k, p, gh, gl, gp);
         const unsigned who = __ballot_sync(0xffffffffu, lane < G && p == gp && (unsigned)(k >> 32) == gh &&
                                                             (unsigned)k == gl);
         const int q = __ffs(who) - 1;
-        const int wq = __shfl_sync(0xffffffffu, (int)(pw >> 32), q);
         const int ps = (int)gp;
         if (tid == 0 && me == 0) a.ipiv[jr] = ps;
         LEAF_TS(j, 2);
-        {
-            // lane c < JB - j: column j + c of the pivot row (DSMEM load from CTA q); staged as prw[warp][c - 1] so
-            // that pr[c] = column j + 1 + c is an aligned shared load, u from lane 0
-            double pv = 0.0;
-            if (lane < JB - j) {
-                const unsigned ra = mapa_u32(smem_u32(&wrow[par][wq][lane < JB ? lane : 0]), q);
-                asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(pv) : "r"(ra) : "memory");
-            }
-            if (lane >= 1 && lane < JB) prw[warp][lane - 1] = pv;  // (lane >= JB - j: zeros)
-            if (lane == 0) prw[warp][JB - 1] = 0.0;
-            u_pull = __shfl_sync(0xffffffffu, pv, 0);
-            __syncwarp();
+        const double* prow = &rec[par][q][2];  // pivot row, columns j + c at c
+        u_pull = prow[0];
 #pragma unroll
-            for (int c = 0; c < JB; c += 2) {
-                const double2 t = *reinterpret_cast<const double2*>(&prw[warp][c]);
-                pr[c] = t.x;
-                pr[c + 1] = t.y;
-            }
-            __syncwarp();  // prw is rewritten by the next column
-        }
+        for (int c = 0; c + 1 < JB; ++c) pr[c] = prow[c + 1];
+        pr[JB - 1] = 0.0;
         const double u = u_pull;
         int was[RPT];  // 0: inactive, 1: pivot row of step j, 2: active (updated)
         double lq[RPT];
