@@ -535,9 +535,10 @@ __global__ void __launch_bounds__(LF_NT, 1) lu_leaf_fast_kernel(LuPanelArgs a)
             // the CTA record (|x| bits, pos, row: columns j + c at c) into every CTA's slot, 16-byte st.async, the
             // G x NCH chunks spread over the warp's lanes (one instruction moves 512 bytes)
             const int NCH = 1 + (JB - j + 1) / 2;  // header + the live columns j .. JB-1 (stale beyond: never used)
+            const float rnch = 1.0f / (float)NCH;  // idx / NCH by a float reciprocal (exact for idx < 2^12)
             const unsigned dst = smem_u32(&rec[par][me][0]);
             for (int idx = lane; idx < G * NCH; idx += 32) {
-                const int rk = idx / NCH, e = idx - rk * NCH;
+                const int rk = (int)(((float)idx + 0.5f) * rnch), e = idx - rk * NCH;
                 double v0, v1;
                 if (e == 0) {
                     v0 = __longlong_as_double((long long)(((unsigned long long)ch << 32) | cl));

@@ -23,6 +23,21 @@ namespace cg = cooperative_groups;
 
 namespace bqrrp {
 
+// Per-phase clock64 stamps of the K-SQR register leaf (experiments only: -DBQRRP_LEAF_TIMING builds, read by
+// tools/leaf_timing.py; never in the product build).
+#ifdef BQRRP_LEAF_TIMING
+__device__ long long g_qleaf_ts[2][64][8];
+#define QLEAF_TS(j, k)                                                                          \
+    do {                                                                                        \
+        if (threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1) && (j) < 64)    \
+            g_qleaf_ts[blockIdx.x == 0 ? 0 : 1][(j)][(k)] = clock64();                          \
+    } while (0)
+#else
+#define QLEAF_TS(j, k) \
+    do {               \
+    } while (0)
+#endif
+
 constexpr int QR_JBMAX = 32;
 constexpr size_t QR_GRID_SMEM = 200 * 1024;  // slab of the cooperative grid leaf (rows per CTA x leaf width)
 constexpr int QR_XSTRIDE = 1 + QR_JBMAX;  // s2, p[1..jb)
@@ -378,6 +393,8 @@ __global__ void __launch_bounds__(QC_THREADS, 1) qr_panel_cluster_kernel(QrClust
 // Register-resident cluster leaf (rows <= 16 x 256): one panel row per thread in registers, push-style DSMEM
 // exchange (see qr_leaf_fast_kernel below).
 constexpr int QL_THREADS = 256, QL_WARPS = QL_THREADS / 32, QL_CLMAX = 16;
+constexpr int QT_LD = 34;  // row stride of the per-warp product tile (doubles): 16-byte aligned, conflict-free reads
+constexpr size_t QL_DYN_SMEM = sizeof(double) * QL_WARPS * 32 * QT_LD;
 
 struct QrLeafArgs {
     double* A;
@@ -411,6 +428,7 @@ __global__ void __launch_bounds__(QL_THREADS, 1) qr_leaf_fast_kernel(QrLeafArgs 
     cg::cluster_group cluster = cg::this_cluster();
     const int CL = (int)cluster.num_blocks(), me = (int)cluster.block_rank();
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, jb = a.jb;
+    extern __shared__ __align__(16) double qtile[];  // [QL_WARPS][32][QT_LD] per-warp product tiles
     __shared__ double wsum[2][QL_WARPS][32];
     __shared__ __align__(16) double slot[2][QL_CLMAX][32];
     __shared__ __align__(16) double prow[2][32];
@@ -435,17 +453,31 @@ __global__ void __launch_bounds__(QL_THREADS, 1) qr_leaf_fast_kernel(QrLeafArgs 
     for (int j = 0; j < JB; ++j) {
         const int par = j & 1;
         const int64_t jr = a.c0 + j;
+        QLEAF_TS(j, 0);
         const double x = (has && r > jr) ? av[0] : 0.0;
-        double q[32];
+        // warp sums of q[m] = x av[m] (q[0] = x^2): each lane writes its 32 products as a row of the warp's
+        // shared-memory tile, lane m sums column m (4 accumulators) — ~85 instructions instead of the 217 of a
+        // shuffle transpose-reduction
+        {
+            double* tile = qtile + warp * (32 * QT_LD);
 #pragma unroll
-        for (int m = 0; m < 32; ++m) q[m] = x * av[m];  // q[0] = x^2
-        wsum[par][warp][lane] = warp_transpose_reduce32(q, lane);
+            for (int m = 0; m < 32; m += 2)
+                *reinterpret_cast<double2*>(&tile[lane * QT_LD + m]) = make_double2(x * av[m], x * av[m + 1]);
+            __syncwarp();
+            double s4[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+            for (int rr = 0; rr < 32; ++rr) s4[rr & 3] += tile[rr * QT_LD + lane];
+            wsum[par][warp][lane] = (s4[0] + s4[1]) + (s4[2] + s4[3]);
+            __syncwarp();  // the tile is rewritten by the next column
+        }
         if (me == 0 && tid == j) {  // the pivot row jr (thread j of CTA 0): its window, for warp 0's push
 #pragma unroll
             for (int m = 0; m < JB; m += 2)
                 *reinterpret_cast<double2*>(&rowstage[par][m]) = make_double2(av[m], av[m + 1]);
         }
+        QLEAF_TS(j, 1);
         __syncthreads();
+        QLEAF_TS(j, 2);
         const unsigned mb = smem_u32(&mbar[par]);
         if (warp == 0) {
             double t = 0.0;
@@ -472,8 +504,10 @@ __global__ void __launch_bounds__(QL_THREADS, 1) qr_leaf_fast_kernel(QrLeafArgs 
                                  : "memory");
             }
         }
+        QLEAF_TS(j, 3);
         if (tid == 0) mbar_arrive_expect_tx(mb, (unsigned)((CL * 32 + 32) * sizeof(double)));
         mbar_wait_parity(mb, (unsigned)((j >> 1) & 1));
+        QLEAF_TS(j, 4);
         double tot = 0.0;
         for (int rk = 0; rk < CL; ++rk) tot += slot[par][rk][lane];
         const double ww = prow[par][lane];
@@ -486,7 +520,9 @@ __global__ void __launch_bounds__(QL_THREADS, 1) qr_leaf_fast_kernel(QrLeafArgs 
             tau = (beta - alpha) / beta;
             denom = alpha - beta;
         }
-        const double vdot = ww + tot / denom;  // slot m: column j + m (m < 32 - j) or c = m + j - 32 (m >= 32 - j)
+        const double rden = 1.0 / denom;      // one division per column; products below (<= 1 ulp from dividing)
+        const double vdot = ww + tot * rden;  // slot m: column j + m (m < 32 - j) or c = m + j - 32 (m >= 32 - j)
+        QLEAF_TS(j, 5);
         cw[warp][lane] = (lane >= 1 && lane < JB - j) ? tau * vdot : 0.0;
         if (me == 0 && warp == 0) {
             if (lane >= JB - j) TcS[j][lane + j - JB] = vdot;
@@ -503,7 +539,7 @@ __global__ void __launch_bounds__(QL_THREADS, 1) qr_leaf_fast_kernel(QrLeafArgs 
                 newj = beta;
                 v = 1.0;
             } else {
-                v = av[0] / denom;
+                v = av[0] * rden;
                 newj = v;
             }
         }
@@ -514,6 +550,7 @@ __global__ void __launch_bounds__(QL_THREADS, 1) qr_leaf_fast_kernel(QrLeafArgs 
             av[m] = fma(-cf.y, v, av[m + 1]);
         }
         av[JB - 1] = newj;
+        QLEAF_TS(j, 6);
         __syncwarp();  // cw is rewritten by the next column
     }
     // write back: R / reflectors in A, explicit V (av[m] = column m again)
@@ -556,13 +593,14 @@ static bool qr_leaf_reg(Ctx& cx, double* A, int64_t ld, int64_t m, int64_t c0, i
     // them in a 1-CTA cluster); a CTA without rows pushes exact zeros, which leave the fixed-order sums unchanged
     const int CL = (int)imax(2, cdiv(rows, QL_THREADS));
     if (CL > QL_CLMAX || jb > 32) return false;
-    static AttrOnce attr_cl;
+    static AttrOnce attr_cl, attr_smem;
     ensure_attr(attr_cl, qr_leaf_fast_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    ensure_attr(attr_smem, qr_leaf_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)QL_DYN_SMEM);
     QrLeafArgs args{A, ld, m, c0, jb, tau, V, T, ldt};
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(CL);
     cfg.blockDim = dim3(QL_THREADS);
-    cfg.dynamicSmemBytes = 0;
+    cfg.dynamicSmemBytes = QL_DYN_SMEM;
     cfg.stream = cx.stream;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
@@ -753,3 +791,10 @@ void sketch_qr(Ctx& cx, double* MskT, int64_t ldm, int64_t w, int64_t d, const R
 }
 
 }  // namespace bqrrp
+
+#ifdef BQRRP_LEAF_TIMING
+extern "C" int bqrrp_debug_qleaf_timing(long long* out)
+{
+    return cudaMemcpyFromSymbol(out, bqrrp::g_qleaf_ts, sizeof(long long) * 2 * 64 * 8) == cudaSuccess ? 0 : -1;
+}
+#endif

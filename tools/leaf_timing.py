@@ -1,7 +1,7 @@
-"""Per-phase cycle breakdown of the K-LU register leaf (experiment, not product): builds a separate copy of the
-library with -DBQRRP_LEAF_TIMING into /tmp, runs one warm leaf through bqrrp_debug_lu_pivots and prints the mean
-clock64 deltas per column for thread 0 of the first and the last CTA of the cluster.
-    python tools/leaf_timing.py [rows] [cols]"""
+"""Per-phase cycle breakdown of the K-LU / K-SQR register leaves (experiment, not product): builds a separate copy
+of the library with -DBQRRP_LEAF_TIMING into /tmp, runs one warm leaf through bqrrp_debug_lu_pivots /
+bqrrp_debug_sketch_qr and prints the mean clock64 deltas per column for thread 0 of the first and the last CTA.
+    python tools/leaf_timing.py [rows] [cols] [lu|qr]"""
 import ctypes
 import glob
 import os
@@ -33,7 +33,10 @@ def build():
 def main():
     rows = int(sys.argv[1]) if len(sys.argv) > 1 else 4096
     cols = int(sys.argv[2]) if len(sys.argv) > 2 else 32
+    kind = sys.argv[3] if len(sys.argv) > 3 else "lu"
     build()
+    if kind == "qr":
+        return qr_main(rows)
     import torch
 
     import paper_2507_00976_b200 as bq
@@ -65,6 +68,35 @@ def main():
             nj += 1
         tot = sum(d.values())
         print(f"{'first' if c == 0 else 'last'} CTA, rows={rows}: cycles per column " +
+              ", ".join(f"{k} {v / nj:.0f}" for k, v in d.items()) + f" | total {tot / nj:.0f}")
+
+
+def qr_main(rows):
+    import torch
+
+    import paper_2507_00976_b200 as bq
+
+    bq._LIB_PATH = LIB
+    L = bq.lib()
+    g = torch.Generator(device="cuda").manual_seed(0)
+    X0 = torch.randn(rows, 32, dtype=torch.float64, device="cuda", generator=g).t()  # WT: 32 x rows -> one leaf
+    for _ in range(3):
+        X = X0.clone().t().contiguous().t()
+        bq.debug_sketch_qr(X)
+    torch.cuda.synchronize()
+    buf = (ctypes.c_longlong * (2 * 64 * 8))()
+    assert L.bqrrp_debug_qleaf_timing(buf) == 0
+    names = ["q+transpose-reduce", "block barrier", "CTA sum+push", "wait", "slot sum+beta/tau", "update"]
+    for c in range(2):
+        d = {n: 0.0 for n in names}
+        nj = 0
+        for j in range(1, 31):
+            t = [buf[(c * 64 + j) * 8 + k] for k in range(8)]
+            for k, n in enumerate(names):
+                d[n] += t[k + 1] - t[k]
+            nj += 1
+        tot = sum(d.values())
+        print(f"K-SQR {'first' if c == 0 else 'last'} CTA, rows={rows}: cycles per column " +
               ", ".join(f"{k} {v / nj:.0f}" for k, v in d.items()) + f" | total {tot / nj:.0f}")
 
 
