@@ -74,6 +74,13 @@ typedef struct bqrrp_options {
      * gathered copy of its columns WHILE the bulk runs (measured slower on B200: the panel and the bulk contend
      * for SMs and the next panel's columns are updated twice).  The result is bitwise the same. */
     int panel_lookahead;
+    /* One-GPU lookahead: SMs of the bulk trailing GEMM.  0 (default) = auto: an iteration whose
+     * bulk GEMM is estimated shorter than the latency-bound chain it overlaps (the sample update and the next pivot
+     * selection) runs it on a green-context partition leaving 32 SMs to that chain, the others on the whole device;
+     * > 0 = every bulk GEMM on a partition of about that many SMs (rounded to the driver's granularity, 8 on
+     * sm_100); -1 = always the whole device (the round-1 schedule).  No partition support in the driver = whole
+     * device.  The result is bitwise the same for every value (fixed tiles, no split-K). */
+    int bulk_sms;
 } bqrrp_options;
 #define BQRRP_DEBUG_FORCE_BREAKDOWN 1
 #define BQRRP_DIST_SHARD_PANEL 1

@@ -11,6 +11,7 @@
 //   a5  compact-WY update of A(s:m, s+k:n) -> R12 and the next trailing matrix (apply_q_1/2)
 //   a7  termination (step bqrrp:termination)
 //   a6  sketch update MskT(c:n, 0:b) -= R12^T (R_sk11 R11^{-1})^T  (step bqrrp:update_sample)
+#include <cuda.h>
 #include <cstring>
 #include <mutex>
 #include <vector>
@@ -43,6 +44,61 @@ cudaMemPool_t lib_pool()
     }
     return pools[dev];
 }
+cudaStream_t green_stream(int sms, int* got)
+{
+    // driver entry points through the runtime (no link-time libcuda dependency)
+    using GetRes = CUresult (*)(CUdevice, CUdevResource*, CUdevResourceType);
+    using Split = CUresult (*)(CUdevResource*, unsigned*, const CUdevResource*, CUdevResource*, unsigned, unsigned);
+    using Desc = CUresult (*)(CUdevResourceDesc*, CUdevResource*, unsigned);
+    using Green = CUresult (*)(CUgreenCtx*, CUdevResourceDesc, CUdevice, unsigned);
+    using GStream = CUresult (*)(CUstream*, CUgreenCtx, unsigned, int);
+    struct Entry {
+        int dev, req, got;
+        cudaStream_t st;
+    };
+    static std::mutex mu;
+    static std::vector<Entry> cache;
+    int dev = 0;
+    BQ_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(mu);
+    for (const Entry& e : cache)
+        if (e.dev == dev && e.req == sms) {
+            *got = e.got;
+            return e.st;
+        }
+    auto entry = [](const char* name) -> void* {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess)
+            return nullptr;
+        return p;
+    };
+    auto getres = (GetRes)entry("cuDeviceGetDevResource");
+    auto split = (Split)entry("cuDevSmResourceSplitByCount");
+    auto desc = (Desc)entry("cuDevResourceGenerateDesc");
+    auto green = (Green)entry("cuGreenCtxCreate");
+    auto gstream = (GStream)entry("cuGreenCtxStreamCreate");
+    Entry e{dev, sms, 0, nullptr};
+    CUdevResource all, part, rest;
+    unsigned ng = 1;
+    CUdevResourceDesc dsc;
+    CUgreenCtx g;
+    CUstream s;
+    int prio_lo = 0, prio_hi = 0;
+    BQ_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+    if (getres && split && desc && green && gstream && getres(dev, &all, CU_DEV_RESOURCE_TYPE_SM) == CUDA_SUCCESS &&
+        split(&part, &ng, &all, &rest, 0, (unsigned)sms) == CUDA_SUCCESS && ng == 1 &&
+        desc(&dsc, &part, 1) == CUDA_SUCCESS && green(&g, dsc, dev, CU_GREEN_CTX_DEFAULT_STREAM) == CUDA_SUCCESS &&
+        gstream(&s, g, CU_STREAM_NON_BLOCKING, prio_lo) == CUDA_SUCCESS) {
+        e.st = (cudaStream_t)s;
+        e.got = (int)part.sm.smCount;
+    }
+    cudaGetLastError();  // a failed probe leaves no sticky runtime error
+    cache.push_back(e);
+    *got = e.got;
+    return e.st;
+}
+
 thread_local long long g_panel_fallbacks = 0;
 std::atomic<unsigned long long> g_launches{0};
 
@@ -243,6 +299,29 @@ struct Sched {
     Ctx* aux = nullptr;
     cudaEvent_t ev_top = nullptr, ev_bulk = nullptr;
     int panel_la = 0;  // bqrrp_options.panel_lookahead: 1 = panel i+1 overlapped with bulk i, else after it
+    Ctx* bulk_part[4] = {};    // the bulk context on SM partitions (green contexts) of part_sms[] SMs, or nullptr
+    int part_sms[4] = {};
+    int nparts = 0;
+    bool part_always = false;  // bqrrp_options.bulk_sms > 0: every bulk on bulk_part[0]
+    // The bulk context of one iteration.  The bulk GEMM (2 (h-k) k t flops) overlaps the latency-bound chain (the
+    // sample update and the next pivot selection: about 9 us per sketch column under the bulk's contention plus its
+    // GEMMs, ~3 w d^2 + 4/3 d^3 flops at ~20 TFLOP/s, plus ~5 us per column for the cooperative-grid LU leaf beyond
+    // 16384 rows).  When the bulk is the shorter of the two it runs on the smallest partition that finishes it
+    // within ~1.15x the chain (the chain itself speeds up with the SMs it gets back), leaving the other SMs to the
+    // chain's cluster kernels (measured: C2 qrcp_wide 196 -> 178 ms with the bulk on 100 SMs,
+    // profiles/bulk_partition_r02.json); otherwise on the whole device.
+    Ctx& bulk_for(int64_t h, int64_t k, int64_t t, int64_t d, int64_t w_next, int num_sms) const
+    {
+        if (nparts == 0) return *bulk;
+        if (part_always) return *bulk_part[0];
+        const double bulk_us = 2.0 * (double)(h - k) * (double)k * (double)t / 34e12 * 1e6;
+        const double dd = (double)d, ww = (double)w_next;
+        const double chain_us = dd * (w_next > 16384 ? 14.0 : 9.0) + (3.0 * ww * dd * dd + 4.0 / 3.0 * dd * dd * dd) / 20e6;
+        Ctx* best = bulk;
+        for (int i = 0; i < nparts; ++i)  // part_sms[] descending: the smallest partition that keeps up
+            if (bulk_us * num_sms / part_sms[i] <= 1.15 * chain_us) best = bulk_part[i];
+        return *best;
+    }
 };
 
 
@@ -500,11 +579,12 @@ static int64_t loop_lookahead(Run& R)
         BQ_CUDA(cudaMemsetAsync(R.hs_state, 0, sizeof(int) * tiles_m * tiles_n, cx.stream));
         wy_top(cx, h, k, t, V, h, R.Tp, C, lda, R.W, R.W2, /*rows=*/k);
         BQ_CUDA(cudaEventRecord(sc.ev_top, cx.stream));
-        BQ_CUDA(cudaStreamWaitEvent(sc.bulk->stream, sc.ev_top, 0));
-        if (sc.bulk->timer) sc.bulk->timer->begin_interval(sc.bulk->stream, PH_APPLY_QT_BULK);
-        wy_bulk(*sc.bulk, h, k, t, V, h, R.W2, C, lda, R.hs_state, R.hs_readers);
-        if (sc.bulk->timer) sc.bulk->timer->end_interval(sc.bulk->stream);
-        BQ_CUDA(cudaEventRecord(sc.ev_bulk, sc.bulk->stream));
+        Ctx& bk = sc.panel_la == 1 ? *sc.bulk : sc.bulk_for(h, k, t, R.d, n - c, cx.num_sms);
+        BQ_CUDA(cudaStreamWaitEvent(bk.stream, sc.ev_top, 0));
+        if (bk.timer) bk.timer->begin_interval(bk.stream, PH_APPLY_QT_BULK);
+        wy_bulk(bk, h, k, t, V, h, R.W2, C, lda, R.hs_state, R.hs_readers);
+        if (bk.timer) bk.timer->end_interval(bk.stream);
+        BQ_CUDA(cudaEventRecord(sc.ev_bulk, bk.stream));
         // ---- a6, then a2 of the next iteration (overlapping the bulk)
         R.sample_update(s, c, ex);
         const int64_t s1 = c, h1 = m - s1, w1 = n - s1;
@@ -692,12 +772,31 @@ static int factor_ex_impl(int64_t m, int64_t n, double* A, int64_t lda, int64_t 
             c->splitk_elems = 0;
         }
         cxa.timer = nullptr;
+        Ctx cxp[3] = {cxb, cxb, cxb};
+        cudaStream_t s_parts[3] = {};
+        int part_sms[3] = {}, nparts = 0;
+        const int bulk_sms = opts ? opts->bulk_sms : 0;
+        if (bulk_sms >= 0 && !(opts && opts->no_lookahead)) {
+            // auto (0): partitions of 132 / 116 / 100 SMs (on 148), chosen per iteration (Sched::bulk_for)
+            const int req[3] = {cx.num_sms - 16, cx.num_sms - 32, cx.num_sms - 48};
+            for (int i = 0; i < (bulk_sms > 0 ? 1 : 3); ++i) {
+                int got = 0;
+                cudaStream_t st = green_stream(bulk_sms > 0 ? bulk_sms : req[i], &got);
+                if (!st || got <= 0 || got >= cx.num_sms) continue;
+                BQ_CUDA(cudaStreamWaitEvent(st, ev_in, 0));
+                s_parts[nparts] = st;
+                part_sms[nparts] = got;
+                cxp[nparts].stream = st;
+                ++nparts;
+            }
+        }
         Timer tm;
         if (opts && opts->phase_ms) {
             tm.on = true;
             tm.st = s_hi;
             cx.timer = &tm;
             cxb.timer = &tm;
+            for (Ctx& c : cxp) c.timer = &tm;
         }
         Sched sc;
         if (!(opts && opts->no_lookahead)) {
@@ -706,11 +805,18 @@ static int factor_ex_impl(int64_t m, int64_t n, double* A, int64_t lda, int64_t 
             sc.ev_top = ev_top;
             sc.ev_bulk = ev_bulk;
             sc.panel_la = opts ? opts->panel_lookahead : 0;
+            for (int i = 0; i < nparts; ++i) {
+                sc.bulk_part[i] = &cxp[i];
+                sc.part_sms[i] = part_sms[i];
+            }
+            sc.nparts = nparts;
+            sc.part_always = bulk_sms > 0;
         }
         int64_t ell = -1;
         int status = 0;
         auto cleanup = [&]() {
-            for (cudaStream_t st : {s_hi, s_lo, s_aux}) {
+            for (cudaStream_t st : {s_hi, s_lo, s_aux, s_parts[0], s_parts[1], s_parts[2]}) {
+                if (!st) continue;
                 cudaEventRecord(ev_done, st);
                 cudaStreamWaitEvent(user, ev_done, 0);
             }

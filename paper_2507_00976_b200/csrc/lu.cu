@@ -445,6 +445,7 @@ __device__ void apply_moves_all(const LuPanelArgs& a, int nmv, const int* mv_src
 template <int JB, int RPT>
 __global__ void __launch_bounds__(LF_NT, 1) lu_leaf_fast_kernel(LuPanelArgs a)
 {
+    LEAF_TS(63, 0);
     cg::cluster_group cluster = cg::this_cluster();
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, jb = a.jb;
     const int G = (int)cluster.num_blocks(), me = (int)cluster.block_rank();
@@ -476,6 +477,7 @@ __global__ void __launch_bounds__(LF_NT, 1) lu_leaf_fast_kernel(LuPanelArgs a)
         for (int c = 0; c < JB; ++c) av[i][c] = (ok && c < jb) ? a.L[rr[i] + (a.c0 + c) * a.ld] : 0.0;
     }
     cluster.sync();  // every peer's mbarriers are initialised before the first push
+    LEAF_TS(63, 1);
 
     // Column j's candidate / record exchange (steps 1-4).  xc[i] = column j of my row i; the warp winner stores
     // its row with the pending step-(j-1) update (multiplier lw[i], pivot row pr, relative to column j-1) applied
@@ -630,6 +632,7 @@ __global__ void __launch_bounds__(LF_NT, 1) lu_leaf_fast_kernel(LuPanelArgs a)
         }
         LEAF_TS(j, 7);
     }
+    LEAF_TS(63, 2);
     // the moved rows: each CTA lists its own (shared memory), every CTA gathers all lists in rank order after one
     // cluster barrier (remote reads), then the cluster moves them in all d columns
 #pragma unroll
@@ -658,8 +661,10 @@ __global__ void __launch_bounds__(LF_NT, 1) lu_leaf_fast_kernel(LuPanelArgs a)
     }
     __syncthreads();
     cluster_arrive();  // done reading the peers' lists: they may exit once every CTA has arrived here
+    LEAF_TS(63, 4);
     const int64_t gtid = (int64_t)me * LF_NT + tid, gstride = (int64_t)G * LF_NT;
     apply_moves_all(a, mv_cnt, mv_src, mv_dst, gtid, gstride);
+    LEAF_TS(63, 3);
     cluster_wait();
 }
 

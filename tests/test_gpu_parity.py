@@ -493,6 +493,21 @@ def test_lookahead_and_serial_schedules_agree(gpu):
         assert r2 == r1 and torch.equal(J2, J1) and torch.equal(tau2, tau1) and torch.equal(Ag2, Ag1), pl
 
 
+@pytest.mark.parametrize("bulk_sms", [-1, 100, 24])
+def test_bulk_partition_is_bitwise_neutral(gpu, bulk_sms):
+    """The bulk trailing GEMM on a green-context SM partition (bqrrp_options.bulk_sms: every iteration on a
+    partition of ~100 or 24 SMs) or on the whole device (-1) gives bitwise the default (auto) factorization: the
+    bulk runs in fixed tiles with no split-K, so only its placement changes."""
+    import torch
+
+    bq = _bq()
+    A = inputs.gaussian(3000, 2500, seed=5)
+    Ag0, tau0, J0, r0 = bq.factor(_dev(A), 256, 256, seed=1)
+    Ag1, tau1, J1, r1 = bq.factor(_dev(A), 256, 256, seed=1, bulk_sms=bulk_sms)
+    assert r1 == r0 == 2500
+    assert torch.equal(J1, J0) and torch.equal(tau1, tau0) and torch.equal(Ag1, Ag0)
+
+
 @pytest.mark.parametrize("shape,b,d,exact_j", [((1, 100), 1, 1, True), ((100, 1), 8, 8, True), ((40, 300), 16, 40, False),
                                                ((333, 77), 100, 120, True), ((257, 257), 64, 64, True),
                                                ((130, 129), 128, 130, True), ((64, 1000), 64, 64, True)])

@@ -1,6 +1,7 @@
 set -x
 mkdir -p gpurun_out/r2f
-timeout 1200 python -m pytest tests/test_gpu_parity.py tests/test_gpu_golden.py -k "lu or sketch_qr or factor_c2 or bench_block or kxk or degenerate or dup" -x -q > gpurun_out/r2f/pytest_lu.log 2>&1; echo "pytest lu rc=$?"; tail -5 gpurun_out/r2f/pytest_lu.log
-for r in 1024 4096 8192 12288 16384; do python tools/leaf_probe.py lu $r 5; done > gpurun_out/r2f/leaf_probe.txt 2>&1; cat gpurun_out/r2f/leaf_probe.txt
-timeout 600 python tools/schedule_ab.py C2 3 > gpurun_out/r2f/ab_c2.txt 2>&1; grep -v '^{' gpurun_out/r2f/ab_c2.txt | head -1
-timeout 600 ncu --set full --import-source on --clock-control none -k regex:lu_leaf_fast -s 2 -c 1 -o gpurun_out/r2f/lu_fast_4096 python tools/leaf_probe.py lu 4096 2 > gpurun_out/r2f/ncu_lu.log 2>&1; echo "ncu lu rc=$?"
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r2f/launches_c2.csv python tools/profile_run.py C2 --warm 0 > gpurun_out/r2f/ncu_c2.log 2>&1; echo "ncu list rc=$?"
+timeout 300 python tools/profile_run.py C2 --no-lookahead > gpurun_out/r2f/c2_serial.txt 2>&1; echo "serial rc=$?"; tail -5 gpurun_out/r2f/c2_serial.txt
+for r in 1024 2048 4096 8192 16384 32768 63488; do python tools/leaf_probe.py lu $r 5; done > gpurun_out/r2f/leaf_lu.txt 2>&1; cat gpurun_out/r2f/leaf_lu.txt
+for r in 1024 2048; do python tools/leaf_probe.py qr $r 5; done > gpurun_out/r2f/leaf_qr.txt 2>&1; cat gpurun_out/r2f/leaf_qr.txt
+gzip -f gpurun_out/r2f/launches_c2.csv

@@ -1,7 +1,4 @@
-set -x
 mkdir -p gpurun_out/r2j
-python -c "import __graft_entry__ as g; g.build()" || exit 1
-timeout 1200 python -m pytest tests/test_gpu_parity.py tests/test_gpu_golden.py -x -q > gpurun_out/r2j/pytest.log 2>&1; echo "pytest rc=$?"; tail -5 gpurun_out/r2j/pytest.log
-for r in 1024 4096 8192 16384; do python tools/leaf_probe.py lu $r 5; done > gpurun_out/r2j/leaf_probe.txt 2>&1; cat gpurun_out/r2j/leaf_probe.txt
-timeout 600 python tools/schedule_ab.py C2 3 > gpurun_out/r2j/ab_c2.txt 2>&1; grep -v '^{' gpurun_out/r2j/ab_c2.txt | head -1
-timeout 600 ncu --set full --import-source on --clock-control none -k regex:lu_leaf_fast -s 2 -c 1 -o gpurun_out/r2j/lu_fast_4096 python tools/leaf_probe.py lu 4096 2 > gpurun_out/r2j/ncu_lu.log 2>&1; echo "ncu lu rc=$?"
+timeout 600 python -m pytest tests/test_gpu_parity.py -k "bulk_partition or lookahead_and_serial or factor_matches_oracle" -x -q > gpurun_out/r2j/pytest.log 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/r2j/pytest.log
+for c in "C2" "8192 128" "16384 256"; do echo "== $c"; timeout 600 python tools/bulk_partition_ab.py $c --reps 3 --sms -1,0; done > gpurun_out/r2j/ab.txt 2>&1; cut -c1-200 gpurun_out/r2j/ab.txt
+python tools/leaf_timing.py 4096 1024 lu > gpurun_out/r2j/lt.txt 2>&1; python tools/leaf_timing.py 16384 1024 lu >> gpurun_out/r2j/lt.txt 2>&1; python tools/leaf_timing.py 1024 1024 lu >> gpurun_out/r2j/lt.txt 2>&1; grep -v warning gpurun_out/r2j/lt.txt | grep "CTA\|leaf"

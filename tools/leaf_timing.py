@@ -69,6 +69,9 @@ def main():
         tot = sum(d.values())
         print(f"{'first' if c == 0 else 'last'} CTA, rows={rows}: cycles per column " +
               ", ".join(f"{k} {v / nj:.0f}" for k, v in d.items()) + f" | total {tot / nj:.0f}")
+        e = [buf[(c * 64 + 63) * 8 + k] for k in range(5)]
+        print(f"   leaf (the last of the {cols}-column LU): prologue {e[1] - e[0]}, column loop {e[2] - e[1]}, "
+              f"move lists {e[4] - e[2]}, row moves over all {cols} columns {e[3] - e[4]} cycles")
 
 
 def qr_main(rows):
