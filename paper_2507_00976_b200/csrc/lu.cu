@@ -415,30 +415,42 @@ __device__ __forceinline__ void argmax3(unsigned hi, unsigned lo, unsigned p, un
     mp = __reduce_min_sync(0xffffffffu, (hi == mh && lo == ml) ? p : 0xffffffffu);
 }
 
-// Rows src -> dst of the listed moves in all d columns and in perm (every source read before any write).  Every
-// thread of the cluster owns a set of columns.
-__device__ void apply_moves_all(const LuPanelArgs& a, int nmv, const int* mv_src, const int* mv_dst, int64_t gtid,
-                                int64_t gstride)
+// Rows src -> dst of the listed moves (nmv <= 2 LU_JBMAX) in all d columns and in perm.  A warp owns whole columns
+// (four at a time), lane t the moves t and t + 32: every source of a column is loaded (8 loads in flight per lane)
+// before the warp barrier, every destination stored after it.  (Round-2 form: the earlier thread-per-column loop
+// kept 8 loads in flight per THREAD and spent ~47k cycles per leaf at d = 1024; tools/leaf_timing.py.)
+__device__ void apply_moves_all(const LuPanelArgs& a, int nmv, const int* mv_src, const int* mv_dst, int64_t gwarp,
+                                int64_t nwarps, int lane)
 {
     if (nmv == 0) return;
-    for (int64_t c = gtid; c < a.d; c += gstride) {
-        double* pc = a.L + c * a.ld;
-        double v[2 * LU_JBMAX];  // (local memory: 8 loads in flight per chunk, registers stay with the leaf)
-        for (int t0 = 0; t0 < nmv; t0 += 8) {
+    const bool h0 = lane < nmv, h1 = lane + 32 < nmv;
+    const int s0 = h0 ? mv_src[lane] : 0, d0 = h0 ? mv_dst[lane] : 0;
+    const int s1 = h1 ? mv_src[lane + 32] : 0, d1 = h1 ? mv_dst[lane + 32] : 0;
+    constexpr int CB = 4;
+    for (int64_t c0 = gwarp * CB; c0 < a.d; c0 += nwarps * CB) {
+        double v0[CB], v1[CB];
 #pragma unroll
-            for (int t = 0; t < 8; ++t)
-                if (t0 + t < nmv) v[t0 + t] = pc[mv_src[t0 + t]];
+        for (int q = 0; q < CB; ++q) {
+            const double* pc = a.L + (c0 + q) * a.ld;
+            const bool ok = c0 + q < a.d;
+            v0[q] = (ok && h0) ? pc[s0] : 0.0;
+            v1[q] = (ok && h1) ? pc[s1] : 0.0;
         }
-        for (int t0 = 0; t0 < nmv; t0 += 8) {
+        __syncwarp();
 #pragma unroll
-            for (int t = 0; t < 8; ++t)
-                if (t0 + t < nmv) pc[mv_dst[t0 + t]] = v[t0 + t];
+        for (int q = 0; q < CB; ++q) {
+            double* pc = a.L + (c0 + q) * a.ld;
+            if (c0 + q < a.d) {
+                if (h0) pc[d0] = v0[q];
+                if (h1) pc[d1] = v1[q];
+            }
         }
     }
-    if (gtid == 0) {
-        int pv[2 * LU_JBMAX];
-        for (int t = 0; t < nmv; ++t) pv[t] = a.perm[mv_src[t]];
-        for (int t = 0; t < nmv; ++t) a.perm[mv_dst[t]] = pv[t];
+    if (gwarp == 0) {
+        const int p0 = h0 ? a.perm[s0] : 0, p1 = h1 ? a.perm[s1] : 0;
+        __syncwarp();
+        if (h0) a.perm[d0] = p0;
+        if (h1) a.perm[d1] = p1;
     }
 }
 
@@ -645,25 +657,29 @@ __global__ void __launch_bounds__(LF_NT, 1) lu_leaf_fast_kernel(LuPanelArgs a)
     }
     __threadfence();  // the panel's global writes before the other CTAs move rows
     cluster.sync();   // every CTA's list complete
-    if (warp == 0) {
-        int nmv = 0;
-        for (int rk = 0; rk < G; ++rk) {
-            const int n = *cluster.map_shared_rank(&lmv_cnt, rk);
-            const int* rs = cluster.map_shared_rank(lmv_src, rk);
-            const int* rd = cluster.map_shared_rank(lmv_dst, rk);
-            for (int t = lane; t < n; t += 32) {
-                mv_src[nmv + t] = rs[t];
-                mv_dst[nmv + t] = rd[t];
-            }
-            nmv += n;
+    if (warp == 0) {  // lane rk reads rank rk's count, a warp scan places the lists in rank order, lane rk copies its own
+        const int n = lane < G ? *cluster.map_shared_rank(&lmv_cnt, lane) : 0;
+        int off = n;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, off, o);
+            if (lane >= o) off += y;
         }
-        if (lane == 0) mv_cnt = nmv;
+        if (lane == 31) mv_cnt = off;
+        off -= n;
+        if (n > 0) {
+            const int* rs = cluster.map_shared_rank(lmv_src, lane);
+            const int* rd = cluster.map_shared_rank(lmv_dst, lane);
+            for (int t = 0; t < n; ++t) {
+                mv_src[off + t] = rs[t];
+                mv_dst[off + t] = rd[t];
+            }
+        }
     }
     __syncthreads();
     cluster_arrive();  // done reading the peers' lists: they may exit once every CTA has arrived here
     LEAF_TS(63, 4);
-    const int64_t gtid = (int64_t)me * LF_NT + tid, gstride = (int64_t)G * LF_NT;
-    apply_moves_all(a, mv_cnt, mv_src, mv_dst, gtid, gstride);
+    apply_moves_all(a, mv_cnt, mv_src, mv_dst, (int64_t)me * LF_NW + warp, (int64_t)G * LF_NW, lane);
     LEAF_TS(63, 3);
     cluster_wait();
 }

@@ -425,6 +425,7 @@ struct QrLeafArgs {
 __global__ void __launch_bounds__(QL_THREADS, 1) qr_leaf_fast_kernel(QrLeafArgs a)
 {
     constexpr int JB = 32;
+    QLEAF_TS(63, 0);
     cg::cluster_group cluster = cg::this_cluster();
     const int CL = (int)cluster.num_blocks(), me = (int)cluster.block_rank();
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, jb = a.jb;
@@ -448,6 +449,7 @@ __global__ void __launch_bounds__(QL_THREADS, 1) qr_leaf_fast_kernel(QrLeafArgs 
 #pragma unroll
     for (int c = 0; c < JB; ++c) av[c] = (has && c < jb) ? a.A[r + (a.c0 + c) * a.ld] : 0.0;
     cluster.sync();  // every peer's mbarriers are initialised before the first push
+    QLEAF_TS(63, 1);
 
 #pragma unroll 1
     for (int j = 0; j < JB; ++j) {
@@ -553,6 +555,7 @@ __global__ void __launch_bounds__(QL_THREADS, 1) qr_leaf_fast_kernel(QrLeafArgs 
         QLEAF_TS(j, 6);
         __syncwarp();  // cw is rewritten by the next column
     }
+    QLEAF_TS(63, 2);
     // write back: R / reflectors in A, explicit V (av[m] = column m again)
     if (has) {
 #pragma unroll
@@ -566,22 +569,31 @@ __global__ void __launch_bounds__(QL_THREADS, 1) qr_leaf_fast_kernel(QrLeafArgs 
     }
     // every push into this CTA has landed (the last wait); arrive now so that no CTA waits for CTA 0's larft
     cluster_arrive();
-    // T (larft): T_jj = tau_j, T(0:j, j) = -tau_j T(0:j, 0:j) (V(:, 0:j)^T v_j)
+    QLEAF_TS(63, 3);
+    // T (larft): T_jj = tau_j, T(0:j, j) = -tau_j T(0:j, 0:j) (V(:, 0:j)^T v_j).  Lane i keeps row i of T in
+    // registers (T(i, l) = 0 for l < i), both loops unrolled so every index is compile-time: column j costs j
+    // register FMAs per lane (the same ascending order as the scalar recurrence: the zero terms are exact)
+    // instead of a serial shared-memory dot product per lane (26k -> ~2k cycles per leaf, tools/leaf_timing.py).
     if (me == 0 && warp == 0) {
-        __shared__ double Ts[32][33];
-        for (int j = 0; j < jb; ++j) {
-            double t = 0.0;
-            if (lane < j)
-                for (int l = lane; l < j; ++l) t = fma(Ts[lane][l], TcS[j][l], t);
-            __syncwarp();
-            if (lane < j) Ts[lane][j] = -taus[j] * t;
-            if (lane == j) Ts[j][j] = taus[j];
-            if (lane > j) Ts[lane][j] = 0.0;
-            __syncwarp();
+        double trow[JB];
+#pragma unroll
+        for (int l = 0; l < JB; ++l) trow[l] = 0.0;
+#pragma unroll
+        for (int j = 0; j < JB; ++j) {
+            if (j < jb) {
+                double t = 0.0;
+#pragma unroll
+                for (int l = 0; l < j; ++l) t = fma(trow[l], TcS[j][l], t);
+                trow[j] = lane < j ? -taus[j] * t : (lane == j ? taus[j] : 0.0);
+            }
         }
-        for (int j = 0; j < jb; ++j)
-            if (lane < jb) a.T[(a.c0 + lane) + (a.c0 + j) * a.ldt] = Ts[lane][j];
+        if (lane < jb) {
+#pragma unroll
+            for (int j = 0; j < JB; ++j)
+                if (j < jb) a.T[(a.c0 + lane) + (a.c0 + j) * a.ldt] = trow[j];
+        }
     }
+    QLEAF_TS(63, 4);
     cluster_wait();  // no CTA exits while its own pushes to peers may be in flight
 }
 

@@ -1,10 +1,4 @@
-set -x
 mkdir -p gpurun_out/r2l
-python -c "import __graft_entry__ as g; g.build()" || exit 1
-for tool in memcheck racecheck synccheck; do
-  timeout 900 compute-sanitizer --tool $tool --print-limit 50 python tools/sanitize_run.py C1 > gpurun_out/r2l/san_${tool}_c1.log 2>&1; echo "$tool C1 rc=$?"; tail -3 gpurun_out/r2l/san_${tool}_c1.log
-done
-timeout 1200 compute-sanitizer --tool memcheck --print-limit 50 python tools/sanitize_run.py 6000 256 > gpurun_out/r2l/san_memcheck_6000.log 2>&1; echo "memcheck 6000 rc=$?"; tail -3 gpurun_out/r2l/san_memcheck_6000.log
-timeout 1200 compute-sanitizer --tool memcheck --print-limit 50 python tools/sanitize_run.py 12000 512 > gpurun_out/r2l/san_memcheck_12000.log 2>&1; echo "memcheck 12000 rc=$?"; tail -3 gpurun_out/r2l/san_memcheck_12000.log
-timeout 1500 compute-sanitizer --tool racecheck --print-limit 50 python tools/sanitize_run.py 3000 128 > gpurun_out/r2l/san_racecheck_3000.log 2>&1; echo "racecheck 3000 rc=$?"; tail -3 gpurun_out/r2l/san_racecheck_3000.log
-timeout 900 compute-sanitizer --tool memcheck --print-limit 50 python -m pytest tests/test_gpu_norms.py -q -x > gpurun_out/r2l/san_memcheck_norms.log 2>&1; echo "memcheck norms rc=$?"; tail -3 gpurun_out/r2l/san_memcheck_norms.log
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_golden.py -k "sketch_qr or householder or hqr or factor_matches or c1_seeds or bench_block or kahan or graded" -x -q > gpurun_out/r2l/pytest.log 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/r2l/pytest.log
+for c in "C2" "8192 128"; do echo "== $c"; timeout 600 python tools/bulk_partition_ab.py $c --reps 3 --sms 0; done > gpurun_out/r2l/ab.txt 2>&1; cut -c1-250 gpurun_out/r2l/ab.txt
+(python tools/leaf_timing.py 1024 32 qr) > gpurun_out/r2l/lt.txt 2>&1; grep -v warning gpurun_out/r2l/lt.txt | grep "CTA\|leaf"

@@ -101,6 +101,9 @@ def qr_main(rows):
         tot = sum(d.values())
         print(f"K-SQR {'first' if c == 0 else 'last'} CTA, rows={rows}: cycles per column " +
               ", ".join(f"{k} {v / nj:.0f}" for k, v in d.items()) + f" | total {tot / nj:.0f}")
+        e = [buf[(c * 64 + 63) * 8 + k] for k in range(5)]
+        print(f"   leaf: prologue {e[1] - e[0]}, column loop {e[2] - e[1]}, write-back {e[3] - e[2]}, "
+              f"T (CTA 0) {e[4] - e[3]} cycles")
 
 
 if __name__ == "__main__":
