@@ -81,6 +81,10 @@ typedef struct bqrrp_options {
      * sm_100); -1 = always the whole device (the round-1 schedule).  No partition support in the driver = whole
      * device.  The result is bitwise the same for every value (fixed tiles, no split-K). */
     int bulk_sms;
+    /* One-GPU lookahead: 0 (default) = K-SQR pipelined with K-LU (left-looking Householder QR of
+     * each 32-column block of sketch columns as soon as K-LU has fixed its pivots, on a third stream); 1 = the
+     * recursive K-SQR after K-LU (the round-1 order).  R_sk agrees to rounding (different operation order). */
+    int no_sqr_pipeline;
 } bqrrp_options;
 #define BQRRP_DEBUG_FORCE_BREAKDOWN 1
 #define BQRRP_DIST_SHARD_PANEL 1

@@ -1,6 +1,8 @@
 // bqrrp_internal.cuh — internal interfaces between the BQRRP kernels and the driver.
 #pragma once
+#include <functional>
 #include <string>
+#include <vector>
 
 #include "../../include/bqrrp.h"
 #include "common.cuh"
@@ -69,7 +71,11 @@ void sketch_apply(Ctx& cx, int64_t m, int64_t n, const double* A, int64_t lda, i
 
 // a2: partial-pivot LU of the w x d matrix L (in place), ipiv[j] = 0-based pivot row, j < min(w,d);
 // perm (w) = the row permutation of piv_transform (J_qr - 1).
-void getrf_pivots(Ctx& cx, double* L, int64_t ld, int64_t w, int64_t d, int* ipiv, int* perm);
+// on_leaf (optional) is called on the host after each leaf is queued with c1 = the number of leading pivots that
+// are final from then on in stream order (perm[0:c1) and ipiv[0:c1)): the K-SQR pipeline starts on them.
+using LeafDone = std::function<void(int64_t c1)>;
+void getrf_pivots(Ctx& cx, double* L, int64_t ld, int64_t w, int64_t d, int* ipiv, int* perm,
+                  const LeafDone* on_leaf = nullptr);
 // Largest sketch-transpose height (w = n - s rows) K-LU's grid leaf holds; largest panel height the
 // Householder panel (HQR variant and CholQR-breakdown fallback) holds.  Checked before any launch.
 int64_t lu_max_rows(int num_sms);
@@ -96,6 +102,30 @@ struct RskDefer {
 };
 void sketch_qr(Ctx& cx, double* MskT, int64_t ldm, int64_t w, int64_t d, const RowBlocks& rows = RowBlocks(),
                const RskDefer* defer = nullptr);
+// The same R_sk, pipelined with K-LU (one-GPU lookahead driver): R_sk(:, 0:p) is the QR of the
+// sketch columns J(0:p) in pivot order, and K-LU fixes them in order, leaf by leaf.  So the Householder QR runs
+// LEFT-looking on its own stream q: as soon as a 32-column block of pivots is final, its sketch columns are
+// gathered (on the critical stream, from the not yet permuted MskT rows perm[c]) into Wq, and q applies the
+// previous blocks' reflectors to it (three GEMMs), factors it with the K-SQR leaf, and extends T (three GEMMs),
+// while K-LU factors the next columns.  finish() joins q and does the rest of sketch_qr (Q_sk, the R_sk(:, d:w)
+// GEMM, the in-place store).  Buffers come from cx's bump allocator at begin (released by finish, LIFO with
+// the LU's own scratch); q allocates nothing.  events: caller-owned pool, reused across calls.
+struct SketchQrPipe {
+    Ctx* cx = nullptr;
+    Ctx* q = nullptr;
+    double* MskT = nullptr;
+    int64_t ldm = 0, w = 0, d = 0, p = 0;
+    double *Wq = nullptr, *V = nullptr, *Tf = nullptr, *tau = nullptr, *W1 = nullptr, *W2 = nullptr;
+    double *xbuf = nullptr, *rowj = nullptr;
+    int64_t gathered = 0, queued = 0;
+    std::vector<cudaEvent_t>* events = nullptr;
+    size_t nev = 0;
+    size_t mark = 0;
+};
+void sketch_qr_pipe_begin(SketchQrPipe& P, Ctx& cx, Ctx& q, std::vector<cudaEvent_t>& events, double* MskT,
+                          int64_t ldm, int64_t w, int64_t d);
+void sketch_qr_pipe_columns(SketchQrPipe& P, const int* perm, int64_t c1);
+void sketch_qr_pipe_finish(SketchQrPipe& P, const RskDefer* defer);
 
 // a3: touched set and gathers
 void touched_from_perm(Ctx& cx, int64_t w, int64_t nlu, const int* perm, Touched& T);

@@ -824,15 +824,16 @@ static int lu_leaf_width(int64_t rows, int num_sms)
 int64_t lu_max_rows(int num_sms) { return (int64_t)num_sms * (200 * 1024 / 8); }
 
 static void getrf_rec(Ctx& cx, double* L, int64_t ld, int64_t w, int64_t d, int64_t c0, int64_t c1, int* ipiv,
-                      int* perm, LuExchange& ex, int leaf)
+                      int* perm, LuExchange& ex, int leaf, const LeafDone* on_leaf)
 {
     int64_t nc = c1 - c0;
     if (nc <= leaf) {
         lu_panel(cx, L, ld, w, d, c0, (int)nc, ipiv, perm, ex);
+        if (on_leaf) (*on_leaf)(c1);  // perm[0:c1) is final now (later leaves only move rows >= c1)
         return;
     }
     int64_t mid = c0 + cdiv(nc / 2, leaf) * leaf;
-    getrf_rec(cx, L, ld, w, d, c0, mid, ipiv, perm, ex, leaf);
+    getrf_rec(cx, L, ld, w, d, c0, mid, ipiv, perm, ex, leaf, on_leaf);
     // (the left half's interchanges were applied to whole rows inside its panels)
     // U12 = L11^{-1} A12 ; A22 -= L21 U12
     int64_t ncr = c1 - mid;
@@ -840,7 +841,7 @@ static void getrf_rec(Ctx& cx, double* L, int64_t ld, int64_t w, int64_t d, int6
     double* A12 = L + c0 + mid * ld;
     trsm_left_lower_unit(cx, mid - c0, ncr, L11, ld, A12, ld);
     gemm(cx, false, false, w - mid, ncr, mid - c0, -1.0, L + mid + c0 * ld, ld, A12, ld, 1.0, L + mid + mid * ld, ld);
-    getrf_rec(cx, L, ld, w, d, mid, c1, ipiv, perm, ex, leaf);
+    getrf_rec(cx, L, ld, w, d, mid, c1, ipiv, perm, ex, leaf, on_leaf);
 }
 
 __global__ void iota_kernel(int64_t n, int* p)
@@ -849,7 +850,7 @@ __global__ void iota_kernel(int64_t n, int* p)
         p[i] = (int)i;
 }
 
-void getrf_pivots(Ctx& cx, double* L, int64_t ld, int64_t w, int64_t d, int* ipiv, int* perm)
+void getrf_pivots(Ctx& cx, double* L, int64_t ld, int64_t w, int64_t d, int* ipiv, int* perm, const LeafDone* on_leaf)
 {
     int64_t nlu = imin(w, d);
     iota_kernel<<<(unsigned)imin(cdiv(w, 256), 1024), 256, 0, cx.stream>>>(w, perm);
@@ -860,7 +861,7 @@ void getrf_pivots(Ctx& cx, double* L, int64_t ld, int64_t w, int64_t d, int* ipi
     ex.xbuf = cx.alloc(2 * (size_t)cx.num_sms * LU_XSTRIDE);
     ex.rowj = cx.alloc(2 * LU_JBMAX);
     int leaf = lu_leaf_width(w, cx.num_sms);
-    getrf_rec(cx, L, ld, w, nlu, 0, nlu, ipiv, perm, ex, leaf);
+    getrf_rec(cx, L, ld, w, nlu, 0, nlu, ipiv, perm, ex, leaf, on_leaf);
     cx.ws_used = mark;
 }
 

@@ -802,6 +802,166 @@ void sketch_qr(Ctx& cx, double* MskT, int64_t ldm, int64_t w, int64_t d, const R
     cx.ws_used = mark;
 }
 
+// ---- the K-SQR pipeline (left-looking, overlapping K-LU; bqrrp_internal.cuh SketchQrPipe)
+
+// Wq(i, c0 + c) = MskT(perm[c0 + c], i) for i < d, c < jb (Wq: d x p, ld d): the sketch columns of pivots c0 ..
+// c0 + jb - 1, read from the not yet permuted transposed sketch (row q of the permuted window = row perm[q]).
+// A 32 x 32 tile per CTA through shared memory: scattered 8-byte reads along the pivot axis, coalesced writes.
+__global__ void gather_sketch_block_kernel(int64_t d, int jb, const double* __restrict__ MskT, int64_t ldm,
+                                           const int* __restrict__ perm, int64_t c0, double* __restrict__ Wq)
+{
+    __shared__ double t[32][33];
+    __shared__ int src[32];
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+    if (threadIdx.x < 32) src[threadIdx.x] = threadIdx.x < jb ? perm[c0 + threadIdx.x] : 0;
+    __syncthreads();
+    for (int64_t i0 = (int64_t)blockIdx.x * 32; i0 < d; i0 += (int64_t)gridDim.x * 32) {
+        for (int c = ty; c < 32; c += 8) {  // lane tx: column i0 + tx of the sketch row src[c]
+            const int64_t i = i0 + tx;
+            t[c][tx] = (c < jb && i < d) ? MskT[src[c] + i * ldm] : 0.0;
+        }
+        __syncthreads();
+        for (int c = ty; c < jb; c += 8) {  // lane tx: row i0 + tx of Wq column c0 + c
+            const int64_t i = i0 + tx;
+            if (i < d) Wq[i + (c0 + c) * d] = t[c][tx];
+        }
+        __syncthreads();
+    }
+}
+
+void sketch_qr_pipe_begin(SketchQrPipe& P, Ctx& cx, Ctx& q, std::vector<cudaEvent_t>& events, double* MskT,
+                          int64_t ldm, int64_t w, int64_t d)
+{
+    P.cx = &cx;
+    P.q = &q;
+    P.events = &events;
+    P.nev = 0;
+    P.MskT = MskT;
+    P.ldm = ldm;
+    P.w = w;
+    P.d = d;
+    P.p = imin(d, w);
+    P.gathered = P.queued = 0;
+    P.mark = cx.ws_used;
+    if (P.p <= 0) return;
+    P.Wq = cx.alloc((size_t)d * P.p);
+    P.V = cx.alloc((size_t)d * P.p);
+    P.Tf = cx.alloc((size_t)P.p * P.p);
+    P.tau = cx.alloc((size_t)P.p);
+    P.W1 = cx.alloc((size_t)d * QR_JBMAX);
+    P.W2 = cx.alloc((size_t)d * QR_JBMAX);
+    P.xbuf = cx.alloc(2 * (size_t)cx.num_sms * QR_XSTRIDE + (size_t)cx.num_sms * QR_JBMAX * QR_JBMAX);
+    P.rowj = cx.alloc(2 * QR_JBMAX);
+    // split-K slices of q's skinny long-K GEMMs (V^T B: c x 32 over K = d), when they fit the temporaries' budget
+    if (d >= 512) {
+        q.splitk_elems = (size_t)16 * QR_JBMAX * d;
+        q.splitk = cx.alloc(q.splitk_elems);
+    } else {
+        q.splitk = nullptr;
+        q.splitk_elems = 0;
+    }
+    BQ_CUDA(cudaMemsetAsync(P.V, 0, sizeof(double) * d * P.p, cx.stream));
+    BQ_CUDA(cudaMemsetAsync(P.Tf, 0, sizeof(double) * P.p * P.p, cx.stream));
+}
+
+static cudaEvent_t pipe_event(SketchQrPipe& P)
+{
+    if (P.nev == P.events->size()) {
+        cudaEvent_t e;
+        BQ_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        P.events->push_back(e);
+    }
+    return (*P.events)[P.nev++];
+}
+
+// Block [c, c + jb) of the sketch QR on q: B = Wq(:, c:c+jb) <- Q_c^T B (Q_c = I - V_c T_c V_c^T, the c reflectors
+// so far), the leaf on B(c:d, :), then T(0:c, c:c+jb) = -T_c (V_c^T V_b) T_bb (the recursive form's T12 merge).
+static void pipe_block(SketchQrPipe& P, int64_t c, int jb)
+{
+    Ctx& q = *P.q;
+    const int64_t d = P.d, p = P.p;
+    double* B = P.Wq + c * d;
+    if (c > 0) {
+        gemm(q, true, false, c, jb, d, 1.0, P.V, d, B, d, 0.0, P.W1, c);          // W1 = V_c^T B
+        gemm(q, true, false, c, jb, c, 1.0, P.Tf, p, P.W1, c, 0.0, P.W2, c);      // W2 = T_c^T W1
+        gemm(q, false, false, d, jb, c, -1.0, P.V, d, P.W2, c, 1.0, B, d);        // B -= V_c W2
+    }
+    qr_panel(q, P.Wq, d, d, c, jb, P.tau, P.V, P.Tf, p, P.xbuf, P.rowj);
+    if (c > 0) {
+        gemm(q, true, false, c, jb, d, 1.0, P.V, d, P.V + c * d, d, 0.0, P.W1, c);  // V_c^T V_b
+        gemm(q, false, false, c, jb, c, 1.0, P.Tf, p, P.W1, c, 0.0, P.W2, c);        // T_c (V_c^T V_b)
+        gemm(q, false, false, c, jb, jb, -1.0, P.W2, c, P.Tf + c + c * p, p, 0.0, P.Tf + c * p, p);
+    }
+}
+
+void sketch_qr_pipe_columns(SketchQrPipe& P, const int* perm, int64_t c1)
+{
+    c1 = imin(c1, P.p);
+    if (c1 > P.gathered) {
+        const int64_t c0 = P.gathered;
+        for (int64_t g = c0; g < c1; g += 32) {
+            const int jb = (int)imin(32, c1 - g);
+            gather_sketch_block_kernel<<<(unsigned)imin(cdiv(P.d, 32), 2 * P.cx->num_sms), 256, 0, P.cx->stream>>>(
+                P.d, jb, P.MskT, P.ldm, perm, g, P.Wq);
+            BQ_LAUNCH_CHECK();
+        }
+        P.gathered = c1;
+    }
+    while (P.queued < P.gathered && (P.gathered - P.queued >= QR_JBMAX || P.gathered == P.p)) {
+        const int jb = (int)imin(QR_JBMAX, P.gathered - P.queued);
+        cudaEvent_t e = pipe_event(P);
+        BQ_CUDA(cudaEventRecord(e, P.cx->stream));
+        BQ_CUDA(cudaStreamWaitEvent(P.q->stream, e, 0));
+        pipe_block(P, P.queued, jb);
+        P.queued += jb;
+    }
+}
+
+void sketch_qr_pipe_finish(SketchQrPipe& P, const RskDefer* defer)
+{
+    Ctx& cx = *P.cx;
+    const int64_t d = P.d, p = P.p, w = P.w, ldm = P.ldm;
+    if (p <= 0) {
+        cx.ws_used = P.mark;
+        return;
+    }
+    if (P.queued < p) throw std::runtime_error("sketch_qr_pipe: K-LU did not finish the pivots");
+    cudaEvent_t e = pipe_event(P);
+    BQ_CUDA(cudaEventRecord(e, P.q->stream));
+    BQ_CUDA(cudaStreamWaitEvent(cx.stream, e, 0));
+    P.q->splitk = nullptr;
+    P.q->splitk_elems = 0;
+    double* MskT = P.MskT;
+    double* Wq = P.Wq;
+    int64_t rest = w - p;
+    if (rest > 0) {
+        // as sketch_qr: Q_sk = I - V T V^T (d x d) explicit, then R_sk(:, p:w)^T = Wsk(:, p:w)^T Q_sk in one GEMM
+        double* Xt = MskT + p;
+        const bool deferred = defer && defer->side;
+        double* Q = deferred ? defer->Q : cx.alloc((size_t)d * d);
+        double* Wt = cx.alloc((size_t)p * d);
+        double* Y = deferred ? defer->Y : cx.alloc((size_t)rest * d);
+        gemm(cx, false, true, p, d, p, 1.0, P.Tf, p, P.V, d, 0.0, Wt, p);
+        BQ_CUDA(cudaMemsetAsync(Q, 0, sizeof(double) * d * d, cx.stream));
+        zero_triangle(cx, 'L', d, d, Q, d, /*unit_diag=*/true);
+        gemm(cx, false, false, d, d, p, -1.0, P.V, d, Wt, p, 1.0, Q, d);
+        if (deferred) {
+            cudaEvent_t e2 = pipe_event(P);
+            BQ_CUDA(cudaEventRecord(e2, cx.stream));
+            BQ_CUDA(cudaStreamWaitEvent(defer->side->stream, e2, 0));
+            Ctx sc = side_ctx(cx, *defer->side, 0);
+            gemm(sc, false, false, rest, d, d, 1.0, Xt, ldm, Q, d, 0.0, Y, rest);
+            copy_matrix(sc, rest, d, Y, rest, Xt, ldm);
+        } else {
+            gemm(cx, false, false, rest, d, d, 1.0, Xt, ldm, Q, d, 0.0, Y, rest, false, 0, /*no_split=*/true);
+            copy_matrix(cx, rest, d, Y, rest, Xt, ldm);
+        }
+    }
+    store_rsk_kernel<<<(unsigned)imin(cdiv(p * d, 256), 4 * cx.num_sms), 256, 0, cx.stream>>>(p, d, Wq, MskT, ldm);
+    BQ_LAUNCH_CHECK();
+    cx.ws_used = P.mark;
+}
+
 }  // namespace bqrrp
 
 #ifdef BQRRP_LEAF_TIMING

@@ -171,7 +171,8 @@ def _worker(rank, world, port, m, n, b, d, seed, gen, out, lookahead, shard, nb)
         full[:, torch.as_tensor(bc.pos, device="cuda")] = A_loc
         dist.all_reduce(full.t())  # the contiguous storage behind the column-major view
         if rank == 0:
-            Ar, taur, Jr, ellr = bq.factor(Ad.clone().t().contiguous().t(), b, d, seed=seed + 1)
+            # the distributed loop runs K-SQR after K-LU (recursive), as the one-GPU entry with sqr_pipeline=False
+            Ar, taur, Jr, ellr = bq.factor(Ad.clone().t().contiguous().t(), b, d, seed=seed + 1, sqr_pipeline=False)
             out["res"] = dict(ell=ell, ellr=ellr, F=full.cpu().numpy(), tau=tau.cpu().numpy(), J=J.cpu().numpy(),
                               Fr=Ar.cpu().numpy(), taur=taur.cpu().numpy(), Jr=Jr.cpu().numpy())
     finally:
@@ -193,7 +194,8 @@ def _run(world, m, n, b, d, gen, lookahead=True, shard=False, nb=0):
                                          (512, 512, 64, 80, 150), (2048, 1024, 256, 256, 0)])
 @pytest.mark.parametrize("world", [2, 3])
 def test_dist_bitwise_equals_single_gpu(gpu, m, n, b, d, gen, world):
-    """Owner panel + lookahead (the defaults): A, tau, J and the rank are bitwise the one-GPU bqrrp_factor's."""
+    """Owner panel + lookahead (the defaults): A, tau, J and the rank are bitwise the one-GPU bqrrp_factor's with the
+    same K-SQR order (no_sqr_pipeline: the distributed loop factors the sketch after K-LU)."""
     r = _run(world, m, n, b, d, gen)
     assert r["ell"] == r["ellr"]
     assert np.array_equal(r["J"], r["Jr"])

@@ -493,6 +493,37 @@ def test_lookahead_and_serial_schedules_agree(gpu):
         assert r2 == r1 and torch.equal(J2, J1) and torch.equal(tau2, tau1) and torch.equal(Ag2, Ag1), pl
 
 
+@pytest.mark.parametrize("shape,b,d", [((3000, 2500), 256, 256), ((2048, 2048), 512, 512), ((1000, 1500), 96, 160),
+                                       ((700, 450), 64, 80)])
+def test_pipelined_sketch_qr_matches_recursive(gpu, shape, b, d):
+    """K-SQR pipelined with K-LU (left-looking blocks on a third stream, the default) against the recursive K-SQR
+    after K-LU: the same pivots (J(:l), rank identical) and the same factorization to rounding, per column; and
+    against the oracle on the smaller shapes."""
+    import torch
+
+    bq = _bq()
+    A = inputs.gaussian(*shape, seed=3)
+    Ag1, tau1, J1, r1 = bq.factor(_dev(A), b, d, seed=4)
+    Ag0, tau0, J0, r0 = bq.factor(_dev(A), b, d, seed=4, sqr_pipeline=False)
+    assert r1 == r0 == min(shape)
+    # wide inputs: the columns past l = m are ordered on rounding noise (DESIGN.md §6), so J(:l) and the first l
+    # columns are compared there
+    l = r0
+
+    def same(Ja, Fa, ta, Jb, Fb, tb):
+        Ja, Jb = np.asarray(Ja), np.asarray(Jb)
+        assert np.array_equal(Ja[:l], Jb[:l])
+        if not np.array_equal(Ja, Jb):
+            Fa, Fb = Fa[:, :l], Fb[:, :l]
+        _parity.compare_factors(Fa, ta, Fb, tb, l)
+
+    same(_host(J1), _host(Ag1), _host(tau1), _host(J0), _host(Ag0), _host(tau0))
+    if shape[0] * shape[1] <= 1500 * 1500:
+        o = oracle.bqrrp(A, b, d, seed=4)
+        assert r1 == o.rank
+        same(_host(J1), _host(Ag1), _host(tau1), o.J, o.A, o.tau)
+
+
 @pytest.mark.parametrize("bulk_sms", [-1, 100, 24])
 def test_bulk_partition_is_bitwise_neutral(gpu, bulk_sms):
     """The bulk trailing GEMM on a green-context SM partition (bqrrp_options.bulk_sms: every iteration on a

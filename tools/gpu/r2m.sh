@@ -1,4 +1,4 @@
-set -x
-python tools/leaf_timing.py 4096 32 > gpurun_out/r2n/leaf_timing.txt 2>&1; python tools/leaf_timing.py 1024 32 >> gpurun_out/r2n/leaf_timing.txt 2>&1; cat gpurun_out/r2n/leaf_timing.txt
-timeout 1200 python bench.py --steps 3 --warmup 3 > gpurun_out/r2n/bench_c3.json 2> gpurun_out/r2n/bench_c3.err; echo "bench rc=$?"; cat gpurun_out/r2n/bench_c3.json; tail -3 gpurun_out/r2n/bench_c3.err
-timeout 900 ncu --set full --clock-control none -k regex:"gather_cols_kernel|scatter_cols_kernel|col_norms_kernel|trailing_rows_kernel" -c 8 -o gpurun_out/r2n/hbm_kernels python tools/hbm_probe.py > gpurun_out/r2n/ncu_hbm.log 2>&1; echo "ncu hbm rc=$?"; tail -3 gpurun_out/r2n/ncu_hbm.log
+mkdir -p gpurun_out/r2m
+timeout 1200 python -m pytest tests/test_gpu_parity.py tests/test_gpu_golden.py -x -q > gpurun_out/r2m/pytest.log 2>&1; echo "pytest rc=$?"; tail -15 gpurun_out/r2m/pytest.log
+for c in "C2" "8192 128" "16384 256" "4096 64"; do echo "== $c"; timeout 600 python tools/bulk_partition_ab.py $c --reps 3 --sms 0; timeout 600 python tools/bulk_partition_ab.py $c --reps 3 --sms 0 --no-pipe; done > gpurun_out/r2m/ab.txt 2>&1; cut -c1-300 gpurun_out/r2m/ab.txt
+echo "== C3" >> gpurun_out/r2m/ab.txt; timeout 600 python tools/bulk_partition_ab.py C3 --reps 1 --sms 0 >> gpurun_out/r2m/ab.txt 2>&1; tail -1 gpurun_out/r2m/ab.txt | cut -c1-300
