@@ -85,6 +85,12 @@ typedef struct bqrrp_options {
      * each 32-column block of sketch columns as soon as K-LU has fixed its pivots, on a third stream); 1 = the
      * recursive K-SQR after K-LU (the round-1 order).  R_sk agrees to rounding (different operation order). */
     int no_sqr_pipeline;
+    /* One-GPU lookahead with the K-SQR pipeline: 1 = K-LU as a right-looking blocked LU with a one-block lookahead
+     * when the sketch transpose fits the register leaf (w <= 16384; each leaf waits only for its own block's update,
+     * the wide trailing update runs on a fourth stream); 0 (default) = the recursive K-LU.  Measured no faster
+     * (C2 369 vs 361 ms: the rank-16/32 trailing updates re-stream the whole w x d block from HBM at every leaf,
+     * DESIGN.md §7.2).  Same pivot decisions (GETF2's); the factors differ by rounding. */
+    int lu_lookahead;
 } bqrrp_options;
 #define BQRRP_DEBUG_FORCE_BREAKDOWN 1
 #define BQRRP_DIST_SHARD_PANEL 1

@@ -301,6 +301,7 @@ struct Sched {
     cudaEvent_t ev_top = nullptr, ev_bulk = nullptr;
     int panel_la = 0;  // bqrrp_options.panel_lookahead: 1 = panel i+1 overlapped with bulk i, else after it
     Ctx* qr = nullptr;  // the pipelined sketch QR's stream (SketchQrPipe), or nullptr: sketch_qr after K-LU
+    Ctx* lu2 = nullptr;  // the lookahead LU's trailing-update stream (getrf_pivots_la), or nullptr: recursive K-LU
     Ctx* bulk_part[4] = {};    // the bulk context on SM partitions (green contexts) of part_sms[] SMs, or nullptr
     int part_sms[4] = {};
     int nparts = 0;
@@ -351,7 +352,8 @@ struct Run {
     int *ipiv, *perm;
     RskDefer rsk;
     std::vector<cudaEvent_t> evs;
-    std::vector<cudaEvent_t> qevs;  // SketchQrPipe's event pool
+    std::vector<cudaEvent_t> qevs;   // SketchQrPipe's event pool
+    std::vector<cudaEvent_t> luevs;  // getrf_pivots_la's event pool
 
     Run(Ctx& cx_, const Sched& sc_, int64_t m_, int64_t n_, double* A_, int64_t lda_, int64_t b_, int64_t d_,
         uint64_t seed_, double* tau_, int64_t* J_, double rank_tol_, int passes_, bool hqr_, int* hf_, HostIO* hio_)
@@ -395,6 +397,7 @@ struct Run {
     {
         for (auto e : evs) cudaEventDestroy(e);
         for (auto e : qevs) cudaEventDestroy(e);
+        for (auto e : luevs) cudaEventDestroy(e);
     }
     cudaEvent_t event()
     {
@@ -452,7 +455,8 @@ struct Run {
             SketchQrPipe P;
             sketch_qr_pipe_begin(P, cx, *sc.qr, qevs, MskT + s, n, w, d);
             const LeafDone on_leaf = [&](int64_t c1) { sketch_qr_pipe_columns(P, perm, c1); };
-            getrf_pivots(cx, Lb, n, w, d, ipiv, perm, &on_leaf);
+            if (!(sc.lu2 && getrf_pivots_la(cx, *sc.lu2, luevs, Lb, n, w, d, ipiv, perm, &on_leaf)))
+                getrf_pivots(cx, Lb, n, w, d, ipiv, perm, &on_leaf);
             touched_from_perm(cx, w, imin(w, d), perm, T);
             permute_rows(cx, d, MskT + s, n, T, rowscr);
             sketch_qr_pipe_finish(P, &rsk);
@@ -766,24 +770,26 @@ static int factor_ex_impl(int64_t m, int64_t n, double* A, int64_t lda, int64_t 
         // low-priority one (Sched); all joined to the caller's stream at entry and exit
         int prio_lo = 0, prio_hi = 0;
         BQ_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
-        cudaStream_t user = cx.stream, s_hi = nullptr, s_lo = nullptr, s_aux = nullptr, s_qr = nullptr;
+        cudaStream_t user = cx.stream, s_hi = nullptr, s_lo = nullptr, s_aux = nullptr, s_qr = nullptr, s_lu = nullptr;
         cudaEvent_t ev_in = nullptr, ev_top = nullptr, ev_bulk = nullptr, ev_done = nullptr;
         BQ_CUDA(cudaStreamCreateWithPriority(&s_hi, cudaStreamNonBlocking, prio_hi));
         BQ_CUDA(cudaStreamCreateWithPriority(&s_lo, cudaStreamNonBlocking, prio_lo));
         BQ_CUDA(cudaStreamCreateWithPriority(&s_aux, cudaStreamNonBlocking, prio_hi));
         BQ_CUDA(cudaStreamCreateWithPriority(&s_qr, cudaStreamNonBlocking, prio_hi));
+        BQ_CUDA(cudaStreamCreateWithPriority(&s_lu, cudaStreamNonBlocking, prio_hi));
         BQ_CUDA(cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming));
         BQ_CUDA(cudaEventCreateWithFlags(&ev_top, cudaEventDisableTiming));
         BQ_CUDA(cudaEventCreateWithFlags(&ev_bulk, cudaEventDisableTiming));
         BQ_CUDA(cudaEventCreateWithFlags(&ev_done, cudaEventDisableTiming));
         BQ_CUDA(cudaEventRecord(ev_in, user));
-        for (cudaStream_t st : {s_hi, s_lo, s_aux, s_qr}) BQ_CUDA(cudaStreamWaitEvent(st, ev_in, 0));
+        for (cudaStream_t st : {s_hi, s_lo, s_aux, s_qr, s_lu}) BQ_CUDA(cudaStreamWaitEvent(st, ev_in, 0));
         cx.stream = s_hi;
-        Ctx cxb = cx, cxa = cx, cxq = cx;
+        Ctx cxb = cx, cxa = cx, cxq = cx, cxl = cx;
         cxb.stream = s_lo;
         cxa.stream = s_aux;
         cxq.stream = s_qr;
-        for (Ctx* c : {&cxb, &cxa, &cxq}) {  // the split-K scratch belongs to the critical stream
+        cxl.stream = s_lu;
+        for (Ctx* c : {&cxb, &cxa, &cxq, &cxl}) {  // the split-K scratch belongs to the critical stream
             c->splitk = nullptr;
             c->splitk_elems = 0;
         }
@@ -791,6 +797,9 @@ static int factor_ex_impl(int64_t m, int64_t n, double* A, int64_t lda, int64_t 
         cxq.timer = nullptr;
         cxq.ws = nullptr;  // the pipelined sketch QR's stream allocates nothing (its buffers come from cx)
         cxq.ws_bytes = cxq.ws_used = 0;
+        cxl.timer = nullptr;
+        cxl.ws = nullptr;  // nor does the lookahead LU's update stream
+        cxl.ws_bytes = cxl.ws_used = 0;
         Ctx cxp[3] = {cxb, cxb, cxb};
         cudaStream_t s_parts[3] = {};
         int part_sms[3] = {}, nparts = 0;
@@ -824,7 +833,10 @@ static int factor_ex_impl(int64_t m, int64_t n, double* A, int64_t lda, int64_t 
             sc.ev_top = ev_top;
             sc.ev_bulk = ev_bulk;
             sc.panel_la = opts ? opts->panel_lookahead : 0;
-            if (!(opts && opts->no_sqr_pipeline)) sc.qr = &cxq;
+            if (!(opts && opts->no_sqr_pipeline)) {
+                sc.qr = &cxq;
+                if (opts && opts->lu_lookahead) sc.lu2 = &cxl;
+            }
             for (int i = 0; i < nparts; ++i) {
                 sc.bulk_part[i] = &cxp[i];
                 sc.part_sms[i] = part_sms[i];
@@ -835,12 +847,12 @@ static int factor_ex_impl(int64_t m, int64_t n, double* A, int64_t lda, int64_t 
         int64_t ell = -1;
         int status = 0;
         auto cleanup = [&]() {
-            for (cudaStream_t st : {s_hi, s_lo, s_aux, s_qr, s_parts[0], s_parts[1], s_parts[2]}) {
+            for (cudaStream_t st : {s_hi, s_lo, s_aux, s_qr, s_lu, s_parts[0], s_parts[1], s_parts[2]}) {
                 if (!st) continue;
                 cudaEventRecord(ev_done, st);
                 cudaStreamWaitEvent(user, ev_done, 0);
             }
-            for (cudaStream_t st : {s_hi, s_lo, s_aux, s_qr}) cudaStreamDestroy(st);
+            for (cudaStream_t st : {s_hi, s_lo, s_aux, s_qr, s_lu}) cudaStreamDestroy(st);
             for (cudaEvent_t e : {ev_in, ev_top, ev_bulk, ev_done}) cudaEventDestroy(e);
             cx.stream = user;
         };

@@ -76,6 +76,11 @@ void sketch_apply(Ctx& cx, int64_t m, int64_t n, const double* A, int64_t lda, i
 using LeafDone = std::function<void(int64_t c1)>;
 void getrf_pivots(Ctx& cx, double* L, int64_t ld, int64_t w, int64_t d, int* ipiv, int* perm,
                   const LeafDone* on_leaf = nullptr);
+// The same pivots by a right-looking blocked LU with a one-block lookahead: the wide trailing update of each leaf
+// on the second stream lu2 (allocates nothing), only the next block's on cx (lu.cu).  false = not applicable (w
+// beyond the register leaf): nothing queued.  evpool: caller-owned events, reused.
+bool getrf_pivots_la(Ctx& cx, Ctx& lu2, std::vector<cudaEvent_t>& evpool, double* L, int64_t ld, int64_t w, int64_t d,
+                     int* ipiv, int* perm, const LeafDone* on_leaf = nullptr);
 // Largest sketch-transpose height (w = n - s rows) K-LU's grid leaf holds; largest panel height the
 // Householder panel (HQR variant and CholQR-breakdown fallback) holds.  Checked before any launch.
 int64_t lu_max_rows(int num_sms);

@@ -50,6 +50,11 @@ struct LuPanelArgs {
     int* perm;   // running row permutation (w)
     double* xbuf;  // exchange: [2][G][LU_XSTRIDE]
     double* rowj;  // exchange: [2][LU_JBMAX]
+    // register leaf only: the columns [mc0, mc1) its row moves are applied to (mc1 < 0: all d), and an optional
+    // record of the moves (mvout[0] = count, mvout[1 + t] = source row, mvout[1 + 2 LU_JBMAX + t] = destination)
+    // for the lookahead LU's deferred row interchanges (getrf_pivots_la)
+    int64_t mc0 = 0, mc1 = -1;
+    int* mvout = nullptr;
 };
 
 constexpr int LU_JBMAX = 32;
@@ -419,39 +424,49 @@ __device__ __forceinline__ void argmax3(unsigned hi, unsigned lo, unsigned p, un
 // (four at a time), lane t the moves t and t + 32: every source of a column is loaded (8 loads in flight per lane)
 // before the warp barrier, every destination stored after it.  (Round-2 form: the earlier thread-per-column loop
 // kept 8 loads in flight per THREAD and spent ~47k cycles per leaf at d = 1024; tools/leaf_timing.py.)
-__device__ void apply_moves_all(const LuPanelArgs& a, int nmv, const int* mv_src, const int* mv_dst, int64_t gwarp,
-                                int64_t nwarps, int lane)
+__device__ void apply_moves_all(double* L, int64_t ld, int64_t cb, int64_t ce, int* perm, int nmv, const int* mv_src,
+                                const int* mv_dst, int64_t gwarp, int64_t nwarps, int lane)
 {
     if (nmv == 0) return;
     const bool h0 = lane < nmv, h1 = lane + 32 < nmv;
     const int s0 = h0 ? mv_src[lane] : 0, d0 = h0 ? mv_dst[lane] : 0;
     const int s1 = h1 ? mv_src[lane + 32] : 0, d1 = h1 ? mv_dst[lane + 32] : 0;
     constexpr int CB = 4;
-    for (int64_t c0 = gwarp * CB; c0 < a.d; c0 += nwarps * CB) {
+    for (int64_t c0 = cb + gwarp * CB; c0 < ce; c0 += nwarps * CB) {
         double v0[CB], v1[CB];
 #pragma unroll
         for (int q = 0; q < CB; ++q) {
-            const double* pc = a.L + (c0 + q) * a.ld;
-            const bool ok = c0 + q < a.d;
+            const double* pc = L + (c0 + q) * ld;
+            const bool ok = c0 + q < ce;
             v0[q] = (ok && h0) ? pc[s0] : 0.0;
             v1[q] = (ok && h1) ? pc[s1] : 0.0;
         }
         __syncwarp();
 #pragma unroll
         for (int q = 0; q < CB; ++q) {
-            double* pc = a.L + (c0 + q) * a.ld;
-            if (c0 + q < a.d) {
+            double* pc = L + (c0 + q) * ld;
+            if (c0 + q < ce) {
                 if (h0) pc[d0] = v0[q];
                 if (h1) pc[d1] = v1[q];
             }
         }
     }
-    if (gwarp == 0) {
-        const int p0 = h0 ? a.perm[s0] : 0, p1 = h1 ? a.perm[s1] : 0;
+    if (perm && gwarp == 0) {
+        const int p0 = h0 ? perm[s0] : 0, p1 = h1 ? perm[s1] : 0;
         __syncwarp();
-        if (h0) a.perm[d0] = p0;
-        if (h1) a.perm[d1] = p1;
+        if (h0) perm[d0] = p0;
+        if (h1) perm[d1] = p1;
     }
+}
+
+// The recorded row moves of one register leaf (LuPanelArgs::mvout) applied to columns [cb, ce) (warp per column).
+__global__ void lu_laswp_kernel(double* L, int64_t ld, int64_t cb, int64_t ce, const int* __restrict__ mv)
+{
+    const int nmv = mv[0];
+    const int lane = threadIdx.x & 31;
+    apply_moves_all(L, ld, cb, ce, nullptr, nmv, mv + 1, mv + 1 + 2 * LU_JBMAX,
+                    (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), (int64_t)gridDim.x * (blockDim.x >> 5),
+                    lane);
 }
 
 template <int JB, int RPT>
@@ -679,7 +694,15 @@ __global__ void __launch_bounds__(LF_NT, 1) lu_leaf_fast_kernel(LuPanelArgs a)
     __syncthreads();
     cluster_arrive();  // done reading the peers' lists: they may exit once every CTA has arrived here
     LEAF_TS(63, 4);
-    apply_moves_all(a, mv_cnt, mv_src, mv_dst, (int64_t)me * LF_NW + warp, (int64_t)G * LF_NW, lane);
+    if (a.mvout && me == 0) {
+        for (int t = tid; t < mv_cnt; t += LF_NT) {
+            a.mvout[1 + t] = mv_src[t];
+            a.mvout[1 + 2 * LU_JBMAX + t] = mv_dst[t];
+        }
+        if (tid == 0) a.mvout[0] = mv_cnt;
+    }
+    apply_moves_all(a.L, a.ld, a.mc0, a.mc1 < 0 ? a.d : a.mc1, a.perm, mv_cnt, mv_src, mv_dst,
+                    (int64_t)me * LF_NW + warp, (int64_t)G * LF_NW, lane);
     LEAF_TS(63, 3);
     cluster_wait();
 }
@@ -711,7 +734,8 @@ static void launch_lu_leaf_fast(Ctx& cx, const LuPanelArgs& a, int G)
     ++g_launches;
 }
 
-static bool lu_panel_reg(Ctx& cx, double* L, int64_t ld, int64_t w, int64_t d, int64_t c0, int jb, int* ipiv, int* perm)
+static bool lu_panel_reg(Ctx& cx, double* L, int64_t ld, int64_t w, int64_t d, int64_t c0, int jb, int* ipiv, int* perm,
+                         int64_t mc0 = 0, int64_t mc1 = -1, int* mvout = nullptr)
 {
     const int64_t rows = w - c0;
     if (jb > 32 || !lu_reg_fits(rows, jb)) return false;
@@ -720,6 +744,9 @@ static bool lu_panel_reg(Ctx& cx, double* L, int64_t ld, int64_t w, int64_t d, i
     // cluster); a CTA without rows offers no candidate
     const int G = (int)imax(2, cdiv(rows, (int64_t)LF_NT * rpt));
     LuPanelArgs a{L, ld, w, d, c0, jb, LF_NT * rpt, ipiv, perm, nullptr, nullptr};
+    a.mc0 = mc0;
+    a.mc1 = mc1;
+    a.mvout = mvout;
     if (jb > 16) {
         if (rpt == 1) launch_lu_leaf_fast<32, 1>(cx, a, G);
         else launch_lu_leaf_fast<32, 2>(cx, a, G);
@@ -863,6 +890,73 @@ void getrf_pivots(Ctx& cx, double* L, int64_t ld, int64_t w, int64_t d, int* ipi
     int leaf = lu_leaf_width(w, cx.num_sms);
     getrf_rec(cx, L, ld, w, nlu, 0, nlu, ipiv, perm, ex, leaf, on_leaf);
     cx.ws_used = mark;
+}
+
+// Right-looking blocked LU with a one-block lookahead, for sketch transposes the register leaf
+// holds (w <= 16384).  Only the pivots are used downstream, so factors left of the current block are never
+// permuted again.  Step c (leaf block B = [c, c + jb)):
+//   crit: leaf(B) — its row moves applied to B only, recorded (mvout);
+//   lu2:  the rest R = [c + jb + jb1, nlu): moves of B, U = L_BB^{-1} A(B, R), A(c+jb:w, R) -= L(c+jb:w, B) U;
+//   crit: the next block N = [c + jb, c + jb + jb1) likewise (after lu2 finished step c - jb, which covered N),
+//         then leaf(N) — so each leaf waits only for one narrow update while lu2 does the wide one.
+// Returns false (nothing queued) when the leaf would not be the register leaf.
+bool getrf_pivots_la(Ctx& cx, Ctx& lu2, std::vector<cudaEvent_t>& evpool, double* L, int64_t ld, int64_t w, int64_t d,
+                     int* ipiv, int* perm, const LeafDone* on_leaf)
+{
+    const int64_t nlu = imin(w, d);
+    const int leaf = lu_leaf_width(w, cx.num_sms);
+    if (nlu <= 0 || !lu_reg_fits(w, leaf)) return false;
+    iota_kernel<<<(unsigned)imin(cdiv(w, 256), 1024), 256, 0, cx.stream>>>(w, perm);
+    BQ_LAUNCH_CHECK();
+    const size_t mark = cx.ws_used;
+    const int64_t nsteps = cdiv(nlu, leaf);
+    const int MVS = 1 + 4 * LU_JBMAX;
+    int* mv = cx.alloc_as<int>((size_t)nsteps * MVS);
+    size_t nev = 0;
+    auto ev = [&]() {
+        if (nev == evpool.size()) {
+            cudaEvent_t e;
+            BQ_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            evpool.push_back(e);
+        }
+        return evpool[nev++];
+    };
+    auto laswp = [&](Ctx& c, int64_t cb, int64_t ce, const int* m) {
+        if (ce <= cb) return;
+        const int64_t warps = cdiv(ce - cb, 4);
+        lu_laswp_kernel<<<(unsigned)imin(cdiv(warps, 8), 4 * (int64_t)c.num_sms), 256, 0, c.stream>>>(L, ld, cb, ce, m);
+        BQ_LAUNCH_CHECK();
+    };
+    // update of columns [cb, ce) by step (c, jb): interchanges, U rows, trailing rows
+    auto update = [&](Ctx& c2, int64_t c, int jb, const int* m, int64_t cb, int64_t ce) {
+        if (ce <= cb) return;
+        laswp(c2, cb, ce, m);
+        trsm_left_lower_unit(c2, jb, ce - cb, L + c + c * ld, ld, L + c + cb * ld, ld);
+        gemm(c2, false, false, w - c - jb, ce - cb, jb, -1.0, L + (c + jb) + c * ld, ld, L + c + cb * ld, ld, 1.0,
+             L + (c + jb) + cb * ld, ld, false, 0, /*no_split=*/true);
+    };
+    cudaEvent_t ev_lu2_prev = nullptr;  // lu2 finished the previous step's rest update
+    for (int64_t step = 0; step < nsteps; ++step) {
+        const int64_t c = step * leaf;
+        const int jb = (int)imin(leaf, nlu - c);
+        int* m = mv + step * MVS;
+        if (!lu_panel_reg(cx, L, ld, w, nlu, c, jb, ipiv, perm, c, c + jb, m))
+            throw std::runtime_error("getrf_pivots_la: register leaf does not fit");
+        if (on_leaf) (*on_leaf)(c + jb);
+        const int64_t n0 = c + jb, n1 = imin(nlu, n0 + leaf);  // the next block [n0, n1), the rest [n1, nlu)
+        if (n0 >= nlu) break;
+        cudaEvent_t e_leaf = ev();
+        BQ_CUDA(cudaEventRecord(e_leaf, cx.stream));
+        BQ_CUDA(cudaStreamWaitEvent(lu2.stream, e_leaf, 0));
+        update(lu2, c, jb, m, n1, nlu);
+        if (ev_lu2_prev) BQ_CUDA(cudaStreamWaitEvent(cx.stream, ev_lu2_prev, 0));  // [n0, n1) had step c - leaf's update
+        update(cx, c, jb, m, n0, n1);
+        ev_lu2_prev = ev();
+        BQ_CUDA(cudaEventRecord(ev_lu2_prev, lu2.stream));
+    }
+    if (ev_lu2_prev) BQ_CUDA(cudaStreamWaitEvent(cx.stream, ev_lu2_prev, 0));
+    cx.ws_used = mark;
+    return true;
 }
 
 }  // namespace bqrrp

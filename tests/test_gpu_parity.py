@@ -494,16 +494,18 @@ def test_lookahead_and_serial_schedules_agree(gpu):
 
 
 @pytest.mark.parametrize("shape,b,d", [((3000, 2500), 256, 256), ((2048, 2048), 512, 512), ((1000, 1500), 96, 160),
-                                       ((700, 450), 64, 80)])
-def test_pipelined_sketch_qr_matches_recursive(gpu, shape, b, d):
-    """K-SQR pipelined with K-LU (left-looking blocks on a third stream, the default) against the recursive K-SQR
-    after K-LU: the same pivots (J(:l), rank identical) and the same factorization to rounding, per column; and
-    against the oracle on the smaller shapes."""
+                                       ((700, 450), 64, 80), ((9000, 9000), 1024, 1024)])
+@pytest.mark.parametrize("lu_la", [True, False])
+def test_pipelined_sketch_qr_matches_recursive(gpu, shape, b, d, lu_la):
+    """K-SQR pipelined with K-LU (left-looking blocks on a third stream, the default) — with K-LU either the
+    recursive LU (default) or the lookahead blocked LU (option) — against the recursive K-SQR after the recursive K-LU: the
+    same pivots (J(:l), rank identical) and the same factorization to rounding, per column; and against the oracle
+    on the smaller shapes."""
     import torch
 
     bq = _bq()
     A = inputs.gaussian(*shape, seed=3)
-    Ag1, tau1, J1, r1 = bq.factor(_dev(A), b, d, seed=4)
+    Ag1, tau1, J1, r1 = bq.factor(_dev(A), b, d, seed=4, lu_lookahead=lu_la)
     Ag0, tau0, J0, r0 = bq.factor(_dev(A), b, d, seed=4, sqr_pipeline=False)
     assert r1 == r0 == min(shape)
     # wide inputs: the columns past l = m are ordered on rounding noise (DESIGN.md §6), so J(:l) and the first l

@@ -1,7 +1,7 @@
 """A/B of the bulk trailing GEMM's SM partition (bqrrp_options.bulk_sms): whole device (-1),
 auto (0) and fixed green-context partitions, event-timed whole factorizations (best of `reps` after a warm-up),
 with the factor checked bitwise against the whole-device run.
-usage: python tools/bulk_partition_ab.py C2|<m> [b] [--reps R] [--sms -1,0,132,116] [--json out.json] [--no-pipe]"""
+usage: python tools/bulk_partition_ab.py C2|<m> [b] [--reps R] [--sms -1,0,132,116] [--json out.json] [--no-pipe] [--lula]"""
 import json
 import os
 import sys
@@ -43,7 +43,7 @@ for s in sms:
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         out = bq.factor(A, b, d, seed=0, workspace=ws, bulk_sms=s, phase_times=(r == reps),
-                        sqr_pipeline="--no-pipe" not in sys.argv)
+                        sqr_pipeline="--no-pipe" not in sys.argv, lu_lookahead="--lula" in sys.argv)
         e1.record()
         torch.cuda.synchronize()
         if r > 0 and r < reps:

@@ -102,6 +102,18 @@ def main():
     print("per kernel (launches, ms, avg us):")
     for nm, (c, t) in sorted(per_name.items(), key=lambda x: -x[1][1])[:30]:
         print(f"  {nm:72s} {c:6d} {t / 1e3:9.2f} {t / c:9.2f}")
+    for sid in sorted(per_stream, key=per_stream.get, reverse=True):
+        if per_stream[sid] < 0.1 * max(per_stream.values()):
+            continue
+        pc = defaultdict(lambda: [0, 0.0])
+        for t0, t1, nm, s_, kind in ks:
+            if s_ == sid:
+                short = nm.split("(")[0][:70]
+                pc[short][0] += 1
+                pc[short][1] += t1 - t0
+        print(f"stream {sid} ({per_stream[sid] / 1e3:.1f} ms busy) per kernel (launches, ms, avg us):")
+        for nm, (c, t) in sorted(pc.items(), key=lambda x: -x[1][1])[:12]:
+            print(f"  {nm:72s} {c:6d} {t / 1e3:9.2f} {t / c:9.2f}")
     if out_json:
         json.dump({"config": name, "m": m, "n": n, "b": b, "d": d, "lookahead": lookahead, "wall_ms": wall_ms,
                    "span_ms": span_ms, "busy_ms": busy / 1e3, "gap_ms": gap_ms, "n_gaps": len(gaps),
