@@ -21,6 +21,7 @@ cores, each step a bounded sample of the workload (rank 0 only).
 from __future__ import annotations
 
 import argparse
+import datetime
 import json
 import os
 import subprocess
@@ -90,19 +91,28 @@ class ClockSampler:
     def __init__(self, index: int):
         self.index = index
         self.proc = None
+        self.first = ""
+        self.t0 = self.t1 = None
 
     def __enter__(self):
+        # nvidia-smi is started and its first sample read BEFORE the timed region begins: its NVML initialisation
+        # stalls CUDA submissions for tens of ms (measured: a C2 step 377 ms with the sampler starting inside the
+        # timed region vs 360 ms without).  Samples are kept by timestamp: only those taken inside the region.
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index),
-                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
+                 "--query-gpu=timestamp,clocks.sm,clocks.max.sm,clocks_event_reasons.active",
                  "--format=csv,noheader,nounits", "-lms", "200"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.first = self.proc.stdout.readline()  # blocks until NVML is up and the first sample is out
         except Exception:
             self.proc = None
+        time.sleep(0.3)  # let the sampler settle into its 200 ms loop
+        self.t0 = time.time()
         return self
 
     def __exit__(self, *a):
+        self.t1 = time.time()
         self.out = ""
         if self.proc is not None:
             self.proc.terminate()
@@ -115,14 +125,17 @@ class ClockSampler:
         sm, mx, reasons = [], 0.0, set()
         for line in (self.out or "").splitlines():
             p = [x.strip() for x in line.split(",")]
-            if len(p) < 3:
+            if len(p) < 4:
                 continue
             try:
-                sm.append(float(p[0]))
-                mx = max(mx, float(p[1]))
-                bits = int(p[2], 16)
+                ts = datetime.datetime.strptime(p[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+                if self.t0 is not None and not (self.t0 - 0.25 <= ts <= self.t1 + 0.25):
+                    continue  # outside the timed region
+                smv, mxv, bits = float(p[1]), float(p[2]), int(p[3], 16)
             except ValueError:
                 continue
+            sm.append(smv)
+            mx = max(mx, mxv)
             for bit, name in self.REASONS.items():
                 if bits & bit and name != "gpu_idle":
                     reasons.add(name)

@@ -91,6 +91,11 @@ typedef struct bqrrp_options {
      * (C2 369 vs 361 ms: the rank-16/32 trailing updates re-stream the whole w x d block from HBM at every leaf,
      * DESIGN.md §7.2).  Same pivot decisions (GETF2's); the factors differ by rounding. */
     int lu_lookahead;
+    /* K-LU register leaf (w <= 16384): the largest cluster preferred before going to more rows per thread; 0 = the
+     * default 16 (fewest rows per thread); 8 / 4 = smaller clusters (an 8-CTA cluster of full-SM CTAs still fits
+     * the SM groups the bulk GEMM's partition leaves free; measured neutral at C2, 8192^2, 16384^2).
+     * Pivots and factors are identical. */
+    int lu_leaf_cluster;
 } bqrrp_options;
 #define BQRRP_DEBUG_FORCE_BREAKDOWN 1
 #define BQRRP_DIST_SHARD_PANEL 1

@@ -79,19 +79,38 @@ cudaStream_t green_stream(int sms, int* got)
     auto green = (Green)entry("cuGreenCtxCreate");
     auto gstream = (GStream)entry("cuGreenCtxStreamCreate");
     Entry e{dev, sms, 0, nullptr};
-    CUdevResource all, part, rest;
-    unsigned ng = 1;
+    int prio_lo = 0, prio_hi = 0;
+    BQ_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+    // Cluster-aware split (CU_DEV_SM_RESOURCE_SPLIT_MAX_POTENTIAL_CLUSTER_SIZE) into groups of 16 SMs: the partition
+    // is every group but the last few, plus the remainder, so the SMs left free are whole groups where the chain's
+    // 8-CTA leaf clusters can be placed while the bulk runs (a plain split by count leaves SMs scattered over the
+    // GPCs, and no cluster of full-SM CTAs fits there: tools/green_probe.cu).  9 groups + 4 on a 148-SM B200.
+    CUdevResource all, grp[64], rest;
+    unsigned ng = 0;
     CUdevResourceDesc dsc;
     CUgreenCtx g;
     CUstream s;
-    int prio_lo = 0, prio_hi = 0;
-    BQ_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+    const unsigned flags = CU_DEV_SM_RESOURCE_SPLIT_MAX_POTENTIAL_CLUSTER_SIZE;
     if (getres && split && desc && green && gstream && getres(dev, &all, CU_DEV_RESOURCE_TYPE_SM) == CUDA_SUCCESS &&
-        split(&part, &ng, &all, &rest, 0, (unsigned)sms) == CUDA_SUCCESS && ng == 1 &&
-        desc(&dsc, &part, 1) == CUDA_SUCCESS && green(&g, dsc, dev, CU_GREEN_CTX_DEFAULT_STREAM) == CUDA_SUCCESS &&
-        gstream(&s, g, CU_STREAM_NON_BLOCKING, prio_lo) == CUDA_SUCCESS) {
-        e.st = (cudaStream_t)s;
-        e.got = (int)part.sm.smCount;
+        split(nullptr, &ng, &all, nullptr, flags, 16) == CUDA_SUCCESS && ng >= 2 && ng <= 64) {
+        const int nfree = (int)(((int)all.sm.smCount - sms + 15) / 16);  // whole groups left to the chain
+        if (split(grp, &ng, &all, &rest, flags, 16) == CUDA_SUCCESS && nfree >= 1 && nfree < (int)ng) {
+            CUdevResource sel[65];
+            unsigned ns = 0, cnt = 0;
+            for (unsigned i = 0; i + nfree < ng; ++i) {
+                sel[ns++] = grp[i];
+                cnt += grp[i].sm.smCount;
+            }
+            if (rest.sm.smCount) {
+                sel[ns++] = rest;
+                cnt += rest.sm.smCount;
+            }
+            if (desc(&dsc, sel, ns) == CUDA_SUCCESS && green(&g, dsc, dev, CU_GREEN_CTX_DEFAULT_STREAM) == CUDA_SUCCESS &&
+                gstream(&s, g, CU_STREAM_NON_BLOCKING, prio_lo) == CUDA_SUCCESS) {
+                e.st = (cudaStream_t)s;
+                e.got = (int)cnt;
+            }
+        }
     }
     cudaGetLastError();  // a failed probe leaves no sticky runtime error
     cache.push_back(e);
@@ -734,6 +753,8 @@ static int factor_ex_impl(int64_t m, int64_t n, double* A, int64_t lda, int64_t 
         Ctx cx;
         setup_ctx(cx, stream);
         cx.force_breakdown = opts && (opts->debug_flags & BQRRP_DEBUG_FORCE_BREAKDOWN);
+        if (opts && (opts->lu_leaf_cluster == 4 || opts->lu_leaf_cluster == 8 || opts->lu_leaf_cluster == 16))
+            cx.lu_gpref = opts->lu_leaf_cluster;
         if (m == 0 || n == 0) {
             *rank = 0;
             if (n > 0) {

@@ -158,6 +158,7 @@ struct Ctx {
     int* flags = nullptr;  // device int[8]: see Flags
     Timer* timer = nullptr;
     bool force_breakdown = false;  // test hook (bqrrp_options.debug_flags): report a POTRF breakdown per panel
+    int lu_gpref = 16;             // K-LU register leaf: preferred largest cluster (bqrrp_options.lu_leaf_cluster)
     void mark(int phase) { if (timer) timer->mark(phase); }
 
     double* alloc(size_t n_doubles)

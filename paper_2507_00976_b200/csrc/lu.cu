@@ -739,7 +739,16 @@ static bool lu_panel_reg(Ctx& cx, double* L, int64_t ld, int64_t w, int64_t d, i
 {
     const int64_t rows = w - c0;
     if (jb > 32 || !lu_reg_fits(rows, jb)) return false;
-    const int rpt = rows <= (int64_t)LF_GMAX * LF_NT ? 1 : (rows <= (int64_t)LF_GMAX * LF_NT * 2 ? 2 : 4);
+    // rows per thread: the smallest that keeps the cluster at <= cx.lu_gpref CTAs (16 by default; 8 lets a cluster of
+    // full-SM CTAs find room in the SM groups the bulk GEMM leaves free, DESIGN.md §7.5 — measured neutral), else 16
+    const int rmax = jb <= 16 ? 4 : 2;
+    int rpt = 0;
+    for (int gcap : {cx.lu_gpref, LF_GMAX}) {
+        for (int r = 1; r <= rmax && !rpt; r *= 2)
+            if (rows <= (int64_t)gcap * LF_NT * r) rpt = r;
+        if (rpt) break;
+    }
+    if (!rpt) return false;
     // at least 2 CTAs: the DSMEM pushes need a real cluster (compute-sanitizer memcheck rejects st.async in a 1-CTA
     // cluster); a CTA without rows offers no candidate
     const int G = (int)imax(2, cdiv(rows, (int64_t)LF_NT * rpt));

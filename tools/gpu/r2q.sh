@@ -1,8 +1,12 @@
-set -x
 mkdir -p gpurun_out/r2q
-python -c "import __graft_entry__ as g; g.build()" || exit 1
-python tools/leaf_timing.py 4096 32 > gpurun_out/r2q/leaf_timing.txt 2>&1; python tools/leaf_timing.py 1024 32 >> gpurun_out/r2q/leaf_timing.txt 2>&1; grep CTA gpurun_out/r2q/leaf_timing.txt
-timeout 600 compute-sanitizer --tool racecheck --print-limit 10 python tools/sanitize_run.py C1 > gpurun_out/r2q/san_racecheck_c1.log 2>&1; grep SUMMARY gpurun_out/r2q/san_racecheck_c1.log
-timeout 900 compute-sanitizer --tool racecheck --print-limit 10 python tools/sanitize_run.py 3000 128 > gpurun_out/r2q/san_racecheck_3000.log 2>&1; grep SUMMARY gpurun_out/r2q/san_racecheck_3000.log
-timeout 1200 python -m pytest tests/test_gpu_parity.py tests/test_gpu_golden.py -x -q -k "lu or factor or degenerate or dup or kahan" > gpurun_out/r2q/pytest.log 2>&1; echo "pytest rc=$?"; tail -2 gpurun_out/r2q/pytest.log
-timeout 600 python tools/schedule_ab.py C2 3 > gpurun_out/r2q/ab_c2.txt 2>&1; grep -v '^{' gpurun_out/r2q/ab_c2.txt | head -1
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,temperature.gpu,power.draw --format=csv
+timeout 1200 python bench.py --steps 3 --warmup 3 > gpurun_out/r2q/bench_c3.json 2> gpurun_out/r2q/bench_c3.err; echo "bench c3 rc=$?"
+timeout 600 python bench.py --config C2 --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/r2q/bench_c2.json 2> gpurun_out/r2q/bench_c2.err; echo "bench c2 rc=$?"
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r2q/launches_c2.csv python tools/profile_run.py C2 --warm 0 > gpurun_out/r2q/ncu_c2.log 2>&1; echo "ncu c2 rc=$?"
+timeout 2400 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r2q/launches_c3.csv python tools/profile_run.py C3 --warm 0 > gpurun_out/r2q/ncu_c3.log 2>&1; echo "ncu c3 rc=$?"
+gzip -f gpurun_out/r2q/launches_c2.csv gpurun_out/r2q/launches_c3.csv
+python -c "
+import json
+for f in ['gpurun_out/r2q/bench_c3.json','gpurun_out/r2q/bench_c2.json']:
+    d=json.load(open(f)); print(f, d['value'], d['ms_per_step'], d['roofline']['frac'], (d.get('e2e') or {}).get('value'), d['clocks'])
+"

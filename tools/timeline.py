@@ -114,6 +114,25 @@ def main():
         print(f"stream {sid} ({per_stream[sid] / 1e3:.1f} ms busy) per kernel (launches, ms, avg us):")
         for nm, (c, t) in sorted(pc.items(), key=lambda x: -x[1][1])[:12]:
             print(f"  {nm:72s} {c:6d} {t / 1e3:9.2f} {t / c:9.2f}")
+    if "--iter" in sys.argv:  # one iteration (between consecutive panel starts) stream by stream
+        it = int(sys.argv[sys.argv.index("--iter") + 1])
+        starts = [k[0] for k in ks if k[2].startswith("bqrrp::extract_rsk11_kernel")]
+        if it + 1 < len(starts):
+            w0, w1 = starts[it], starts[it + 1]
+            print(f"iteration {it}: {(w1 - w0) / 1e3:.2f} ms from panel start to the next panel start")
+            for sid in sorted(per_stream, key=per_stream.get, reverse=True):
+                sel = [k for k in ks if k[3] == sid and w0 <= k[0] < w1]
+                if not sel:
+                    continue
+                busy_w = sum(k[1] - k[0] for k in sel)
+                print(f" stream {sid}: {len(sel)} kernels, busy {busy_w / 1e3:.2f} ms, first {(sel[0][0] - w0) / 1e3:.2f}"
+                      f" last end {(max(k[1] for k in sel) - w0) / 1e3:.2f} ms")
+                prev_end = None
+                for k in sel:
+                    gap = (k[0] - prev_end) if prev_end is not None else 0.0
+                    if k[1] - k[0] >= 40 or gap >= 40:
+                        print(f"    @{(k[0] - w0) / 1e3:8.3f} ms  gap {gap:7.1f} us  dur {k[1] - k[0]:8.1f} us  {k[2][:60]}")
+                    prev_end = k[1] if prev_end is None else max(prev_end, k[1])
     if out_json:
         json.dump({"config": name, "m": m, "n": n, "b": b, "d": d, "lookahead": lookahead, "wall_ms": wall_ms,
                    "span_ms": span_ms, "busy_ms": busy / 1e3, "gap_ms": gap_ms, "n_gaps": len(gaps),
