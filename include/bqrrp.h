@@ -96,6 +96,11 @@ typedef struct bqrrp_options {
      * the SM groups the bulk GEMM's partition leaves free; measured neutral at C2, 8192^2, 16384^2).
      * Pivots and factors are identical. */
     int lu_leaf_cluster;
+    /* With the K-SQR pipeline: 0 (default) = for d <= 1024, each block's T merge (T(0:c, b) = -T_c (V_c^T V_b) T_bb,
+     * three GEMMs) on a fifth stream, overlapping the next block's V^T B product (larger d: on the pipeline's own
+     * stream, measured better at C3); 1 = always on the pipeline's own stream.  Identical results (same GEMMs, same
+     * order per element). */
+    int no_sqr_merge_stream;
 } bqrrp_options;
 #define BQRRP_DEBUG_FORCE_BREAKDOWN 1
 #define BQRRP_DIST_SHARD_PANEL 1

@@ -37,7 +37,7 @@ class Options(ctypes.Structure):
                 ("dist_nb", ctypes.c_int64), ("debug_flags", ctypes.c_int), ("dist_flags", ctypes.c_int),
                 ("panel_lookahead", ctypes.c_int), ("bulk_sms", ctypes.c_int),
                 ("no_sqr_pipeline", ctypes.c_int), ("lu_lookahead", ctypes.c_int),
-                ("lu_leaf_cluster", ctypes.c_int)]
+                ("lu_leaf_cluster", ctypes.c_int), ("no_sqr_merge_stream", ctypes.c_int)]
 
 
 def lib() -> ctypes.CDLL:
@@ -124,8 +124,10 @@ def workspace_query(m: int, n: int, b: int, d: int) -> int:
 
 
 def _options(rank_tol, cholqr_passes, phases, hqr_fallback=True, lookahead=True, debug_force_breakdown=False,
-             dist_nb=0, panel_lookahead=0, bulk_sms=0, sqr_pipeline=True, lu_lookahead=False, lu_leaf_cluster=0):
+             dist_nb=0, panel_lookahead=0, bulk_sms=0, sqr_pipeline=True, lu_lookahead=False, lu_leaf_cluster=0,
+             sqr_merge_stream=True):
     o = Options()
+    o.no_sqr_merge_stream = 0 if sqr_merge_stream else 1
     o.lu_leaf_cluster = int(lu_leaf_cluster)
     o.lu_lookahead = 1 if lu_lookahead else 0
     o.no_sqr_pipeline = 0 if sqr_pipeline else 1
@@ -145,7 +147,7 @@ def factor(A, b: int, d: int | None = None, seed: int = 0, rank_tol: float | Non
            workspace=None, tau=None, J=None, stream=None, phase_times: bool = False, hqr_fallback: bool = True,
            lookahead: bool = True, debug_force_breakdown: bool = False, panel_lookahead: int = 0,
            bulk_sms: int = 0, sqr_pipeline: bool = True, lu_lookahead: bool = False,
-           lu_leaf_cluster: int = 0):
+           lu_leaf_cluster: int = 0, sqr_merge_stream: bool = True):
     """BQRRP of A in place (Alg. 1); returns (A, tau, J, rank[, phase_ms dict]).
 
     A: float64 CUDA tensor in column-major layout (m x n); overwritten in GEQP3 format.
@@ -177,7 +179,8 @@ def factor(A, b: int, d: int | None = None, seed: int = 0, rank_tol: float | Non
     phases = (ctypes.c_float * len(PHASES))() if phase_times else None
     opts = _options(rank_tol, cholqr_passes, phases, hqr_fallback, lookahead, debug_force_breakdown,
                     panel_lookahead=panel_lookahead, bulk_sms=bulk_sms, sqr_pipeline=sqr_pipeline,
-                    lu_lookahead=lu_lookahead, lu_leaf_cluster=lu_leaf_cluster)
+                    lu_lookahead=lu_lookahead, lu_leaf_cluster=lu_leaf_cluster,
+                    sqr_merge_stream=sqr_merge_stream)
     st = lib().bqrrp_factor_ex(m, n, ctypes.c_void_p(A.data_ptr()), lda, b, d, seed, ctypes.c_void_p(tau.data_ptr()),
                                ctypes.c_void_p(J.data_ptr()), ctypes.byref(rank), ws_ptr, ws_bytes,
                                _stream_ptr(stream), ctypes.byref(opts))

@@ -321,6 +321,7 @@ struct Sched {
     int panel_la = 0;  // bqrrp_options.panel_lookahead: 1 = panel i+1 overlapped with bulk i, else after it
     Ctx* qr = nullptr;  // the pipelined sketch QR's stream (SketchQrPipe), or nullptr: sketch_qr after K-LU
     Ctx* lu2 = nullptr;  // the lookahead LU's trailing-update stream (getrf_pivots_la), or nullptr: recursive K-LU
+    Ctx* qr2 = nullptr;  // the pipelined sketch QR's T-merge stream, or nullptr: T merged on qr
     Ctx* bulk_part[4] = {};    // the bulk context on SM partitions (green contexts) of part_sms[] SMs, or nullptr
     int part_sms[4] = {};
     int nparts = 0;
@@ -472,7 +473,7 @@ struct Run {
         copy_matrix(cx, w, d, MskT + s, n, Lb, n);
         if (sc.qr) {  // K-SQR pipelined with K-LU (left-looking, its own stream)
             SketchQrPipe P;
-            sketch_qr_pipe_begin(P, cx, *sc.qr, qevs, MskT + s, n, w, d);
+            sketch_qr_pipe_begin(P, cx, *sc.qr, qevs, MskT + s, n, w, d, sc.qr2);
             const LeafDone on_leaf = [&](int64_t c1) { sketch_qr_pipe_columns(P, perm, c1); };
             if (!(sc.lu2 && getrf_pivots_la(cx, *sc.lu2, luevs, Lb, n, w, d, ipiv, perm, &on_leaf)))
                 getrf_pivots(cx, Lb, n, w, d, ipiv, perm, &on_leaf);
@@ -791,26 +792,29 @@ static int factor_ex_impl(int64_t m, int64_t n, double* A, int64_t lda, int64_t 
         // low-priority one (Sched); all joined to the caller's stream at entry and exit
         int prio_lo = 0, prio_hi = 0;
         BQ_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
-        cudaStream_t user = cx.stream, s_hi = nullptr, s_lo = nullptr, s_aux = nullptr, s_qr = nullptr, s_lu = nullptr;
+        cudaStream_t user = cx.stream, s_hi = nullptr, s_lo = nullptr, s_aux = nullptr, s_qr = nullptr, s_lu = nullptr,
+                     s_qr2 = nullptr;
         cudaEvent_t ev_in = nullptr, ev_top = nullptr, ev_bulk = nullptr, ev_done = nullptr;
         BQ_CUDA(cudaStreamCreateWithPriority(&s_hi, cudaStreamNonBlocking, prio_hi));
         BQ_CUDA(cudaStreamCreateWithPriority(&s_lo, cudaStreamNonBlocking, prio_lo));
         BQ_CUDA(cudaStreamCreateWithPriority(&s_aux, cudaStreamNonBlocking, prio_hi));
         BQ_CUDA(cudaStreamCreateWithPriority(&s_qr, cudaStreamNonBlocking, prio_hi));
         BQ_CUDA(cudaStreamCreateWithPriority(&s_lu, cudaStreamNonBlocking, prio_hi));
+        BQ_CUDA(cudaStreamCreateWithPriority(&s_qr2, cudaStreamNonBlocking, prio_hi));
         BQ_CUDA(cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming));
         BQ_CUDA(cudaEventCreateWithFlags(&ev_top, cudaEventDisableTiming));
         BQ_CUDA(cudaEventCreateWithFlags(&ev_bulk, cudaEventDisableTiming));
         BQ_CUDA(cudaEventCreateWithFlags(&ev_done, cudaEventDisableTiming));
         BQ_CUDA(cudaEventRecord(ev_in, user));
-        for (cudaStream_t st : {s_hi, s_lo, s_aux, s_qr, s_lu}) BQ_CUDA(cudaStreamWaitEvent(st, ev_in, 0));
+        for (cudaStream_t st : {s_hi, s_lo, s_aux, s_qr, s_lu, s_qr2}) BQ_CUDA(cudaStreamWaitEvent(st, ev_in, 0));
         cx.stream = s_hi;
-        Ctx cxb = cx, cxa = cx, cxq = cx, cxl = cx;
+        Ctx cxb = cx, cxa = cx, cxq = cx, cxl = cx, cxq2 = cx;
         cxb.stream = s_lo;
         cxa.stream = s_aux;
         cxq.stream = s_qr;
         cxl.stream = s_lu;
-        for (Ctx* c : {&cxb, &cxa, &cxq, &cxl}) {  // the split-K scratch belongs to the critical stream
+        cxq2.stream = s_qr2;
+        for (Ctx* c : {&cxb, &cxa, &cxq, &cxl, &cxq2}) {  // the split-K scratch belongs to the critical stream
             c->splitk = nullptr;
             c->splitk_elems = 0;
         }
@@ -821,6 +825,9 @@ static int factor_ex_impl(int64_t m, int64_t n, double* A, int64_t lda, int64_t 
         cxl.timer = nullptr;
         cxl.ws = nullptr;  // nor does the lookahead LU's update stream
         cxl.ws_bytes = cxl.ws_used = 0;
+        cxq2.timer = nullptr;
+        cxq2.ws = nullptr;  // nor the sketch QR's T-merge stream
+        cxq2.ws_bytes = cxq2.ws_used = 0;
         Ctx cxp[3] = {cxb, cxb, cxb};
         cudaStream_t s_parts[3] = {};
         int part_sms[3] = {}, nparts = 0;
@@ -856,6 +863,10 @@ static int factor_ex_impl(int64_t m, int64_t n, double* A, int64_t lda, int64_t 
             sc.panel_la = opts ? opts->panel_lookahead : 0;
             if (!(opts && opts->no_sqr_pipeline)) {
                 sc.qr = &cxq;
+                // the T-merge stream pays where the sketch-QR chain is on the critical path (d <= 1024: C2 -0.6 %,
+                // 4096^2..8192^2 -2 %); at d = 2048 (C3) the pivot selection hides behind the bulk GEMM and the
+                // extra stream only adds contention (+0.1-0.3 %, profiles/r02/sqr_merge_stream_ab_r02.txt)
+                if (!(opts && opts->no_sqr_merge_stream) && d <= 1024) sc.qr2 = &cxq2;
                 if (opts && opts->lu_lookahead) sc.lu2 = &cxl;
             }
             for (int i = 0; i < nparts; ++i) {
@@ -868,12 +879,12 @@ static int factor_ex_impl(int64_t m, int64_t n, double* A, int64_t lda, int64_t 
         int64_t ell = -1;
         int status = 0;
         auto cleanup = [&]() {
-            for (cudaStream_t st : {s_hi, s_lo, s_aux, s_qr, s_lu, s_parts[0], s_parts[1], s_parts[2]}) {
+            for (cudaStream_t st : {s_hi, s_lo, s_aux, s_qr, s_lu, s_qr2, s_parts[0], s_parts[1], s_parts[2]}) {
                 if (!st) continue;
                 cudaEventRecord(ev_done, st);
                 cudaStreamWaitEvent(user, ev_done, 0);
             }
-            for (cudaStream_t st : {s_hi, s_lo, s_aux, s_qr, s_lu}) cudaStreamDestroy(st);
+            for (cudaStream_t st : {s_hi, s_lo, s_aux, s_qr, s_lu, s_qr2}) cudaStreamDestroy(st);
             for (cudaEvent_t e : {ev_in, ev_top, ev_bulk, ev_done}) cudaEventDestroy(e);
             cx.stream = user;
         };

@@ -118,17 +118,20 @@ void sketch_qr(Ctx& cx, double* MskT, int64_t ldm, int64_t w, int64_t d, const R
 struct SketchQrPipe {
     Ctx* cx = nullptr;
     Ctx* q = nullptr;
+    Ctx* q2 = nullptr;  // optional: the T-merge GEMMs of each block on a second stream (overlapping the next block)
     double* MskT = nullptr;
     int64_t ldm = 0, w = 0, d = 0, p = 0;
     double *Wq = nullptr, *V = nullptr, *Tf = nullptr, *tau = nullptr, *W1 = nullptr, *W2 = nullptr;
     double *xbuf = nullptr, *rowj = nullptr;
+    double *W3 = nullptr, *W4 = nullptr;  // q2's scratch
+    cudaEvent_t ev_t = nullptr;           // q2 finished the previous block's T merge
     int64_t gathered = 0, queued = 0;
     std::vector<cudaEvent_t>* events = nullptr;
     size_t nev = 0;
     size_t mark = 0;
 };
 void sketch_qr_pipe_begin(SketchQrPipe& P, Ctx& cx, Ctx& q, std::vector<cudaEvent_t>& events, double* MskT,
-                          int64_t ldm, int64_t w, int64_t d);
+                          int64_t ldm, int64_t w, int64_t d, Ctx* q2 = nullptr);
 void sketch_qr_pipe_columns(SketchQrPipe& P, const int* perm, int64_t c1);
 void sketch_qr_pipe_finish(SketchQrPipe& P, const RskDefer* defer);
 

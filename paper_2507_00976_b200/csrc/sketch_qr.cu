@@ -830,10 +830,12 @@ __global__ void gather_sketch_block_kernel(int64_t d, int jb, const double* __re
 }
 
 void sketch_qr_pipe_begin(SketchQrPipe& P, Ctx& cx, Ctx& q, std::vector<cudaEvent_t>& events, double* MskT,
-                          int64_t ldm, int64_t w, int64_t d)
+                          int64_t ldm, int64_t w, int64_t d, Ctx* q2)
 {
     P.cx = &cx;
     P.q = &q;
+    P.q2 = q2;
+    P.ev_t = nullptr;
     P.events = &events;
     P.nev = 0;
     P.MskT = MskT;
@@ -853,12 +855,19 @@ void sketch_qr_pipe_begin(SketchQrPipe& P, Ctx& cx, Ctx& q, std::vector<cudaEven
     P.xbuf = cx.alloc(2 * (size_t)cx.num_sms * QR_XSTRIDE + (size_t)cx.num_sms * QR_JBMAX * QR_JBMAX);
     P.rowj = cx.alloc(2 * QR_JBMAX);
     // split-K slices of q's skinny long-K GEMMs (V^T B: c x 32 over K = d), when they fit the temporaries' budget
-    if (d >= 512) {
-        q.splitk_elems = (size_t)16 * QR_JBMAX * d;
-        q.splitk = cx.alloc(q.splitk_elems);
-    } else {
-        q.splitk = nullptr;
-        q.splitk_elems = 0;
+    for (Ctx* c : {&q, q2}) {
+        if (!c) continue;
+        if (d >= 512) {
+            c->splitk_elems = (size_t)16 * QR_JBMAX * d;
+            c->splitk = cx.alloc(c->splitk_elems);
+        } else {
+            c->splitk = nullptr;
+            c->splitk_elems = 0;
+        }
+    }
+    if (q2) {
+        P.W3 = cx.alloc((size_t)d * QR_JBMAX);
+        P.W4 = cx.alloc((size_t)d * QR_JBMAX);
     }
     BQ_CUDA(cudaMemsetAsync(P.V, 0, sizeof(double) * d * P.p, cx.stream));
     BQ_CUDA(cudaMemsetAsync(P.Tf, 0, sizeof(double) * P.p * P.p, cx.stream));
@@ -883,14 +892,30 @@ static void pipe_block(SketchQrPipe& P, int64_t c, int jb)
     double* B = P.Wq + c * d;
     if (c > 0) {
         gemm(q, true, false, c, jb, d, 1.0, P.V, d, B, d, 0.0, P.W1, c);          // W1 = V_c^T B
+        if (P.ev_t) BQ_CUDA(cudaStreamWaitEvent(q.stream, P.ev_t, 0));             // T_c complete (q2)
         gemm(q, true, false, c, jb, c, 1.0, P.Tf, p, P.W1, c, 0.0, P.W2, c);      // W2 = T_c^T W1
         gemm(q, false, false, d, jb, c, -1.0, P.V, d, P.W2, c, 1.0, B, d);        // B -= V_c W2
     }
     qr_panel(q, P.Wq, d, d, c, jb, P.tau, P.V, P.Tf, p, P.xbuf, P.rowj);
     if (c > 0) {
-        gemm(q, true, false, c, jb, d, 1.0, P.V, d, P.V + c * d, d, 0.0, P.W1, c);  // V_c^T V_b
-        gemm(q, false, false, c, jb, c, 1.0, P.Tf, p, P.W1, c, 0.0, P.W2, c);        // T_c (V_c^T V_b)
-        gemm(q, false, false, c, jb, jb, -1.0, P.W2, c, P.Tf + c + c * p, p, 0.0, P.Tf + c * p, p);
+        // T merge; on q2 it overlaps the next block's W1 = V^T B (which needs V, not T)
+        Ctx* m = &q;
+        double *M1 = P.W1, *M2 = P.W2;
+        if (P.q2) {
+            cudaEvent_t e = pipe_event(P);
+            BQ_CUDA(cudaEventRecord(e, q.stream));
+            BQ_CUDA(cudaStreamWaitEvent(P.q2->stream, e, 0));
+            m = P.q2;
+            M1 = P.W3;
+            M2 = P.W4;
+        }
+        gemm(*m, true, false, c, jb, d, 1.0, P.V, d, P.V + c * d, d, 0.0, M1, c);  // V_c^T V_b
+        gemm(*m, false, false, c, jb, c, 1.0, P.Tf, p, M1, c, 0.0, M2, c);          // T_c (V_c^T V_b)
+        gemm(*m, false, false, c, jb, jb, -1.0, M2, c, P.Tf + c + c * p, p, 0.0, P.Tf + c * p, p);
+        if (P.q2) {
+            P.ev_t = pipe_event(P);
+            BQ_CUDA(cudaEventRecord(P.ev_t, P.q2->stream));
+        }
     }
 }
 
@@ -926,11 +951,14 @@ void sketch_qr_pipe_finish(SketchQrPipe& P, const RskDefer* defer)
         return;
     }
     if (P.queued < p) throw std::runtime_error("sketch_qr_pipe: K-LU did not finish the pivots");
-    cudaEvent_t e = pipe_event(P);
-    BQ_CUDA(cudaEventRecord(e, P.q->stream));
-    BQ_CUDA(cudaStreamWaitEvent(cx.stream, e, 0));
-    P.q->splitk = nullptr;
-    P.q->splitk_elems = 0;
+    for (Ctx* c : {P.q, P.q2}) {
+        if (!c) continue;
+        cudaEvent_t e = pipe_event(P);
+        BQ_CUDA(cudaEventRecord(e, c->stream));
+        BQ_CUDA(cudaStreamWaitEvent(cx.stream, e, 0));
+        c->splitk = nullptr;
+        c->splitk_elems = 0;
+    }
     double* MskT = P.MskT;
     double* Wq = P.Wq;
     int64_t rest = w - p;

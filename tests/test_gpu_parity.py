@@ -526,6 +526,19 @@ def test_pipelined_sketch_qr_matches_recursive(gpu, shape, b, d, lu_la):
         same(_host(J1), _host(Ag1), _host(tau1), o.J, o.A, o.tau)
 
 
+def test_sqr_merge_stream_is_bitwise_neutral(gpu):
+    """The pipelined K-SQR's T merges on their own stream (default) or on the pipeline's stream: the same GEMMs in
+    the same order per element, so the factorization is bitwise identical."""
+    import torch
+
+    bq = _bq()
+    A = inputs.gaussian(3000, 2600, seed=9)
+    Ag0, tau0, J0, r0 = bq.factor(_dev(A), 512, 512, seed=1)
+    Ag1, tau1, J1, r1 = bq.factor(_dev(A), 512, 512, seed=1, sqr_merge_stream=False)
+    assert r0 == r1 == 2600
+    assert torch.equal(J1, J0) and torch.equal(tau1, tau0) and torch.equal(Ag1, Ag0)
+
+
 @pytest.mark.parametrize("bulk_sms", [-1, 100, 24])
 def test_bulk_partition_is_bitwise_neutral(gpu, bulk_sms):
     """The bulk trailing GEMM on a green-context SM partition (bqrrp_options.bulk_sms: every iteration on a
