@@ -46,7 +46,7 @@ CONFIGS = {
 ORACLE_SAMPLE = {"C1": (1024, 1024), "C2": (4096, 4096), "C3": (4096, 4096), "C4": (16384, 1024)}
 
 PEAKS_FILE = os.path.join(ROOT, "profiles", "fp64_peak_r01.json")
-NCU_SUMMARY = os.path.join(ROOT, "profiles", "ncu_summary_r01.json")
+NCU_SUMMARY = os.path.join(ROOT, "profiles", "r02", "ncu_summary_r02.json")
 
 
 def canonical_flops(m: int, n: int) -> float:
@@ -383,7 +383,8 @@ def main():
     try:
         ns = json.load(open(NCU_SUMMARY))
         traffic = ns.get("dgemm_trailing_dram_bytes_per_launch")
-        traffic_note = ("dram read+write bytes of ONE launch (the C3 iteration-0 bulk GEMM, ncu --set full); its "
+        traffic_note = ("dram read+write bytes of ONE launch (the C3 iteration-0 bulk GEMM, ncu --set full, 32-row "
+                        "rasterisation groups); its "
                         "algorithmic bytes: %.4g" % ns.get("algorithmic_bytes_per_launch", float("nan")))
     except Exception:
         pass

@@ -22,7 +22,10 @@
 namespace bqrrp {
 
 constexpr int GEMM_BK = 16;
-constexpr int GROUP_M = 8;  // tile-rows per rasterisation group
+#ifndef BQRRP_GROUP_M
+#define BQRRP_GROUP_M 32
+#endif
+constexpr int GROUP_M = BQRRP_GROUP_M;  // tile-rows per rasterisation group (experiments: -DBQRRP_GROUP_M=…)
 
 __device__ __forceinline__ void dmma_884(double& c0, double& c1, double a, double b)
 {
