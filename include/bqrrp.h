@@ -101,6 +101,11 @@ typedef struct bqrrp_options {
      * stream, measured better at C3); 1 = always on the pipeline's own stream.  Identical results (same GEMMs, same
      * order per element). */
     int no_sqr_merge_stream;
+    /* K-LU cooperative grid leaf (sketch transposes taller than the cluster leaves hold, w > ~25k): at most this many
+     * CTAs.  0 (default) = per iteration in the lookahead: 32 when the bulk GEMM is estimated longer than the pivot
+     * selection it overlaps (fewer CTAs hold more rows each, with narrower leaves, and the other SMs stay with the
+     * bulk: C3 -0.9 %), else one per SM.  Same pivots, bitwise the same factorization. */
+    int lu_grid_ctas;
 } bqrrp_options;
 #define BQRRP_DEBUG_FORCE_BREAKDOWN 1
 #define BQRRP_DIST_SHARD_PANEL 1

@@ -37,7 +37,8 @@ class Options(ctypes.Structure):
                 ("dist_nb", ctypes.c_int64), ("debug_flags", ctypes.c_int), ("dist_flags", ctypes.c_int),
                 ("panel_lookahead", ctypes.c_int), ("bulk_sms", ctypes.c_int),
                 ("no_sqr_pipeline", ctypes.c_int), ("lu_lookahead", ctypes.c_int),
-                ("lu_leaf_cluster", ctypes.c_int), ("no_sqr_merge_stream", ctypes.c_int)]
+                ("lu_leaf_cluster", ctypes.c_int), ("no_sqr_merge_stream", ctypes.c_int),
+                ("lu_grid_ctas", ctypes.c_int)]
 
 
 def lib() -> ctypes.CDLL:
@@ -125,8 +126,9 @@ def workspace_query(m: int, n: int, b: int, d: int) -> int:
 
 def _options(rank_tol, cholqr_passes, phases, hqr_fallback=True, lookahead=True, debug_force_breakdown=False,
              dist_nb=0, panel_lookahead=0, bulk_sms=0, sqr_pipeline=True, lu_lookahead=False, lu_leaf_cluster=0,
-             sqr_merge_stream=True):
+             sqr_merge_stream=True, lu_grid_ctas=0):
     o = Options()
+    o.lu_grid_ctas = int(lu_grid_ctas)
     o.no_sqr_merge_stream = 0 if sqr_merge_stream else 1
     o.lu_leaf_cluster = int(lu_leaf_cluster)
     o.lu_lookahead = 1 if lu_lookahead else 0
@@ -147,7 +149,7 @@ def factor(A, b: int, d: int | None = None, seed: int = 0, rank_tol: float | Non
            workspace=None, tau=None, J=None, stream=None, phase_times: bool = False, hqr_fallback: bool = True,
            lookahead: bool = True, debug_force_breakdown: bool = False, panel_lookahead: int = 0,
            bulk_sms: int = 0, sqr_pipeline: bool = True, lu_lookahead: bool = False,
-           lu_leaf_cluster: int = 0, sqr_merge_stream: bool = True):
+           lu_leaf_cluster: int = 0, sqr_merge_stream: bool = True, lu_grid_ctas: int = 0):
     """BQRRP of A in place (Alg. 1); returns (A, tau, J, rank[, phase_ms dict]).
 
     A: float64 CUDA tensor in column-major layout (m x n); overwritten in GEQP3 format.
@@ -180,7 +182,7 @@ def factor(A, b: int, d: int | None = None, seed: int = 0, rank_tol: float | Non
     opts = _options(rank_tol, cholqr_passes, phases, hqr_fallback, lookahead, debug_force_breakdown,
                     panel_lookahead=panel_lookahead, bulk_sms=bulk_sms, sqr_pipeline=sqr_pipeline,
                     lu_lookahead=lu_lookahead, lu_leaf_cluster=lu_leaf_cluster,
-                    sqr_merge_stream=sqr_merge_stream)
+                    sqr_merge_stream=sqr_merge_stream, lu_grid_ctas=lu_grid_ctas)
     st = lib().bqrrp_factor_ex(m, n, ctypes.c_void_p(A.data_ptr()), lda, b, d, seed, ctypes.c_void_p(tau.data_ptr()),
                                ctypes.c_void_p(J.data_ptr()), ctypes.byref(rank), ws_ptr, ws_bytes,
                                _stream_ptr(stream), ctypes.byref(opts))

@@ -333,13 +333,31 @@ struct Sched {
     // within ~1.15x the chain (the chain itself speeds up with the SMs it gets back), leaving the other SMs to the
     // chain's cluster kernels (measured: C2 qrcp_wide 196 -> 178 ms with the bulk on 100 SMs,
     // profiles/bulk_partition_r02.json); otherwise on the whole device.
+    static double bulk_est_us(int64_t h, int64_t k, int64_t t)
+    {
+        return 2.0 * (double)(h - k) * (double)k * (double)t / 34e12 * 1e6;
+    }
+    static double chain_est_us(int64_t d, int64_t w_next)
+    {
+        const double dd = (double)d, ww = (double)w_next;
+        return dd * (w_next > 16384 ? 14.0 : 9.0) + (3.0 * ww * dd * dd + 4.0 / 3.0 * dd * dd * dd) / 20e6;
+    }
+    // K-LU's cooperative grid leaf (w > ~25k rows) for the next pivot selection: capped at 32 CTAs (narrower leaves,
+    // the other SMs stay with the bulk GEMM) when the bulk is the long pole — the leaf's every launch otherwise
+    // drains the whole device of bulk CTAs (C3 13.41 -> 13.30 s; 16 / 24 / 48 / 64 CTAs measured 13.41 / 13.33 /
+    // 13.31 / 13.32 s, profiles/r02/lu_grid_cap_ab_r02.txt) — else one CTA per SM (the leaf on the critical path).
+    int lu_grid_for(int64_t h, int64_t k, int64_t t, int64_t d, int64_t w_next) const
+    {
+        if (lu_grid_user > 0) return lu_grid_user;
+        return bulk_est_us(h, k, t) > chain_est_us(d, w_next) ? 32 : 0;
+    }
+    int lu_grid_user = 0;  // bqrrp_options.lu_grid_ctas (> 0: always that cap)
     Ctx& bulk_for(int64_t h, int64_t k, int64_t t, int64_t d, int64_t w_next, int num_sms) const
     {
         if (nparts == 0) return *bulk;
         if (part_always) return *bulk_part[0];
-        const double bulk_us = 2.0 * (double)(h - k) * (double)k * (double)t / 34e12 * 1e6;
-        const double dd = (double)d, ww = (double)w_next;
-        const double chain_us = dd * (w_next > 16384 ? 14.0 : 9.0) + (3.0 * ww * dd * dd + 4.0 / 3.0 * dd * dd * dd) / 20e6;
+        const double bulk_us = bulk_est_us(h, k, t);
+        const double chain_us = chain_est_us(d, w_next);
         Ctx* best = bulk;
         for (int i = 0; i < nparts; ++i)  // part_sms[] descending: the smallest partition that keeps up
             if (bulk_us * num_sms / part_sms[i] <= 1.15 * chain_us) best = bulk_part[i];
@@ -627,6 +645,7 @@ static int64_t loop_lookahead(Run& R)
         R.sample_update(s, c, ex);
         const int64_t s1 = c, h1 = m - s1, w1 = n - s1;
         const int64_t kmax1 = imin(imin(b, w1), h1);
+        cx.lu_grid_max = sc.lu_grid_for(h, k, t, R.d, w1);
         R.pivots(i + 1, s1);
         double* Cb = A + s1 + s1 * lda;  // = C + k rows: the bulk's rows, columns from the next window's start
         if (sc.panel_la != 1) {
@@ -756,6 +775,7 @@ static int factor_ex_impl(int64_t m, int64_t n, double* A, int64_t lda, int64_t 
         cx.force_breakdown = opts && (opts->debug_flags & BQRRP_DEBUG_FORCE_BREAKDOWN);
         if (opts && (opts->lu_leaf_cluster == 4 || opts->lu_leaf_cluster == 8 || opts->lu_leaf_cluster == 16))
             cx.lu_gpref = opts->lu_leaf_cluster;
+        if (opts && opts->lu_grid_ctas > 0) cx.lu_grid_max = opts->lu_grid_ctas;  // (lookahead: per iteration)
         if (m == 0 || n == 0) {
             *rank = 0;
             if (n > 0) {
@@ -861,6 +881,7 @@ static int factor_ex_impl(int64_t m, int64_t n, double* A, int64_t lda, int64_t 
             sc.ev_top = ev_top;
             sc.ev_bulk = ev_bulk;
             sc.panel_la = opts ? opts->panel_lookahead : 0;
+            sc.lu_grid_user = opts ? opts->lu_grid_ctas : 0;
             if (!(opts && opts->no_sqr_pipeline)) {
                 sc.qr = &cxq;
                 // the T-merge stream pays where the sketch-QR chain is on the critical path (d <= 1024: C2 -0.6 %,

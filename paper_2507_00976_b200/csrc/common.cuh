@@ -159,6 +159,7 @@ struct Ctx {
     Timer* timer = nullptr;
     bool force_breakdown = false;  // test hook (bqrrp_options.debug_flags): report a POTRF breakdown per panel
     int lu_gpref = 16;             // K-LU register leaf: preferred largest cluster (bqrrp_options.lu_leaf_cluster)
+    int lu_grid_max = 0;           // K-LU cooperative grid leaf: at most this many CTAs (0 = num_sms)
     void mark(int phase) { if (timer) timer->mark(phase); }
 
     double* alloc(size_t n_doubles)

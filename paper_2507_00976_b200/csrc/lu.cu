@@ -822,7 +822,7 @@ static void lu_panel(Ctx& cx, double* L, int64_t ld, int64_t w, int64_t d, int64
     if (lu_panel_cluster(cx, L, ld, w, d, c0, jb, ipiv, perm)) return;
     int64_t rows = w - c0;
     // few enough CTAs that the barrier stays cheap, enough that the slab fits shared memory
-    const int gmax = cx.num_sms;
+    const int gmax = cx.lu_grid_max > 0 ? (int)imin(cx.lu_grid_max, cx.num_sms) : cx.num_sms;
     int G = (int)imin(gmax, imax(1, cdiv(rows, 256)));
     int R = (int)cdiv(rows, G);
     if ((size_t)R * jb * sizeof(double) > 200 * 1024) {
@@ -896,7 +896,7 @@ void getrf_pivots(Ctx& cx, double* L, int64_t ld, int64_t w, int64_t d, int* ipi
     LuExchange ex;
     ex.xbuf = cx.alloc(2 * (size_t)cx.num_sms * LU_XSTRIDE);
     ex.rowj = cx.alloc(2 * LU_JBMAX);
-    int leaf = lu_leaf_width(w, cx.num_sms);
+    int leaf = lu_leaf_width(w, cx.lu_grid_max > 0 ? (int)imin(cx.lu_grid_max, cx.num_sms) : cx.num_sms);
     getrf_rec(cx, L, ld, w, nlu, 0, nlu, ipiv, perm, ex, leaf, on_leaf);
     cx.ws_used = mark;
 }

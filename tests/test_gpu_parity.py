@@ -539,6 +539,23 @@ def test_sqr_merge_stream_is_bitwise_neutral(gpu):
     assert torch.equal(J1, J0) and torch.equal(tau1, tau0) and torch.equal(Ag1, Ag0)
 
 
+@pytest.mark.parametrize("ctas", [32, 148, 16])
+def test_lu_grid_leaf_cap_same_factorization(gpu, ctas):
+    """A wide input whose sketch transpose needs K-LU's cooperative grid leaf (w > 25.6k rows): capping that leaf at
+    16 / 32 CTAs (narrower leaves, more rows per CTA) or running it on every SM gives the same pivots, hence bitwise
+    the same factorization (J(:l), tau, the first l columns) as the default schedule (lookahead: the cap applies
+    where the bulk GEMM is the long pole)."""
+    import torch
+
+    bq = _bq()
+    A = inputs.gaussian(640, 30000, seed=13)
+    Ag0, tau0, J0, r0 = bq.factor(_dev(A), 256, 256, seed=3)
+    Ag1, tau1, J1, r1 = bq.factor(_dev(A), 256, 256, seed=3, lu_grid_ctas=ctas)
+    assert r0 == r1 == 640
+    # m < n: the pivots past l = m are decided on rounding noise (the last iteration has h < d rows, DESIGN.md §6)
+    assert torch.equal(J1[:r0], J0[:r0]) and torch.equal(tau1, tau0) and torch.equal(Ag1[:, :r0], Ag0[:, :r0])
+
+
 @pytest.mark.parametrize("bulk_sms", [-1, 100, 24])
 def test_bulk_partition_is_bitwise_neutral(gpu, bulk_sms):
     """The bulk trailing GEMM on a green-context SM partition (bqrrp_options.bulk_sms: every iteration on a

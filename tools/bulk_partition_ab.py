@@ -1,7 +1,7 @@
 """A/B of the bulk trailing GEMM's SM partition (bqrrp_options.bulk_sms): whole device (-1),
 auto (0) and fixed green-context partitions, event-timed whole factorizations (best of `reps` after a warm-up),
 with the factor checked bitwise against the whole-device run.
-usage: python tools/bulk_partition_ab.py C2|<m> [b] [--reps R] [--sms -1,0,132,116] [--json out.json] [--no-pipe] [--lula] [--panel-la 1] [--lucl 8|16] [--no-merge-stream]"""
+usage: python tools/bulk_partition_ab.py C2|<m> [b] [--reps R] [--sms -1,0,132,116] [--json out.json] [--no-pipe] [--lula] [--panel-la 1] [--lucl 8|16] [--no-merge-stream] [--lu-grid N]"""
 import json
 import os
 import sys
@@ -45,7 +45,7 @@ for s in sms:
         out = bq.factor(A, b, d, seed=0, workspace=ws, bulk_sms=s, phase_times=(r == reps or "--phases" in sys.argv),
                         sqr_pipeline="--no-pipe" not in sys.argv, lu_lookahead="--lula" in sys.argv,
                         panel_lookahead=int(arg("--panel-la", "0")), lu_leaf_cluster=int(arg("--lucl", "0")),
-                        sqr_merge_stream="--no-merge-stream" not in sys.argv)
+                        sqr_merge_stream="--no-merge-stream" not in sys.argv, lu_grid_ctas=int(arg("--lu-grid", "0")))
         e1.record()
         torch.cuda.synchronize()
         if r > 0 and r < reps:
