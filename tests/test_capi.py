@@ -102,3 +102,28 @@ def test_missing_library_fails_loudly(monkeypatch):
         bq.lib()
     with pytest.raises(ImportError):
         bq.workspace_query(64, 64, 16, 16)
+
+
+def test_options_struct_layout_matches_header(tmp_path):
+    """The ctypes mirror of bqrrp_options (the binding's Options) has the header's size and field offsets: a C
+    program compiled against include/bqrrp.h prints them (gcc, no GPU)."""
+    import shutil
+    import subprocess
+
+    import paper_2507_00976_b200 as bq
+
+    if shutil.which("gcc") is None:
+        pytest.skip("gcc not available")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    names = [f[0] for f in bq.Options._fields_]
+    src = tmp_path / "layout.c"
+    src.write_text("#include <stdio.h>\n#include <stddef.h>\n#include \"bqrrp.h\"\nint main(void) {\n"
+                   "  printf(\"size %zu\\n\", sizeof(bqrrp_options));\n"
+                   + "".join(f"  printf(\"{n} %zu\\n\", offsetof(bqrrp_options, {n}));\n" for n in names)
+                   + "  return 0;\n}\n")
+    exe = tmp_path / "layout"
+    subprocess.check_call(["gcc", "-I", os.path.join(root, "include"), str(src), "-o", str(exe)])
+    out = dict(line.split() for line in subprocess.check_output([str(exe)], text=True).splitlines())
+    assert int(out["size"]) == ctypes.sizeof(bq.Options)
+    for n in names:
+        assert int(out[n]) == getattr(bq.Options, n).offset, n
