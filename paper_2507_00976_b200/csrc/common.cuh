@@ -144,8 +144,8 @@ inline cudaError_t lib_malloc_async(T** p, size_t bytes, cudaStream_t st)
 
 // A low-priority stream confined to a partition of about `sms` SMs of the current device (a driver green
 // context, created once per device and size and kept for the process).  The bulk trailing GEMM
-// runs there when it is shorter than the latency-bound chain it overlaps, so the chain's cluster kernels never
-// wait for SMs to drain.  nullptr when the driver has no green contexts; *got = the partition's SM count.
+// runs there when it is shorter than the latency-bound chain it overlaps, leaving whole SM groups to the chain's
+// kernels.  nullptr when the driver has no green contexts; *got = the partition's SM count.
 cudaStream_t green_stream(int sms, int* got);
 
 struct Ctx {

@@ -573,7 +573,7 @@ __global__ void __launch_bounds__(QL_THREADS, 1) qr_leaf_fast_kernel(QrLeafArgs 
     // T (larft): T_jj = tau_j, T(0:j, j) = -tau_j T(0:j, 0:j) (V(:, 0:j)^T v_j).  Lane i keeps row i of T in
     // registers (T(i, l) = 0 for l < i), both loops unrolled so every index is compile-time: column j costs j
     // register FMAs per lane (the same ascending order as the scalar recurrence: the zero terms are exact)
-    // instead of a serial shared-memory dot product per lane (26k -> ~2k cycles per leaf, tools/leaf_timing.py).
+    // instead of a serial shared-memory dot product per lane (26k -> 8.4k cycles per leaf, tools/leaf_timing.py).
     if (me == 0 && warp == 0) {
         double trow[JB];
 #pragma unroll
