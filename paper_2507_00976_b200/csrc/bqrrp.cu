@@ -327,7 +327,7 @@ struct Sched {
     int nparts = 0;
     bool part_always = false;  // bqrrp_options.bulk_sms > 0: every bulk on bulk_part[0]
     // The bulk context of one iteration.  The bulk GEMM (2 (h-k) k t flops) overlaps the latency-bound chain (the
-    // sample update and the next pivot selection: about 9 us per sketch column under the bulk's contention plus its
+    // sample update and the next pivot selection: about 7 us per sketch column under the bulk's contention plus its
     // GEMMs, ~3 w d^2 + 4/3 d^3 flops at ~20 TFLOP/s, plus ~5 us per column for the cooperative-grid LU leaf beyond
     // 16384 rows).  When the bulk is the shorter of the two it runs on the smallest partition that finishes it
     // within ~1.15x the chain (the chain itself speeds up with the SMs it gets back), leaving the other SMs to the
@@ -340,7 +340,10 @@ struct Sched {
     static double chain_est_us(int64_t d, int64_t w_next)
     {
         const double dd = (double)d, ww = (double)w_next;
-        return dd * (w_next > 16384 ? 14.0 : 9.0) + (3.0 * ww * dd * dd + 4.0 / 3.0 * dd * dd * dd) / 20e6;
+#ifndef BQRRP_CHAIN_US_PER_COL  // tuned with the K-SQR pipeline: 5 / 7 / 9 / 12 us, profiles/r02/chain_constant_ab_r02.txt
+#define BQRRP_CHAIN_US_PER_COL 7.0
+#endif
+        return dd * (w_next > 16384 ? 14.0 : BQRRP_CHAIN_US_PER_COL) + (3.0 * ww * dd * dd + 4.0 / 3.0 * dd * dd * dd) / 20e6;
     }
     // K-LU's cooperative grid leaf (w > ~25k rows) for the next pivot selection: capped at 32 CTAs (narrower leaves,
     // the other SMs stay with the bulk GEMM) when the bulk is the long pole — the leaf's every launch otherwise

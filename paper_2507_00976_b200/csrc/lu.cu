@@ -251,7 +251,6 @@ __global__ void __launch_bounds__(LU_THREADS, 1) lu_panel_cluster_kernel(LuPanel
     __shared__ int64_t red_i[LU_THREADS / 32];
     __shared__ double pivrow[LU_JBMAX], oldrow[LU_JBMAX];
     __shared__ int64_t s_piv;
-    __shared__ int s_win;
     __shared__ int64_t spiv[LU_JBMAX], trow[2 * LU_JBMAX], tsrc[2 * LU_JBMAX];
     __shared__ int s_nt;
     const int64_t rbeg = a.c0 + (int64_t)me * R;

@@ -1,7 +1,7 @@
 """A/B of the bulk trailing GEMM's SM partition (bqrrp_options.bulk_sms): whole device (-1),
 auto (0) and fixed green-context partitions, event-timed whole factorizations (best of `reps` after a warm-up),
 with the factor checked bitwise against the whole-device run.
-usage: python tools/bulk_partition_ab.py C2|<m> [b] [--reps R] [--sms -1,0,132,116] [--json out.json] [--no-pipe] [--lula] [--panel-la 1] [--lucl 8|16] [--no-merge-stream] [--lu-grid N]"""
+usage: python tools/bulk_partition_ab.py C2|<m> [b] [--reps R] [--sms -1,0,132,116] [--json out.json] [--no-pipe] [--lula] [--panel-la 1] [--lucl 8|16] [--no-merge-stream] [--lu-grid N] [--lib path.so]"""
 import json
 import os
 import sys
@@ -20,6 +20,8 @@ def arg(name, default):
     return sys.argv[sys.argv.index(name) + 1] if name in sys.argv else default
 
 
+if "--lib" in sys.argv:  # an experimental build of the library (e.g. other compile-time constants)
+    bq._LIB_PATH = arg("--lib", "")
 name = sys.argv[1]
 if name.isdigit():
     m = n = int(name)
