@@ -465,7 +465,8 @@ struct Run {
         BQ_CUDA(cudaMemsetAsync(cx.flags, 0, sizeof(int) * F_NFLAGS, cx.stream));
         if (hio) {  // S^T lives in the column scratch until the loop starts
             sketch_operator_T(cx, m, d, seed, colscr, m);
-            const int64_t chunk = imax(b, cdiv(n, 16));
+            // 64 chunks: the first sketch GEMM waits for 1/64 of A instead of 1/16 (C3: ~10 instead of ~40 ms of PCIe)
+            const int64_t chunk = imax(b, cdiv(n, 64));
             for (int64_t c0 = 0; c0 < n; c0 += chunk) {
                 const int64_t nc = imin(chunk, n - c0);
                 BQ_CUDA(cudaMemcpy2DAsync(A + c0 * lda, lda * sizeof(double), hio->A_in + c0 * hio->ld_host,
